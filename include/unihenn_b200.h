@@ -1,0 +1,122 @@
+/*
+ * unihenn_b200.h -- C-ABI of the B200-native RNS-CKKS engine behind the
+ * reference's operator boundary (pkg/src/slotcnn/he_backend.py:155-253).
+ *
+ * The reference has no native code and no FFI; its boundary is the Python
+ * class `Backend` (encode / _plain / encrypt / decrypt / add / mul_plain /
+ * mul_cipher / rotate).  Each entry point below is what a drop-in GPU
+ * `Backend` binds through ctypes; the comment on each
+ * names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Every uint64_t* / int64_t* / double* argument is a DEVICE pointer on the
+ *    context's device, except the host arrays of uh_ctx_create.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    asynchronous on that stream; scratch comes from the stream-ordered pool.
+ *  - Polynomials are in evaluation ("slot") order: entry j < N/2 holds
+ *    a(psi^(5^j)), entry N/2+j holds a(psi^(-5^j)); rotation by r slots is a
+ *    cyclic shift of each half.  Residues are canonical, in [0, q).
+ *  - A polynomial list is n_polys polys of nl limbs, poly p limb k at
+ *    base + (p*pstride + k)*N; limb k < nq is modulus k, a further limb is the
+ *    special prime P (modulus index count-1).  A batch of B ciphertexts with ls
+ *    stored limbs is the list of 2B polys (c0,c1 of ct 0, c0,c1 of ct 1, ...)
+ *    with pstride = ls.  Level l uses limbs 0..l.
+ *  - Key-switching keys: [l+1 digits][2][key_limbs][N] with limbs
+ *    (q_0..q_{key_limbs-2}, P); usable at every level <= key_limbs - 2.
+ *  - Return value: 0 on success, nonzero on error; uh_last_error() gives the
+ *    message (thread-local).  The Python wrapper raises
+ *    LevelExhausted / SlotMismatch / OversizedInput itself before calling.
+ */
+#ifndef UNIHENN_B200_H
+#define UNIHENN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct uh_ctx uh_ctx;
+
+int uh_abi_version(void);
+const char *uh_last_error(void);
+
+/* Parameter set -> device context.  Replaces HEParams' role as the space
+ * description (he_backend.py:34-77): moduli = q_0..q_depth, P; psi[i] a
+ * primitive 2N-th root of unity mod moduli[i]. */
+int uh_ctx_create(uh_ctx **out, uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_t count,
+                  int device);
+int uh_ctx_destroy(uh_ctx *ctx);
+
+/* Forward (coefficients -> slot order) or inverse NTT, in place.
+ * Building block of encode (he_backend.py:176-190) and of every key switch. */
+int uh_ntt(uh_ctx *ctx, uint64_t *data, int n_polys, int nl, int nq, int pstride, int inverse, void *stream);
+
+/* Elementwise op over a polynomial list: 0 add, 1 sub, 2 mul, 3 out += a*b,
+ * 4 negate, 5 copy.  b poly index = p % b_polys, or (p/2) % (-b_polys) when
+ * b_polys < 0 (one plaintext per ciphertext).  add == Backend.add
+ * (he_backend.py:215-224). */
+int uh_elementwise(uh_ctx *ctx, int op, uint64_t *out, const uint64_t *a, const uint64_t *b, int n_polys,
+                   int b_polys, int nl, int nq, int out_ps, int a_ps, int b_ps, void *stream);
+
+/* Divide by the modulus of the top limb with centred rounding (rescale when
+ * top_mod = nl, ModDown when top_mod = P): in n_polys x (nl+1) -> out n_polys x nl. */
+int uh_divide_top(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int n_polys, int nl, int top_mod, int out_ps,
+                  int in_ps, void *stream);
+
+/* Rescale of a ciphertext batch at `level` (the level-1 of he_backend.py:226-247). */
+int uh_rescale(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,
+               void *stream);
+
+/* Hybrid key switching pieces: ModUp (one digit per q_j, centred lift) into
+ * D[n_polys][l+1][l+2][N]; inner product with a key, the Galois shift r folded
+ * into the D reads -> u[n_polys][2][l+2][N]; full key switch -> [n_polys][2][l+1][N]. */
+int uh_modup(uh_ctx *ctx, uint64_t *D, const uint64_t *in, int n_polys, int level, int in_ps, void *stream);
+int uh_key_inner(uh_ctx *ctx, uint64_t *u, const uint64_t *D, const uint64_t *key, int key_limbs, int n_polys,
+                 int level, int64_t r, void *stream);
+int uh_keyswitch(uh_ctx *ctx, uint64_t *out, const uint64_t *d, int n_polys, int level, int d_ps,
+                 const uint64_t *key, int key_limbs, void *stream);
+
+/* Backend.rotate (he_backend.py:249-253): left rotation by r slots
+ * (np.roll(v, -r)); r = 0 is a copy. */
+int uh_rotate(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,
+              const uint64_t *key, int key_limbs, int64_t r, void *stream);
+
+/* Backend.mul_plain (he_backend.py:226-235): ct x pt then rescale; pt encoded
+ * at scale q_level.  pt_batched: one plaintext per ciphertext instead of one shared. */
+int uh_mul_plain_rescale(uh_ctx *ctx, uint64_t *out, const uint64_t *ct, const uint64_t *pt, int B, int level,
+                         int out_ls, int ct_ls, int pt_ls, int pt_batched, void *stream);
+
+/* Backend.mul_cipher (he_backend.py:237-247): tensor, relinearise with rk, rescale. */
+int uh_mul_relin_rescale(uh_ctx *ctx, uint64_t *out, const uint64_t *a, const uint64_t *b, int B, int level,
+                         int out_ls, int a_ls, int b_ls, const uint64_t *rk, int rk_limbs, void *stream);
+
+/* Keys.  Secret: ternary, evaluation form over all `count` moduli, [count][N]. */
+int uh_secret_gen(uh_ctx *ctx, uint64_t *s_eval, uint64_t seed, void *stream);
+int uh_galois_keygen(uh_ctx *ctx, uint64_t *key, const uint64_t *s_eval, uint64_t seed, int64_t r, int level,
+                     void *stream);
+int uh_relin_keygen(uh_ctx *ctx, uint64_t *key, const uint64_t *s_eval, uint64_t seed, int level, void *stream);
+
+/* Backend.encrypt (he_backend.py:202-204): secret-key encryption of B
+ * plaintexts (pt_ls < 0: one plaintext for all) at `level`; ct b uses
+ * randomness id ct_id0 + b. */
+int uh_encrypt(uh_ctx *ctx, uint64_t *out, const uint64_t *pt, const uint64_t *s_eval, int B, int level,
+               int out_ls, int pt_ls, uint64_t seed, uint64_t ct_id0, void *stream);
+
+/* Backend.decrypt (he_backend.py:206-207), first half: c0 + c1*s on q_0,
+ * inverse NTT, centred -> double coefficients [B][N]. */
+int uh_decrypt_coeffs(uh_ctx *ctx, double *out, const uint64_t *ct, const uint64_t *s_eval, int B, int ct_ls,
+                      void *stream);
+
+/* Backend.encode (he_backend.py:176-190) on the device: canonical embedding
+ * of real slot vectors [n_polys][N/2] at `scale` -> rounded int64 coefficients
+ * [n_polys][N]; from_signed reduces them into nl limbs and NTTs. */
+int uh_encode_coeffs(uh_ctx *ctx, int64_t *coef, const double *slots, int n_polys, double scale, void *stream);
+int uh_from_signed(uh_ctx *ctx, uint64_t *out, const int64_t *coef, int n_polys, int nl, int out_ps, void *stream);
+/* decrypt, second half: coefficients -> slot values [n_polys][N/2]. */
+int uh_decode_coeffs(uh_ctx *ctx, double *slots, const double *coef, int n_polys, double scale, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,101 @@
+// Shared device primitives of the B200 RNS-CKKS engine (sm_100a).
+//
+// 64-bit modular arithmetic built from 32-bit IMAD: every prime is < 2^62,
+// residues are canonical in [0, q) in memory, products are formed as 128-bit
+// values (IMAD.WIDE.U32 partial products) and reduced with
+//   * Shoup multiplication when one operand is a precomputed constant
+//     (NTT twiddles, q_l^-1, P^-1, 2^64 mod q), and
+//   * a 128-bit -> [0,q) reduction (`reduce128`) for variable x variable
+//     products, which also closes lazily accumulated multiply-add chains
+//     (key-switching inner products, plaintext-weight MACs).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace uh {
+
+typedef unsigned __int128 u128;
+
+// Per-modulus constants (device resident, one entry per RNS prime).
+struct Mod {
+    uint64_t q;      // the prime, q < 2^62
+    uint64_t bar;    // floor(2^64 / q)
+    uint64_t r64;    // 2^64 mod q
+    uint64_t r64s;   // Shoup companion of r64: floor(r64 * 2^64 / q)
+    uint64_t ninv;   // N^-1 mod q
+    uint64_t ninvs;  // Shoup companion
+    uint64_t pad0, pad1;
+};
+
+__device__ __forceinline__ uint64_t mulhi(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
+
+// Shoup: x * w mod q for any x < 2^64, given ws = floor(w * 2^64 / q); result in [0, 2q).
+__device__ __forceinline__ uint64_t shoup_lazy(uint64_t x, uint64_t w, uint64_t ws, uint64_t q) {
+    uint64_t qh = mulhi(x, ws);
+    return x * w - qh * q;
+}
+__device__ __forceinline__ uint64_t csub(uint64_t x, uint64_t q) { return x >= q ? x - q : x; }
+__device__ __forceinline__ uint64_t shoup(uint64_t x, uint64_t w, uint64_t ws, uint64_t q) {
+    return csub(shoup_lazy(x, w, ws, q), q);
+}
+// x mod q within [0, 2q) for any x < 2^64.
+__device__ __forceinline__ uint64_t barrett_lite(uint64_t x, const Mod &m) {
+    return x - mulhi(x, m.bar) * m.q;
+}
+// (hi * 2^64 + lo) mod q, canonical.
+__device__ __forceinline__ uint64_t reduce128(uint64_t hi, uint64_t lo, const Mod &m) {
+    uint64_t s = shoup_lazy(hi, m.r64, m.r64s, m.q) + barrett_lite(lo, m);  // < 4q < 2^64
+    s = s >= 2 * m.q ? s - 2 * m.q : s;
+    return csub(s, m.q);
+}
+__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, const Mod &m) {
+    return reduce128(mulhi(a, b), a * b, m);
+}
+__device__ __forceinline__ uint64_t addmod(uint64_t a, uint64_t b, uint64_t q) { return csub(a + b, q); }
+__device__ __forceinline__ uint64_t submod(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
+
+// 128-bit accumulator for lazy multiply-add chains.
+struct Acc {
+    uint64_t lo, hi;
+    __device__ __forceinline__ void zero() { lo = 0; hi = 0; }
+    __device__ __forceinline__ void mac(uint64_t a, uint64_t b) {
+        uint64_t pl = a * b, ph = mulhi(a, b);
+        lo += pl;
+        hi += ph + (lo < pl);
+    }
+    __device__ __forceinline__ void add(uint64_t a) {
+        lo += a;
+        hi += (lo < a);
+    }
+    __device__ __forceinline__ uint64_t reduce(const Mod &m) const { return reduce128(hi, lo, m); }
+};
+
+// Centred lift of x in [0, p) reduced into q: x > (p-1)/2 represents x - p.
+__device__ __forceinline__ uint64_t centred_to(uint64_t x, uint64_t p, const Mod &mq) {
+    if (x > (p - 1) / 2) {
+        uint64_t neg = p - x;  // in (0, p/2]
+        uint64_t r = neg < mq.q ? neg : csub(barrett_lite(neg, mq), mq.q);
+        return r == 0 ? 0 : mq.q - r;
+    }
+    return x < mq.q ? x : csub(barrett_lite(x, mq), mq.q);
+}
+
+// -- counter-based RNG (bit-identical to oracle/ckks_oracle.c) ---------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t rng_stream(uint64_t seed, uint64_t tag, uint64_t a, uint64_t b) {
+    return mix64(mix64(mix64(mix64(seed) ^ tag) ^ a) ^ b);
+}
+__device__ __forceinline__ uint64_t rng_draw(uint64_t stream, uint64_t i) { return mix64(stream ^ mix64(i)); }
+
+enum : uint64_t { TAG_SECRET = 1, TAG_ENC_A = 2, TAG_ENC_E = 3, TAG_KSK_A = 4, TAG_KSK_E = 5 };
+
+// limb index -> modulus index for a basis of `nq` q-limbs (moduli base..base+nq-1)
+// optionally followed by P (modulus index sp).
+__device__ __forceinline__ int limb_mod(int k, int nq, int base, int sp) { return k < nq ? base + k : sp; }
+
+}  // namespace uh

@@ -1,0 +1,129 @@
+// Context creation: per-prime constants, twiddle tables and slot-order tables,
+// computed once on the host (exact 128-bit arithmetic) and kept in HBM.
+#include "engine.cuh"
+#include "ops.cuh"
+
+namespace uh {
+
+namespace {
+typedef unsigned __int128 hu128;
+
+uint64_t h_mulmod(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)(((hu128)a * b) % q); }
+uint64_t h_pow(uint64_t b, uint64_t e, uint64_t q) {
+    uint64_t r = 1 % q;
+    b %= q;
+    while (e) {
+        if (e & 1) r = h_mulmod(r, b, q);
+        b = h_mulmod(b, b, q);
+        e >>= 1;
+    }
+    return r;
+}
+uint64_t h_inv(uint64_t a, uint64_t q) { return h_pow(a % q, q - 2, q); }
+uint64_t h_shoup(uint64_t w, uint64_t q) { return (uint64_t)(((hu128)w << 64) / q); }
+uint32_t h_brv(uint32_t x, uint32_t bits) {
+    uint32_t r = 0;
+    for (uint32_t i = 0; i < bits; i++) { r = (r << 1) | (x & 1); x >>= 1; }
+    return r;
+}
+template <class T> T *upload(const std::vector<T> &v) {
+    T *d = nullptr;
+    UH_CHECK(cudaMalloc(&d, v.size() * sizeof(T)));
+    UH_CHECK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+}
+}  // namespace
+
+Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_t count, int device) {
+    if (n < 4 || (n & (n - 1))) throw std::invalid_argument("n must be a power of two >= 4");
+    if (count < 2) throw std::invalid_argument("need at least one q prime and the special prime");
+    for (uint32_t i = 0; i < count; i++) {
+        if (moduli[i] >= (1ULL << 62) || moduli[i] % (2ULL * n) != 1)
+            throw std::invalid_argument("every modulus must be < 2^62 and congruent to 1 mod 2N");
+    }
+    UH_CHECK(cudaSetDevice(device));
+    Ctx *c = new Ctx();
+    c->device = device;
+    c->n = n;
+    c->count = count;
+    while ((1u << c->logn) < n) c->logn++;
+    if (n >= 8192) {
+        c->n1 = 1u << (c->logn / 2);
+        c->n2 = n / c->n1;
+    }
+    c->h_q.assign(moduli, moduli + count);
+
+    std::vector<Mod> mods(count);
+    std::vector<uint64_t> tw((size_t)count * n), tws((size_t)count * n), itw((size_t)count * n),
+        itws((size_t)count * n);
+    for (uint32_t m = 0; m < count; m++) {
+        uint64_t q = moduli[m];
+        if (h_pow(psi[m], n, q) != q - 1) throw std::invalid_argument("psi is not a primitive 2N-th root of unity");
+        Mod &md = mods[m];
+        md.q = q;
+        md.bar = (uint64_t)((((hu128)1) << 64) / q);
+        md.r64 = (uint64_t)((((hu128)1) << 64) % q);
+        md.r64s = h_shoup(md.r64, q);
+        md.ninv = h_inv(n, q);
+        md.ninvs = h_shoup(md.ninv, q);
+        std::vector<uint64_t> pw(n), ipw(n);
+        uint64_t ip = h_inv(psi[m], q);
+        pw[0] = 1;
+        ipw[0] = 1;
+        for (uint32_t i = 1; i < n; i++) {
+            pw[i] = h_mulmod(pw[i - 1], psi[m], q);
+            ipw[i] = h_mulmod(ipw[i - 1], ip, q);
+        }
+        for (uint32_t i = 0; i < n; i++) {
+            uint32_t e = h_brv(i, c->logn);
+            size_t at = (size_t)m * n + i;
+            tw[at] = pw[e];
+            tws[at] = h_shoup(pw[e], q);
+            itw[at] = ipw[e];
+            itws[at] = h_shoup(ipw[e], q);
+        }
+    }
+    // slot tables
+    uint32_t half = n / 2, two_n = 2 * n;
+    std::vector<int32_t> dlog(two_n, -1), pos(half), neg(half), sob(n);
+    uint64_t e = 1;
+    for (uint32_t j = 0; j < half; j++) {
+        dlog[e] = (int32_t)j;
+        dlog[two_n - e] = (int32_t)(half + j);
+        pos[j] = (int32_t)((e - 1) / 2);
+        neg[j] = (int32_t)((two_n - e - 1) / 2);
+        e = e * 5 % two_n;
+    }
+    for (uint32_t k = 0; k < n; k++) sob[k] = dlog[2 * h_brv(k, c->logn) + 1];
+    // cross-modulus inverses
+    std::vector<uint64_t> inv((size_t)count * count, 0), invs((size_t)count * count, 0);
+    for (uint32_t i = 0; i < count; i++)
+        for (uint32_t j = 0; j < count; j++) {
+            if (i == j) continue;
+            uint64_t v = h_inv(moduli[j] % moduli[i], moduli[i]);
+            inv[(size_t)i * count + j] = v;
+            invs[(size_t)i * count + j] = h_shoup(v, moduli[i]);
+        }
+    c->d_mods = upload(mods);
+    c->d_psi = upload(tw);
+    c->d_psis = upload(tws);
+    c->d_ipsi = upload(itw);
+    c->d_ipsis = upload(itws);
+    c->d_sob = upload(sob);
+    c->d_inv = upload(inv);
+    c->d_invs = upload(invs);
+    c->d_pos = upload(pos);
+    c->d_neg = upload(neg);
+    return c;
+}
+
+void ctx_destroy(Ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (void *p : {(void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis, (void *)c->d_ipsi, (void *)c->d_ipsis,
+                    (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_pos, (void *)c->d_neg})
+        if (p) cudaFree(p);
+    delete c;
+}
+
+}  // namespace uh

@@ -1,0 +1,62 @@
+// Internal host-side interface of the engine (not part of the C-ABI).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <stdexcept>
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace uh {
+
+struct Ctx {
+    int device = 0;
+    uint32_t n = 0, logn = 0, count = 0;  // count = depth + 2 moduli (q_0..q_depth, P)
+    uint32_t n1 = 0, n2 = 0;              // two-pass NTT split, n = n1 * n2 (n1 = 0: one pass)
+    std::vector<uint64_t> h_q;
+    Mod *d_mods = nullptr;               // [count]
+    uint64_t *d_psi = nullptr, *d_psis = nullptr;    // [count][n] psi^brv(i), Shoup companions
+    uint64_t *d_ipsi = nullptr, *d_ipsis = nullptr;  // [count][n] psi^-brv(i)
+    int32_t *d_sob = nullptr;            // [n] slot-order index of bit-reversed NTT output k
+    uint64_t *d_inv = nullptr, *d_invs = nullptr;  // [count][count]: q_j^-1 mod q_i at [i*count+j]
+    int32_t *d_pos = nullptr;            // [n/2] index (5^j mod 2N - 1)/2 : slot j -> odd exponent slot
+    int32_t *d_neg = nullptr;            // [n/2] index (2N - 5^j - 1)/2
+    int sp() const { return (int)count - 1; }
+};
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define UH_CHECK(x)                                                                            \
+    do {                                                                                       \
+        cudaError_t e__ = (x);                                                                 \
+        if (e__ != cudaSuccess)                                                                \
+            throw ::uh::CudaError(std::string(#x) + ": " + cudaGetErrorString(e__));           \
+    } while (0)
+#define UH_LAUNCH_CHECK() UH_CHECK(cudaGetLastError())
+
+// stream-ordered scratch buffer
+struct Scratch {
+    void *p = nullptr;
+    cudaStream_t s;
+    Scratch(size_t bytes, cudaStream_t st) : s(st) {
+        if (bytes) UH_CHECK(cudaMallocAsync(&p, bytes, s));
+    }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    template <class T> T *as() { return static_cast<T *>(p); }
+    Scratch(const Scratch &) = delete;
+    Scratch &operator=(const Scratch &) = delete;
+};
+
+// ---- ntt.cu ----
+// In-place forward (coefficients -> slot order) / inverse NTT of n_polys
+// polynomials of nl limbs each, limb k reduced modulo limb_mod(k, nq, sp).
+// Poly p, limb k lives at data + (p * pstride + k) * n; limb k < nq uses
+// modulus base + k, limbs >= nq use the special prime.
+void ntt_forward(const Ctx &c, uint64_t *data, int n_polys, int nl, int nq, int base, int pstride, cudaStream_t s);
+void ntt_inverse(const Ctx &c, uint64_t *data, int n_polys, int nl, int nq, int base, int pstride, cudaStream_t s);
+
+}  // namespace uh

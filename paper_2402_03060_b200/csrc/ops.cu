@@ -1,0 +1,303 @@
+// RNS-CKKS operations on batches of ciphertexts (sm_100a): elementwise
+// arithmetic, rescale / ModDown (divide by the top prime), ModUp, the
+// key-switching inner product with the Galois automorphism folded into its
+// reads (slot order makes X -> X^(5^r) a cyclic shift of each half), rotation,
+// ct x pt and ct x ct (+ relinearisation) followed by rescale.
+//
+// Definitions follow oracle/ckks_oracle.c exactly (centred lifts, digit
+// decomposition one digit per q_j, special prime P), so results are bit-exact
+// against the oracle on every residue.
+#include "ops.cuh"
+
+namespace uh {
+
+namespace {
+
+constexpr int kTB = 256;
+
+inline int grid_for(size_t total, int tb = kTB) {
+    size_t g = (total + tb - 1) / tb;
+    const size_t cap = 148u * 64u;  // grid-stride beyond ~64 CTAs / SM
+    return (int)(g < cap ? (g ? g : 1) : cap);
+}
+
+__device__ __forceinline__ uint32_t rot_index(uint32_t n, uint32_t half, uint32_t r) {
+    uint32_t h = n >= half ? half : 0;
+    uint32_t j = n - h + r;
+    j = j >= half ? j - half : j;
+    return h + j;
+}
+
+__global__ void k_elementwise(int op, uint64_t *out, const uint64_t *a, const uint64_t *b, int n_polys, int b_polys,
+                              int b_div, int nl, int nq, int sp, int out_ps, int a_ps, int b_ps, int logn,
+                              const Mod *__restrict__ mods) {
+    size_t total = ((size_t)n_polys * nl) << logn;
+    size_t nmask = ((size_t)1 << logn) - 1;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        size_t n = idx & nmask, t = idx >> logn;
+        int k = (int)(t % nl), p = (int)(t / nl);
+        const Mod &m = mods[limb_mod(k, nq, 0, sp)];
+        size_t oi = (((size_t)p * out_ps + k) << logn) | n;
+        uint64_t av = a[(((size_t)p * a_ps + k) << logn) | n];
+        uint64_t bv = 0;
+        if (op != OP_NEG && op != OP_COPY) bv = b[(((size_t)((p / b_div) % b_polys) * b_ps + k) << logn) | n];
+        uint64_t r;
+        switch (op) {
+            case OP_ADD: r = addmod(av, bv, m.q); break;
+            case OP_SUB: r = submod(av, bv, m.q); break;
+            case OP_MUL: r = mulmod(av, bv, m); break;
+            case OP_MAC: r = addmod(out[oi], mulmod(av, bv, m), m.q); break;
+            case OP_NEG: r = av ? m.q - av : 0; break;
+            default: r = av; break;
+        }
+        out[oi] = r;
+    }
+}
+
+// dst[p][n] = src[p][limb]  (gather one limb of every poly into a compact list)
+__global__ void k_gather_limb(uint64_t *dst, const uint64_t *src, int n_polys, int limb, int src_ps, int logn) {
+    size_t total = (size_t)n_polys << logn;
+    size_t nmask = ((size_t)1 << logn) - 1;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        size_t n = idx & nmask, p = idx >> logn;
+        dst[idx] = src[((p * src_ps + limb) << logn) | n];
+    }
+}
+
+// T[p][k][n] = centred(top[p][n], q_top) mod q_k,  k < nl
+__global__ void k_expand_centred(uint64_t *T, const uint64_t *top, int n_polys, int nl, int top_mod, int logn,
+                                 const Mod *__restrict__ mods) {
+    size_t total = ((size_t)n_polys * nl) << logn;
+    size_t nmask = ((size_t)1 << logn) - 1;
+    uint64_t qt = mods[top_mod].q;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        size_t n = idx & nmask, t = idx >> logn;
+        int k = (int)(t % nl);
+        size_t p = t / nl;
+        T[idx] = centred_to(top[(p << logn) | n], qt, mods[k]);
+    }
+}
+
+// out[p][k] = (in[p][k] - T[p][k]) * q_top^-1 mod q_k
+__global__ void k_divide_finish(uint64_t *out, const uint64_t *in, const uint64_t *T, int n_polys, int nl,
+                                int top_mod, int count, int out_ps, int in_ps, int logn, const Mod *__restrict__ mods,
+                                const uint64_t *__restrict__ inv, const uint64_t *__restrict__ invs) {
+    size_t total = ((size_t)n_polys * nl) << logn;
+    size_t nmask = ((size_t)1 << logn) - 1;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        size_t n = idx & nmask, t = idx >> logn;
+        int k = (int)(t % nl);
+        size_t p = t / nl;
+        uint64_t q = mods[k].q;
+        uint64_t w = inv[(size_t)k * count + top_mod], ws = invs[(size_t)k * count + top_mod];
+        uint64_t x = in[((p * in_ps + k) << logn) | n];
+        out[((p * out_ps + k) << logn) | n] = shoup(submod(x, T[idx], q), w, ws, q);
+    }
+}
+
+// D[p][j][k][n] = centred(C[p][j][n], q_j) mod p_k, k over (q_0..q_{L-1}, P)
+__global__ void k_modup_expand(uint64_t *D, const uint64_t *C, int n_polys, int L, int sp, int logn,
+                               const Mod *__restrict__ mods) {
+    size_t total = ((size_t)n_polys * L * (L + 1)) << logn;
+    size_t nmask = ((size_t)1 << logn) - 1;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        size_t n = idx & nmask, t = idx >> logn;
+        int k = (int)(t % (L + 1));
+        size_t pj = t / (L + 1);  // p * L + j
+        int j = (int)(pj % L);
+        uint64_t x = C[(pj << logn) | n];
+        D[idx] = (k == j) ? x : centred_to(x, mods[j].q, mods[limb_mod(k, L, 0, sp)]);
+    }
+}
+
+__global__ void k_key_inner(uint64_t *u, const uint64_t *D, const uint64_t *key, int key_limbs, int n_polys, int L,
+                            int sp, uint32_t r, int logn, const Mod *__restrict__ mods) {
+    const int LP = L + 1;
+    size_t total = ((size_t)n_polys * LP) << logn;
+    size_t nmask = ((size_t)1 << logn) - 1;
+    uint32_t half = 1u << (logn - 1);
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        size_t n = idx & nmask, t = idx >> logn;
+        int k = (int)(t % LP);
+        size_t p = t / LP;
+        const Mod &m = mods[limb_mod(k, L, 0, sp)];
+        int kk = k < L ? k : key_limbs - 1;
+        size_t src = rot_index((uint32_t)n, half, r);
+        Acc a0, a1;
+        a0.zero();
+        a1.zero();
+        for (int j = 0; j < L; j++) {
+            uint64_t d = D[((((p * L + j) * LP) + k) << logn) | src];
+            a0.mac(d, key[((((size_t)j * 2 + 0) * key_limbs + kk) << logn) | n]);
+            a1.mac(d, key[((((size_t)j * 2 + 1) * key_limbs + kk) << logn) | n]);
+        }
+        u[((((p * 2 + 0) * LP) + k) << logn) | n] = a0.reduce(m);
+        u[((((p * 2 + 1) * LP) + k) << logn) | n] = a1.reduce(m);
+    }
+}
+
+// out c0 = rot(in c0) + ks0, c1 = ks1
+__global__ void k_rot_finish(uint64_t *out, const uint64_t *in, const uint64_t *ks, int B, int L, int out_ls,
+                             int in_ls, uint32_t r, int logn, const Mod *__restrict__ mods) {
+    size_t total = ((size_t)B * 2 * L) << logn;
+    size_t nmask = ((size_t)1 << logn) - 1;
+    uint32_t half = 1u << (logn - 1);
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        size_t n = idx & nmask, t = idx >> logn;
+        int k = (int)(t % L);
+        size_t bc = t / L;  // b * 2 + comp
+        int comp = (int)(bc & 1);
+        size_t b = bc >> 1;
+        uint64_t v = ks[idx];
+        if (comp == 0) {
+            uint64_t x = in[(((b * 2) * in_ls + k) << logn) | rot_index((uint32_t)n, half, r)];
+            v = addmod(v, x, mods[k].q);
+        }
+        out[((bc * out_ls + k) << logn) | n] = v;
+    }
+}
+
+// tensor product: T[b][0] = a0 b0, T[b][1] = a0 b1 + a1 b0, D2[b] = a1 b1
+__global__ void k_tensor(uint64_t *T, uint64_t *D2, const uint64_t *a, const uint64_t *b, int B, int L, int a_ls,
+                         int b_ls, int logn, const Mod *__restrict__ mods) {
+    size_t total = ((size_t)B * L) << logn;
+    size_t nmask = ((size_t)1 << logn) - 1;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        size_t n = idx & nmask, t = idx >> logn;
+        int k = (int)(t % L);
+        size_t bb = t / L;
+        const Mod &m = mods[k];
+        uint64_t a0 = a[(((bb * 2) * a_ls + k) << logn) | n], a1 = a[(((bb * 2 + 1) * a_ls + k) << logn) | n];
+        uint64_t b0 = b[(((bb * 2) * b_ls + k) << logn) | n], b1 = b[(((bb * 2 + 1) * b_ls + k) << logn) | n];
+        Acc d1;
+        d1.zero();
+        d1.mac(a0, b1);
+        d1.mac(a1, b0);
+        T[(((bb * 2) * L + k) << logn) | n] = mulmod(a0, b0, m);
+        T[(((bb * 2 + 1) * L + k) << logn) | n] = d1.reduce(m);
+        D2[idx] = mulmod(a1, b1, m);
+    }
+}
+
+}  // namespace
+
+void elementwise(const Ctx &c, int op, uint64_t *out, const uint64_t *a, const uint64_t *b, int n_polys, int b_polys,
+                 int nl, int nq, int out_ps, int a_ps, int b_ps, cudaStream_t s) {
+    size_t total = ((size_t)n_polys * nl) << c.logn;
+    if (!total) return;
+    int b_div = 1;
+    if (b_polys < 0) {  // broadcast b over the two components of each ciphertext
+        b_polys = -b_polys;
+        b_div = 2;
+    }
+    k_elementwise<<<grid_for(total), kTB, 0, s>>>(op, out, a, b, n_polys, b_polys > 0 ? b_polys : 1, b_div, nl, nq,
+                                                 c.sp(), out_ps, a_ps, b_ps, (int)c.logn, c.d_mods);
+    UH_LAUNCH_CHECK();
+}
+
+void divide_top(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, int nl, int top_mod, int out_ps,
+                int in_ps, cudaStream_t s) {
+    if (!n_polys) return;
+    size_t N = c.n;
+    Scratch top((size_t)n_polys * N * 8, s), T((size_t)n_polys * nl * N * 8, s);
+    k_gather_limb<<<grid_for((size_t)n_polys * N), kTB, 0, s>>>(top.as<uint64_t>(), in, n_polys, nl, in_ps,
+                                                                 (int)c.logn);
+    UH_LAUNCH_CHECK();
+    bool is_sp = top_mod == c.sp();
+    ntt_inverse(c, top.as<uint64_t>(), n_polys, 1, is_sp ? 0 : 1, is_sp ? 0 : top_mod, 1, s);
+    if (nl == 0) return;
+    k_expand_centred<<<grid_for((size_t)n_polys * nl * N), kTB, 0, s>>>(T.as<uint64_t>(), top.as<uint64_t>(), n_polys,
+                                                                        nl, top_mod, (int)c.logn, c.d_mods);
+    UH_LAUNCH_CHECK();
+    ntt_forward(c, T.as<uint64_t>(), n_polys, nl, nl, 0, nl, s);
+    k_divide_finish<<<grid_for((size_t)n_polys * nl * N), kTB, 0, s>>>(out, in, T.as<uint64_t>(), n_polys, nl, top_mod,
+                                                                       (int)c.count, out_ps, in_ps, (int)c.logn,
+                                                                       c.d_mods, c.d_inv, c.d_invs);
+    UH_LAUNCH_CHECK();
+}
+
+void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level, int in_ps, cudaStream_t s) {
+    int L = level + 1;
+    size_t N = c.n;
+    Scratch C((size_t)n_polys * L * N * 8, s);
+    elementwise(c, OP_COPY, C.as<uint64_t>(), in, nullptr, n_polys, 1, L, L, L, in_ps, 0, s);
+    ntt_inverse(c, C.as<uint64_t>(), n_polys, L, L, 0, L, s);
+    size_t total = (size_t)n_polys * L * (L + 1) * N;
+    k_modup_expand<<<grid_for(total), kTB, 0, s>>>(D, C.as<uint64_t>(), n_polys, L, c.sp(), (int)c.logn, c.d_mods);
+    UH_LAUNCH_CHECK();
+    ntt_forward(c, D, n_polys * L, L + 1, L, 0, L + 1, s);
+}
+
+void key_inner(const Ctx &c, uint64_t *u, const uint64_t *D, const uint64_t *key, int key_limbs, int n_polys,
+               int level, int64_t r, cudaStream_t s) {
+    int L = level + 1;
+    int64_t half = c.n / 2;
+    uint32_t rr = (uint32_t)(((r % half) + half) % half);
+    size_t total = (size_t)n_polys * (L + 1) * c.n;
+    k_key_inner<<<grid_for(total), kTB, 0, s>>>(u, D, key, key_limbs, n_polys, L, c.sp(), rr, (int)c.logn, c.d_mods);
+    UH_LAUNCH_CHECK();
+}
+
+void keyswitch(const Ctx &c, uint64_t *out, const uint64_t *d, int n_polys, int level, int d_ps, const uint64_t *key,
+               int key_limbs, int64_t r, cudaStream_t s) {
+    int L = level + 1;
+    size_t N = c.n;
+    Scratch D((size_t)n_polys * L * (L + 1) * N * 8, s), u((size_t)n_polys * 2 * (L + 1) * N * 8, s);
+    modup(c, D.as<uint64_t>(), d, n_polys, level, d_ps, s);
+    key_inner(c, u.as<uint64_t>(), D.as<uint64_t>(), key, key_limbs, n_polys, level, r, s);
+    divide_top(c, out, u.as<uint64_t>(), n_polys * 2, L, c.sp(), L, L + 1, s);
+}
+
+void ct_rotate(const Ctx &c, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,
+               const uint64_t *key, int key_limbs, int64_t r, cudaStream_t s) {
+    int L = level + 1;
+    int64_t half = c.n / 2;
+    uint32_t rr = (uint32_t)(((r % half) + half) % half);
+    if (rr == 0) {
+        elementwise(c, OP_COPY, out, in, nullptr, 2 * B, 1, L, L, out_ls, in_ls, 0, s);
+        return;
+    }
+    size_t N = c.n;
+    Scratch ks((size_t)B * 2 * L * N * 8, s);
+    keyswitch(c, ks.as<uint64_t>(), in + (size_t)in_ls * N, B, level, 2 * in_ls, key, key_limbs, rr, s);
+    k_rot_finish<<<grid_for((size_t)B * 2 * L * N), kTB, 0, s>>>(out, in, ks.as<uint64_t>(), B, L, out_ls, in_ls, rr,
+                                                                 (int)c.logn, c.d_mods);
+    UH_LAUNCH_CHECK();
+}
+
+void ct_rescale(const Ctx &c, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,
+                cudaStream_t s) {
+    divide_top(c, out, in, 2 * B, level, level, out_ls, in_ls, s);
+}
+
+void ct_mul_relin_rescale(const Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *b, int B, int level,
+                          int out_ls, int a_ls, int b_ls, const uint64_t *rk, int rk_limbs, cudaStream_t s) {
+    int L = level + 1;
+    size_t N = c.n;
+    Scratch T((size_t)B * 2 * L * N * 8, s), D2((size_t)B * L * N * 8, s), KS((size_t)B * 2 * L * N * 8, s);
+    k_tensor<<<grid_for((size_t)B * L * N), kTB, 0, s>>>(T.as<uint64_t>(), D2.as<uint64_t>(), a, b, B, L, a_ls, b_ls,
+                                                         (int)c.logn, c.d_mods);
+    UH_LAUNCH_CHECK();
+    keyswitch(c, KS.as<uint64_t>(), D2.as<uint64_t>(), B, level, L, rk, rk_limbs, 0, s);
+    elementwise(c, OP_ADD, T.as<uint64_t>(), T.as<uint64_t>(), KS.as<uint64_t>(), 2 * B, 2 * B, L, L, L, L, L, s);
+    divide_top(c, out, T.as<uint64_t>(), 2 * B, level, level, out_ls, L, s);
+}
+
+void ct_mul_plain_rescale(const Ctx &c, uint64_t *out, const uint64_t *ct, const uint64_t *pt, int B, int level,
+                          int out_ls, int ct_ls, int pt_ls, int pt_batched, cudaStream_t s) {
+    int L = level + 1;
+    size_t N = c.n;
+    Scratch T((size_t)B * 2 * L * N * 8, s);
+    elementwise(c, OP_MUL, T.as<uint64_t>(), ct, pt, 2 * B, pt_batched ? -B : 1, L, L, L, ct_ls, pt_ls, s);
+    divide_top(c, out, T.as<uint64_t>(), 2 * B, level, level, out_ls, L, s);
+}
+
+}  // namespace uh

@@ -1,0 +1,71 @@
+// Internal host-side launchers of the RNS-CKKS operations (ops.cu, keys.cu).
+//
+// Layout conventions.  A polynomial list is `n_polys` polynomials of `nl`
+// limbs, poly p limb k at base + (p * pstride + k) * N, evaluation (slot)
+// order unless stated.  A ciphertext batch of B ciphertexts at level l with
+// `ls` stored limbs per polynomial is the list of 2B polys (c0, c1 of ct 0,
+// c0, c1 of ct 1, ...) with pstride = ls >= l + 1.  Limb k < nq is modulus k,
+// the optional extra limb is the special prime P.
+#pragma once
+#include "engine.cuh"
+
+namespace uh {
+
+Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_t count, int device);
+void ctx_destroy(Ctx *c);
+
+enum BinOp : int { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_MAC = 3, OP_NEG = 4, OP_COPY = 5 };
+
+// out[p] = op(a[p], b[p % b_polys]) over nl limbs, moduli 0..nq-1 (+P).
+void elementwise(const Ctx &c, int op, uint64_t *out, const uint64_t *a, const uint64_t *b, int n_polys,
+                 int b_polys, int nl, int nq, int out_ps, int a_ps, int b_ps, cudaStream_t s);
+
+// Divide by the top limb's modulus with centred rounding:
+// in: n_polys x (nl + 1) limbs, limb nl has modulus `top_mod`, limbs 0..nl-1
+// moduli 0..nl-1.  out: n_polys x nl limbs.  Used for rescale (top_mod = l)
+// and ModDown (top_mod = P).
+void divide_top(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, int nl, int top_mod, int out_ps,
+                int in_ps, cudaStream_t s);
+
+// ModUp of n_polys polys at level l (L = l + 1 limbs, strided in_ps) into
+// D = [n_polys][L digits][L + 1 limbs (q_0..q_l, P)][N], compact.
+void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level, int in_ps, cudaStream_t s);
+
+// u[p][comp][k] = sum_j rot_r(D[p][j][k]) * key[j][comp][kk],  comp = 0, 1,
+// k over (q_0..q_l, P); key limbs (q_0..q_{key_limbs-2}, P). u compact [n_polys][2][L+1][N].
+void key_inner(const Ctx &c, uint64_t *u, const uint64_t *D, const uint64_t *key, int key_limbs, int n_polys,
+               int level, int64_t r, cudaStream_t s);
+
+// Key switch of n_polys polys d (level l): out[p][comp] (compact [n_polys][2][L][N]).
+void keyswitch(const Ctx &c, uint64_t *out, const uint64_t *d, int n_polys, int level, int d_ps,
+               const uint64_t *key, int key_limbs, int64_t r, cudaStream_t s);
+
+// Ciphertext ops on batches (see layout above).
+void ct_rotate(const Ctx &c, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,
+               const uint64_t *key, int key_limbs, int64_t r, cudaStream_t s);
+void ct_rescale(const Ctx &c, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,
+                cudaStream_t s);
+void ct_mul_relin_rescale(const Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *b, int B, int level,
+                          int out_ls, int a_ls, int b_ls, const uint64_t *rk, int rk_limbs, cudaStream_t s);
+void ct_mul_plain_rescale(const Ctx &c, uint64_t *out, const uint64_t *ct, const uint64_t *pt, int B, int level,
+                          int out_ls, int ct_ls, int pt_ls, int pt_batched, cudaStream_t s);
+
+// Randomness, keys, encryption.
+void secret_gen(const Ctx &c, uint64_t *s_eval, uint64_t seed, cudaStream_t st);
+void switch_keygen(const Ctx &c, uint64_t *key, const uint64_t *s_eval, const uint64_t *s_from_eval,
+                   uint64_t seed, uint64_t key_id, int level, cudaStream_t st);
+void galois_keygen(const Ctx &c, uint64_t *key, const uint64_t *s_eval, uint64_t seed, int64_t r, int level,
+                   cudaStream_t st);
+void relin_keygen(const Ctx &c, uint64_t *key, const uint64_t *s_eval, uint64_t seed, int level, cudaStream_t st);
+void encrypt(const Ctx &c, uint64_t *out, const uint64_t *pt, const uint64_t *s_eval, int B, int level, int out_ls,
+             int pt_ls, uint64_t seed, uint64_t ct_id0, cudaStream_t st);
+void decrypt_coeffs(const Ctx &c, double *out, const uint64_t *ct, const uint64_t *s_eval, int B, int ct_ls,
+                    cudaStream_t st);
+
+// Encoding: signed int64 coefficients -> evaluation form over moduli 0..nl-1.
+void from_signed(const Ctx &c, uint64_t *out, const int64_t *coef, int n_polys, int nl, int out_ps, cudaStream_t s);
+// canonical embedding with cuFFT (fp64): slots [n_polys][N/2] -> rounded int64 coefficients.
+void encode_coeffs(const Ctx &c, int64_t *coef, const double *slots, int n_polys, double scale, cudaStream_t s);
+void decode_coeffs(const Ctx &c, double *slots, const double *coef, int n_polys, double scale, cudaStream_t s);
+
+}  // namespace uh

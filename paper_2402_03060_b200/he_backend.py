@@ -1,0 +1,361 @@
+"""GPU RNS-CKKS backend with the reference's operator interface.
+
+Drop-in for ``slotcnn.Backend`` (``pkg/src/slotcnn/he_backend.py:155-253``):
+same constructor argument, same ``params``/``counter`` attributes, same
+methods with the same argument meaning, level rules, op census and
+exceptions -- but a ciphertext is a real RNS-CKKS ciphertext resident in
+HBM and every operation is a kernel launch of the sm_100a engine
+(``include/unihenn_b200.h``) through ctypes.  No operation has a CPU
+fallback: if the engine library is missing the backend raises.
+
+Representation
+--------------
+* :class:`CipherVector` holds ``data``: an int64 (bit pattern = uint64)
+  CUDA tensor ``[B, 2, Ls, N]`` of evaluation-form residues, ``level``
+  (limbs ``0..level`` are live, ``Ls >= level + 1``) and the CKKS ``scale``.
+  ``B`` independent ciphertexts ride every launch (the batch dimension of
+  SURVEY.md section 7); the reference's single ciphertext is ``B = 1``.
+* :class:`PlainVector` keeps the reference's level-less float64 slot vector
+  (``he_backend.py:83-90``) and lazily caches its device encodings per
+  ``(level, scale)``.
+
+Level and scale rules (reference semantics, he_backend.py:215-253)
+------------------------------------------------------------------
+* ``mul_plain`` consumes one level: the plaintext is encoded at scale
+  ``q_level`` and the product is rescaled by ``q_level``, so the ciphertext
+  scale is unchanged.  An all-ones plaintext (``layers.drop_level``) is a
+  pure modulus drop.
+* ``mul_cipher`` consumes one level (tensor, relinearise, rescale); scale
+  becomes ``s_a * s_b / q_level``.
+* ``add`` of two ciphertexts works at the minimum level (limbs above it are
+  ignored); ``add`` of a plaintext encodes it at the ciphertext's scale.
+* ``rotate`` keeps the level; ``rotate(c, 0)`` is free (still counted).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .counter import OpCounter, diff_snapshots
+from .errors import LevelExhausted, OversizedInput, ScaleMismatch, SlotMismatch
+from .params import DEFAULT_PARAMS, HEParams, rns_chain
+
+__all__ = ["HEParams", "DEFAULT_PARAMS", "PlainVector", "CipherVector", "OpCounter", "diff_snapshots",
+           "Backend", "GpuBackend"]
+
+OP_ADD, OP_SUB, OP_MUL, OP_MAC, OP_NEG, OP_COPY = range(6)
+
+
+def _ptr(t: torch.Tensor):
+    return ctypes_vp(t.data_ptr())
+
+
+def ctypes_vp(x: int):
+    import ctypes
+
+    return ctypes.c_void_p(x)
+
+
+@dataclass(eq=False)
+class PlainVector:
+    """An encoded plaintext: one float64 value per slot ([B, slots] when batched)."""
+
+    values: np.ndarray
+    _dev: dict = field(default_factory=dict, repr=False)
+
+    def __len__(self) -> int:
+        return self.values.shape[-1]
+
+
+@dataclass(eq=False)
+class CipherVector:
+    """A batch of ``B`` RNS-CKKS ciphertexts at one level and scale."""
+
+    data: torch.Tensor
+    level: int
+    scale: float
+    backend: object = field(repr=False, default=None)
+
+    def __len__(self) -> int:
+        return self.data.shape[-1] // 2
+
+    @property
+    def batch(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def ls(self) -> int:
+        return self.data.shape[2]
+
+    @property
+    def values(self) -> np.ndarray:
+        """Decrypted slots (debug view; the reference exposes the plain values here)."""
+        return self.backend.decrypt(self)
+
+
+class GpuBackend:
+    """Executes the reference's slot operations as RNS-CKKS on one B200."""
+
+    def __init__(self, params: HEParams = DEFAULT_PARAMS, device: int | None = None):
+        if not torch.cuda.is_available():
+            raise _lib.DeviceError("GpuBackend needs a CUDA device (the engine has no CPU fallback)")
+        self.params = params
+        self.counter = OpCounter()
+        self.chain = rns_chain(params)
+        self.n = params.poly_degree
+        self.depth = params.depth
+        self.count = len(self.chain.moduli)
+        self.sp = self.count - 1
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.scale0 = float(2 ** params.scale_bits)
+        self._ctx = ctypes_vp(0)
+        import ctypes
+
+        moduli = (ctypes.c_uint64 * self.count)(*self.chain.moduli)
+        psi = (ctypes.c_uint64 * self.count)(*self.chain.psi)
+        with torch.cuda.device(self.device):
+            torch.cuda.init()
+            _lib.call("uh_ctx_create", ctypes.byref(self._ctx), self.n, ctypes.cast(moduli, ctypes.c_void_p),
+                      ctypes.cast(psi, ctypes.c_void_p), self.count, self.device.index)
+            self.secret = self._empty(self.count, self.n)
+            _lib.call("uh_secret_gen", self._ctx, _ptr(self.secret), params.seed, self._stream())
+        self._gk = {}
+        self._rk = None
+        self._ct_id = 0
+
+    def __del__(self):
+        try:
+            if self._ctx and self._ctx.value:
+                torch.cuda.synchronize(self.device)
+                _lib.call("uh_ctx_destroy", self._ctx)
+                self._ctx = ctypes_vp(0)
+        except Exception:
+            pass
+
+    # -- plumbing -----------------------------------------------------------
+    def _stream(self):
+        return ctypes_vp(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _empty(self, *shape) -> torch.Tensor:
+        return torch.empty(shape, dtype=torch.int64, device=self.device)
+
+    def modulus(self, i: int) -> int:
+        return self.chain.moduli[i]
+
+    def _call(self, name, *args):
+        _lib.call(name, self._ctx, *args)
+
+    # -- keys (lazily generated at the highest level they are first needed) ----
+    def galois_key(self, r: int, level: int) -> torch.Tensor:
+        r %= self.params.num_slots
+        key = self._gk.get(r)
+        if key is None or key.shape[0] < level + 1:
+            key = self._empty(level + 1, 2, level + 2, self.n)
+            self._call("uh_galois_keygen", _ptr(key), _ptr(self.secret), self.params.seed, r, level, self._stream())
+            self._gk[r] = key
+        return key
+
+    def relin_key(self, level: int) -> torch.Tensor:
+        if self._rk is None or self._rk.shape[0] < level + 1:
+            key = self._empty(level + 1, 2, level + 2, self.n)
+            self._call("uh_relin_keygen", _ptr(key), _ptr(self.secret), self.params.seed, level, self._stream())
+            self._rk = key
+        return self._rk
+
+    def prepare_keys(self, offsets, level: int, relin_level: int | None = None) -> None:
+        """Generate every Galois key in ``offsets`` (and the relin key) up front."""
+        for r in offsets:
+            if r % self.params.num_slots:
+                self.galois_key(r, level)
+        if relin_level is not None:
+            self.relin_key(relin_level)
+
+    # -- encoding (he_backend.py:170-200) ---------------------------------------
+    def encode(self, data) -> PlainVector:
+        """Encode a vector of at most ``num_slots`` reals, zero-filling the rest."""
+        arr = np.asarray(data, dtype=np.float64)
+        if arr.ndim == 0:
+            arr = arr.reshape(1)
+        if arr.ndim != 1:
+            raise OversizedInput(f"encode expects a 1-D vector, got shape {arr.shape}")
+        n = self.params.num_slots
+        if arr.size > n:
+            raise OversizedInput(f"vector of length {arr.size} does not fit into {n} slots")
+        out = np.zeros(n, dtype=np.float64)
+        out[: arr.size] = arr
+        return PlainVector(out)
+
+    def encode_batch(self, rows) -> PlainVector:
+        """Batched plaintext: ``rows`` is ``[B, <= num_slots]``; encrypts to a B-ciphertext batch."""
+        arr = np.asarray(rows, dtype=np.float64)
+        if arr.ndim != 2:
+            raise OversizedInput(f"encode_batch expects a 2-D array, got shape {arr.shape}")
+        n = self.params.num_slots
+        if arr.shape[1] > n:
+            raise OversizedInput(f"vector of length {arr.shape[1]} does not fit into {n} slots")
+        out = np.zeros((arr.shape[0], n), dtype=np.float64)
+        out[:, : arr.shape[1]] = arr
+        return PlainVector(out)
+
+    def _plain(self, arr: np.ndarray) -> PlainVector:
+        return PlainVector(arr)
+
+    def plain_device(self, p: PlainVector, level: int, scale: float) -> torch.Tensor:
+        """Evaluation-form encoding of ``p`` over limbs 0..level at ``scale`` ([B or 1, L, N])."""
+        key = (level, scale)
+        t = p._dev.get(key)
+        if t is None:
+            t = self.encode_device(torch.from_numpy(np.ascontiguousarray(p.values.reshape(-1, p.values.shape[-1]))),
+                                   level, scale)
+            p._dev[key] = t
+        return t
+
+    def encode_device(self, slots: torch.Tensor, level: int, scale: float) -> torch.Tensor:
+        """slots float64 [R, num_slots] (host or device) -> [R, level+1, N] evaluation form."""
+        vals = slots.to(device=self.device, dtype=torch.float64).contiguous()
+        rows = vals.shape[0]
+        peak = float(vals.abs().max()) if vals.numel() else 0.0
+        if peak * scale >= 2.0 ** 62:
+            raise OversizedInput(f"value {peak} at scale 2^{math.log2(scale):.1f} overflows the encoder")
+        coef = torch.empty((rows, self.n), dtype=torch.int64, device=self.device)
+        st = self._stream()
+        self._call("uh_encode_coeffs", _ptr(coef), _ptr(vals), rows, float(scale), st)
+        out = self._empty(rows, level + 1, self.n)
+        self._call("uh_from_signed", _ptr(out), _ptr(coef), rows, level + 1, level + 1, st)
+        return out
+
+    # -- encrypt / decrypt (he_backend.py:202-207) --------------------------------
+    def encrypt(self, plain: PlainVector) -> CipherVector:
+        """Fresh ciphertext(s) at the full level budget."""
+        lev = self.depth
+        pt = self.plain_device(plain, lev, self.scale0)
+        B = pt.shape[0]
+        out = self._empty(B, 2, lev + 1, self.n)
+        self._call("uh_encrypt", _ptr(out), _ptr(pt), _ptr(self.secret), B, lev, lev + 1, lev + 1,
+                   self.params.seed, self._ct_id, self._stream())
+        self._ct_id += B
+        plain._dev.pop((lev, self.scale0), None)  # inputs are encrypted once; do not pin them
+        return CipherVector(out, lev, self.scale0, self)
+
+    def decrypt_device(self, c: CipherVector) -> torch.Tensor:
+        """Slot values [B, num_slots] as a float64 CUDA tensor."""
+        B = c.batch
+        coef = torch.empty((B, self.n), dtype=torch.float64, device=self.device)
+        st = self._stream()
+        self._call("uh_decrypt_coeffs", _ptr(coef), _ptr(c.data), _ptr(self.secret), B, c.ls, st)
+        slots = torch.empty((B, self.params.num_slots), dtype=torch.float64, device=self.device)
+        self._call("uh_decode_coeffs", _ptr(slots), _ptr(coef), B, float(c.scale), st)
+        return slots
+
+    def decrypt(self, c: CipherVector) -> np.ndarray:
+        out = self.decrypt_device(c).cpu().numpy()
+        return out[0] if out.shape[0] == 1 else out
+
+    # -- arithmetic (he_backend.py:211-253) -----------------------------------------
+    def _check_width(self, a, b) -> None:
+        if len(a) != len(b):
+            raise SlotMismatch(f"operand widths differ: {len(a)} vs {len(b)}")
+
+    def add(self, a: CipherVector, b) -> CipherVector:
+        """Slot-wise sum; free of level cost."""
+        self._check_width(a, b)
+        st = self._stream()
+        if isinstance(b, PlainVector):
+            lev = a.level
+            self.counter.record("add", lev)
+            pt = self.plain_device(b, lev, a.scale)
+            L = lev + 1
+            out = self._empty(a.batch, 2, L, self.n)
+            # c0 += pt (broadcast or one per ciphertext), c1 copied
+            self._call("uh_elementwise", OP_ADD, _ptr(out), _ptr(a.data), _ptr(pt), a.batch, pt.shape[0],
+                       L, L, 2 * L, 2 * a.ls, L, st)
+            self._call("uh_elementwise", OP_COPY, ctypes_vp(out.data_ptr() + L * self.n * 8),
+                       ctypes_vp(a.data.data_ptr() + a.ls * self.n * 8), ctypes_vp(0), a.batch, 1, L, L, 2 * L,
+                       2 * a.ls, 0, st)
+            return CipherVector(out, lev, a.scale, self)
+        lev = min(a.level, b.level)
+        self._check_scale(a, b)
+        self._check_batch(a, b)
+        self.counter.record("add", lev)
+        L = lev + 1
+        out = self._empty(a.batch, 2, L, self.n)
+        self._call("uh_elementwise", OP_ADD, _ptr(out), _ptr(a.data), _ptr(b.data), 2 * a.batch, 2 * a.batch,
+                   L, L, L, a.ls, b.ls, st)
+        return CipherVector(out, lev, a.scale, self)
+
+    def sub(self, a: CipherVector, b: CipherVector) -> CipherVector:
+        lev = min(a.level, b.level)
+        self._check_scale(a, b)
+        self._check_batch(a, b)
+        L = lev + 1
+        out = self._empty(a.batch, 2, L, self.n)
+        self._call("uh_elementwise", OP_SUB, _ptr(out), _ptr(a.data), _ptr(b.data), 2 * a.batch, 2 * a.batch,
+                   L, L, L, a.ls, b.ls, self._stream())
+        return CipherVector(out, lev, a.scale, self)
+
+    def _check_scale(self, a: CipherVector, b: CipherVector) -> None:
+        if abs(a.scale - b.scale) > 1e-9 * max(a.scale, b.scale):
+            raise ScaleMismatch(f"cannot add ciphertexts at scales {a.scale!r} and {b.scale!r}")
+
+    def _check_batch(self, a: CipherVector, b: CipherVector) -> None:
+        if a.batch != b.batch:
+            raise SlotMismatch(f"ciphertext batches differ: {a.batch} vs {b.batch}")
+
+    def mul_plain(self, cipher: CipherVector, plain: PlainVector) -> CipherVector:
+        """Slot-wise ciphertext-plaintext product; consumes one level."""
+        if cipher.level < 1:
+            raise LevelExhausted("ciphertext has no multiplication budget left")
+        self._check_width(cipher, plain)
+        lev = cipher.level
+        self.counter.record("pt_mult", lev)
+        if plain.values.ndim == 1 and np.all(plain.values == 1.0):
+            return CipherVector(cipher.data, lev - 1, cipher.scale, self)  # modulus drop (value unchanged)
+        ql = float(self.modulus(lev))
+        pt = self.plain_device(plain, lev, ql)
+        B = cipher.batch
+        out = self._empty(B, 2, lev, self.n)
+        self._call("uh_mul_plain_rescale", _ptr(out), _ptr(cipher.data), _ptr(pt), B, lev, lev, cipher.ls,
+                   lev + 1, 1 if pt.shape[0] > 1 else 0, self._stream())
+        return CipherVector(out, lev - 1, cipher.scale, self)
+
+    def mul_cipher(self, a: CipherVector, b: CipherVector) -> CipherVector:
+        """Slot-wise ciphertext-ciphertext product; consumes one level."""
+        lev = min(a.level, b.level)
+        if lev < 1:
+            raise LevelExhausted("ciphertext has no multiplication budget left")
+        self._check_width(a, b)
+        self._check_batch(a, b)
+        self.counter.record("ct_mult", lev)
+        rk = self.relin_key(lev)
+        out = self._empty(a.batch, 2, lev, self.n)
+        self._call("uh_mul_relin_rescale", _ptr(out), _ptr(a.data), _ptr(b.data), a.batch, lev, lev, a.ls, b.ls,
+                   _ptr(rk), rk.shape[2], self._stream())
+        return CipherVector(out, lev - 1, a.scale * b.scale / float(self.modulus(lev)), self)
+
+    def rotate(self, cipher: CipherVector, r: int) -> CipherVector:
+        """Cyclic left shift by ``r`` slots (negative ``r`` shifts right)."""
+        r = r % self.params.num_slots
+        self.counter.record("rotation", cipher.level)
+        if r == 0:
+            return CipherVector(cipher.data, cipher.level, cipher.scale, self)
+        lev = cipher.level
+        key = self.galois_key(r, lev)
+        out = self._empty(cipher.batch, 2, lev + 1, self.n)
+        self._call("uh_rotate", _ptr(out), _ptr(cipher.data), cipher.batch, lev, lev + 1, cipher.ls, _ptr(key),
+                   key.shape[2], r, self._stream())
+        return CipherVector(out, lev, cipher.scale, self)
+
+    def drop_to(self, cipher: CipherVector, level: int) -> CipherVector:
+        """Modulus drop to ``level`` (no census entry; used by level alignment)."""
+        if level > cipher.level:
+            raise ValueError("cannot raise a ciphertext's level")
+        return CipherVector(cipher.data, level, cipher.scale, self)
+
+
+# The reference's name for the operator class.
+Backend = GpuBackend
