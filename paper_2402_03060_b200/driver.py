@@ -1,0 +1,213 @@
+"""Inference driver over the operator boundary.
+
+* :func:`infer` / :func:`run_inference` / :func:`verify_against_oracle` keep
+  the reference's signatures and results (``pkg/src/slotcnn/engine.py:129-265``):
+  encrypt the packed channels, align the level to the model depth, apply every
+  layer, decrypt, unpack the valid positions, one metrics row per layer from
+  the backend's op counter.  ``backend=`` is the injection point
+  (engine.py:141); the default is the GPU backend.
+* :func:`infer_batch` / :func:`run_batch` are the batch-aware driver
+  (SURVEY.md section 8(f).3): ``B`` packed ciphertext groups travel as one
+  B-batched ciphertext per channel, so every kernel launch covers the whole
+  batch.  With ``fused=True`` conv / avgpool / square run the hoisted fused
+  GPU paths (:mod:`paper_2402_03060_b200.fused`); the op census is the same.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import planner
+from .counter import diff_snapshots
+from .errors import SlotCnnError
+from .planner import FC, AvgPool2d, Conv1d, Conv2d, Square, reference_infer, trace_layout, validate
+from .schedule import CipherState, LayoutState, apply_layer, drop_level, fc_operation_counts, valid_positions
+
+
+@dataclass
+class CostModel:
+    """Abstract per-op prices (engine.py:41-62), kept for metric-row parity."""
+
+    kappa: float = 3.0
+
+    def price(self, kind: str, poly_degree: int, level: int) -> float:
+        n = float(poly_degree)
+        if kind == "rotation":
+            return n * math.log2(n) * level * level
+        if kind == "pt_mult":
+            return n * level
+        if kind == "ct_mult":
+            return self.kappa * n * level
+        if kind == "add":
+            return n
+        raise ValueError(f"unknown operation kind {kind!r}")
+
+
+@dataclass
+class LayerMetrics:
+    name: str
+    rotations: int
+    pt_mults: int
+    ct_mults: int
+    adds: int
+    level_after: int
+    est_cost: float
+    hist: dict = field(default_factory=dict, repr=False)
+    detail: dict = field(default_factory=dict, repr=False)
+
+    def to_dict(self) -> dict:
+        return {"layer": self.name, "rotations": self.rotations, "pt_mults": self.pt_mults,
+                "ct_mults": self.ct_mults, "adds": self.adds, "level_after": self.level_after,
+                "est_cost": self.est_cost}
+
+
+@dataclass
+class OpMetrics:
+    per_layer: list
+    poly_degree: int
+    depth: int
+    total_mults: int
+    input_channels: int
+
+    def totals(self) -> dict:
+        keys = ("rotations", "pt_mults", "ct_mults", "adds", "est_cost")
+        return {k: sum(getattr(r, k) for r in self.per_layer) for k in keys}
+
+    def to_dict(self) -> dict:
+        return {"per_layer": [r.to_dict() for r in self.per_layer], "totals": self.totals()}
+
+
+def _row(name, before, backend, level_after, cost, n) -> LayerMetrics:
+    tot, hist = diff_snapshots(before, backend.counter.snapshot())
+    est = sum(cnt * cost.price(kind, n, lvl) for (kind, lvl), cnt in hist.items())
+    return LayerMetrics(name, tot["rotations"], tot["pt_mults"], tot["ct_mults"], tot["adds"], level_after, est, hist)
+
+
+def _default_backend(params):
+    from .he_backend import GpuBackend
+
+    return GpuBackend(params)
+
+
+def _run_layers(m, state, backend, cost, n, fused):
+    apply = apply_layer
+    if fused:
+        from .fused import apply_layer_fused as apply
+    rows = []
+    static = trace_layout(m)
+    total = sum(r.mults for r in static)
+    if m.layers:
+        before = backend.counter.snapshot()
+        state = drop_level(backend, state, total)
+        rows.append(_row("Drop Level", before, backend, state.level, cost, n))
+    for layer, st in zip(m.layers, static):
+        before = backend.counter.snapshot()
+        state = apply(backend, state, layer)
+        row = _row(st.name, before, backend, state.level, cost, n)
+        if isinstance(layer, FC):
+            row.detail = fc_operation_counts(layer.dat_in, layer.dat_out)
+        rows.append(row)
+    return state, rows, total
+
+
+def _input_layout(m, plan) -> LayoutState:
+    return LayoutState(interval=1, w_img=m.width, h_img=m.height, w_in=m.width, h_in=m.height, channels=m.channels,
+                       pending_const=1.0, gaps_zero=True, batch_offsets=plan.offsets, footprint=plan.footprint)
+
+
+def _extract(decrypted, final: LayoutState, offsets) -> list:
+    pos = valid_positions(final)
+    outs = []
+    for off in offsets:
+        vec = np.concatenate([decrypted[ch][off + pos] for ch in range(final.channels)])
+        if final.pending_const != 1.0:
+            vec = vec * final.pending_const
+        outs.append(vec)
+    return outs
+
+
+def infer(m, packed_inputs, params, plan, n_samples=None, cost_model=None, backend=None, fused=False):
+    """One encrypted inference over a packed batch (engine.py:129-193)."""
+    report = validate(m, params)
+    if not report.ok:
+        raise SlotCnnError("model failed validation: " + "; ".join(v["message"] for v in report.violations))
+    backend = backend or _default_backend(params)
+    cost = cost_model or CostModel()
+    n = params.poly_degree
+    cts = [backend.encrypt(backend.encode(pv.values)) for pv in packed_inputs]
+    state, rows, total = _run_layers(m, CipherState(cts, _input_layout(m, plan)), backend, cost, n, fused)
+    decrypted = [backend.decrypt(ct) for ct in state.cts]
+    count = plan.capacity if n_samples is None else n_samples
+    outputs = _extract(decrypted, state.layout, plan.offsets[:count])
+    return outputs, OpMetrics(rows, n, params.depth, total, m.channels)
+
+
+def run_inference(m, samples, params, alignment: int = 1, plan=None, cost_model=None, backend=None, fused=False):
+    if plan is None:
+        plan = planner.footprint(m, params, alignment)
+    flat = [planner.flatten_input(s) for s in samples]
+    outputs, metrics = infer(m, planner.batch_pack(flat, plan), params, plan, n_samples=len(samples),
+                             cost_model=cost_model, backend=backend, fused=fused)
+    return outputs, metrics, plan
+
+
+def pack_groups(m, groups, plan) -> np.ndarray:
+    """[B groups of <= capacity samples] -> slot planes [channels, B, num_slots]."""
+    planes = np.zeros((m.channels, len(groups), plan.num_slots))
+    for b, group in enumerate(groups):
+        packed = planner.batch_pack([planner.flatten_input(s) for s in group], plan)
+        for ch, pv in enumerate(packed):
+            planes[ch, b] = pv.values
+    return planes
+
+
+def infer_batch(m, planes, params, plan, backend, counts=None, cost_model=None, fused=True):
+    """Encrypted inference of ``B`` packed ciphertext groups in one pass.
+
+    ``planes`` is ``[channels, B, num_slots]`` (host numpy, or a float64
+    tensor).  Returns ``(outputs[B][count_b], metrics)``.
+    """
+    report = validate(m, params)
+    if not report.ok:
+        raise SlotCnnError("model failed validation: " + "; ".join(v["message"] for v in report.violations))
+    cost = cost_model or CostModel()
+    cts = [backend.encrypt(backend.encode_batch(planes[ch])) for ch in range(m.channels)]
+    state, rows, total = _run_layers(m, CipherState(cts, _input_layout(m, plan)), backend, cost,
+                                     params.poly_degree, fused)
+    dec = [np.atleast_2d(backend.decrypt(ct)) for ct in state.cts]
+    B = dec[0].shape[0]
+    outputs = []
+    for b in range(B):
+        cnt = plan.capacity if counts is None else counts[b]
+        outputs.append(_extract([d[b] for d in dec], state.layout, plan.offsets[:cnt]))
+    return outputs, OpMetrics(rows, params.poly_degree, params.depth, total, m.channels)
+
+
+def verify_against_oracle(m, params, n_trials: int = 20, seed: int = 0, tol: float = 1e-3, alignment: int = 1,
+                          backend_factory=None, fused=False) -> dict:
+    """Batched encrypted inference vs the plaintext forward pass (engine.py:233-265).
+
+    ``tol`` defaults to the CKKS tolerance of the north star (1e-3 absolute)
+    instead of the simulator's 1e-9.
+    """
+    rng = np.random.default_rng(seed)
+    plan = planner.footprint(m, params, alignment)
+    max_err = err_sum = 0.0
+    agree = done = 0
+    while done < n_trials:
+        k = min(n_trials - done, plan.capacity)
+        samples = rng.uniform(0.0, 1.0, size=(k, m.channels, m.height, m.width))
+        be = backend_factory(params) if backend_factory else None
+        outputs, _, _ = run_inference(m, samples, params, plan=plan, backend=be, fused=fused)
+        for i in range(k):
+            ref = reference_infer(m, samples[i])
+            err = float(np.max(np.abs(outputs[i] - ref))) if ref.size else 0.0
+            max_err = max(max_err, err)
+            err_sum += err
+            agree += int(np.argmax(outputs[i]) == np.argmax(ref))
+        done += k
+    return {"trials": n_trials, "max_abs_err": max_err, "mean_abs_err": err_sum / n_trials if n_trials else 0.0,
+            "argmax_agreement": agree / n_trials if n_trials else 1.0, "tol": tol, "ok": max_err <= tol}

@@ -1,0 +1,63 @@
+"""End-to-end encrypted inference on the GPU backend.
+
+Decrypted logits vs the plaintext forward pass (tolerance 1e-3 absolute as
+the north star states; the achieved error is asserted far tighter), argmax
+agreement, and an op census / level trace identical to the reference
+schedule's (run here over the slot restatement, pinned to the reference by
+tests/golden/).
+"""
+
+import numpy as np
+import pytest
+
+from oracle.slot_sim import SimBackend
+from paper_2402_03060_b200 import driver, planner
+from paper_2402_03060_b200.he_backend import GpuBackend
+from paper_2402_03060_b200.params import HEParams
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3  # north star: decrypted logits within 1e-3 absolute
+M2_TRACE = [7, 6, 5, 5, 4, 3, 3, 1, 0]
+
+
+def _samples(m, k, seed):
+    return list(np.random.default_rng(seed).uniform(0.0, 1.0, size=(k, m.channels, m.height, m.width)))
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["oplevel", "fused"])
+@pytest.mark.parametrize("params", [HEParams(poly_degree=1 << 12, depth=7, scale_bits=40),
+                                    HEParams(poly_degree=1 << 15, depth=9, scale_bits=40)],
+                         ids=lambda p: f"N{p.poly_degree}")
+def test_lenet1_matches_plaintext(params, fused):
+    m = planner.lenet1(seed=0)
+    plan = planner.footprint(m, params)
+    samples = _samples(m, plan.capacity, seed=1)
+    be = GpuBackend(params)
+    outs, metrics, _ = driver.run_inference(m, samples, params, plan=plan, backend=be, fused=fused)
+    errs = []
+    for s, y in zip(samples, outs):
+        ref = planner.reference_infer(m, s)
+        errs.append(float(np.max(np.abs(y - ref))))
+        assert np.argmax(y) == np.argmax(ref)
+    assert max(errs) < TOL
+    assert max(errs) < 1e-5, f"CKKS error {max(errs):.3e} larger than expected"
+    assert [r.level_after for r in metrics.per_layer] == M2_TRACE
+    sim = SimBackend(params)
+    _, sim_metrics, _ = driver.run_inference(m, samples, params, plan=plan, backend=sim)
+    assert metrics.totals() == sim_metrics.totals()
+    assert be.counter.by_level == sim.counter.by_level
+
+
+def test_batched_equals_solo_within_tolerance():
+    params = HEParams(poly_degree=1 << 12, depth=7, scale_bits=40)
+    m = planner.lenet1(seed=2)
+    plan = planner.footprint(m, params)
+    groups = [_samples(m, plan.capacity, seed=10 + b) for b in range(3)]
+    be = GpuBackend(params)
+    planes = driver.pack_groups(m, groups, plan)
+    outs, metrics = driver.infer_batch(m, planes, params, plan, be, fused=True)
+    for b, group in enumerate(groups):
+        for s, y in zip(group, outs[b]):
+            assert np.max(np.abs(y - planner.reference_infer(m, s))) < 1e-5
+    assert [r.level_after for r in metrics.per_layer] == M2_TRACE
