@@ -40,6 +40,11 @@ typedef struct uh_ctx uh_ctx;
 
 int uh_abi_version(void);
 const char *uh_last_error(void);
+/* Number of engine kernel launches so far in this process (bench evidence). */
+unsigned long long uh_launch_count(void);
+/* Integer-pipe peaks measured on the context's device (HOST array of 3):
+ * IMAD/s, lazy 128-bit multiply-accumulate/s, reduced 64-bit mulmod/s. */
+int uh_bench_peaks(uh_ctx *ctx, double *rates);
 
 /* Parameter set -> device context.  Replaces HEParams' role as the space
  * description (he_backend.py:34-77): moduli = q_0..q_depth, P; psi[i] a
@@ -115,6 +120,28 @@ int uh_encode_coeffs(uh_ctx *ctx, int64_t *coef, const double *slots, int n_poly
 int uh_from_signed(uh_ctx *ctx, uint64_t *out, const int64_t *coef, int n_polys, int nl, int out_ps, void *stream);
 /* decrypt, second half: coefficients -> slot values [n_polys][N/2]. */
 int uh_decode_coeffs(uh_ctx *ctx, double *slots, const double *coef, int n_polys, double scale, void *stream);
+/* as uh_from_signed but into the QP basis (q_0..q_{nq-1}, P): plaintext weight masks for the hoisted layers. */
+int uh_from_signed_qp(uh_ctx *ctx, uint64_t *out, const int64_t *coef, int n_polys, int nq, int out_ps,
+                      void *stream);
+
+/* Hoisted, fused convolution (replaces the op stream of layers.conv,
+ * layers.py:165-196: K^2*ch_in rotations + ch_out*ch_in*K^2 masked products +
+ * adds).  X: [I][B][2][xls][N] input ciphertexts at `level`; D: their c1 ModUp
+ * (uh_modup over the I*B c1 polys); masks: [O][I][T][level+2][N] weight masks
+ * in the QP basis encoded at scale q_level; keys: DEVICE array of T device
+ * pointers to Galois keys (entry ignored when shifts[t] == 0) and key_limbs:
+ * DEVICE int32 [T] their limb counts (each >= level + 2); shifts: DEVICE
+ * int32 [T] in [0, N/2).  acc: [O][B][2][level+2][N], the QP-basis sum
+ * sum_{i,t} masks[o][i][t] * P * rot_t(ct_i); ModDown (uh_divide_top with P)
+ * then rescale give the layer output before the bias. */
+int uh_conv_hoisted_mac(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D,
+                        const uint64_t *masks, const uint64_t *const *keys, const int32_t *key_limbs,
+                        const int32_t *shifts, int B, int I, int T, int O, int level, void *stream);
+/* Hoisted rotation sum (layers.avgpool, layers.py:213-218): out[C][B][2][level+2][N]
+ * = sum_t P * rot_t(ct_c) in the QP basis; ModDown gives the pooled ciphertexts. */
+int uh_rot_sum_hoisted(uh_ctx *ctx, uint64_t *out, const uint64_t *X, int xls, const uint64_t *D,
+                       const uint64_t *const *keys, const int32_t *key_limbs, const int32_t *shifts, int B, int C,
+                       int T, int level, void *stream);
 
 #ifdef __cplusplus
 }

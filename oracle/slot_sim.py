@@ -6,6 +6,8 @@ per multiplication, optional fixed-point quantisation) so the schedule and
 the decrypted-output parity can be checked on the GPU box, where the
 reference package is absent.  Pinned against the reference itself by
 tests/test_schedule_vs_reference.py and the golden vectors in tests/golden/.
+Batch-aware (values may be [B, slots]) so the batched driver and the
+multi-rank sharding can be exercised on CPU.
 """
 
 from __future__ import annotations
@@ -23,7 +25,7 @@ class SimPlain:
     values: np.ndarray
 
     def __len__(self):
-        return self.values.size
+        return self.values.shape[-1]
 
 
 @dataclass(eq=False)
@@ -32,7 +34,7 @@ class SimCipher:
     level: int
 
     def __len__(self):
-        return self.values.size
+        return self.values.shape[-1]
 
 
 class SimBackend:
@@ -61,6 +63,12 @@ class SimBackend:
         out[: arr.size] = arr
         return SimPlain(self._q(out))
 
+    def encode_batch(self, rows):
+        arr = np.asarray(rows, dtype=np.float64)
+        out = np.zeros((arr.shape[0], self.params.num_slots))
+        out[:, : arr.shape[1]] = arr
+        return SimPlain(self._q(out))
+
     def _plain(self, arr):
         return SimPlain(self._q(arr))
 
@@ -71,8 +79,8 @@ class SimBackend:
         return c.values.copy()
 
     def _w(self, a, b):
-        if a.values.size != b.values.size:
-            raise SlotMismatch(f"operand widths differ: {a.values.size} vs {b.values.size}")
+        if len(a) != len(b):
+            raise SlotMismatch(f"operand widths differ: {len(a)} vs {len(b)}")
 
     def add(self, a, b):
         self._w(a, b)
@@ -98,4 +106,4 @@ class SimBackend:
     def rotate(self, c, r):
         r = r % self.params.num_slots
         self.counter.record("rotation", c.level)
-        return SimCipher(np.roll(c.values, -r), c.level)
+        return SimCipher(np.roll(c.values, -r, axis=-1), c.level)

@@ -40,8 +40,17 @@ SIGNATURES = {
     "uh_encode_coeffs": [_vp, _vp, _vp, _c_int, _c_dbl, _vp],
     "uh_from_signed": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp],
     "uh_decode_coeffs": [_vp, _vp, _vp, _c_int, _c_dbl, _vp],
+    "uh_from_signed_qp": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp],
+    "uh_conv_hoisted_mac": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int,
+                            _c_int, _vp],
+    "uh_rot_sum_hoisted": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp],
 }
-EXTRA = {"uh_abi_version": ([], _c_int), "uh_last_error": ([], ctypes.c_char_p)}
+EXTRA = {"uh_abi_version": ([], _c_int), "uh_last_error": ([], ctypes.c_char_p),
+         "uh_launch_count": ([], ctypes.c_ulonglong), "uh_bench_peaks": ([_vp, _vp], _c_int)}
+
+
+def launch_count() -> int:
+    return int(load().uh_launch_count())
 
 _LIB = None
 
@@ -65,9 +74,33 @@ def load():
     return _LIB
 
 
+PROFILE = None  # set to a list to record (name, start_event, end_event) around every call
+
+
 def call(name: str, *args) -> None:
     lib = load()
-    rc = getattr(lib, name)(*args)
+    if PROFILE is not None:
+        import torch
+
+        s = torch.cuda.current_stream()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        rc = getattr(lib, name)(*args)
+        e1.record(s)
+        PROFILE.append((name, e0, e1))
+    else:
+        rc = getattr(lib, name)(*args)
     if rc != 0:
         msg = lib.uh_last_error().decode(errors="replace")
         raise DeviceError(f"{name}: {msg}")
+
+
+def profile_summary(records) -> list:
+    """[(name, calls, total_ms)] sorted by total time (events must be complete)."""
+    agg = {}
+    for name, e0, e1 in records:
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += e0.elapsed_time(e1)
+    return sorted(((k, v[0], v[1]) for k, v in agg.items()), key=lambda x: -x[2])

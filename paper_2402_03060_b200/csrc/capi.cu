@@ -9,6 +9,10 @@ struct uh_ctx {
     uh::Ctx *c;
 };
 
+namespace uh {
+std::atomic<unsigned long long> g_launch_count{0};
+}
+
 namespace {
 thread_local std::string g_err;
 
@@ -45,6 +49,12 @@ void check_level(const uh::Ctx &c, int level) {
 extern "C" {
 
 __attribute__((visibility("default"))) int uh_abi_version(void) { return 1; }
+__attribute__((visibility("default"))) unsigned long long uh_launch_count(void) {
+    return uh::g_launch_count.load(std::memory_order_relaxed);
+}
+__attribute__((visibility("default"))) int uh_bench_peaks(uh_ctx *ctx, double *rates) {
+    return guard([&] { uh::bench_peaks(C(ctx), rates); });
+}
 __attribute__((visibility("default"))) const char *uh_last_error(void) { return g_err.c_str(); }
 
 __attribute__((visibility("default"))) int uh_ctx_create(uh_ctx **out, uint32_t n, const uint64_t *moduli,
@@ -228,7 +238,41 @@ __attribute__((visibility("default"))) int uh_from_signed(uh_ctx *ctx, uint64_t 
     return guard([&] {
         const uh::Ctx &c = C(ctx);
         need(nl >= 1 && nl <= (int)c.count - 1, "bad limb count");
-        uh::from_signed(c, out, coef, n_polys, nl, out_ps, S(stream));
+        uh::from_signed(c, out, coef, n_polys, nl, 0, out_ps, S(stream));
+    });
+}
+
+__attribute__((visibility("default"))) int uh_from_signed_qp(uh_ctx *ctx, uint64_t *out, const int64_t *coef,
+                                                             int n_polys, int nq, int out_ps, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        need(nq >= 1 && nq <= (int)c.count - 1, "bad limb count");
+        uh::from_signed(c, out, coef, n_polys, nq, 1, out_ps, S(stream));
+    });
+}
+
+__attribute__((visibility("default"))) int uh_conv_hoisted_mac(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls,
+                                                               const uint64_t *D, const uint64_t *masks,
+                                                               const uint64_t *const *keys, const int32_t *key_limbs,
+                                                               const int32_t *shifts, int B, int I, int T, int O,
+                                                               int level, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(B > 0 && I > 0 && T > 0 && O > 0 && xls >= level + 1, "bad shape");
+        uh::conv_hoisted_mac(c, acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, level, S(stream));
+    });
+}
+
+__attribute__((visibility("default"))) int uh_rot_sum_hoisted(uh_ctx *ctx, uint64_t *out, const uint64_t *X, int xls,
+                                                              const uint64_t *D, const uint64_t *const *keys,
+                                                              const int32_t *key_limbs, const int32_t *shifts, int B,
+                                                              int C_, int T, int level, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(B > 0 && C_ > 0 && T > 0 && xls >= level + 1, "bad shape");
+        uh::rot_sum_hoisted(c, out, X, xls, D, keys, key_limbs, shifts, B, C_, T, level, S(stream));
     });
 }
 

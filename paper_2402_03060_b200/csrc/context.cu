@@ -42,6 +42,13 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
             throw std::invalid_argument("every modulus must be < 2^62 and congruent to 1 mod 2N");
     }
     UH_CHECK(cudaSetDevice(device));
+    // Scratch comes from the device's default stream-ordered pool; keep freed
+    // blocks cached across synchronisations instead of returning them to the
+    // driver (the default threshold 0 would re-map pages every step).
+    cudaMemPool_t pool;
+    UH_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = ~0ull;
+    UH_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     Ctx *c = new Ctx();
     c->device = device;
     c->n = n;

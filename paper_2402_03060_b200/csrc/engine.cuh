@@ -1,5 +1,6 @@
 // Internal host-side interface of the engine (not part of the C-ABI).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -34,7 +35,14 @@ struct CudaError : std::runtime_error {
         if (e__ != cudaSuccess)                                                                \
             throw ::uh::CudaError(std::string(#x) + ": " + cudaGetErrorString(e__));           \
     } while (0)
-#define UH_LAUNCH_CHECK() UH_CHECK(cudaGetLastError())
+// every kernel launch of the engine is followed by UH_LAUNCH_CHECK, which also
+// counts it (uh_launch_count(): the bench's gpu_launches evidence)
+extern std::atomic<unsigned long long> g_launch_count;
+#define UH_LAUNCH_CHECK()                                          \
+    do {                                                           \
+        ::uh::g_launch_count.fetch_add(1, std::memory_order_relaxed); \
+        UH_CHECK(cudaGetLastError());                              \
+    } while (0)
 
 // stream-ordered scratch buffer
 struct Scratch {

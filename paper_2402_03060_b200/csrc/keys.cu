@@ -173,8 +173,8 @@ __global__ void k_centred_double(double *out, const uint64_t *M, size_t total, c
     }
 }
 
-__global__ void k_from_signed(uint64_t *out, const int64_t *coef, int n_polys, int nl, int out_ps, int logn,
-                              const Mod *__restrict__ mods) {
+__global__ void k_from_signed(uint64_t *out, const int64_t *coef, int n_polys, int nl, int nq, int sp, int out_ps,
+                              int logn, const Mod *__restrict__ mods) {
     size_t total = ((size_t)n_polys * nl) << logn;
     size_t nmask = ((size_t)1 << logn) - 1;
     for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -182,7 +182,7 @@ __global__ void k_from_signed(uint64_t *out, const int64_t *coef, int n_polys, i
         size_t n = idx & nmask, t = idx >> logn;
         int k = (int)(t % nl);
         size_t p = t / nl;
-        out[((p * out_ps + k) << logn) | n] = signed_to(coef[(p << logn) | n], mods[k]);
+        out[((p * out_ps + k) << logn) | n] = signed_to(coef[(p << logn) | n], mods[limb_mod(k, nq, 0, sp)]);
     }
 }
 
@@ -328,11 +328,13 @@ void decrypt_coeffs(const Ctx &c, double *out, const uint64_t *ct, const uint64_
     UH_LAUNCH_CHECK();
 }
 
-void from_signed(const Ctx &c, uint64_t *out, const int64_t *coef, int n_polys, int nl, int out_ps, cudaStream_t s) {
-    k_from_signed<<<grid_for((size_t)n_polys * nl * c.n), kTB, 0, s>>>(out, coef, n_polys, nl, out_ps, (int)c.logn,
-                                                                      c.d_mods);
+void from_signed(const Ctx &c, uint64_t *out, const int64_t *coef, int n_polys, int nq, int special, int out_ps,
+                 cudaStream_t s) {
+    int nl = nq + (special ? 1 : 0);
+    k_from_signed<<<grid_for((size_t)n_polys * nl * c.n), kTB, 0, s>>>(out, coef, n_polys, nl, nq, c.sp(), out_ps,
+                                                                      (int)c.logn, c.d_mods);
     UH_LAUNCH_CHECK();
-    ntt_forward(c, out, n_polys, nl, nl, 0, out_ps, s);
+    ntt_forward(c, out, n_polys, nl, nq, 0, out_ps, s);
 }
 
 void encode_coeffs(const Ctx &c, int64_t *coef, const double *slots, int n_polys, double scale, cudaStream_t s) {

@@ -1,0 +1,104 @@
+// Integer-pipe peak microbenchmarks (the modmul roofline denominator).
+//
+// The engine's work is 64-bit modular multiply-accumulate built from 32-bit
+// IMAD; there is no vendor-published "IMAD peak" for B200, so the bench
+// measures it on the box: (1) raw 32-bit IMAD issue rate, (2) the rate of the
+// engine's lazy 128-bit multiply-accumulate (Acc::mac) and (3) of a fully
+// reduced 64-bit modular product (mulmod), all register-resident with 8
+// independent chains per thread and a grid of 148 x 8 CTAs.
+#include "ops.cuh"
+
+namespace uh {
+namespace {
+
+__global__ void k_imad_peak(uint32_t *out, int iters, uint32_t seed) {
+    uint32_t a[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) a[i] = seed + threadIdx.x * 8 + i;
+    const uint32_t m = 0x9E3779B1u + blockIdx.x;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) a[i] = a[i] * m + 0x7F4A7C15u;
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s ^= a[i];
+    if (s == 0x12345678u) out[0] = s;
+}
+
+__global__ void k_mac_peak(uint64_t *out, int iters, uint64_t seed) {
+    Acc acc[8];
+    uint64_t x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        acc[i].zero();
+        x[i] = (seed + threadIdx.x * 8 + i) & ((1ull << 60) - 1);
+    }
+    const uint64_t w = (0x0FEDCBA987654321ull + blockIdx.x) & ((1ull << 60) - 1);
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            acc[i].mac(x[i], w);
+            x[i] ^= acc[i].lo;  // keep operands live and varying (XOR: ALU pipe)
+        }
+    }
+    uint64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s ^= acc[i].lo ^ acc[i].hi;
+    if (s == 0x1234567812345678ull) out[0] = s;
+}
+
+__global__ void k_mulmod_peak(uint64_t *out, int iters, uint64_t seed, Mod m) {
+    uint64_t x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = (seed + threadIdx.x * 8 + i) % m.q;
+    const uint64_t w = (0x0FEDCBA987654321ull + blockIdx.x) % m.q;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) x[i] = mulmod(x[i], w, m);
+    }
+    uint64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s ^= x[i];
+    if (s == 0x1234567812345678ull) out[0] = s;
+}
+
+template <class F> double time_ms(F &&launch) {
+    cudaEvent_t a, b;
+    UH_CHECK(cudaEventCreate(&a));
+    UH_CHECK(cudaEventCreate(&b));
+    launch();  // warm-up
+    UH_CHECK(cudaEventRecord(a));
+    launch();
+    UH_CHECK(cudaEventRecord(b));
+    UH_CHECK(cudaEventSynchronize(b));
+    float ms = 0;
+    UH_CHECK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms;
+}
+
+}  // namespace
+
+// rates[0] = IMAD/s, rates[1] = 128-bit MAC/s, rates[2] = reduced mulmod/s (60-bit prime)
+void bench_peaks(const Ctx &c, double *rates) {
+    int sms = 0;
+    UH_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    const double lanes = (double)blocks * threads;
+    uint64_t *out = nullptr;
+    UH_CHECK(cudaMalloc(&out, 64));
+    Mod m;
+    UH_CHECK(cudaMemcpy(&m, c.d_mods, sizeof(Mod), cudaMemcpyDeviceToHost));
+    double ms = time_ms([&] { k_imad_peak<<<blocks, threads>>>((uint32_t *)out, iters, 7u); });
+    rates[0] = lanes * iters * 8 / (ms * 1e-3);
+    ms = time_ms([&] { k_mac_peak<<<blocks, threads>>>(out, iters, 7ull); });
+    rates[1] = lanes * iters * 8 / (ms * 1e-3);
+    ms = time_ms([&] { k_mulmod_peak<<<blocks, threads>>>(out, iters / 2, 7ull, m); });
+    rates[2] = lanes * (iters / 2) * 8 / (ms * 1e-3);
+    UH_CHECK(cudaGetLastError());
+    cudaFree(out);
+}
+
+}  // namespace uh

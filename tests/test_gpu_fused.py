@@ -1,0 +1,47 @@
+"""Fused / hoisted GPU layers vs the op-level schedule, layer by layer.
+
+Both paths run on the GPU backend from the same input state; decrypted
+outputs must agree to CKKS rounding (one ModDown + rescale per output instead
+of one per product) and the op census of each layer must be identical.
+"""
+
+import numpy as np
+import pytest
+
+from paper_2402_03060_b200 import driver, fused, planner, schedule
+from paper_2402_03060_b200.he_backend import GpuBackend
+from paper_2402_03060_b200.params import HEParams
+from paper_2402_03060_b200.schedule import CipherState
+
+pytestmark = pytest.mark.gpu
+
+
+def _dec(be, state):
+    return np.stack([np.atleast_2d(be.decrypt(c)) for c in state.cts])
+
+
+@pytest.mark.parametrize("batch", [1, 3])
+def test_layers_fused_equal_oplevel(batch):
+    params = HEParams(poly_degree=1 << 12, depth=7, scale_bits=40)
+    m = planner.lenet1(seed=5)
+    plan = planner.footprint(m, params)
+    be = GpuBackend(params)
+    rng = np.random.default_rng(8)
+    groups = [list(rng.uniform(0, 1, size=(plan.capacity, 1, 28, 28))) for _ in range(batch)]
+    planes = driver.pack_groups(m, groups, plan)
+    ct = be.encrypt(be.encode_batch(planes[0]))
+    state = schedule.drop_level(be, CipherState([ct], driver._input_layout(m, plan)), 7)
+    for layer in m.layers[:6]:  # conv, square, pool, conv, square, pool
+        c0 = be.counter.snapshot()
+        ref = schedule.apply_layer(be, state, layer)
+        c1 = be.counter.snapshot()
+        got = fused.apply_layer_fused(be, state, layer)
+        c2 = be.counter.snapshot()
+        from paper_2402_03060_b200.counter import diff_snapshots
+
+        assert diff_snapshots(c0, c1) == diff_snapshots(c1, c2), type(layer).__name__
+        assert got.layout == ref.layout and got.level == ref.level
+        a, b = _dec(be, ref), _dec(be, got)
+        scale = max(1.0, float(np.max(np.abs(a))))
+        assert np.max(np.abs(a - b)) / scale < 1e-7, type(layer).__name__
+        state = ref
