@@ -276,6 +276,20 @@ __attribute__((visibility("default"))) int uh_rot_sum_hoisted(uh_ctx *ctx, uint6
     });
 }
 
+__attribute__((visibility("default"))) int uh_hoisted_mac(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls,
+                                                          const uint64_t *D, const uint64_t *masks,
+                                                          const uint64_t *const *keys, const int32_t *key_limbs,
+                                                          const int32_t *shifts, int B, int I, int T, int O, int diag,
+                                                          int level, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(B > 0 && I > 0 && T > 0 && O > 0 && xls >= level + 1, "bad shape");
+        need(!diag || I == T, "diagonal terms need I == T");
+        uh::hoisted_mac(c, acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, diag, level, S(stream));
+    });
+}
+
 __attribute__((visibility("default"))) int uh_decode_coeffs(uh_ctx *ctx, double *slots, const double *coef,
                                                             int n_polys, double scale, void *stream) {
     return guard([&] { uh::decode_coeffs(C(ctx), slots, coef, n_polys, scale, S(stream)); });

@@ -1,0 +1,197 @@
+// Generic hoisted rotation-MAC kernel (sm_100a): the one kernel behind every
+// fused layer path.
+//
+//   acc[o][b] (QP basis) = sum over terms q of  M[o][q] (.) P * rot_{s_t}(ct_{i}[b])
+//
+// terms: dense  q = (i, t) for i < I, t < T      (conv: I x T taps, O outputs)
+//        diag   q = i = t for i < I (= T)          (sum of differently shifted inputs)
+// M: weight masks in the QP basis ([O][Q][L+1][N]), or none (M = 1).
+// P * rot_s(ct) is never materialised: for each term the rotated, key-switched
+// ciphertext in the QP basis is formed on the fly from the hoisted ModUp
+// digits D of the input (a shifted read -- slot order turns X -> X^(5^s) into
+// a cyclic shift of each half) and the Galois key of tap t:
+//   v0 = P*c0[rot n] + sum_j D_j[rot n] * K_t[j][0],   v1 = sum_j D_j[rot n] * K_t[j][1]
+// (shift 0: v = P * ct).  v is staged in shared memory for a tile of TB
+// ciphertexts x 32 coefficients and immediately multiply-accumulated into
+// every output's 128-bit accumulators, so each mask value read from HBM/L2
+// serves 2*TB products and each key value TB ciphertexts.
+//
+// CTA: W warps; lane <-> coefficient n (coalesced 256-byte rows of every
+// operand); grid = (B/TB tiles fastest, N/32 coefficient tiles, L+1 limbs),
+// so CTAs sharing the same masks/keys run back to back and hit L2.
+#include "ops.cuh"
+
+namespace uh {
+namespace {
+
+constexpr int kTBatch = 8;   // ciphertexts per CTA tile
+constexpr int kTChunk = 4;   // terms staged per shared-memory chunk
+constexpr int kFold = 56;    // terms between folds of the 128-bit accumulators
+
+__device__ __forceinline__ uint32_t rot_index(uint32_t n, uint32_t half, uint32_t r) {
+    uint32_t h = n >= half ? half : 0;
+    uint32_t j = n - h + r;
+    j = j >= half ? j - half : j;
+    return h + j;
+}
+
+// lazily reduced (hi*2^64 + lo) mod q in [0, 4q)
+__device__ __forceinline__ uint64_t reduce128_lazy(uint64_t hi, uint64_t lo, const Mod &m) {
+    return shoup_lazy(hi, m.r64, m.r64s, m.q) + barrett_lite(lo, m);
+}
+
+template <int PPW>
+__global__ void __launch_bounds__(384) k_hoisted_mac(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X,
+                                                    int xls, const uint64_t *__restrict__ D,
+                                                    const uint64_t *__restrict__ masks,
+                                                    const uint64_t *const *__restrict__ keys,
+                                                    const int32_t *__restrict__ key_limbs,
+                                                    const int32_t *__restrict__ shifts, int B, int I, int T, int O,
+                                                    int diag, int L, int sp, int logn, const Mod *__restrict__ mods) {
+    __shared__ uint64_t sv[2][kTChunk][kTBatch][2][32];
+    const int LP = L + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b0 = blockIdx.x * kTBatch;
+    const uint32_t n = blockIdx.y * 32 + lane;
+    const int k = blockIdx.z;
+    const size_t N = (size_t)1 << logn;
+    const uint32_t half = (uint32_t)(N >> 1);
+    const Mod m = mods[limb_mod(k, L, 0, sp)];
+    const bool qlimb = k < L;
+    const uint64_t P = mods[sp].q;
+    const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
+    const int Q = diag ? I : I * T;
+    const int npairs = O * kTBatch;
+
+    Acc acc[PPW][2];
+#pragma unroll
+    for (int j = 0; j < PPW; j++) {
+        acc[j][0].zero();
+        acc[j][1].zero();
+    }
+    int since_fold = 0;
+    int buf = 0;
+    for (int q0 = 0; q0 < Q; q0 += kTChunk) {
+        // ---- phase A: rotated, key-switched inputs of this chunk into shared memory ----
+        for (int it = threadIdx.x; it < kTChunk * kTBatch * 32; it += blockDim.x) {
+            const int ln = it & 31, rest = it >> 5;
+            const int bt = rest % kTBatch, qc = rest / kTBatch;
+            const int q = q0 + qc, b = b0 + bt;
+            uint64_t v0 = 0, v1 = 0;
+            if (q < Q && b < B) {
+                const int i = diag ? q : q / T, t = diag ? q : q % T;
+                const uint32_t nn = blockIdx.y * 32 + ln;
+                const uint64_t *c0 = X + (((size_t)(i * B + b) * 2 * xls) << logn);
+                const uint32_t r = (uint32_t)shifts[t];
+                if (r == 0) {
+                    if (qlimb) {
+                        v0 = mulmod(Pk, c0[((size_t)k << logn) | nn], m);
+                        v1 = mulmod(Pk, c0[((size_t)(xls + k) << logn) | nn], m);
+                    }
+                } else {
+                    const size_t src = rot_index(nn, half, r);
+                    const uint64_t *Di = D + (((size_t)(i * B + b) * L * LP + k) << logn);
+                    const uint64_t *key = keys[t];
+                    const int kl = key_limbs[t], kk = qlimb ? k : kl - 1;
+                    const uint64_t *k0 = key + (((size_t)kk) << logn) + nn;
+                    const size_t kstride = (size_t)kl << logn;  // comp stride; digit stride = 2 * kstride
+                    Acc a0, a1;
+                    a0.zero();
+                    a1.zero();
+                    for (int j = 0; j < L; j++) {
+                        const uint64_t d = Di[(((size_t)j * LP) << logn) + src];
+                        a0.mac(d, k0[(2 * j) * kstride]);
+                        a1.mac(d, k0[(2 * j + 1) * kstride]);
+                    }
+                    if (qlimb) a0.mac(Pk, c0[((size_t)k << logn) | src]);
+                    v0 = csub(reduce128_lazy(a0.hi, a0.lo, m), 2 * m.q);
+                    v1 = csub(reduce128_lazy(a1.hi, a1.lo, m), 2 * m.q);
+                }
+            }
+            sv[buf][qc][bt][0][ln] = v0;
+            sv[buf][qc][bt][1][ln] = v1;
+        }
+        __syncthreads();
+        // ---- phase B: multiply-accumulate into every (output, ciphertext) pair ----
+        const int qn = min(kTChunk, Q - q0);
+        for (int qc = 0; qc < qn; qc++) {
+            const int q = q0 + qc;
+#pragma unroll
+            for (int j = 0; j < PPW; j++) {
+                const int p = warp * PPW + j;  // a warp's pairs share one output -> one mask load per term
+                if (p < npairs) {
+                    const int o = p / kTBatch, bt = p % kTBatch;
+                    const uint64_t v0 = sv[buf][qc][bt][0][lane], v1 = sv[buf][qc][bt][1][lane];
+                    if (masks) {
+                        const uint64_t mv = masks[((((size_t)o * Q + q) * LP + k) << logn) + n];
+                        acc[j][0].mac(mv, v0);
+                        acc[j][1].mac(mv, v1);
+                    } else {
+                        acc[j][0].add(v0);
+                        acc[j][1].add(v1);
+                    }
+                }
+            }
+            if (++since_fold == kFold) {
+                since_fold = 0;
+#pragma unroll
+                for (int j = 0; j < PPW; j++)
+                    for (int cc = 0; cc < 2; cc++) {
+                        uint64_t rr = reduce128_lazy(acc[j][cc].hi, acc[j][cc].lo, m);
+                        acc[j][cc].lo = rr;
+                        acc[j][cc].hi = 0;
+                    }
+            }
+        }
+        buf ^= 1;  // the other buffer is free: every thread passed the barrier after using it
+    }
+#pragma unroll
+    for (int j = 0; j < PPW; j++) {
+        const int p = warp * PPW + j;  // a warp's pairs share one output -> one mask load per term
+        if (p < npairs) {
+            const int o = p / kTBatch, b = b0 + p % kTBatch;
+            if (b < B) {
+                uint64_t *dst = acc_out + (((((size_t)o * B + b) * 2) * LP + k) << logn) + n;
+                dst[0] = acc[j][0].reduce(m);
+                dst[(size_t)LP << logn] = acc[j][1].reduce(m);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D, const uint64_t *masks,
+                 const uint64_t *const *keys, const int32_t *key_limbs, const int32_t *shifts, int B, int I, int T,
+                 int O, int diag, int level, cudaStream_t s) {
+    const int L = level + 1;
+    const int pairs = O * kTBatch;
+    // warps x pairs-per-warp covering O * TB (output, ciphertext) pairs
+    const int W = pairs >= 96 ? 12 : 8;
+    const int ppw = (pairs + W - 1) / W;
+    dim3 grid((B + kTBatch - 1) / kTBatch, (unsigned)(c.n / 32), L + 1);
+    if (c.n < 32) throw std::invalid_argument("hoisted kernels need N >= 32");
+    auto go = [&](auto tag) {
+        constexpr int PP = decltype(tag)::value;
+        k_hoisted_mac<PP><<<grid, W * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, diag,
+                                                  L, c.sp(), (int)c.logn, c.d_mods);
+    };
+    if (ppw <= 1) go(std::integral_constant<int, 1>());
+    else if (ppw <= 2) go(std::integral_constant<int, 2>());
+    else if (ppw <= 4) go(std::integral_constant<int, 4>());
+    else if (ppw <= 8) go(std::integral_constant<int, 8>());
+    else if (ppw <= 12) go(std::integral_constant<int, 12>());
+    else {
+        // very wide layers: split the outputs
+        for (int o0 = 0; o0 < O; o0 += 12) {
+            int oc = std::min(12, O - o0);
+            hoisted_mac(c, acc + (size_t)o0 * B * 2 * (L + 1) * c.n, X, xls, D,
+                        masks ? masks + (size_t)o0 * (diag ? I : I * T) * (L + 1) * c.n : nullptr, keys, key_limbs,
+                        shifts, B, I, T, oc, diag, level, s);
+        }
+        return;
+    }
+    UH_LAUNCH_CHECK();
+}
+
+}  // namespace uh

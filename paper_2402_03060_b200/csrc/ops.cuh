@@ -72,6 +72,11 @@ void from_signed(const Ctx &c, uint64_t *out, const int64_t *coef, int n_polys, 
 void conv_hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D,
                       const uint64_t *masks, const uint64_t *const *keys, const int32_t *key_limbs, const int32_t *shifts, int B,
                       int I, int T, int O, int level, cudaStream_t s);
+// hoist.cu -- generic hoisted rotation-MAC: acc[O][B][2][L+1][N] (QP) = sum over terms q of
+// masks[o][q] * P * rot_{shifts[t]}(ct_i); terms dense (i, t) or diag (i == t); masks may be null (= 1).
+void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D, const uint64_t *masks,
+                 const uint64_t *const *keys, const int32_t *key_limbs, const int32_t *shifts, int B, int I, int T,
+                 int O, int diag, int level, cudaStream_t s);
 // microbench.cu: rates[0] = IMAD/s, rates[1] = 128-bit MAC/s, rates[2] = reduced mulmod/s
 void bench_peaks(const Ctx &c, double *rates);
 // pool: out[C][B][2][L+1][N] (QP basis) = sum_t P * rot_t(ct_c)

@@ -243,11 +243,216 @@ def square(backend, state: CipherState) -> CipherState:
                        replace(lay, pending_const=lay.pending_const * lay.pending_const))
 
 
+# -- flatten and FC through the generic hoisted kernel -----------------------------------
+#
+# A masked rotation rot_s(m .* x) equals rot_s(m) .* rot_s(x) (the automorphism
+# is a ring homomorphism), so every "multiply by a mask, then rotate" stage of
+# flatten (layers.py:281-339) becomes "rotate the SAME input by every shift
+# (hoisted) and multiply by pre-rotated masks", i.e. the conv kernel with one
+# input per channel.  Channel packing, the FC wrap fix and the FC folds are
+# mask-free sums of rotations (one ModDown each).  Rotations are executed one
+# level above where the reference records them; the census records the
+# reference's levels.
+
+
+def _hoist(backend, X, level, shifts, masks, O, diag, B):
+    """acc [O][B][2][level+2][N] of uh_hoisted_mac over stacked inputs X [I][B][2][level+1][N]."""
+    L, LP, n = level + 1, level + 2, backend.n
+    I = X.shape[0]
+    st = backend._stream()
+    D = backend._empty(I, B, L, LP, n)
+    backend._call("uh_modup", _vp(D), _vp(X.data_ptr() + L * n * 8), I * B, level, 2 * L, st)
+    sh, ptrs, keys, limbs = _rotation_plan(backend, shifts, level)
+    acc = backend._empty(O, B, 2, LP, n)
+    backend._call("uh_hoisted_mac", _vp(acc), _vp(X), L, _vp(D), _vp(masks) if masks is not None else _vp(0),
+                  _vp(ptrs), _vp(limbs), _vp(sh), B, I, len(shifts), O, 1 if diag else 0, level, st)
+    del keys, D
+    return acc
+
+
+def _finish(backend, acc, level, rescale: bool):
+    """ModDown (and optionally rescale) of acc [O][B][2][L+1][N] -> [O][B][2][L or L-1][N]."""
+    O, B = acc.shape[0], acc.shape[1]
+    L, LP, n = level + 1, level + 2, backend.n
+    st = backend._stream()
+    md = backend._empty(O, B, 2, L, n)
+    backend._call("uh_divide_top", _vp(md), _vp(acc), O * B * 2, L, backend.sp, L, LP, st)
+    if not rescale:
+        return md
+    out = backend._empty(O, B, 2, level, n)
+    backend._call("uh_rescale", _vp(out), _vp(md), O * B, level, level, L, st)
+    return out
+
+
+def _rows_bank(backend, key, rows_np, level, scale):
+    """Cached QP-basis encoding [R, level+2, N] of host slot rows."""
+    return _bank(backend, key, lambda: encode_rows_qp(
+        backend, torch.from_numpy(np.ascontiguousarray(rows_np)).to(backend.device), level, scale))
+
+
+def _masked_rotation_stage(backend, X, level, B, plan, tag):
+    """sum_c rot_{s_c}(m_c .* x) for every channel of X ([C][B]...), one level consumed."""
+    masks_np = np.stack([np.roll(m, -s) for m, s in plan])  # pre-rotated masks
+    bank = _rows_bank(backend, tag + (level,), masks_np, level, float(backend.modulus(level)))
+    C = X.shape[0]
+    Xb = X.reshape(1, C * B, 2, level + 1, backend.n)
+    acc = _hoist(backend, Xb, level, [s for _, s in plan], bank.view(1, len(plan), level + 2, backend.n), 1, False,
+                 C * B)
+    out = _finish(backend, acc, level, rescale=True)  # [1][C*B][2][level][N]
+    return out.view(C, B, 2, level, backend.n)
+
+
+def flatten(backend, state: CipherState) -> CipherState:
+    if not _is_gpu(backend):
+        return schedule.flatten(backend, state)
+    from dataclasses import replace
+
+    from .errors import LevelExhausted
+    from .he_backend import CipherVector
+    from .planner import flatten_dispatch
+
+    lay = state.layout
+    ns, n = backend.params.num_slots, backend.n
+    iv, w_in, h_in = lay.interval, lay.w_in, lay.h_in
+    span = lay.w_img * iv
+    masked, row_rm, col_rm = flatten_dispatch(lay.gaps_zero, lay.pending_const == 1.0, iv, w_in, h_in)
+    level = min(c.level for c in state.cts)
+    C, B = len(state.cts), state.cts[0].batch
+    scale = state.cts[0].scale
+    cnt = backend.counter
+    need = int(masked or row_rm) + int(col_rm)
+    if level < need:
+        raise LevelExhausted("ciphertext has no multiplication budget left")
+    X = stack_cts(backend, state.cts, level)
+
+    def masked_census(plan, lev):
+        cnt.record("pt_mult", lev, C * len(plan))
+        nz = sum(1 for _, s in plan if s)
+        cnt.record("rotation", lev - 1, C * nz)
+        cnt.record("add", lev - 1, C * (len(plan) - 1))
+
+    if masked:
+        plan = []
+        for c in range(w_in):
+            region = np.zeros(lay.footprint)
+            region[np.arange(h_in) * span + c * iv] = lay.pending_const
+            plan.append((schedule.tile_region(ns, lay, region), c * (iv - 1)))
+        masked_census(plan, level)
+        X = _masked_rotation_stage(backend, X, level, B, plan, ("flat_m", lay))
+        level -= 1
+    elif row_rm:
+        shifts = [0] + [s * (iv - 1) for s in range(1, iv)]
+        cnt.record("rotation", level, C * (iv - 1))
+        cnt.record("add", level, C * (iv - 1))
+        Xb = X.reshape(1, C * B, 2, level + 1, n)
+        acc = _hoist(backend, Xb, level, shifts, None, 1, False, C * B)
+        X = _finish(backend, acc, level, rescale=False).view(C, B, 2, level + 1, n)
+        plan = []
+        for b in range(math_ceil(w_in / iv)):
+            region = np.zeros(lay.footprint)
+            base = b * iv * iv
+            for r in range(h_in):
+                region[r * span + base:r * span + base + iv] = 1.0
+            plan.append((schedule.tile_region(ns, lay, region), b * iv * (iv - 1)))
+        masked_census(plan, level)
+        X = _masked_rotation_stage(backend, X, level, B, plan, ("flat_r", lay))
+        level -= 1
+    if col_rm:
+        plan = []
+        for r in range(h_in):
+            region = np.zeros(lay.footprint)
+            region[r * span:r * span + w_in] = 1.0
+            plan.append((schedule.tile_region(ns, lay, region), r * (span - w_in)))
+        masked_census(plan, level)
+        X = _masked_rotation_stage(backend, X, level, B, plan, ("flat_c", lay))
+        level -= 1
+    flat = w_in * h_in
+    if C > 1:
+        cnt.record("rotation", level, C - 1)
+        cnt.record("add", level, C - 1)
+        X = X[:, :, :, :level + 1].contiguous() if X.shape[3] != level + 1 else X
+        acc = _hoist(backend, X, level, [-ch * flat for ch in range(C)], None, 1, True, B)
+        out = _finish(backend, acc, level, rescale=False)[0]
+    else:
+        out = X[0]
+    new_lay = replace(lay, interval=1, w_in=flat * lay.channels, h_in=1, channels=1, pending_const=1.0,
+                      gaps_zero=True)
+    return CipherState([CipherVector(out, level, scale, backend)], new_lay)
+
+
+def math_ceil(x):
+    import math
+
+    return math.ceil(x)
+
+
+def fc(backend, state: CipherState, layer) -> CipherState:
+    if not _is_gpu(backend):
+        return schedule.fc(backend, state, layer)
+    from dataclasses import replace
+
+    from .errors import LevelExhausted, NotFlattened, ShapeMismatch
+    from .he_backend import CipherVector
+
+    lay = state.layout
+    if not (lay.interval == 1 and lay.h_in == 1 and lay.channels == 1):
+        raise NotFlattened("fully connected layer requires a flattened input")
+    if lay.w_in != layer.dat_in:
+        raise ShapeMismatch(f"fc expects {layer.dat_in} inputs, flattened vector has {lay.w_in}")
+    ct = state.cts[0]
+    level, B, n = ct.level, ct.batch, backend.n
+    if level < 1:
+        raise LevelExhausted("ciphertext has no multiplication budget left")
+    d_out = layer.dat_out
+    reps, window, masks = schedule.fc_masks(layer, lay, backend.params.num_slots)
+    scale = ct.scale
+    cnt = backend.counter
+    # stage 1: front / wrap diagonals (rotation o of the input, two masks each)
+    cnt.record("rotation", level, d_out - 1)
+    cnt.record("pt_mult", level, 2 * d_out)
+    cnt.record("add", level - 1, 2 * (d_out - 1))
+    rows = np.stack([f for f, _ in masks] + [w for _, w in masks])  # [2 * d_out, slots]: o=0 front, o=1 wrap
+    bank = _rows_bank(backend, ("fc", id(layer), lay), rows, level, float(backend.modulus(level)))
+    X = stack_cts(backend, [ct], level)
+    acc = _hoist(backend, X, level, list(range(d_out)), bank.view(2, d_out, level + 2, n), 2, False, B)
+    fw = _finish(backend, acc, level, rescale=True)  # [2][B][2][level][N]
+    level -= 1
+    # stage 2: summed = front + rot(wrap, -window)
+    cnt.record("rotation", level, 1)
+    cnt.record("add", level, 1)
+    acc = _hoist(backend, fw, level, [0, -window], None, 1, True, B)
+    summed = _finish(backend, acc, level, rescale=False)  # [1][B][2][level+1][N]
+    # stage 3: folds sum_i rot(summed, i * d_out)
+    if reps > 1:
+        cnt.record("rotation", level, reps - 1)
+        cnt.record("add", level, reps - 1)
+        acc = _hoist(backend, summed, level, [i * d_out for i in range(reps)], None, 1, False, B)
+        summed = _finish(backend, acc, level, rescale=False)
+    out = summed[0]
+    # bias at valid positions of every sample region
+    cnt.record("add", level, 1)
+    bias = np.zeros(lay.footprint)
+    bias[:d_out] = layer.bias
+    bias_t = _bank(backend, ("fc_bias", id(layer), lay, level, scale), lambda: backend.encode_device(
+        torch.from_numpy(schedule.tile_region(backend.params.num_slots, lay, bias))[None], level, scale))
+    Lo = level + 1
+    backend._call("uh_elementwise", OP_ADD, _vp(out), _vp(out), _vp(bias_t), B, 1, Lo, Lo, 2 * Lo, 2 * Lo, Lo,
+                  backend._stream())
+    return CipherState([CipherVector(out, level, scale, backend)],
+                       replace(lay, w_in=d_out, pending_const=1.0, gaps_zero=False))
+
+
 def apply_layer_fused(backend, state: CipherState, layer) -> CipherState:
+    from .planner import FC, Flatten
+
     if isinstance(layer, (Conv2d, Conv1d)):
         return conv(backend, state, layer)
     if isinstance(layer, AvgPool2d):
         return avgpool(backend, state, layer)
     if isinstance(layer, Square):
         return square(backend, state)
+    if isinstance(layer, Flatten):
+        return flatten(backend, state)
+    if isinstance(layer, FC):
+        return fc(backend, state, layer)
     return schedule.apply_layer(backend, state, layer)

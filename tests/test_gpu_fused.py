@@ -31,7 +31,7 @@ def test_layers_fused_equal_oplevel(batch):
     planes = driver.pack_groups(m, groups, plan)
     ct = be.encrypt(be.encode_batch(planes[0]))
     state = schedule.drop_level(be, CipherState([ct], driver._input_layout(m, plan)), 7)
-    for layer in m.layers[:6]:  # conv, square, pool, conv, square, pool
+    for layer in m.layers:  # conv, square, pool, conv, square, pool, flatten, fc
         c0 = be.counter.snapshot()
         ref = schedule.apply_layer(be, state, layer)
         c1 = be.counter.snapshot()
@@ -45,3 +45,26 @@ def test_layers_fused_equal_oplevel(batch):
         scale = max(1.0, float(np.max(np.abs(a))))
         assert np.max(np.abs(a - b)) / scale < 1e-7, type(layer).__name__
         state = ref
+
+
+@pytest.mark.parametrize("name", ["M1", "M6", "M7"])
+def test_builtin_models_fused_vs_plaintext(name):
+    """Row-removal flatten (M1, M6), conv1d (M7), multi-FC models through the fused path."""
+    params = HEParams(poly_degree=1 << 13, depth=8, scale_bits=40)
+    m = planner.builtin(name, seed=1)
+    # scale the uniform [-0.5, 0.5) weights down so squared activations stay O(1) at 2^40 precision
+    for layer in m.layers:
+        if hasattr(layer, "weights"):
+            layer.weights = layer.weights * 0.2
+    plan = planner.footprint(m, params)
+    be = GpuBackend(params)
+    samples = list(np.random.default_rng(2).uniform(0, 1, size=(min(plan.capacity, 4), m.channels, m.height,
+                                                                   m.width)))
+    outs, metrics, _ = driver.run_inference(m, samples, params, plan=plan, backend=be, fused=True)
+    from oracle.slot_sim import SimBackend
+
+    _, ref_metrics, _ = driver.run_inference(m, samples, params, plan=plan, backend=SimBackend(params))
+    assert [r.to_dict() for r in metrics.per_layer] == [r.to_dict() for r in ref_metrics.per_layer]
+    for s, y in zip(samples, outs):
+        ref = planner.reference_infer(m, s)
+        assert np.max(np.abs(y - ref)) < 1e-5 * max(1.0, float(np.max(np.abs(ref))))
