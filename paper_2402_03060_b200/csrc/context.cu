@@ -102,6 +102,31 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
         e = e * 5 % two_n;
     }
     for (uint32_t k = 0; k < n; k++) sob[k] = dlog[2 * h_brv(k, c->logn) + 1];
+    // pass-2 block selection and per-slot element index for the coalesced
+    // slot-order I/O of the fast NTT (see ntt_fast.cu, cta_slot)
+    std::vector<int32_t> bsel, csl;
+    if (c->n1) {
+        const uint32_t n1 = c->n1, n2 = c->n2, G = 4096 / n2, per_half = (n1 / 2) / G;
+        bsel.assign(n1, -1);
+        csl.assign(n, 0);
+        std::vector<int32_t> k_of(n);
+        for (uint32_t k = 0; k < n; k++) {
+            csl[sob[k]] = (int32_t)(k % n2);
+            k_of[sob[k]] = (int32_t)k;
+        }
+        for (uint32_t blk = 0; blk < n1; blk++) {
+            uint32_t s0 = (uint32_t)sob[(size_t)blk * n2];
+            uint32_t h = s0 / half, j0 = (s0 % half) % (n1 / 2);
+            bsel[(size_t)(h * per_half + j0 / G) * G + j0 % G] = (int32_t)blk;
+        }
+        for (uint32_t x = 0; x < n1 / G; x++)
+            for (uint32_t i = 0; i < 4096; i++) {
+                uint32_t h = x / per_half, js = (x % per_half) * G;
+                uint32_t s = h * half + js + i % G + (n1 / 2) * (i / G);
+                if (bsel[(size_t)x * G + i % G] != k_of[s] / (int32_t)n2)
+                    throw std::logic_error("NTT pass-2 slot layout invariant violated");
+            }
+    }
     // cross-modulus inverses
     std::vector<uint64_t> inv((size_t)count * count, 0), invs((size_t)count * count, 0);
     for (uint32_t i = 0; i < count; i++)
@@ -111,6 +136,17 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
             inv[(size_t)i * count + j] = v;
             invs[(size_t)i * count + j] = h_shoup(v, moduli[i]);
         }
+    std::vector<ulonglong2> tw2((size_t)count * n), itw2((size_t)count * n);
+    for (size_t i = 0; i < tw2.size(); i++) {
+        tw2[i] = make_ulonglong2(tw[i], tws[i]);
+        itw2[i] = make_ulonglong2(itw[i], itws[i]);
+    }
+    if (c->n1) {
+        c->d_bsel = upload(bsel);
+        c->d_csl = upload(csl);
+    }
+    c->d_tw2 = upload(tw2);
+    c->d_itw2 = upload(itw2);
     c->d_mods = upload(mods);
     c->d_psi = upload(tw);
     c->d_psis = upload(tws);
@@ -127,7 +163,8 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
 void ctx_destroy(Ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    for (void *p : {(void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis, (void *)c->d_ipsi, (void *)c->d_ipsis,
+    for (void *p : {(void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
+                    (void *)c->d_ipsi, (void *)c->d_ipsis,
                     (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_pos, (void *)c->d_neg})
         if (p) cudaFree(p);
     delete c;

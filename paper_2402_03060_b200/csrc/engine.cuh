@@ -18,7 +18,10 @@ struct Ctx {
     Mod *d_mods = nullptr;               // [count]
     uint64_t *d_psi = nullptr, *d_psis = nullptr;    // [count][n] psi^brv(i), Shoup companions
     uint64_t *d_ipsi = nullptr, *d_ipsis = nullptr;  // [count][n] psi^-brv(i)
+    ulonglong2 *d_tw2 = nullptr, *d_itw2 = nullptr;  // [count][n] interleaved (w, w') pairs of the above
     int32_t *d_sob = nullptr;            // [n] slot-order index of bit-reversed NTT output k
+    int32_t *d_bsel = nullptr;           // [n1] pass-2 block of CTA x, position g (ntt_fast.cu)
+    int32_t *d_csl = nullptr;            // [n] element index inside its pass-2 block, per slot
     uint64_t *d_inv = nullptr, *d_invs = nullptr;  // [count][count]: q_j^-1 mod q_i at [i*count+j]
     int32_t *d_pos = nullptr;            // [n/2] index (5^j mod 2N - 1)/2 : slot j -> odd exponent slot
     int32_t *d_neg = nullptr;            // [n/2] index (2N - 5^j - 1)/2

@@ -25,7 +25,7 @@ namespace uh {
 namespace {
 
 constexpr int kTBatch = 8;   // ciphertexts per CTA tile
-constexpr int kTChunk = 4;   // terms staged per shared-memory chunk
+constexpr int kTChunk = 3;   // terms staged per shared-memory chunk (768 items: 2 / 3 per thread at 12 / 8 warps)
 constexpr int kFold = 56;    // terms between folds of the 128-bit accumulators
 
 __device__ __forceinline__ uint32_t rot_index(uint32_t n, uint32_t half, uint32_t r) {
@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(384) k_hoisted_mac(uint64_t *__restrict__ acc_
                     Acc a0, a1;
                     a0.zero();
                     a1.zero();
-                    for (int j = 0; j < L; j++) {
+#pragma unroll 4
+                    for (int j = 0; j < L; j++) {  // unrolled: keep 12 independent loads in flight
                         const uint64_t d = Di[(((size_t)j * LP) << logn) + src];
                         a0.mac(d, k0[(2 * j) * kstride]);
                         a1.mac(d, k0[(2 * j + 1) * kstride]);

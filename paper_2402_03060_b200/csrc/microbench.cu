@@ -48,6 +48,43 @@ __global__ void k_mac_peak(uint64_t *out, int iters, uint64_t seed) {
     if (s == 0x1234567812345678ull) out[0] = s;
 }
 
+__global__ void k_macc_peak(uint64_t *out, int iters, uint64_t seed) {  // plain-C MAC form
+    Acc acc[8];
+    uint64_t x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        acc[i].zero();
+        x[i] = (seed + threadIdx.x * 8 + i) & ((1ull << 60) - 1);
+    }
+    const uint64_t w = (0x0FEDCBA987654321ull + blockIdx.x) & ((1ull << 60) - 1);
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            acc[i].mac_c(x[i], w);
+            x[i] ^= acc[i].lo;
+        }
+    }
+    uint64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s ^= acc[i].lo ^ acc[i].hi;
+    if (s == 0x1234567812345678ull) out[0] = s;
+}
+
+__global__ void k_shoup_peak(uint64_t *out, int iters, uint64_t seed, Mod m) {  // lazy Shoup (NTT butterfly core)
+    uint64_t x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = (seed + threadIdx.x * 8 + i) % m.q;
+    const uint64_t w = m.r64, ws = m.r64s;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) x[i] = shoup_lazy(x[i], w, ws, m.q);
+    }
+    uint64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s ^= x[i];
+    if (s == 0x1234567812345678ull) out[0] = s;
+}
+
 __global__ void k_mulmod_peak(uint64_t *out, int iters, uint64_t seed, Mod m) {
     uint64_t x[8];
 #pragma unroll
@@ -97,6 +134,10 @@ void bench_peaks(const Ctx &c, double *rates) {
     rates[1] = lanes * iters * 8 / (ms * 1e-3);
     ms = time_ms([&] { k_mulmod_peak<<<blocks, threads>>>(out, iters / 2, 7ull, m); });
     rates[2] = lanes * (iters / 2) * 8 / (ms * 1e-3);
+    ms = time_ms([&] { k_macc_peak<<<blocks, threads>>>(out, iters, 7ull); });
+    rates[3] = lanes * iters * 8 / (ms * 1e-3);
+    ms = time_ms([&] { k_shoup_peak<<<blocks, threads>>>(out, iters, 7ull, m); });
+    rates[4] = lanes * iters * 8 / (ms * 1e-3);
     UH_CHECK(cudaGetLastError());
     cudaFree(out);
 }

@@ -14,6 +14,7 @@
 // N2-blocks and scatters to slot order.  Small N runs in one pass per limb.
 // Butterflies use Shoup twiddle products (precomputed companions).
 #include "engine.cuh"
+#include "ntt_fast.cuh"
 
 namespace uh {
 
@@ -225,6 +226,19 @@ void ntt_forward(const Ctx &c, uint64_t *data, int n_polys, int nl, int nq, int 
         UH_LAUNCH_CHECK();
         return;
     }
+    if (ntt_fast_supported(c)) {
+        NttJob J;
+        J.nl = nl;
+        J.nq = nq;
+        J.base = base;
+        J.sp = c.sp();
+        J.src = data;
+        J.src_ps = pstride;
+        J.dst = data;
+        J.dst_ps = pstride;
+        ntt_fast_forward(c, J, limbs, s);
+        return;
+    }
     Scratch tmp((size_t)limbs * n * sizeof(uint64_t), s);
     int n1 = (int)c.n1, n2 = (int)c.n2, g = pass2_group(c);
     dim3 g1(n2 / kCols, limbs), g2(n1 / g, limbs);
@@ -244,6 +258,19 @@ void ntt_inverse(const Ctx &c, uint64_t *data, int n_polys, int nl, int nq, int 
         k_ntt_inv_small<<<limbs, kThreads, n * sizeof(uint64_t), s>>>(data, nl, nq, base, c.sp(), pstride, n, c.d_mods,
                                                                     c.d_ipsi, c.d_ipsis, c.d_sob);
         UH_LAUNCH_CHECK();
+        return;
+    }
+    if (ntt_fast_supported(c)) {
+        NttJob J;
+        J.nl = nl;
+        J.nq = nq;
+        J.base = base;
+        J.sp = c.sp();
+        J.src = data;
+        J.src_ps = pstride;
+        J.dst = data;
+        J.dst_ps = pstride;
+        ntt_fast_inverse(c, J, limbs, s);
         return;
     }
     Scratch tmp((size_t)limbs * n * sizeof(uint64_t), s);

@@ -1,0 +1,390 @@
+// Register-tiled two-pass negacyclic NTT for N >= 2^13 (sm_100a).
+//
+// N = N1 * N2 viewed as an N1 x N2 row-major matrix.
+//   pass 1: a CTA owns 32 columns (lane <-> column: every global access is a
+//           256-byte coalesced row segment); the first log2(N1) Cooley-Tukey
+//           stages run as two register-resident radix-2^a sub-networks with one
+//           shared-memory exchange in between.
+//   pass 2: a CTA owns 4096/N2 contiguous N2-blocks; the remaining log2(N2)
+//           stages again run as two register radix sub-networks around one
+//           (bank-conflict-padded) shared-memory exchange; the epilogue
+//           reduces to [0, q) and scatters to slot order.
+// Butterflies are Harvey's lazy ones (values in [0, 4q) forward, [0, 2q)
+// inverse; every prime is < 2^62) with Shoup twiddles read as interleaved
+// (w, w') 16-byte pairs.  The inverse mirrors both passes (Gentleman-Sande).
+//
+// Load / store transforms are fused into the passes, so no extra HBM round
+// trip is needed for:
+//   mode PLAIN  -- strided limbs in, strided limbs out (in place allowed);
+//   mode MODUP  -- ModUp: limb (p, j, k) loads centred(C[p][j], q_j) mod q_k;
+//   mode DIVIDE -- rescale / ModDown: limb (p, k) loads centred(top[p], q_top)
+//                  mod q_k and the epilogue writes (in[p][k] - y) * q_top^-1.
+#include "ntt_fast.cuh"
+
+namespace uh {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct LimbInfo {
+    int mod;
+    const uint64_t *src;
+    uint64_t qsrc;  // 0: plain load, else centred lift from modulus qsrc
+    uint64_t *dst;
+    const uint64_t *in;  // DIVIDE
+    uint64_t w, ws;      // DIVIDE: q_top^-1 mod q_k (Shoup pair)
+};
+
+__device__ __forceinline__ LimbInfo limb_info(const NttJob &J, int f, int logn, const Mod *__restrict__ mods) {
+    LimbInfo li;
+    li.qsrc = 0;
+    li.in = nullptr;
+    li.w = li.ws = 0;
+    if (J.mode == NTT_MODUP) {
+        const int LP = J.L + 1;
+        const int k = f % LP, pj = f / LP, j = pj % J.L;
+        li.mod = limb_mod(k, J.L, 0, J.sp);
+        li.src = J.src + ((size_t)pj << logn);
+        li.qsrc = mods[j].q;
+        li.dst = J.dst + ((size_t)f << logn);
+    } else {
+        const int p = f / J.nl, k = f - p * J.nl;
+        li.mod = limb_mod(k, J.nq, J.base, J.sp);
+        li.dst = J.dst + (((size_t)p * J.dst_ps + k) << logn);
+        if (J.mode == NTT_DIVIDE) {
+            li.src = J.src + ((size_t)p << logn);
+            li.qsrc = mods[J.top_mod].q;
+            li.in = J.in + (((size_t)p * J.in_ps + k) << logn);
+            li.w = J.inv[(size_t)k * J.count + J.top_mod];
+            li.ws = J.invs[(size_t)k * J.count + J.top_mod];
+        } else {
+            li.src = J.src + (((size_t)p * J.src_ps + k) << logn);
+        }
+    }
+    return li;
+}
+
+__device__ __forceinline__ uint64_t load_in(const LimbInfo &li, size_t idx, const Mod &m) {
+    uint64_t x = li.src[idx];
+    return li.qsrc ? centred_to(x, li.qsrc, m) : x;
+}
+
+// Harvey CT butterfly: x, y in [0, 4q) -> [0, 4q)
+__device__ __forceinline__ void ct(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q) {
+    uint64_t q2 = 2 * q;
+    uint64_t u = x >= q2 ? x - q2 : x;
+    uint64_t t = shoup_lazy(y, w.x, w.y, q);
+    x = u + t;
+    y = u - t + q2;
+}
+// Harvey GS butterfly: x, y in [0, 2q) -> [0, 2q)
+__device__ __forceinline__ void gs(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q) {
+    uint64_t q2 = 2 * q;
+    uint64_t s = x + y;
+    uint64_t d = x - y + q2;
+    x = s >= q2 ? s - q2 : s;
+    y = shoup_lazy(d, w.x, w.y, q);
+}
+__device__ __forceinline__ uint64_t reduce4q(uint64_t x, uint64_t q) {
+    x = x >= 2 * q ? x - 2 * q : x;
+    return x >= q ? x - q : x;
+}
+__device__ __forceinline__ ulonglong2 tw(const ulonglong2 *__restrict__ t, int i) { return __ldg(t + i); }
+
+// forward radix network on R register values (elements base + S*x), stages with
+// distance dx = R/2 .. 1; twiddle index = m0 * (1 << s) + off(s) + x / (2 dx)
+template <int R>
+__device__ __forceinline__ void fwd_strided(uint64_t (&v)[R], const ulonglong2 *__restrict__ T, int m0, int moff,
+                                            uint64_t q) {
+    int m = m0, off = moff;
+#pragma unroll
+    for (int dx = R / 2; dx >= 1; dx >>= 1) {
+#pragma unroll
+        for (int x = 0; x < R; x++) {
+            if (x & dx) continue;
+            ct(v[x], v[x + dx], tw(T, m + off + x / (2 * dx)), q);
+        }
+        m <<= 1;
+        off <<= 1;
+    }
+}
+template <int R>
+__device__ __forceinline__ void inv_strided(uint64_t (&v)[R], const ulonglong2 *__restrict__ T, int mlast,
+                                            int offlast, uint64_t q) {
+    // mirror of fwd_strided: distances 1 .. R/2, m halves each stage
+    int m = mlast, off = offlast;
+#pragma unroll
+    for (int dx = 1; dx <= R / 2; dx <<= 1) {
+#pragma unroll
+        for (int x = 0; x < R; x++) {
+            if (x & dx) continue;
+            gs(v[x], v[x + dx], tw(T, m + off + x / (2 * dx)), q);
+        }
+        m >>= 1;
+        off >>= 1;
+    }
+}
+
+// ---------------- pass 1 (columns), N1 = 2^A ----------------
+template <int A>
+struct P1 {
+    static constexpr int N1 = 1 << A, A1 = (A + 1) / 2, A2 = A - A1;
+    static constexpr int R1 = 1 << A1, S1 = 1 << A2, R2 = 1 << A2;
+    static constexpr int GS = S1 * 32 / kThreads;  // strided groups per thread
+    static constexpr int GC = R1 * 32 / kThreads;  // contiguous groups per thread
+};
+
+template <int A>
+__global__ void __launch_bounds__(kThreads) k_fwd_p1(NttJob J, uint64_t *__restrict__ tmp, int logn,
+                                                    const Mod *__restrict__ mods,
+                                                    const ulonglong2 *__restrict__ twd) {
+    using C = P1<A>;
+    __shared__ uint64_t sm[C::N1 * 32];
+    const int f = blockIdx.y, lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int n2 = 1 << (logn - A);
+    const int col = blockIdx.x * 32 + lane;
+    const LimbInfo li = limb_info(J, f, logn, mods);
+    const Mod m = mods[li.mod];
+    const uint64_t q = m.q;
+    const ulonglong2 *T = twd + ((size_t)li.mod << logn);
+#pragma unroll
+    for (int g = 0; g < C::GS; g++) {
+        const int r0 = wq + 8 * g;  // < S1
+        uint64_t v[C::R1];
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) v[x] = load_in(li, (size_t)(r0 + C::S1 * x) * n2 + col, m);
+        fwd_strided<C::R1>(v, T, 1, 0, q);
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) sm[(r0 + C::S1 * x) * 32 + lane] = v[x];
+    }
+    __syncthreads();
+    uint64_t *out = tmp + ((size_t)f << logn);
+#pragma unroll
+    for (int g = 0; g < C::GC; g++) {
+        const int grp = wq + 8 * g;  // < R1
+        const int r0 = grp * C::R2;
+        uint64_t v[C::R2];
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) v[z] = sm[(r0 + z) * 32 + lane];
+        // stages m = R1 .. N1/2 on contiguous rows r0 + z: twiddle m + (r0 + z) / (2t)
+        fwd_strided<C::R2>(v, T, C::R1, grp, q);
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) out[(size_t)(r0 + z) * n2 + col] = v[z];
+    }
+}
+
+template <int A>
+__global__ void __launch_bounds__(kThreads) k_inv_pb(NttJob J, const uint64_t *__restrict__ tmp, int logn,
+                                                    const Mod *__restrict__ mods,
+                                                    const ulonglong2 *__restrict__ itwd) {
+    using C = P1<A>;
+    __shared__ uint64_t sm[C::N1 * 32];
+    const int f = blockIdx.y, lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int n2 = 1 << (logn - A);
+    const int col = blockIdx.x * 32 + lane;
+    const LimbInfo li = limb_info(J, f, logn, mods);
+    const Mod m = mods[li.mod];
+    const uint64_t q = m.q;
+    const ulonglong2 *T = itwd + ((size_t)li.mod << logn);
+    const uint64_t *in = tmp + ((size_t)f << logn);
+#pragma unroll
+    for (int g = 0; g < C::GC; g++) {
+        const int grp = wq + 8 * g;
+        const int r0 = grp * C::R2;
+        uint64_t v[C::R2];
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) v[z] = in[(size_t)(r0 + z) * n2 + col];
+        // mirror of the forward contiguous stages: last stage m = N1/2 with offset grp * (R2/2)
+        inv_strided<C::R2>(v, T, C::N1 / 2, grp * (C::R2 / 2), q);
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) sm[(r0 + z) * 32 + lane] = v[z];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < C::GS; g++) {
+        const int r0 = wq + 8 * g;
+        uint64_t v[C::R1];
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) v[x] = sm[(r0 + C::S1 * x) * 32 + lane];
+        inv_strided<C::R1>(v, T, C::R1 / 2, 0, q);
+#pragma unroll
+        for (int x = 0; x < C::R1; x++)
+            li.dst[(size_t)(r0 + C::S1 * x) * n2 + col] = csub(shoup_lazy(v[x], m.ninv, m.ninvs, q), q);
+    }
+}
+
+// ---------------- pass 2 (contiguous blocks), N2 = 2^B ----------------
+template <int B>
+struct P2 {
+    static constexpr int N2 = 1 << B, B1 = 4, B2 = B - 4;
+    static constexpr int R1 = 16, S = N2 / 16, R2 = 1 << B2;
+    static constexpr int G = 4096 / N2;                  // blocks per CTA
+    static constexpr int GC = (4096 / R2) / kThreads;    // contiguous groups per thread
+    static constexpr int PAD = N2 + N2 / 16;             // padded block stride in shared memory
+    __device__ static int at(int g, int c) { return g * PAD + c + (c >> 4); }
+};
+
+// Slot-order I/O of pass 2.  Block blk of the N1 x N2 view evaluates at the
+// coset e0 * {x = 1 mod 2N/N2... }: its N2 outputs land on slots
+// {h * N/2 + j0 + (N1/2) * v : v < N2} (one half h, one residue j0 mod N1/2).
+// CTA x takes the G blocks with half h = x / (N1/(2G)) and residues
+// j0 = (x mod N1/(2G)) * G + g, so its 4096 slots are G-long contiguous runs
+// at stride N1/2: slot i of the CTA (i < 4096, increasing) is
+//   h * N/2 + j_start + (i mod G) + (N1/2) * (i / G),
+// and reading/writing them in that order is coalesced.  csl[slot] is the
+// element index c of the slot inside its block (host table).
+template <int B>
+__device__ __forceinline__ size_t cta_slot(int i, int logn) {
+    using C = P2<B>;
+    const int n1 = 1 << (logn - B);
+    const int per_half = (n1 / 2) / C::G;
+    const int h = blockIdx.x / per_half, js = (blockIdx.x % per_half) * C::G;
+    return ((size_t)h << (logn - 1)) + js + (i % C::G) + (size_t)(n1 / 2) * (i / C::G);
+}
+
+template <int B>
+__global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *__restrict__ tmp, int logn,
+                                                    const Mod *__restrict__ mods,
+                                                    const ulonglong2 *__restrict__ twd,
+                                                    const int32_t *__restrict__ bsel,
+                                                    const int32_t *__restrict__ csl) {
+    using C = P2<B>;
+    __shared__ uint64_t sm[C::G * C::PAD];
+    const int f = blockIdx.y, tid = threadIdx.x;
+    const int n1 = 1 << (logn - B);
+    const int *sel = bsel + blockIdx.x * C::G;
+    const LimbInfo li = limb_info(J, f, logn, mods);
+    const Mod m = mods[li.mod];
+    const uint64_t q = m.q;
+    const ulonglong2 *T = twd + ((size_t)li.mod << logn);
+    const uint64_t *in = tmp + ((size_t)f << logn);
+    {
+        const int g = tid / C::S, c0 = tid % C::S, blk = sel[g];
+        uint64_t v[C::R1];
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) v[x] = in[(size_t)blk * C::N2 + c0 + C::S * x];
+        // local stages m' = 1..8: global twiddle index m' * (n1 + blk) + x / (2 dx)
+        fwd_strided<C::R1>(v, T, n1 + blk, 0, q);
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) sm[C::at(g, c0 + C::S * x)] = v[x];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int gi = 0; gi < C::GC; gi++) {
+        const int grp = tid + kThreads * gi;
+        const int per = C::N2 / C::R2;
+        const int g = grp / per, c = (grp % per) * C::R2, blk = sel[g];
+        uint64_t v[C::R2];
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) v[z] = sm[C::at(g, c + z)];
+        // local stages m' = 16 .. N2/2 on contiguous c + z
+        fwd_strided<C::R2>(v, T, 16 * (n1 + blk), (c / C::R2) , q);
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = reduce4q(v[z], q);
+    }
+    __syncthreads();
+    // coalesced slot-order epilogue
+    for (int i = tid; i < 4096; i += kThreads) {
+        const size_t s = cta_slot<B>(i, logn);
+        const uint64_t y = sm[C::at(i % C::G, csl[s])];
+        if (J.mode == NTT_DIVIDE)
+            li.dst[s] = csub(shoup_lazy(submod(li.in[s], y, q), li.w, li.ws, q), q);
+        else
+            li.dst[s] = y;
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(kThreads) k_inv_pa(NttJob J, uint64_t *__restrict__ tmp, int logn,
+                                                    const Mod *__restrict__ mods,
+                                                    const ulonglong2 *__restrict__ itwd,
+                                                    const int32_t *__restrict__ bsel,
+                                                    const int32_t *__restrict__ csl) {
+    using C = P2<B>;
+    __shared__ uint64_t sm[C::G * C::PAD];
+    const int f = blockIdx.y, tid = threadIdx.x;
+    const int n1 = 1 << (logn - B);
+    const int *sel = bsel + blockIdx.x * C::G;
+    const LimbInfo li = limb_info(J, f, logn, mods);
+    const Mod m = mods[li.mod];
+    const uint64_t q = m.q;
+    const ulonglong2 *T = itwd + ((size_t)li.mod << logn);
+    // coalesced slot-order gather into the blocks' shared-memory tiles
+    for (int i = tid; i < 4096; i += kThreads) {
+        const size_t s = cta_slot<B>(i, logn);
+        sm[C::at(i % C::G, csl[s])] = load_in(li, s, m);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int gi = 0; gi < C::GC; gi++) {
+        const int grp = tid + kThreads * gi;
+        const int per = C::N2 / C::R2;
+        const int g = grp / per, c = (grp % per) * C::R2, blk = sel[g];
+        uint64_t v[C::R2];
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) v[z] = sm[C::at(g, c + z)];
+        // mirror of the forward contiguous stages: last local stage m' = N2/2
+        inv_strided<C::R2>(v, T, (C::N2 / 2) * (n1 + blk), (c / C::R2) * (C::R2 / 2), q);
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = v[z];
+    }
+    __syncthreads();
+    {
+        const int g = tid / C::S, c0 = tid % C::S, blk = sel[g];
+        uint64_t v[C::R1];
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) v[x] = sm[C::at(g, c0 + C::S * x)];
+        inv_strided<C::R1>(v, T, 8 * (n1 + blk), 0, q);
+        uint64_t *out = tmp + ((size_t)f << logn);
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) out[(size_t)blk * C::N2 + c0 + C::S * x] = v[x];
+    }
+}
+
+template <int A, int B>
+void run_fwd(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
+    Scratch tmp((size_t)limbs * c.n * 8, s);
+    dim3 g1((1u << B) / 32, limbs), g2((1u << A) / P2<B>::G, limbs);
+    k_fwd_p1<A><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2);
+    UH_LAUNCH_CHECK();
+    k_fwd_p2<B><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2, c.d_bsel,
+                                        c.d_csl);
+    UH_LAUNCH_CHECK();
+}
+
+template <int A, int B>
+void run_inv(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
+    Scratch tmp((size_t)limbs * c.n * 8, s);
+    dim3 g1((1u << B) / 32, limbs), g2((1u << A) / P2<B>::G, limbs);
+    k_inv_pa<B><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_bsel,
+                                        c.d_csl);
+    UH_LAUNCH_CHECK();
+    k_inv_pb<A><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2);
+    UH_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+bool ntt_fast_supported(const Ctx &c) { return c.logn >= 13 && c.logn <= 15; }
+
+void ntt_fast_forward(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
+    if (limbs <= 0) return;
+    switch (c.logn) {
+        case 13: run_fwd<6, 7>(c, J, limbs, s); break;
+        case 14: run_fwd<7, 7>(c, J, limbs, s); break;
+        case 15: run_fwd<7, 8>(c, J, limbs, s); break;
+        default: throw std::invalid_argument("fast NTT supports 2^13 <= N <= 2^15");
+    }
+}
+
+void ntt_fast_inverse(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
+    if (limbs <= 0) return;
+    switch (c.logn) {
+        case 13: run_inv<6, 7>(c, J, limbs, s); break;
+        case 14: run_inv<7, 7>(c, J, limbs, s); break;
+        case 15: run_inv<7, 8>(c, J, limbs, s); break;
+        default: throw std::invalid_argument("fast NTT supports 2^13 <= N <= 2^15");
+    }
+}
+
+}  // namespace uh

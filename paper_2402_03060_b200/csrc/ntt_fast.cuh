@@ -1,0 +1,34 @@
+// Job description of the register-tiled two-pass NTT (ntt_fast.cu).
+#pragma once
+#include "engine.cuh"
+
+namespace uh {
+
+enum NttMode : int { NTT_PLAIN = 0, NTT_MODUP = 1, NTT_DIVIDE = 2 };
+
+// One launch transforms `limbs` limbs; limb f is decoded per mode:
+//  PLAIN : p = f / nl, k = f % nl; modulus limb_mod(k, nq, base, sp);
+//          src row  src + (p * src_ps + k) * N,  dst row dst + (p * dst_ps + k) * N.
+//  MODUP : (p, j, k) = f over [n][L][L+1]; modulus limb_mod(k, L, 0, sp);
+//          forward input centred(src[p * L + j], q_j); dst row dst + f * N.
+//  DIVIDE: p = f / nl, k = f % nl, modulus k; forward input centred(src[p], q_top);
+//          epilogue dst[p][k] = (in[p][k] - y) * q_top^-1 (rows at p * dst_ps / p * in_ps).
+struct NttJob {
+    int mode = NTT_PLAIN;
+    int nl = 1, nq = 1, base = 0, sp = 0;
+    const uint64_t *src = nullptr;
+    int src_ps = 1;
+    uint64_t *dst = nullptr;
+    int dst_ps = 1;
+    int L = 0;
+    const uint64_t *in = nullptr;
+    int in_ps = 1;
+    int top_mod = 0, count = 0;
+    const uint64_t *inv = nullptr, *invs = nullptr;
+};
+
+bool ntt_fast_supported(const Ctx &c);
+void ntt_fast_forward(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s);
+void ntt_fast_inverse(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s);
+
+}  // namespace uh

@@ -8,6 +8,7 @@
 // decomposition one digit per q_j, special prime P), so results are bit-exact
 // against the oracle on every residue.
 #include "ops.cuh"
+#include "ntt_fast.cuh"
 
 namespace uh {
 
@@ -207,11 +208,41 @@ void divide_top(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, in
                 int in_ps, cudaStream_t s) {
     if (!n_polys) return;
     size_t N = c.n;
+    bool is_sp = top_mod == c.sp();
+    if (ntt_fast_supported(c)) {
+        Scratch top((size_t)n_polys * N * 8, s);
+        NttJob Ji;  // top limb -> coefficients
+        Ji.nl = 1;
+        Ji.nq = is_sp ? 0 : 1;
+        Ji.base = is_sp ? 0 : top_mod;
+        Ji.sp = c.sp();
+        Ji.src = in + (size_t)nl * N;
+        Ji.src_ps = in_ps;
+        Ji.dst = top.as<uint64_t>();
+        Ji.dst_ps = 1;
+        ntt_fast_inverse(c, Ji, n_polys, s);
+        if (nl == 0) return;
+        NttJob Jf;  // centred lift into every lower limb, NTT, (in - t) * q_top^-1 epilogue
+        Jf.mode = NTT_DIVIDE;
+        Jf.nl = nl;
+        Jf.nq = nl;
+        Jf.sp = c.sp();
+        Jf.src = top.as<uint64_t>();
+        Jf.dst = out;
+        Jf.dst_ps = out_ps;
+        Jf.in = in;
+        Jf.in_ps = in_ps;
+        Jf.top_mod = top_mod;
+        Jf.count = (int)c.count;
+        Jf.inv = c.d_inv;
+        Jf.invs = c.d_invs;
+        ntt_fast_forward(c, Jf, n_polys * nl, s);
+        return;
+    }
     Scratch top((size_t)n_polys * N * 8, s), T((size_t)n_polys * nl * N * 8, s);
     k_gather_limb<<<grid_for((size_t)n_polys * N), kTB, 0, s>>>(top.as<uint64_t>(), in, n_polys, nl, in_ps,
                                                                  (int)c.logn);
     UH_LAUNCH_CHECK();
-    bool is_sp = top_mod == c.sp();
     ntt_inverse(c, top.as<uint64_t>(), n_polys, 1, is_sp ? 0 : 1, is_sp ? 0 : top_mod, 1, s);
     if (nl == 0) return;
     k_expand_centred<<<grid_for((size_t)n_polys * nl * N), kTB, 0, s>>>(T.as<uint64_t>(), top.as<uint64_t>(), n_polys,
@@ -228,6 +259,25 @@ void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level
     int L = level + 1;
     size_t N = c.n;
     Scratch C((size_t)n_polys * L * N * 8, s);
+    if (ntt_fast_supported(c)) {
+        NttJob Ji;  // every digit to coefficients (strided in -> compact C)
+        Ji.nl = L;
+        Ji.nq = L;
+        Ji.sp = c.sp();
+        Ji.src = in;
+        Ji.src_ps = in_ps;
+        Ji.dst = C.as<uint64_t>();
+        Ji.dst_ps = L;
+        ntt_fast_inverse(c, Ji, n_polys * L, s);
+        NttJob Jf;  // centred lift of digit j into every QP limb, fused into the forward NTT's loads
+        Jf.mode = NTT_MODUP;
+        Jf.L = L;
+        Jf.sp = c.sp();
+        Jf.src = C.as<uint64_t>();
+        Jf.dst = D;
+        ntt_fast_forward(c, Jf, n_polys * L * (L + 1), s);
+        return;
+    }
     elementwise(c, OP_COPY, C.as<uint64_t>(), in, nullptr, n_polys, 1, L, L, L, in_ps, 0, s);
     ntt_inverse(c, C.as<uint64_t>(), n_polys, L, L, 0, L, s);
     size_t total = (size_t)n_polys * L * (L + 1) * N;

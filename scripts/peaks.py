@@ -1,0 +1,17 @@
+"""Integer-pipe peaks of this GPU (uh_bench_peaks)."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+from paper_2402_03060_b200 import _lib  # noqa: E402
+from paper_2402_03060_b200.he_backend import GpuBackend  # noqa: E402
+from paper_2402_03060_b200.params import HEParams  # noqa: E402
+
+be = GpuBackend(HEParams(poly_degree=1 << 12, depth=2, scale_bits=40))
+r = np.zeros(5)
+_lib.call("uh_bench_peaks", be._ctx, ctypes.c_void_p(r.ctypes.data))
+for name, v in zip(["IMAD", "MAC128 (ptx chain)", "mulmod (reduced)", "MAC128 (C form)", "Shoup lazy"], r):
+    print(f"{name:22s} {v / 1e12:8.3f} T/s")

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 import torch
 
-from gpu_util import dev, host, stream, vp
+from tests.gpu_util import dev, host, stream, vp
 from oracle.ckks_oracle import Oracle, encode_coeffs, decode_coeffs
 from paper_2402_03060_b200 import _lib
 from paper_2402_03060_b200.he_backend import GpuBackend
