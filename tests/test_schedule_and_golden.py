@@ -80,6 +80,25 @@ def test_against_reference_package(reference_slotcnn, name):
         assert [r.detail for r in r_met.per_layer] == [r.detail for r in m_met.per_layer]
 
 
+def test_reference_engine_over_ckks_backend(reference_slotcnn):
+    """Drop-in at the plugin point: the reference's own run_inference (engine.py:196)
+    and layers.py, unchanged, drive a real RNS-CKKS backend with our interface."""
+    from oracle.ckks_oracle import OracleBackend
+
+    sc = reference_slotcnn
+    from tests.golden.make_golden import lenet1_ref
+
+    rm = lenet1_ref(0)
+    ref_params = sc.HEParams(poly_degree=1 << 11, depth=7, scale_bits=40)
+    be = OracleBackend(HEParams.from_dict(ref_params.to_dict()))
+    samples = list(np.random.default_rng(1).uniform(0, 1, size=(1, 1, 28, 28)))  # capacity 1 at N=2^11
+    outs, metrics, _ = sc.run_inference(rm, samples, ref_params, backend=be)
+    for s, y in zip(samples, outs):
+        assert np.max(np.abs(y - sc.reference_infer(rm, s))) < 1e-5
+    sim_outs, sim_metrics, _ = sc.run_inference(rm, samples, ref_params)
+    assert [r.to_dict() for r in metrics.per_layer] == [r.to_dict() for r in sim_metrics.per_layer]
+
+
 def test_validation_matches_reference(reference_slotcnn):
     sc = reference_slotcnn
     # config 1 as written (depth 3) fails the reference's depth rule; depth 4 passes
