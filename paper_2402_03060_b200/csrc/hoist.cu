@@ -40,8 +40,11 @@ __device__ __forceinline__ uint64_t reduce128_lazy(uint64_t hi, uint64_t lo, con
     return shoup_lazy(hi, m.r64, m.r64s, m.q) + barrett_lite(lo, m);
 }
 
+constexpr int kMaxL = 12;  // phase-A digit loop fully unrolled (predicated) up to this many limbs
+
 template <int PPW>
-__global__ void __launch_bounds__(384) k_hoisted_mac(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X,
+__global__ void __launch_bounds__(PPW == 8 ? 384 : 256) k_hoisted_mac(uint64_t *__restrict__ acc_out,
+                                                                      const uint64_t *__restrict__ X,
                                                     int xls, const uint64_t *__restrict__ D,
                                                     const uint64_t *__restrict__ masks,
                                                     const uint64_t *const *__restrict__ keys,
@@ -71,9 +74,23 @@ __global__ void __launch_bounds__(384) k_hoisted_mac(uint64_t *__restrict__ acc_
     }
     int since_fold = 0;
     int buf = 0;
+    constexpr int W = PPW == 8 ? 12 : 8;
+    constexpr int ITEMS = kTChunk * kTBatch / W;  // phase-A items per thread (2 or 3)
+    static_assert(ITEMS * W == kTChunk * kTBatch, "phase-A items must tile the chunk");
+    const int o_w = (warp * PPW) / kTBatch;  // every pair of this warp has the same output
+    const bool warp_active = warp * PPW < npairs;
     for (int q0 = 0; q0 < Q; q0 += kTChunk) {
+        // prefetch this chunk's weight masks (consumed after the barrier, latency hidden by phase A)
+        uint64_t mpre[kTChunk];
+#pragma unroll
+        for (int qc = 0; qc < kTChunk; qc++)
+            mpre[qc] = (masks && warp_active && q0 + qc < Q)
+                           ? masks[((((size_t)o_w * Q + q0 + qc) * LP + k) << logn) + n]
+                           : 0;
         // ---- phase A: rotated, key-switched inputs of this chunk into shared memory ----
-        for (int it = threadIdx.x; it < kTChunk * kTBatch * 32; it += blockDim.x) {
+#pragma unroll
+        for (int ii = 0; ii < ITEMS; ii++) {
+            const int it = threadIdx.x + ii * W * 32;
             const int ln = it & 31, rest = it >> 5;
             const int bt = rest % kTBatch, qc = rest / kTBatch;
             const int q = q0 + qc, b = b0 + bt;
@@ -98,11 +115,13 @@ __global__ void __launch_bounds__(384) k_hoisted_mac(uint64_t *__restrict__ acc_
                     Acc a0, a1;
                     a0.zero();
                     a1.zero();
-#pragma unroll 4
-                    for (int j = 0; j < L; j++) {  // unrolled: keep 12 independent loads in flight
-                        const uint64_t d = Di[(((size_t)j * LP) << logn) + src];
-                        a0.mac(d, k0[(2 * j) * kstride]);
-                        a1.mac(d, k0[(2 * j + 1) * kstride]);
+#pragma unroll
+                    for (int j = 0; j < kMaxL; j++) {  // fully unrolled: all digit/key loads in flight
+                        if (j < L) {
+                            const uint64_t d = Di[(((size_t)j * LP) << logn) + src];
+                            a0.mac(d, k0[(2 * j) * kstride]);
+                            a1.mac(d, k0[(2 * j + 1) * kstride]);
+                        }
                     }
                     if (qlimb) a0.mac(Pk, c0[((size_t)k << logn) | src]);
                     v0 = csub(reduce128_lazy(a0.hi, a0.lo, m), 2 * m.q);
@@ -115,18 +134,18 @@ __global__ void __launch_bounds__(384) k_hoisted_mac(uint64_t *__restrict__ acc_
         __syncthreads();
         // ---- phase B: multiply-accumulate into every (output, ciphertext) pair ----
         const int qn = min(kTChunk, Q - q0);
-        for (int qc = 0; qc < qn; qc++) {
-            const int q = q0 + qc;
+#pragma unroll
+        for (int qc = 0; qc < kTChunk; qc++) {
+            if (qc >= qn) break;
 #pragma unroll
             for (int j = 0; j < PPW; j++) {
-                const int p = warp * PPW + j;  // a warp's pairs share one output -> one mask load per term
+                const int p = warp * PPW + j;
                 if (p < npairs) {
-                    const int o = p / kTBatch, bt = p % kTBatch;
+                    const int bt = p % kTBatch;
                     const uint64_t v0 = sv[buf][qc][bt][0][lane], v1 = sv[buf][qc][bt][1][lane];
                     if (masks) {
-                        const uint64_t mv = masks[((((size_t)o * Q + q) * LP + k) << logn) + n];
-                        acc[j][0].mac(mv, v0);
-                        acc[j][1].mac(mv, v1);
+                        acc[j][0].mac(mpre[qc], v0);
+                        acc[j][1].mac(mpre[qc], v1);
                     } else {
                         acc[j][0].add(v0);
                         acc[j][1].add(v1);
@@ -166,10 +185,11 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
                  const uint64_t *const *keys, const int32_t *key_limbs, const int32_t *shifts, int B, int I, int T,
                  int O, int diag, int level, cudaStream_t s) {
     const int L = level + 1;
+    if (L > kMaxL) throw std::invalid_argument("hoisted kernel supports up to 12 live limbs");
     const int pairs = O * kTBatch;
-    // warps x pairs-per-warp covering O * TB (output, ciphertext) pairs
-    const int W = pairs >= 96 ? 12 : 8;
-    const int ppw = (pairs + W - 1) / W;
+    // warps x pairs-per-warp covering O * TB (output, ciphertext) pairs; every warp serves one output
+    const int ppw = pairs > 32 ? 8 : (pairs > 16 ? 4 : (pairs > 8 ? 2 : 1));
+    const int W = ppw == 8 ? 12 : 8;  // must match the kernel's compile-time W
     dim3 grid((B + kTBatch - 1) / kTBatch, (unsigned)(c.n / 32), L + 1);
     if (c.n < 32) throw std::invalid_argument("hoisted kernels need N >= 32");
     auto go = [&](auto tag) {
@@ -177,13 +197,13 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
         k_hoisted_mac<PP><<<grid, W * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, diag,
                                                   L, c.sp(), (int)c.logn, c.d_mods);
     };
-    if (ppw <= 1) go(std::integral_constant<int, 1>());
-    else if (ppw <= 2) go(std::integral_constant<int, 2>());
-    else if (ppw <= 4) go(std::integral_constant<int, 4>());
-    else if (ppw <= 8) go(std::integral_constant<int, 8>());
-    else if (ppw <= 12) go(std::integral_constant<int, 12>());
-    else {
-        // very wide layers: split the outputs
+    if (O <= 12) {
+        if (ppw == 1) go(std::integral_constant<int, 1>());
+        else if (ppw == 2) go(std::integral_constant<int, 2>());
+        else if (ppw == 4) go(std::integral_constant<int, 4>());
+        else go(std::integral_constant<int, 8>());
+    } else {
+        // very wide layers: split the outputs in groups of 12 (12 warps x 8 pairs)
         for (int o0 = 0; o0 < O; o0 += 12) {
             int oc = std::min(12, O - o0);
             hoisted_mac(c, acc + (size_t)o0 * B * 2 * (L + 1) * c.n, X, xls, D,

@@ -41,12 +41,14 @@ __device__ __forceinline__ LimbInfo limb_info(const NttJob &J, int f, int logn, 
     li.in = nullptr;
     li.w = li.ws = 0;
     if (J.mode == NTT_MODUP) {
+        // limbs (p, j, k) with k != j (the diagonal limb D_j[j] is the input limb itself: copied, not transformed)
         const int LP = J.L + 1;
-        const int k = f % LP, pj = f / LP, j = pj % J.L;
+        const int kk = f % J.L, pj = f / J.L, j = pj % J.L;
+        const int k = kk + (kk >= j);
         li.mod = limb_mod(k, J.L, 0, J.sp);
         li.src = J.src + ((size_t)pj << logn);
         li.qsrc = mods[j].q;
-        li.dst = J.dst + ((size_t)f << logn);
+        li.dst = J.dst + (((size_t)pj * LP + k) << logn);
     } else {
         const int p = f / J.nl, k = f - p * J.nl;
         li.mod = limb_mod(k, J.nq, J.base, J.sp);

@@ -9,8 +9,9 @@ enum NttMode : int { NTT_PLAIN = 0, NTT_MODUP = 1, NTT_DIVIDE = 2 };
 // One launch transforms `limbs` limbs; limb f is decoded per mode:
 //  PLAIN : p = f / nl, k = f % nl; modulus limb_mod(k, nq, base, sp);
 //          src row  src + (p * src_ps + k) * N,  dst row dst + (p * dst_ps + k) * N.
-//  MODUP : (p, j, k) = f over [n][L][L+1]; modulus limb_mod(k, L, 0, sp);
-//          forward input centred(src[p * L + j], q_j); dst row dst + f * N.
+//  MODUP : (p, j, k') = f over [n][L][L], k = k' + (k' >= j) skips the diagonal;
+//          modulus limb_mod(k, L, 0, sp); forward input centred(src[p * L + j], q_j);
+//          dst row dst + ((p * L + j) * (L + 1) + k) * N.
 //  DIVIDE: p = f / nl, k = f % nl, modulus k; forward input centred(src[p], q_top);
 //          epilogue dst[p][k] = (in[p][k] - y) * q_top^-1 (rows at p * dst_ps / p * in_ps).
 struct NttJob {

@@ -57,6 +57,18 @@ __global__ void k_elementwise(int op, uint64_t *out, const uint64_t *a, const ui
 }
 
 // dst[p][n] = src[p][limb]  (gather one limb of every poly into a compact list)
+// D[p][j][j] = in[p][j]: the diagonal ModUp limb is the (evaluation-form) input limb itself
+__global__ void k_modup_diag(uint64_t *D, const uint64_t *in, int n_polys, int L, int in_ps, int logn) {
+    size_t total = ((size_t)n_polys * L) << logn;
+    size_t nmask = ((size_t)1 << logn) - 1;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        size_t n = idx & nmask, t = idx >> logn;
+        size_t j = t % L, p = t / L;
+        D[((((p * L + j) * (L + 1)) + j) << logn) | n] = in[((p * in_ps + j) << logn) | n];
+    }
+}
+
 __global__ void k_gather_limb(uint64_t *dst, const uint64_t *src, int n_polys, int limb, int src_ps, int logn) {
     size_t total = (size_t)n_polys << logn;
     size_t nmask = ((size_t)1 << logn) - 1;
@@ -275,7 +287,9 @@ void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level
         Jf.sp = c.sp();
         Jf.src = C.as<uint64_t>();
         Jf.dst = D;
-        ntt_fast_forward(c, Jf, n_polys * L * (L + 1), s);
+        ntt_fast_forward(c, Jf, n_polys * L * L, s);
+        k_modup_diag<<<grid_for((size_t)n_polys * L * N), kTB, 0, s>>>(D, in, n_polys, L, in_ps, (int)c.logn);
+        UH_LAUNCH_CHECK();
         return;
     }
     elementwise(c, OP_COPY, C.as<uint64_t>(), in, nullptr, n_polys, 1, L, L, L, in_ps, 0, s);
