@@ -70,6 +70,13 @@ int uh_elementwise(uh_ctx *ctx, int op, uint64_t *out, const uint64_t *a, const 
 int uh_divide_top(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int n_polys, int nl, int top_mod, int out_ps,
                   int in_ps, void *stream);
 
+/* Fused ModDown + rescale of QP-basis accumulators: in n_polys x (level+2) limbs
+ * (q_0..q_level, P) -> out n_polys x level limbs, centred division by q_level * P
+ * (the single division the hoisted layers need per output; rounding differs
+ * from ModDown-then-rescale by < 1 unit). */
+int uh_divide_top2(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int n_polys, int level, int out_ps, int in_ps,
+                   void *stream);
+
 /* Rescale of a ciphertext batch at `level` (the level-1 of he_backend.py:226-247). */
 int uh_rescale(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,
                void *stream);
@@ -96,6 +103,11 @@ int uh_mul_plain_rescale(uh_ctx *ctx, uint64_t *out, const uint64_t *ct, const u
 /* Backend.mul_cipher (he_backend.py:237-247): tensor, relinearise with rk, rescale. */
 int uh_mul_relin_rescale(uh_ctx *ctx, uint64_t *out, const uint64_t *a, const uint64_t *b, int B, int level,
                          int out_ls, int a_ls, int b_ls, const uint64_t *rk, int rk_limbs, void *stream);
+
+/* Fused-path Backend.mul_cipher: relinearise in the QP basis (u + P*(d0, d1)) and
+ * divide once by q_level * P (uh_divide_top2); used by the batched square layer. */
+int uh_mul_relin_rescale_fused(uh_ctx *ctx, uint64_t *out, const uint64_t *a, const uint64_t *b, int B, int level,
+                               int out_ls, int a_ls, int b_ls, const uint64_t *rk, int rk_limbs, void *stream);
 
 /* Keys.  Secret: ternary, evaluation form over all `count` moduli, [count][N]. */
 int uh_secret_gen(uh_ctx *ctx, uint64_t *s_eval, uint64_t seed, void *stream);

@@ -26,12 +26,14 @@ SIGNATURES = {
     "uh_elementwise": [_vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_divide_top": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_rescale": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp],
+    "uh_divide_top2": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_modup": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp],
     "uh_key_inner": [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_i64, _vp],
     "uh_keyswitch": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
     "uh_rotate": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_i64, _vp],
     "uh_mul_plain_rescale": [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_mul_relin_rescale": [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
+    "uh_mul_relin_rescale_fused": [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
     "uh_secret_gen": [_vp, _vp, _c_u64, _vp],
     "uh_galois_keygen": [_vp, _vp, _vp, _c_u64, _c_i64, _c_int, _vp],
     "uh_relin_keygen": [_vp, _vp, _vp, _c_u64, _c_int, _vp],

@@ -112,6 +112,18 @@ __attribute__((visibility("default"))) int uh_divide_top(uh_ctx *ctx, uint64_t *
     });
 }
 
+__attribute__((visibility("default"))) int uh_divide_top2(uh_ctx *ctx, uint64_t *out, const uint64_t *in,
+                                                          int n_polys, int level, int out_ps, int in_ps,
+                                                          void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(level >= 1, "fused ModDown + rescale needs level >= 1");
+        need(out != in, "out of place");
+        uh::divide_top2(c, out, in, n_polys, level, out_ps, in_ps, S(stream));
+    });
+}
+
 __attribute__((visibility("default"))) int uh_rescale(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int B,
                                                       int level, int out_ls, int in_ls, void *stream) {
     return guard([&] {
@@ -188,6 +200,19 @@ __attribute__((visibility("default"))) int uh_mul_relin_rescale(uh_ctx *ctx, uin
         need(level >= 1, "no multiplication budget left");
         need(rk_limbs >= level + 2, "relinearisation key truncated below the requested level");
         uh::ct_mul_relin_rescale(c, out, a, b, B, level, out_ls, a_ls, b_ls, rk, rk_limbs, S(stream));
+    });
+}
+
+__attribute__((visibility("default"))) int uh_mul_relin_rescale_fused(uh_ctx *ctx, uint64_t *out, const uint64_t *a,
+                                                                      const uint64_t *b, int B, int level, int out_ls,
+                                                                      int a_ls, int b_ls, const uint64_t *rk,
+                                                                      int rk_limbs, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(level >= 1, "no multiplication budget left");
+        need(rk_limbs >= level + 2, "relinearisation key truncated below the requested level");
+        uh::ct_mul_relin_rescale_fused(c, out, a, b, B, level, out_ls, a_ls, b_ls, rk, rk_limbs, S(stream));
     });
 }
 

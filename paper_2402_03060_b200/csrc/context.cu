@@ -145,6 +145,12 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
         c->d_bsel = upload(bsel);
         c->d_csl = upload(csl);
     }
+    std::vector<ulonglong2> pmod(count);
+    for (uint32_t i = 0; i < count; i++) {
+        uint64_t pm = moduli[count - 1] % moduli[i];
+        pmod[i] = make_ulonglong2(pm, h_shoup(pm, moduli[i]));
+    }
+    c->d_pmod = upload(pmod);
     c->d_tw2 = upload(tw2);
     c->d_itw2 = upload(itw2);
     c->d_mods = upload(mods);
@@ -163,7 +169,7 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
 void ctx_destroy(Ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    for (void *p : {(void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
+    for (void *p : {(void *)c->d_pmod, (void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
                     (void *)c->d_ipsi, (void *)c->d_ipsis,
                     (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_pos, (void *)c->d_neg})
         if (p) cudaFree(p);

@@ -23,6 +23,7 @@ struct Ctx {
     int32_t *d_bsel = nullptr;           // [n1] pass-2 block of CTA x, position g (ntt_fast.cu)
     int32_t *d_csl = nullptr;            // [n] element index inside its pass-2 block, per slot
     uint64_t *d_inv = nullptr, *d_invs = nullptr;  // [count][count]: q_j^-1 mod q_i at [i*count+j]
+    ulonglong2 *d_pmod = nullptr;        // [count] (P mod q_i, Shoup companion)
     int32_t *d_pos = nullptr;            // [n/2] index (5^j mod 2N - 1)/2 : slot j -> odd exponent slot
     int32_t *d_neg = nullptr;            // [n/2] index (2N - 5^j - 1)/2
     int sp() const { return (int)count - 1; }

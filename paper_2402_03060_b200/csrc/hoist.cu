@@ -42,8 +42,9 @@ __device__ __forceinline__ uint64_t reduce128_lazy(uint64_t hi, uint64_t lo, con
 
 constexpr int kMaxL = 12;  // phase-A digit loop fully unrolled (predicated) up to this many limbs
 
-template <int PPW>
-__global__ void __launch_bounds__(PPW == 8 ? 384 : 256) k_hoisted_mac(uint64_t *__restrict__ acc_out,
+// 8-warp CTAs are capped at 64 registers (4 CTAs / SM), 24-warp CTAs at 85 (1 CTA / SM)
+template <int PPW, int W>
+__global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1) k_hoisted_mac(uint64_t *__restrict__ acc_out,
                                                                       const uint64_t *__restrict__ X,
                                                     int xls, const uint64_t *__restrict__ D,
                                                     const uint64_t *__restrict__ masks,
@@ -74,7 +75,6 @@ __global__ void __launch_bounds__(PPW == 8 ? 384 : 256) k_hoisted_mac(uint64_t *
     }
     int since_fold = 0;
     int buf = 0;
-    constexpr int W = PPW == 8 ? 12 : 8;
     constexpr int ITEMS = kTChunk * kTBatch / W;  // phase-A items per thread (2 or 3)
     static_assert(ITEMS * W == kTChunk * kTBatch, "phase-A items must tile the chunk");
     const int o_w = (warp * PPW) / kTBatch;  // every pair of this warp has the same output
@@ -187,21 +187,35 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
     const int L = level + 1;
     if (L > kMaxL) throw std::invalid_argument("hoisted kernel supports up to 12 live limbs");
     const int pairs = O * kTBatch;
-    // warps x pairs-per-warp covering O * TB (output, ciphertext) pairs; every warp serves one output
-    const int ppw = pairs > 32 ? 8 : (pairs > 16 ? 4 : (pairs > 8 ? 2 : 1));
-    const int W = ppw == 8 ? 12 : 8;  // must match the kernel's compile-time W
     dim3 grid((B + kTBatch - 1) / kTBatch, (unsigned)(c.n / 32), L + 1);
     if (c.n < 32) throw std::invalid_argument("hoisted kernels need N >= 32");
-    auto go = [&](auto tag) {
-        constexpr int PP = decltype(tag)::value;
-        k_hoisted_mac<PP><<<grid, W * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, diag,
-                                                  L, c.sp(), (int)c.logn, c.d_mods);
+    // warps x pairs-per-warp covering O * TB (output, ciphertext) pairs; every warp serves one output.
+    // "wide" (default): 24 warps (register cap 85 -> 24 resident warps / SM for latency hiding);
+    // "narrow": 8 or 12 warps with up to 8 pairs each (UH_HOIST_CFG=narrow).
+    static const bool narrow = [] {
+        const char *e = getenv("UH_HOIST_CFG");
+        return e && std::string(e) == "narrow";
+    }();
+    auto go = [&](auto ppw_tag, auto w_tag) {
+        constexpr int PP = decltype(ppw_tag)::value, WW = decltype(w_tag)::value;
+        k_hoisted_mac<PP, WW><<<grid, WW * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O,
+                                                      diag, L, c.sp(), (int)c.logn, c.d_mods);
     };
+    using std::integral_constant;
     if (O <= 12) {
-        if (ppw == 1) go(std::integral_constant<int, 1>());
-        else if (ppw == 2) go(std::integral_constant<int, 2>());
-        else if (ppw == 4) go(std::integral_constant<int, 4>());
-        else go(std::integral_constant<int, 8>());
+        // measured (B200, N=2^15): 24 warps win when phase B is heavy (O >= 3), 8-warp CTAs when it is not
+        if (narrow || O <= 2) {
+            const int ppw = pairs > 32 ? 8 : (pairs > 16 ? 4 : (pairs > 8 ? 2 : 1));
+            if (ppw == 1) go(integral_constant<int, 1>(), integral_constant<int, 8>());
+            else if (ppw == 2) go(integral_constant<int, 2>(), integral_constant<int, 8>());
+            else if (ppw == 4) go(integral_constant<int, 4>(), integral_constant<int, 8>());
+            else go(integral_constant<int, 8>(), integral_constant<int, 12>());
+        } else {
+            const int ppw = pairs > 48 ? 4 : (pairs > 24 ? 2 : 1);
+            if (ppw == 1) go(integral_constant<int, 1>(), integral_constant<int, 24>());
+            else if (ppw == 2) go(integral_constant<int, 2>(), integral_constant<int, 24>());
+            else go(integral_constant<int, 4>(), integral_constant<int, 24>());
+        }
     } else {
         // very wide layers: split the outputs in groups of 12 (12 warps x 8 pairs)
         for (int o0 = 0; o0 < O; o0 += 12) {

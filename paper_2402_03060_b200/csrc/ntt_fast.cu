@@ -28,18 +28,49 @@ constexpr int kThreads = 256;
 
 struct LimbInfo {
     int mod;
+    int mode;
     const uint64_t *src;
     uint64_t qsrc;  // 0: plain load, else centred lift from modulus qsrc
     uint64_t *dst;
-    const uint64_t *in;  // DIVIDE
+    const uint64_t *in;  // DIVIDE / DIVIDE2
     uint64_t w, ws;      // DIVIDE: q_top^-1 mod q_k (Shoup pair)
+    // DIVIDE2
+    const uint64_t *src2;
+    uint64_t w2, ws2;     // P^-1 mod q_k
+    uint64_t P, qpk;      // P, (q_top * P) mod q_k
+    ulonglong2 pinv;      // P^-1 mod q_top (Shoup pair)
+    ulonglong2 pk;        // P mod q_k (Shoup pair)
+    Mod mt;               // the top modulus
 };
 
 __device__ __forceinline__ LimbInfo limb_info(const NttJob &J, int f, int logn, const Mod *__restrict__ mods) {
     LimbInfo li;
+    li.mode = J.mode;
     li.qsrc = 0;
     li.in = nullptr;
     li.w = li.ws = 0;
+    if (J.mode == NTT_DIVIDE2) {
+        const int p = f / J.nl, k = f - p * J.nl;
+        const int t = J.top_mod, sp = J.sp, cnt = J.count;
+        const Mod m = mods[k];
+        li.mod = k;
+        li.src = J.src + ((size_t)(2 * p) << logn);
+        li.src2 = li.src + ((size_t)1 << logn);
+        li.qsrc = 1;
+        li.dst = J.dst + (((size_t)p * J.dst_ps + k) << logn);
+        li.in = J.in + (((size_t)p * J.in_ps + k) << logn);
+        li.w = J.inv[(size_t)k * cnt + t];
+        li.ws = J.invs[(size_t)k * cnt + t];
+        li.w2 = J.inv[(size_t)k * cnt + sp];
+        li.ws2 = J.invs[(size_t)k * cnt + sp];
+        li.mt = mods[t];
+        li.P = mods[sp].q;
+        li.pinv = make_ulonglong2(J.inv[(size_t)t * cnt + sp], J.invs[(size_t)t * cnt + sp]);
+        li.pk = J.pmod[k];
+        const uint64_t qtk = li.mt.q < m.q ? li.mt.q : csub(barrett_lite(li.mt.q, m), m.q);
+        li.qpk = mulmod(qtk, li.pk.x, m);
+        return li;
+    }
     if (J.mode == NTT_MODUP) {
         // limbs (p, j, k) with k != j (the diagonal limb D_j[j] is the input limb itself: copied, not transformed)
         const int LP = J.L + 1;
@@ -66,7 +97,21 @@ __device__ __forceinline__ LimbInfo limb_info(const NttJob &J, int f, int logn, 
     return li;
 }
 
+// centred CRT lift of (a = x mod q_t, b = x mod P) in (-q_t P / 2, q_t P / 2), reduced into q_k
+__device__ __forceinline__ uint64_t crt2_to(uint64_t a, uint64_t b, const LimbInfo &li, const Mod &m) {
+    const uint64_t qt = li.mt.q;
+    const uint64_t bt = b < qt ? b : csub(barrett_lite(b, li.mt), qt);
+    const uint64_t y = shoup(submod(a, bt, qt), li.pinv.x, li.pinv.y, qt);  // x = b + P * y, y in [0, q_t)
+    const uint64_t h = (qt - 1) >> 1;
+    const bool neg = y > h || (y == h && b > (li.P - 1) / 2);
+    const uint64_t yk = y < m.q ? y : csub(barrett_lite(y, m), m.q);
+    const uint64_t bk = b < m.q ? b : csub(barrett_lite(b, m), m.q);
+    const uint64_t t = addmod(bk, shoup(yk, li.pk.x, li.pk.y, m.q), m.q);
+    return neg ? submod(t, li.qpk, m.q) : t;
+}
+
 __device__ __forceinline__ uint64_t load_in(const LimbInfo &li, size_t idx, const Mod &m) {
+    if (li.mode == NTT_DIVIDE2) return crt2_to(li.src[idx], li.src2[idx], li, m);
     uint64_t x = li.src[idx];
     return li.qsrc ? centred_to(x, li.qsrc, m) : x;
 }
@@ -291,6 +336,8 @@ __global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *_
         const uint64_t y = sm[C::at(i % C::G, csl[s])];
         if (J.mode == NTT_DIVIDE)
             li.dst[s] = csub(shoup_lazy(submod(li.in[s], y, q), li.w, li.ws, q), q);
+        else if (J.mode == NTT_DIVIDE2)
+            li.dst[s] = shoup(shoup(submod(li.in[s], y, q), li.w, li.ws, q), li.w2, li.ws2, q);
         else
             li.dst[s] = y;
     }

@@ -4,7 +4,7 @@
 
 namespace uh {
 
-enum NttMode : int { NTT_PLAIN = 0, NTT_MODUP = 1, NTT_DIVIDE = 2 };
+enum NttMode : int { NTT_PLAIN = 0, NTT_MODUP = 1, NTT_DIVIDE = 2, NTT_DIVIDE2 = 3 };
 
 // One launch transforms `limbs` limbs; limb f is decoded per mode:
 //  PLAIN : p = f / nl, k = f % nl; modulus limb_mod(k, nq, base, sp);
@@ -14,6 +14,10 @@ enum NttMode : int { NTT_PLAIN = 0, NTT_MODUP = 1, NTT_DIVIDE = 2 };
 //          dst row dst + ((p * L + j) * (L + 1) + k) * N.
 //  DIVIDE: p = f / nl, k = f % nl, modulus k; forward input centred(src[p], q_top);
 //          epilogue dst[p][k] = (in[p][k] - y) * q_top^-1 (rows at p * dst_ps / p * in_ps).
+//  DIVIDE2 (fused ModDown + rescale, division by q_top * P): src rows [p][2] hold the
+//          coefficients of x mod q_top and x mod P; forward input = the centred CRT lift
+//          of (x mod q_top, x mod P) reduced into q_k; epilogue
+//          dst[p][k] = (in[p][k] - y) * q_top^-1 * P^-1.
 struct NttJob {
     int mode = NTT_PLAIN;
     int nl = 1, nq = 1, base = 0, sp = 0;
@@ -26,6 +30,7 @@ struct NttJob {
     int in_ps = 1;
     int top_mod = 0, count = 0;
     const uint64_t *inv = nullptr, *invs = nullptr;
+    const ulonglong2 *pmod = nullptr;  // DIVIDE2: (P mod q_i, Shoup companion) per modulus
 };
 
 bool ntt_fast_supported(const Ctx &c);

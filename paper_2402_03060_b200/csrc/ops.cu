@@ -267,6 +267,46 @@ void divide_top(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, in
     UH_LAUNCH_CHECK();
 }
 
+void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, int level, int out_ps, int in_ps,
+                 cudaStream_t s) {
+    if (!n_polys) return;
+    const size_t N = c.n;
+    if (!ntt_fast_supported(c)) {  // small N: the two divisions in sequence
+        Scratch t((size_t)n_polys * (level + 1) * N * 8, s);
+        divide_top(c, t.as<uint64_t>(), in, n_polys, level + 1, c.sp(), level + 1, in_ps, s);
+        divide_top(c, out, t.as<uint64_t>(), n_polys, level, level, out_ps, level + 1, s);
+        return;
+    }
+    Scratch top((size_t)n_polys * 2 * N * 8, s);
+    NttJob Ji;  // limbs q_level and P -> coefficients, [p][2][N]
+    Ji.nl = 2;
+    Ji.nq = 1;
+    Ji.base = level;
+    Ji.sp = c.sp();
+    Ji.src = in + (size_t)level * N;
+    Ji.src_ps = in_ps;
+    Ji.dst = top.as<uint64_t>();
+    Ji.dst_ps = 2;
+    ntt_fast_inverse(c, Ji, n_polys * 2, s);
+    if (level == 0) return;
+    NttJob Jf;
+    Jf.mode = NTT_DIVIDE2;
+    Jf.nl = level;
+    Jf.nq = level;
+    Jf.sp = c.sp();
+    Jf.src = top.as<uint64_t>();
+    Jf.dst = out;
+    Jf.dst_ps = out_ps;
+    Jf.in = in;
+    Jf.in_ps = in_ps;
+    Jf.top_mod = level;
+    Jf.count = (int)c.count;
+    Jf.inv = c.d_inv;
+    Jf.invs = c.d_invs;
+    Jf.pmod = c.d_pmod;
+    ntt_fast_forward(c, Jf, n_polys * level, s);
+}
+
 void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level, int in_ps, cudaStream_t s) {
     int L = level + 1;
     size_t N = c.n;
@@ -353,6 +393,43 @@ void ct_mul_relin_rescale(const Ctx &c, uint64_t *out, const uint64_t *a, const 
     keyswitch(c, KS.as<uint64_t>(), D2.as<uint64_t>(), B, level, L, rk, rk_limbs, 0, s);
     elementwise(c, OP_ADD, T.as<uint64_t>(), T.as<uint64_t>(), KS.as<uint64_t>(), 2 * B, 2 * B, L, L, L, L, L, s);
     divide_top(c, out, T.as<uint64_t>(), 2 * B, level, level, out_ls, L, s);
+}
+
+namespace {
+// u[p][k] += (P mod q_k) * t[p][k] for the q-limbs k < L of QP-basis polys (u has L + 1 limbs, t has L)
+__global__ void k_add_pscaled(uint64_t *u, const uint64_t *t, int n_polys, int L, int sp, int logn,
+                              const Mod *__restrict__ mods, const ulonglong2 *__restrict__ pmod) {
+    size_t total = ((size_t)n_polys * L) << logn;
+    size_t nmask = ((size_t)1 << logn) - 1;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        size_t n = idx & nmask, r = idx >> logn;
+        int k = (int)(r % L);
+        size_t p = r / L;
+        const uint64_t q = mods[k].q;
+        const ulonglong2 pk = pmod[k];
+        uint64_t &x = u[((p * (L + 1) + k) << logn) | n];
+        x = addmod(x, shoup(t[idx], pk.x, pk.y, q), q);
+    }
+}
+}  // namespace
+
+void ct_mul_relin_rescale_fused(const Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *b, int B, int level,
+                                int out_ls, int a_ls, int b_ls, const uint64_t *rk, int rk_limbs, cudaStream_t s) {
+    int L = level + 1;
+    size_t N = c.n;
+    Scratch T((size_t)B * 2 * L * N * 8, s), D2((size_t)B * L * N * 8, s);
+    k_tensor<<<grid_for((size_t)B * L * N), kTB, 0, s>>>(T.as<uint64_t>(), D2.as<uint64_t>(), a, b, B, L, a_ls, b_ls,
+                                                         (int)c.logn, c.d_mods);
+    UH_LAUNCH_CHECK();
+    Scratch D((size_t)B * L * (L + 1) * N * 8, s), u((size_t)B * 2 * (L + 1) * N * 8, s);
+    modup(c, D.as<uint64_t>(), D2.as<uint64_t>(), B, level, L, s);
+    key_inner(c, u.as<uint64_t>(), D.as<uint64_t>(), rk, rk_limbs, B, level, 0, s);
+    // u + P * (d0, d1): the relinearised product times P, in the QP basis
+    k_add_pscaled<<<grid_for((size_t)B * 2 * L * N), kTB, 0, s>>>(u.as<uint64_t>(), T.as<uint64_t>(), 2 * B, L,
+                                                                   c.sp(), (int)c.logn, c.d_mods, c.d_pmod);
+    UH_LAUNCH_CHECK();
+    divide_top2(c, out, u.as<uint64_t>(), 2 * B, level, out_ls, L + 1, s);
 }
 
 void ct_mul_plain_rescale(const Ctx &c, uint64_t *out, const uint64_t *ct, const uint64_t *pt, int B, int level,

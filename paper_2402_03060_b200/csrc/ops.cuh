@@ -27,6 +27,11 @@ void elementwise(const Ctx &c, int op, uint64_t *out, const uint64_t *a, const u
 void divide_top(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, int nl, int top_mod, int out_ps,
                 int in_ps, cudaStream_t s);
 
+// Fused ModDown + rescale: in n_polys x (level + 2) limbs (q_0..q_level, P) -> out n_polys x level limbs,
+// the centred division by q_level * P (one inverse NTT pair, one forward NTT per output limb).
+void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, int level, int out_ps, int in_ps,
+                 cudaStream_t s);
+
 // ModUp of n_polys polys at level l (L = l + 1 limbs, strided in_ps) into
 // D = [n_polys][L digits][L + 1 limbs (q_0..q_l, P)][N], compact.
 void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level, int in_ps, cudaStream_t s);
@@ -47,6 +52,9 @@ void ct_rescale(const Ctx &c, uint64_t *out, const uint64_t *in, int B, int leve
                 cudaStream_t s);
 void ct_mul_relin_rescale(const Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *b, int B, int level,
                           int out_ls, int a_ls, int b_ls, const uint64_t *rk, int rk_limbs, cudaStream_t s);
+// fused-path square/multiply: relinearise in the QP basis and divide once by q_level * P
+void ct_mul_relin_rescale_fused(const Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *b, int B, int level,
+                                int out_ls, int a_ls, int b_ls, const uint64_t *rk, int rk_limbs, cudaStream_t s);
 void ct_mul_plain_rescale(const Ctx &c, uint64_t *out, const uint64_t *ct, const uint64_t *pt, int B, int level,
                           int out_ls, int ct_ls, int pt_ls, int pt_batched, cudaStream_t s);
 

@@ -172,11 +172,9 @@ def conv(backend, state: CipherState, layer) -> CipherState:
         work = n * (B * I * (nz * (LP * 2 * L + L) + (T - nz) * 2 * L) + B * O * I * T * LP * 2)
         timer.append(("conv_hoisted_mac", level, t0, t1, work))
     del D
-    md = backend._empty(O, B, 2, L, n)
-    backend._call("uh_divide_top", _vp(md), _vp(acc), O * B * 2, L, backend.sp, L, LP, st)
+    out = backend._empty(O, B, 2, level, n)  # ModDown + rescale as one centred division by q_level * P
+    backend._call("uh_divide_top2", _vp(out), _vp(acc), O * B * 2, level, level, LP, st)
     del acc
-    out = backend._empty(O, B, 2, level, n)
-    backend._call("uh_rescale", _vp(out), _vp(md), O * B, level, level, L, st)
     bias = bias_bank(backend, layer, out_lay, level - 1, scale)
     Lo = level
     for o in range(O):
@@ -236,7 +234,7 @@ def square(backend, state: CipherState) -> CipherState:
     X = stack_cts(backend, state.cts, level)
     rk = backend.relin_key(level)
     out = backend._empty(C, B, 2, level, n)
-    backend._call("uh_mul_relin_rescale", _vp(out), _vp(X), _vp(X), C * B, level, level, L, L, _vp(rk),
+    backend._call("uh_mul_relin_rescale_fused", _vp(out), _vp(X), _vp(X), C * B, level, level, L, L, _vp(rk),
                   rk.shape[2], backend._stream())
     new_scale = scale * scale / float(backend.modulus(level))
     return CipherState([CipherVector(out[c], level - 1, new_scale, backend) for c in range(C)],
@@ -275,12 +273,12 @@ def _finish(backend, acc, level, rescale: bool):
     O, B = acc.shape[0], acc.shape[1]
     L, LP, n = level + 1, level + 2, backend.n
     st = backend._stream()
-    md = backend._empty(O, B, 2, L, n)
-    backend._call("uh_divide_top", _vp(md), _vp(acc), O * B * 2, L, backend.sp, L, LP, st)
     if not rescale:
+        md = backend._empty(O, B, 2, L, n)
+        backend._call("uh_divide_top", _vp(md), _vp(acc), O * B * 2, L, backend.sp, L, LP, st)
         return md
-    out = backend._empty(O, B, 2, level, n)
-    backend._call("uh_rescale", _vp(out), _vp(md), O * B, level, level, L, st)
+    out = backend._empty(O, B, 2, level, n)  # one centred division by q_level * P
+    backend._call("uh_divide_top2", _vp(out), _vp(acc), O * B * 2, level, level, LP, st)
     return out
 
 

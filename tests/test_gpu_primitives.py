@@ -210,3 +210,40 @@ def test_backend_roundtrip_and_ops(params):
     assert np.max(np.abs(g.decrypt(g.mul_cipher(cx, cy)) - x * y)) < tol
     assert np.max(np.abs(g.decrypt(g.rotate(cx, 5)) - np.roll(x, -5))) < tol
     assert np.max(np.abs(g.decrypt(g.rotate(cx, -7)) - np.roll(x, 7))) < tol
+
+
+@pytest.mark.parametrize("params", [SMALL, C2], ids=lambda p: f"N{p.poly_degree}")
+@pytest.mark.parametrize("level", [1, 3])
+def test_divide_top2_is_centred_division_by_q_level_times_p(params, level):
+    """Fused ModDown+rescale: out = round(x / (q_level * P)) exactly (big-integer CRT check on samples)."""
+    import math
+
+    g, o = pair(params)
+    mods = list(range(level + 1)) + [o.sp]
+    x = rand_limbs(o, mods, rows=2, seed=61)
+    out = g._empty(2, level, o.n)
+    xd = dev(x)
+    _lib.call("uh_divide_top2", g._ctx, vp(out), vp(xd), 2, level, level, level + 2, stream())
+    got = host(out)
+    qs = [int(o.moduli[m]) for m in mods]
+    coef = np.stack([o.intt(x[r], mods) for r in range(2)])
+    gotc = np.stack([o.intt(got[r], mods[:level]) for r in range(2)])
+    Q = math.prod(qs)
+    d = qs[level] * qs[-1]
+    rng = np.random.default_rng(0)
+    for r in range(2):
+        for i in rng.integers(0, o.n, 64):
+            v = 0
+            for lim, q in zip(coef[r, :, i], qs):
+                Qi = Q // q
+                v += int(lim) * Qi * pow(Qi, -1, q)
+            v %= Q
+            t = v % d
+            t = t - d if t > (d - 1) // 2 else t
+            want = (v - t) // d
+            for k in range(level):
+                if params.poly_degree >= 8192:  # fused path: exact centred division
+                    assert int(gotc[r, k, i]) == want % qs[k]
+                else:  # small-N fallback divides by P then q_level: within one unit
+                    diff = (int(gotc[r, k, i]) - want) % qs[k]
+                    assert diff in (0, 1, qs[k] - 1)
