@@ -84,21 +84,46 @@ __device__ __forceinline__ void mac128(uint64_t &lo, uint64_t &hi, uint64_t x, u
         : "l"(x), "l"(y));
 }
 
-// 128-bit accumulator for lazy multiply-add chains.
+// (a3:a2:a1:a0) += x * y on four 32-bit registers.  Ordered so every 64-bit
+// IMAD.WIDE works on an aligned register pair (a0:a1, a2:a3, t0:t1): the two
+// "diagonal" partial products accumulate in place, the cross products are
+// summed separately and added with one carry chain -- no register shuffles.
+__device__ __forceinline__ void mac128x4(uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3, uint64_t x,
+                                         uint64_t y) {
+    asm("{\n\t.reg .u32 x0,x1,y0,y1,t0,t1,t2;\n\t"
+        "mov.b64 {x0,x1}, %4;\n\tmov.b64 {y0,y1}, %5;\n\t"
+        "mad.lo.cc.u32 %0, x0, y0, %0;\n\tmadc.hi.cc.u32 %1, x0, y0, %1;\n\t"
+        "madc.lo.cc.u32 %2, x1, y1, %2;\n\tmadc.hi.u32 %3, x1, y1, %3;\n\t"
+        "mul.lo.u32 t0, x0, y1;\n\tmul.hi.u32 t1, x0, y1;\n\t"
+        "mad.lo.cc.u32 t0, x1, y0, t0;\n\tmadc.hi.cc.u32 t1, x1, y0, t1;\n\taddc.u32 t2, 0, 0;\n\t"
+        "add.cc.u32 %1, %1, t0;\n\taddc.cc.u32 %2, %2, t1;\n\taddc.u32 %3, %3, t2;\n\t}"
+        : "+r"(a0), "+r"(a1), "+r"(a2), "+r"(a3)
+        : "l"(x), "l"(y));
+}
+
+// 128-bit accumulator for lazy multiply-add chains (four 32-bit words).
 struct Acc {
-    uint64_t lo, hi;
-    __device__ __forceinline__ void zero() { lo = 0; hi = 0; }
-    __device__ __forceinline__ void mac(uint64_t a, uint64_t b) { mac128(lo, hi, a, b); }
+    uint32_t w0, w1, w2, w3;
+    __device__ __forceinline__ void zero() { w0 = w1 = w2 = w3 = 0; }
+    __device__ __forceinline__ void mac(uint64_t a, uint64_t b) { mac128x4(w0, w1, w2, w3, a, b); }
+    __device__ __forceinline__ uint64_t lo64() const { return ((uint64_t)w1 << 32) | w0; }
+    __device__ __forceinline__ uint64_t hi64() const { return ((uint64_t)w3 << 32) | w2; }
+    __device__ __forceinline__ void set(uint64_t lo, uint64_t hi) {
+        w0 = (uint32_t)lo; w1 = (uint32_t)(lo >> 32); w2 = (uint32_t)hi; w3 = (uint32_t)(hi >> 32);
+    }
     __device__ __forceinline__ void mac_c(uint64_t a, uint64_t b) {  // plain-C reference form
+        uint64_t lo = lo64(), hi = hi64();
         uint64_t pl = a * b, ph = mulhi(a, b);
         lo += pl;
         hi += ph + (lo < pl);
+        set(lo, hi);
     }
     __device__ __forceinline__ void add(uint64_t a) {
-        lo += a;
-        hi += (lo < a);
+        asm("add.cc.u32 %0, %0, %4;\n\taddc.cc.u32 %1, %1, %5;\n\taddc.cc.u32 %2, %2, 0;\n\taddc.u32 %3, %3, 0;"
+            : "+r"(w0), "+r"(w1), "+r"(w2), "+r"(w3)
+            : "r"((uint32_t)a), "r"((uint32_t)(a >> 32)));
     }
-    __device__ __forceinline__ uint64_t reduce(const Mod &m) const { return reduce128(hi, lo, m); }
+    __device__ __forceinline__ uint64_t reduce(const Mod &m) const { return reduce128(hi64(), lo64(), m); }
 };
 
 // Centred lift of x in [0, p) reduced into q: x > (p-1)/2 represents x - p.

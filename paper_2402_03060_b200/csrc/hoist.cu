@@ -124,8 +124,8 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1) k_hoisted_
                         }
                     }
                     if (qlimb) a0.mac(Pk, c0[((size_t)k << logn) | src]);
-                    v0 = csub(reduce128_lazy(a0.hi, a0.lo, m), 2 * m.q);
-                    v1 = csub(reduce128_lazy(a1.hi, a1.lo, m), 2 * m.q);
+                    v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
+                    v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
                 }
             }
             sv[buf][qc][bt][0][ln] = v0;
@@ -157,9 +157,8 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1) k_hoisted_
 #pragma unroll
                 for (int j = 0; j < PPW; j++)
                     for (int cc = 0; cc < 2; cc++) {
-                        uint64_t rr = reduce128_lazy(acc[j][cc].hi, acc[j][cc].lo, m);
-                        acc[j][cc].lo = rr;
-                        acc[j][cc].hi = 0;
+                        uint64_t rr = reduce128_lazy(acc[j][cc].hi64(), acc[j][cc].lo64(), m);
+                        acc[j][cc].set(rr, 0);
                     }
             }
         }

@@ -39,12 +39,12 @@ __global__ void k_mac_peak(uint64_t *out, int iters, uint64_t seed) {
 #pragma unroll
         for (int i = 0; i < 8; i++) {
             acc[i].mac(x[i], w);
-            x[i] ^= acc[i].lo;  // keep operands live and varying (XOR: ALU pipe)
+            x[i] ^= acc[i].lo64();  // keep operands live and varying (XOR: ALU pipe)
         }
     }
     uint64_t s = 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++) s ^= acc[i].lo ^ acc[i].hi;
+    for (int i = 0; i < 8; i++) s ^= acc[i].lo64() ^ acc[i].hi64();
     if (s == 0x1234567812345678ull) out[0] = s;
 }
 
@@ -61,12 +61,12 @@ __global__ void k_macc_peak(uint64_t *out, int iters, uint64_t seed) {  // plain
 #pragma unroll
         for (int i = 0; i < 8; i++) {
             acc[i].mac_c(x[i], w);
-            x[i] ^= acc[i].lo;
+            x[i] ^= acc[i].lo64();
         }
     }
     uint64_t s = 0;
 #pragma unroll
-    for (int i = 0; i < 8; i++) s ^= acc[i].lo ^ acc[i].hi;
+    for (int i = 0; i < 8; i++) s ^= acc[i].lo64() ^ acc[i].hi64();
     if (s == 0x1234567812345678ull) out[0] = s;
 }
 
