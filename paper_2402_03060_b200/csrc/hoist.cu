@@ -42,30 +42,39 @@ __device__ __forceinline__ uint64_t reduce128_lazy(uint64_t hi, uint64_t lo, con
 
 constexpr int kMaxL = 12;  // phase-A digit loop fully unrolled (predicated) up to this many limbs
 
-// 8-warp CTAs are capped at 64 registers (4 CTAs / SM), 24-warp CTAs at 85 (1 CTA / SM)
+// 8-warp CTAs are capped at 64 registers (4 CTAs / SM), 24-warp CTAs at 85 (1 CTA / SM).
+// All element offsets are 32-bit (the host checks every operand has < 2^32 elements).
+constexpr int kMaxTerms = 512;  // per-term metadata staged in shared memory
+
 template <int PPW, int W>
-__global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1) k_hoisted_mac(uint64_t *__restrict__ acc_out,
-                                                                      const uint64_t *__restrict__ X,
-                                                    int xls, const uint64_t *__restrict__ D,
-                                                    const uint64_t *__restrict__ masks,
-                                                    const uint64_t *const *__restrict__ keys,
-                                                    const int32_t *__restrict__ key_limbs,
-                                                    const int32_t *__restrict__ shifts, int B, int I, int T, int O,
-                                                    int diag, int L, int sp, int logn, const Mod *__restrict__ mods) {
+__global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
+    k_hoisted_mac(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
+                  const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
+                  const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
+                  const int32_t *__restrict__ shifts, int B, int I, int T, int O, int diag, int L, int sp, int logn,
+                  const Mod *__restrict__ mods) {
     __shared__ uint64_t sv[2][kTChunk][kTBatch][2][32];
+    __shared__ const uint64_t *s_key[kMaxTerms];
+    __shared__ uint32_t s_shift[kMaxTerms];
+    __shared__ uint32_t s_kstride[kMaxTerms];  // key limbs << logn: one key component
     const int LP = L + 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b0 = blockIdx.x * kTBatch;
     const uint32_t n = blockIdx.y * 32 + lane;
     const int k = blockIdx.z;
-    const size_t N = (size_t)1 << logn;
-    const uint32_t half = (uint32_t)(N >> 1);
+    const uint32_t N = 1u << logn, half = N >> 1;
     const Mod m = mods[limb_mod(k, L, 0, sp)];
     const bool qlimb = k < L;
     const uint64_t P = mods[sp].q;
     const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
     const int Q = diag ? I : I * T;
     const int npairs = O * kTBatch;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        s_key[t] = keys[t];
+        s_shift[t] = (uint32_t)shifts[t];
+        s_kstride[t] = (uint32_t)key_limbs[t] << logn;
+    }
+    __syncthreads();
 
     Acc acc[PPW][2];
 #pragma unroll
@@ -75,17 +84,20 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1) k_hoisted_
     }
     int since_fold = 0;
     int buf = 0;
-    constexpr int ITEMS = kTChunk * kTBatch / W;  // phase-A items per thread (2 or 3)
+    constexpr int ITEMS = kTChunk * kTBatch / W;  // phase-A items per thread (1, 2 or 3)
     static_assert(ITEMS * W == kTChunk * kTBatch, "phase-A items must tile the chunk");
     const int o_w = (warp * PPW) / kTBatch;  // every pair of this warp has the same output
     const bool warp_active = warp * PPW < npairs;
+    const uint32_t dstride = (uint32_t)LP << logn;  // between digits of one D block
+    const uint32_t mask_row = ((uint32_t)k << logn) + n;
+    int i0 = 0, t0 = 0;  // (input, tap) of term q0, advanced incrementally (no runtime division)
     for (int q0 = 0; q0 < Q; q0 += kTChunk) {
         // prefetch this chunk's weight masks (consumed after the barrier, latency hidden by phase A)
         uint64_t mpre[kTChunk];
 #pragma unroll
         for (int qc = 0; qc < kTChunk; qc++)
             mpre[qc] = (masks && warp_active && q0 + qc < Q)
-                           ? masks[((((size_t)o_w * Q + q0 + qc) * LP + k) << logn) + n]
+                           ? masks[(((uint32_t)o_w * Q + q0 + qc) * dstride) + mask_row]
                            : 0;
         // ---- phase A: rotated, key-switched inputs of this chunk into shared memory ----
 #pragma unroll
@@ -96,34 +108,43 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1) k_hoisted_
             const int q = q0 + qc, b = b0 + bt;
             uint64_t v0 = 0, v1 = 0;
             if (q < Q && b < B) {
-                const int i = diag ? q : q / T, t = diag ? q : q % T;
+                int i, t;
+                if (diag) {
+                    i = t = q;
+                } else {
+                    i = i0;
+                    t = t0 + qc;
+                    while (t >= T) {
+                        t -= T;
+                        i++;
+                    }
+                }
                 const uint32_t nn = blockIdx.y * 32 + ln;
-                const uint64_t *c0 = X + (((size_t)(i * B + b) * 2 * xls) << logn);
-                const uint32_t r = (uint32_t)shifts[t];
+                const uint32_t ib = (uint32_t)(i * B + b);
+                const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
+                const uint32_t r = s_shift[t];
                 if (r == 0) {
                     if (qlimb) {
-                        v0 = mulmod(Pk, c0[((size_t)k << logn) | nn], m);
-                        v1 = mulmod(Pk, c0[((size_t)(xls + k) << logn) | nn], m);
+                        v0 = mulmod(Pk, c0[nn], m);
+                        v1 = mulmod(Pk, c0[((uint32_t)xls << logn) + nn], m);
                     }
                 } else {
-                    const size_t src = rot_index(nn, half, r);
-                    const uint64_t *Di = D + (((size_t)(i * B + b) * L * LP + k) << logn);
-                    const uint64_t *key = keys[t];
-                    const int kl = key_limbs[t], kk = qlimb ? k : kl - 1;
-                    const uint64_t *k0 = key + (((size_t)kk) << logn) + nn;
-                    const size_t kstride = (size_t)kl << logn;  // comp stride; digit stride = 2 * kstride
+                    const uint32_t src = rot_index(nn, half, r);
+                    const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
+                    const uint32_t ks = s_kstride[t];
+                    const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + nn;
                     Acc a0, a1;
                     a0.zero();
                     a1.zero();
 #pragma unroll
                     for (int j = 0; j < kMaxL; j++) {  // fully unrolled: all digit/key loads in flight
                         if (j < L) {
-                            const uint64_t d = Di[(((size_t)j * LP) << logn) + src];
-                            a0.mac(d, k0[(2 * j) * kstride]);
-                            a1.mac(d, k0[(2 * j + 1) * kstride]);
+                            const uint64_t d = Di[j * dstride];
+                            a0.mac(d, k0[(2 * j) * ks]);
+                            a1.mac(d, k0[(2 * j + 1) * ks]);
                         }
                     }
-                    if (qlimb) a0.mac(Pk, c0[((size_t)k << logn) | src]);
+                    if (qlimb) a0.mac(Pk, c0[src]);
                     v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
                     v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
                 }
@@ -163,16 +184,21 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1) k_hoisted_
             }
         }
         buf ^= 1;  // the other buffer is free: every thread passed the barrier after using it
+        t0 += kTChunk;
+        while (t0 >= T) {
+            t0 -= T;
+            i0++;
+        }
     }
 #pragma unroll
     for (int j = 0; j < PPW; j++) {
-        const int p = warp * PPW + j;  // a warp's pairs share one output -> one mask load per term
+        const int p = warp * PPW + j;
         if (p < npairs) {
             const int o = p / kTBatch, b = b0 + p % kTBatch;
             if (b < B) {
-                uint64_t *dst = acc_out + (((((size_t)o * B + b) * 2) * LP + k) << logn) + n;
+                uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
                 dst[0] = acc[j][0].reduce(m);
-                dst[(size_t)LP << logn] = acc[j][1].reduce(m);
+                dst[dstride] = acc[j][1].reduce(m);
             }
         }
     }
@@ -185,6 +211,11 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
                  int O, int diag, int level, cudaStream_t s) {
     const int L = level + 1;
     if (L > kMaxL) throw std::invalid_argument("hoisted kernel supports up to 12 live limbs");
+    if (T > kMaxTerms) throw std::invalid_argument("hoisted kernel supports up to 512 taps");
+    const double lim = 4294967295.0;  // 32-bit element offsets inside the kernel
+    if ((double)I * B * 2 * xls * c.n > lim || (double)I * B * L * (L + 1) * c.n > lim ||
+        (double)O * B * 2 * (L + 1) * c.n > lim || (double)O * (diag ? I : I * T) * (L + 1) * c.n > lim)
+        throw std::invalid_argument("hoisted kernel operand exceeds 2^32 elements: split the batch");
     const int pairs = O * kTBatch;
     dim3 grid((B + kTBatch - 1) / kTBatch, (unsigned)(c.n / 32), L + 1);
     if (c.n < 32) throw std::invalid_argument("hoisted kernels need N >= 32");
