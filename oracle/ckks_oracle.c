@@ -60,6 +60,12 @@ static uint64_t powmod(uint64_t b, uint64_t e, uint64_t q) {
     return r;
 }
 static uint64_t invmod(uint64_t a, uint64_t q) { return powmod(a, q - 2, q); }
+/* x * w mod q via Shoup's precomputed quotient ws = floor(w * 2^64 / q); exact, canonical output */
+static inline uint64_t shoupmul(uint64_t x, uint64_t w, uint64_t ws, uint64_t q) {
+    uint64_t qh = (uint64_t)(((u128)x * ws) >> 64);
+    uint64_t r = x * w - qh * q;
+    return r >= q ? r - q : r;
+}
 
 /* signed value -> residue mod q */
 static inline uint64_t from_signed(int64_t v, uint64_t q) {
@@ -91,6 +97,8 @@ typedef struct {
     uint64_t *q;        /* [count] */
     uint64_t *psi_rev;  /* [count][n]  psi^brv(i)        */
     uint64_t *ipsi_rev; /* [count][n]  psi^-brv(i)       */
+    uint64_t *psi_sh;   /* [count][n]  Shoup companions floor(w * 2^64 / q) */
+    uint64_t *ipsi_sh;
     uint64_t *n_inv;    /* [count]                        */
     uint64_t *psi;      /* [count]                        */
     int32_t *slot_of_brv; /* [n] */
@@ -113,6 +121,8 @@ OR_API or_ctx *or_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi
     c->n_inv = (uint64_t *)malloc(sizeof(uint64_t) * count);
     c->psi_rev = (uint64_t *)malloc(sizeof(uint64_t) * count * n);
     c->ipsi_rev = (uint64_t *)malloc(sizeof(uint64_t) * count * n);
+    c->psi_sh = (uint64_t *)malloc(sizeof(uint64_t) * count * n);
+    c->ipsi_sh = (uint64_t *)malloc(sizeof(uint64_t) * count * n);
     c->slot_of_brv = (int32_t *)malloc(sizeof(int32_t) * n);
     memcpy(c->slot_of_brv, slot_of_brv, sizeof(int32_t) * n);
     for (uint32_t m = 0; m < count; m++) {
@@ -125,6 +135,8 @@ OR_API or_ctx *or_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi
             uint32_t e = brv(i, c->logn);
             c->psi_rev[(size_t)m * n + i] = powmod(psi[m], e, q);
             c->ipsi_rev[(size_t)m * n + i] = powmod(ip, e, q);
+            c->psi_sh[(size_t)m * n + i] = (uint64_t)(((u128)c->psi_rev[(size_t)m * n + i] << 64) / q);
+            c->ipsi_sh[(size_t)m * n + i] = (uint64_t)(((u128)c->ipsi_rev[(size_t)m * n + i] << 64) / q);
         }
     }
     return c;
@@ -133,6 +145,7 @@ OR_API or_ctx *or_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi
 OR_API void or_destroy(or_ctx *c) {
     if (!c) return;
     free(c->q); free(c->psi); free(c->n_inv); free(c->psi_rev); free(c->ipsi_rev);
+    free(c->psi_sh); free(c->ipsi_sh);
     free(c->slot_of_brv); free(c);
 }
 
@@ -141,14 +154,14 @@ OR_API void or_destroy(or_ctx *c) {
 OR_API void or_ntt(const or_ctx *c, uint32_t m, uint64_t *a) {
     const uint32_t n = c->n;
     const uint64_t q = c->q[m];
-    const uint64_t *w = c->psi_rev + (size_t)m * n;
+    const uint64_t *w = c->psi_rev + (size_t)m * n, *ws = c->psi_sh + (size_t)m * n;
     uint64_t *tmp = (uint64_t *)malloc(sizeof(uint64_t) * n);
     memcpy(tmp, a, sizeof(uint64_t) * n);
     for (uint32_t len = 1, t = n / 2; len < n; len <<= 1, t >>= 1) {
         for (uint32_t i = 0; i < len; i++) {
-            uint64_t wi = w[len + i];
+            uint64_t wi = w[len + i], wsi = ws[len + i];
             for (uint32_t j = 2 * i * t; j < 2 * i * t + t; j++) {
-                uint64_t u = tmp[j], v = mulmod(tmp[j + t], wi, q);
+                uint64_t u = tmp[j], v = shoupmul(tmp[j + t], wi, wsi, q);
                 tmp[j] = addmod(u, v, q);
                 tmp[j + t] = submod(u, v, q);
             }
@@ -162,16 +175,16 @@ OR_API void or_ntt(const or_ctx *c, uint32_t m, uint64_t *a) {
 OR_API void or_intt(const or_ctx *c, uint32_t m, uint64_t *a) {
     const uint32_t n = c->n;
     const uint64_t q = c->q[m];
-    const uint64_t *w = c->ipsi_rev + (size_t)m * n;
+    const uint64_t *w = c->ipsi_rev + (size_t)m * n, *ws = c->ipsi_sh + (size_t)m * n;
     uint64_t *tmp = (uint64_t *)malloc(sizeof(uint64_t) * n);
     for (uint32_t k = 0; k < n; k++) tmp[k] = a[c->slot_of_brv[k]];
     for (uint32_t len = n / 2, t = 1; len >= 1; len >>= 1, t <<= 1) {
         for (uint32_t i = 0; i < len; i++) {
-            uint64_t wi = w[len + i];
+            uint64_t wi = w[len + i], wsi = ws[len + i];
             for (uint32_t j = 2 * i * t; j < 2 * i * t + t; j++) {
                 uint64_t u = tmp[j], v = tmp[j + t];
                 tmp[j] = addmod(u, v, q);
-                tmp[j + t] = mulmod(submod(u, v, q), wi, q);
+                tmp[j + t] = shoupmul(submod(u, v, q), wi, wsi, q);
             }
         }
         if (len == 1) break;
@@ -332,10 +345,10 @@ OR_API void or_key_inner(const or_ctx *c, uint64_t *out, const uint64_t *D, cons
                 u128 acc = 0;
                 for (uint32_t j = 0; j < L; j++) {
                     acc += (u128)D[((size_t)j * LP + k) * n + i] *
-                           key[(((size_t)j * 2 + comp) * key_limbs + kk) * n + i];
-                    acc %= q;
+                           key[(((size_t)j * 2 + comp) * key_limbs + kk) * n + i];  /* < 2^124 per 16 terms */
+                    if ((j & 15) == 15) acc %= q;
                 }
-                dst[i] = (uint64_t)acc;
+                dst[i] = (uint64_t)(acc % q);
             }
         }
     }

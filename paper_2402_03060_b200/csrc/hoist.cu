@@ -86,19 +86,24 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
     int buf = 0;
     constexpr int ITEMS = kTChunk * kTBatch / W;  // phase-A items per thread (1, 2 or 3)
     static_assert(ITEMS * W == kTChunk * kTBatch, "phase-A items must tile the chunk");
-    const int o_w = (warp * PPW) / kTBatch;  // every pair of this warp has the same output
-    const bool warp_active = warp * PPW < npairs;
+    // a warp's PPW (output, ciphertext) pairs form a PO x PB block: each shared-memory v is
+    // loaded once for PO outputs and each mask once for PB ciphertexts
+    constexpr int PB = PPW == 4 ? 2 : PPW, PO = PPW / PB, WB = kTBatch / PB;
+    const int o_a = (warp / WB) * PO, b_a = (warp % WB) * PB;
+    const bool warp_active = o_a < O && warp * PPW < npairs;
     const uint32_t dstride = (uint32_t)LP << logn;  // between digits of one D block
     const uint32_t mask_row = ((uint32_t)k << logn) + n;
     int i0 = 0, t0 = 0;  // (input, tap) of term q0, advanced incrementally (no runtime division)
     for (int q0 = 0; q0 < Q; q0 += kTChunk) {
         // prefetch this chunk's weight masks (consumed after the barrier, latency hidden by phase A)
-        uint64_t mpre[kTChunk];
+        uint64_t mpre[kTChunk][PO];
 #pragma unroll
         for (int qc = 0; qc < kTChunk; qc++)
-            mpre[qc] = (masks && warp_active && q0 + qc < Q)
-                           ? masks[(((uint32_t)o_w * Q + q0 + qc) * dstride) + mask_row]
-                           : 0;
+#pragma unroll
+            for (int d = 0; d < PO; d++)
+                mpre[qc][d] = (masks && warp_active && o_a + d < O && q0 + qc < Q)
+                                  ? masks[(((uint32_t)(o_a + d) * Q + q0 + qc) * dstride) + mask_row]
+                                  : 0;
         // ---- phase A: rotated, key-switched inputs of this chunk into shared memory ----
 #pragma unroll
         for (int ii = 0; ii < ITEMS; ii++) {
@@ -158,18 +163,21 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
 #pragma unroll
         for (int qc = 0; qc < kTChunk; qc++) {
             if (qc >= qn) break;
+            if (warp_active) {
 #pragma unroll
-            for (int j = 0; j < PPW; j++) {
-                const int p = warp * PPW + j;
-                if (p < npairs) {
-                    const int bt = p % kTBatch;
+                for (int db = 0; db < PB; db++) {
+                    const int bt = b_a + db;
                     const uint64_t v0 = sv[buf][qc][bt][0][lane], v1 = sv[buf][qc][bt][1][lane];
-                    if (masks) {
-                        acc[j][0].mac(mpre[qc], v0);
-                        acc[j][1].mac(mpre[qc], v1);
-                    } else {
-                        acc[j][0].add(v0);
-                        acc[j][1].add(v1);
+#pragma unroll
+                    for (int d = 0; d < PO; d++) {
+                        const int j = d * PB + db;
+                        if (masks) {
+                            acc[j][0].mac(mpre[qc][d], v0);
+                            acc[j][1].mac(mpre[qc][d], v1);
+                        } else {
+                            acc[j][0].add(v0);
+                            acc[j][1].add(v1);
+                        }
                     }
                 }
             }
@@ -192,9 +200,8 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
     }
 #pragma unroll
     for (int j = 0; j < PPW; j++) {
-        const int p = warp * PPW + j;
-        if (p < npairs) {
-            const int o = p / kTBatch, b = b0 + p % kTBatch;
+        const int o = o_a + j / PB, b = b0 + b_a + j % PB;
+        if (warp_active && o < O) {
             if (b < B) {
                 uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
                 dst[0] = acc[j][0].reduce(m);

@@ -100,6 +100,67 @@ __global__ void k_mulmod_peak(uint64_t *out, int iters, uint64_t seed, Mod m) {
     if (s == 0x1234567812345678ull) out[0] = s;
 }
 
+// exact modular multiply-accumulate on the FP64 pipe for q < 2^50:
+// x*y = p + e exactly (fma), r = p - rint(p/q)*q + e exactly, sum r exactly (< 2^53)
+__device__ __forceinline__ double fmac(double acc, double x, double y, double q, double qinv) {
+    const double magic = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest integer trick
+    double p = x * y;
+    double e = fma(x, y, -p);
+    double qt = fma(p, qinv, magic) - magic;
+    double r = fma(-qt, q, p);
+    return acc + (r + e);
+}
+
+__global__ void k_fp64mac_peak(double *out, int iters, double seed, double q, double qinv) {
+    double acc[8], x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        acc[i] = 0;
+        x[i] = fmod(seed * (threadIdx.x * 8 + i + 1), q);
+    }
+    const double w = fmod(1234567.0 * (blockIdx.x + 3), q);
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            acc[i] = fmac(acc[i], x[i], w, q, qinv);
+            x[i] = acc[i] > q ? x[i] - 1.0 : x[i] + 1.0;  // keep operands varying
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s += acc[i];
+    if (s == 1.2345) out[0] = s;
+}
+
+// both pipes: half the chains on IMAD (128-bit integer MAC), half on FP64
+__global__ void k_mixed_peak(uint64_t *out, int iters, uint64_t seed, double q, double qinv) {
+    Acc acc[4];
+    uint64_t x[4];
+    double facc[4], fx[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        acc[i].zero();
+        x[i] = (seed + threadIdx.x * 8 + i) & ((1ull << 60) - 1);
+        facc[i] = 0;
+        fx[i] = (double)((seed + threadIdx.x * 4 + i) % (uint64_t)q);
+    }
+    const uint64_t w = (0x0FEDCBA987654321ull + blockIdx.x) & ((1ull << 60) - 1);
+    const double fw = 987654321.0 + blockIdx.x;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            acc[i].mac(x[i], w);
+            x[i] ^= acc[i].lo64();
+            facc[i] = fmac(facc[i], fx[i], fw, q, qinv);
+            fx[i] = facc[i] > q ? fx[i] - 1.0 : fx[i] + 1.0;
+        }
+    }
+    uint64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) s ^= acc[i].lo64() ^ acc[i].hi64() ^ (uint64_t)facc[i];
+    if (s == 0x1234567812345678ull) out[0] = s;
+}
+
 template <class F> double time_ms(F &&launch) {
     cudaEvent_t a, b;
     UH_CHECK(cudaEventCreate(&a));
@@ -138,6 +199,11 @@ void bench_peaks(const Ctx &c, double *rates) {
     rates[3] = lanes * iters * 8 / (ms * 1e-3);
     ms = time_ms([&] { k_shoup_peak<<<blocks, threads>>>(out, iters, 7ull, m); });
     rates[4] = lanes * iters * 8 / (ms * 1e-3);
+    const double q40 = 1099511623297.0;  // a 40-bit NTT prime
+    ms = time_ms([&] { k_fp64mac_peak<<<blocks, threads>>>((double *)out, iters, 3.0, q40, 1.0 / q40); });
+    rates[5] = lanes * iters * 8 / (ms * 1e-3);
+    ms = time_ms([&] { k_mixed_peak<<<blocks, threads>>>(out, iters, 7ull, q40, 1.0 / q40); });
+    rates[6] = lanes * iters * 8 / (ms * 1e-3);
     UH_CHECK(cudaGetLastError());
     cudaFree(out);
 }

@@ -1,4 +1,4 @@
-"""Integer-pipe peaks of this GPU (uh_bench_peaks)."""
+"""Integer- and FP64-pipe peaks of this GPU (uh_bench_peaks)."""
 import ctypes
 import os
 import sys
@@ -10,8 +10,12 @@ from paper_2402_03060_b200 import _lib  # noqa: E402
 from paper_2402_03060_b200.he_backend import GpuBackend  # noqa: E402
 from paper_2402_03060_b200.params import HEParams  # noqa: E402
 
-be = GpuBackend(HEParams(poly_degree=1 << 12, depth=2, scale_bits=40))
-r = np.zeros(5)
-_lib.call("uh_bench_peaks", be._ctx, ctypes.c_void_p(r.ctypes.data))
-for name, v in zip(["IMAD", "MAC128 (ptx chain)", "mulmod (reduced)", "MAC128 (C form)", "Shoup lazy"], r):
-    print(f"{name:22s} {v / 1e12:8.3f} T/s")
+NAMES = ["IMAD", "MAC128 (engine, IMAD.WIDE chain)", "mulmod (reduced)", "MAC128 (plain-C form)",
+         "Shoup lazy", "FP64 exact modMAC (q<2^50)", "mixed IMAD+FP64 MAC"]
+
+if __name__ == "__main__":
+    be = GpuBackend(HEParams(poly_degree=1 << 12, depth=2, scale_bits=40))
+    r = np.zeros(8)
+    _lib.call("uh_bench_peaks", be._ctx, ctypes.c_void_p(r.ctypes.data))
+    for name, v in zip(NAMES, r):
+        print(f"{name:36s} {v / 1e12:8.3f} T/s")
