@@ -100,71 +100,82 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def cpu_baseline(n_ct=1):
-    """CPU oracle port: op-level schedule over the C oracle (OpenMP), one ciphertext."""
-    from oracle.ckks_oracle import OracleBackend
-    from paper_2402_03060_b200 import driver, planner
+class CpuPort:
+    """The CPU oracle port of the path (op-level schedule over the C oracle, OpenMP
+    over all host cores), keys generated once; one step = one ciphertext
+    (20 images) through the whole LeNet-1 schedule."""
 
-    params, m = _params(), _model()
-    plan = planner.footprint(m, params)
-    rng = np.random.default_rng(7)
-    samples = list(rng.uniform(0, 1, size=(plan.capacity, 1, 28, 28)))
-    be = OracleBackend(params)
-    # keys outside the timed region (73 Galois keys + relin key at their first-use levels)
-    sim_warm = time.perf_counter()
-    from oracle.slot_sim import SimBackend
+    def __init__(self):
+        from oracle.ckks_oracle import OracleBackend
+        from oracle.slot_sim import SimBackend
+        from paper_2402_03060_b200 import driver, planner
 
-    sim = SimBackend(params)
-    seen = {}
+        self.driver, self.planner = driver, planner
+        self.params, self.m = _params(), _model()
+        params = self.params
+        self.plan = planner.footprint(self.m, params)
+        rng = np.random.default_rng(7)
+        self.samples = list(rng.uniform(0, 1, size=(self.plan.capacity, 1, 28, 28)))
+        self.be = OracleBackend(params)
+        t0 = time.perf_counter()
+        seen = {}
 
-    class Rec(SimBackend):
-        def rotate(self, c, r):
-            rr = r % params.num_slots
-            if rr:
-                seen[rr] = max(seen.get(rr, -1), c.level)
-            return super().rotate(c, r)
+        class Rec(SimBackend):  # records which Galois / relin keys the schedule needs, at which level
+            def rotate(self, c, r):
+                rr = r % params.num_slots
+                if rr:
+                    seen[rr] = max(seen.get(rr, -1), c.level)
+                return super().rotate(c, r)
 
-        def mul_cipher(self, a, b):
-            seen["relin"] = max(seen.get("relin", -1), min(a.level, b.level))
-            return super().mul_cipher(a, b)
+            def mul_cipher(self, a, b):
+                seen["relin"] = max(seen.get("relin", -1), min(a.level, b.level))
+                return super().mul_cipher(a, b)
 
-    driver.run_inference(m, samples, params, plan=plan, backend=Rec(params))
-    for r, lev in seen.items():
-        if r == "relin":
-            be.relin_key(lev)
-        else:
-            be.galois_key(r, lev)
-    keygen_s = time.perf_counter() - sim_warm
-    t0 = time.perf_counter()
-    outs, _, _ = driver.run_inference(m, samples, params, plan=plan, backend=be)
-    dt = time.perf_counter() - t0
-    err = max(float(np.max(np.abs(o - planner.reference_infer(m, s)))) for o, s in zip(outs, samples))
-    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return {"value": plan.capacity / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"1 ciphertext ({plan.capacity} images) through the full LeNet-1 schedule, op-level, "
-                      f"N=2^15, C oracle with OpenMP; {dt:.1f} s (+{keygen_s:.1f} s keygen untimed)",
-            "max_abs_err_vs_plaintext": err}
+        driver.run_inference(self.m, self.samples, params, plan=self.plan, backend=Rec(params))
+        for r, lev in seen.items():
+            self.be.relin_key(lev) if r == "relin" else self.be.galois_key(r, lev)
+        self.keygen_s = time.perf_counter() - t0
+        self.threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+    def step(self) -> float:
+        t0 = time.perf_counter()
+        outs, _, _ = self.driver.run_inference(self.m, self.samples, self.params, plan=self.plan, backend=self.be)
+        dt = time.perf_counter() - t0
+        self.err = max(float(np.max(np.abs(o - self.planner.reference_infer(self.m, s))))
+                       for o, s in zip(outs, self.samples))
+        return dt
+
+    def describe(self, dt) -> dict:
+        cap = self.plan.capacity
+        return {"value": cap / dt, "unit": UNIT, "cores": self.threads, "kind": "port",
+                "sample": f"1 ciphertext ({cap} images) through the full LeNet-1 schedule per step, op-level, "
+                          f"N=2^15, C oracle with OpenMP on {self.threads} threads; {dt:.1f} s/step "
+                          f"(+{self.keygen_s:.1f} s keygen, untimed)",
+                "max_abs_err_vs_plaintext": self.err}
+
+
+def cpu_baseline():
+    port = CpuPort()
+    return port.describe(port.step())
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    steps, warm = args.steps, args.warmup
-    from oracle.ckks_oracle import OracleBackend  # noqa: F401  (fail early if the oracle is missing)
-
-    vals = []
-    cb = None
-    for i in range(warm + steps):
-        cb = cpu_baseline()
-        if i >= warm:
-            vals.append(cb["value"])
-    v = float(np.mean(vals)) if vals else cb["value"]
+    port = CpuPort()
+    for _ in range(args.warmup):
+        port.step()
+    times = [port.step() for _ in range(args.steps)]
+    dt = float(np.mean(times))
+    cb = port.describe(dt)
+    v = cb["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": steps, "warmup": warm, "ms_per_step": 1e3 * 20 / v, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues)", "data": "synthetic",
-            "config": _config(1, 1),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "port", "sample": cb["sample"]},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": _config(1, 1), "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference = the CPU oracle port of the RNS-CKKS path (the reference package itself is a "
+                    "float64 slot simulator without encryption; SEAL is not available)"}
     print(json.dumps(line), flush=True)
 
 

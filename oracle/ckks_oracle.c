@@ -437,3 +437,14 @@ OR_API void or_to_double_centred(const or_ctx *c, double *out, const uint64_t *i
         out[i] = x > (q - 1) / 2 ? -(double)(q - x) : (double)x;
     }
 }
+
+/* Forward / inverse NTT of L limbs (limb l modulo moduli[mods[l]]), OpenMP over limbs. */
+OR_API void or_ntt_many(const or_ctx *c, uint64_t *a, const int32_t *mods, uint32_t L, int inverse) {
+#pragma omp parallel for schedule(dynamic)
+    for (uint32_t l = 0; l < L; l++) {
+        if (inverse)
+            or_intt(c, (uint32_t)mods[l], a + (size_t)l * c->n);
+        else
+            or_ntt(c, (uint32_t)mods[l], a + (size_t)l * c->n);
+    }
+}

@@ -74,6 +74,7 @@ def lib():
             "or_ntt": (None, [vp, u32, _u64p]),
             "or_intt": (None, [vp, u32, _u64p]),
             "or_ntt_naive": (None, [vp, u32, _u64p, _u64p]),
+            "or_ntt_many": (None, [vp, _u64p, _i32p, u32, ctypes.c_int]),
             "or_add": (None, [vp, _u64p, _u64p, _u64p, _i32p, u32]),
             "or_sub": (None, [vp, _u64p, _u64p, _u64p, _i32p, u32]),
             "or_mul": (None, [vp, _u64p, _u64p, _u64p, _i32p, u32]),
@@ -172,18 +173,12 @@ class Oracle:
     # transforms
     def ntt(self, limbs: np.ndarray, mods) -> np.ndarray:
         out = np.array(limbs, dtype=np.uint64, copy=True).reshape(len(mods), self.n)
-        for l, m in enumerate(mods):
-            row = np.ascontiguousarray(out[l])
-            lib().or_ntt(self._ctx, int(m), row)
-            out[l] = row
+        lib().or_ntt_many(self._ctx, out, np.ascontiguousarray(mods, dtype=np.int32), len(mods), 0)
         return out
 
     def intt(self, limbs: np.ndarray, mods) -> np.ndarray:
         out = np.array(limbs, dtype=np.uint64, copy=True).reshape(len(mods), self.n)
-        for l, m in enumerate(mods):
-            row = np.ascontiguousarray(out[l])
-            lib().or_intt(self._ctx, int(m), row)
-            out[l] = row
+        lib().or_ntt_many(self._ctx, out, np.ascontiguousarray(mods, dtype=np.int32), len(mods), 1)
         return out
 
     def ntt_naive(self, limb: np.ndarray, m: int) -> np.ndarray:

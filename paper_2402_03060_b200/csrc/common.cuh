@@ -101,6 +101,42 @@ __device__ __forceinline__ void mac128x4(uint32_t &a0, uint32_t &a1, uint32_t &a
         : "l"(x), "l"(y));
 }
 
+// Split accumulator: A = sum x0*y0 + (x1*y1 << 64) (a0..a3) and C = sum of the
+// cross products x0*y1 + x1*y0 (c0:c1, carries counted in c2); value = A + (C << 32).
+// Every IMAD.WIDE accumulates into an aligned register pair in place (no moves).
+struct AccS {
+    uint32_t a0, a1, a2, a3, c0, c1, c2;
+    __device__ __forceinline__ void zero() { a0 = a1 = a2 = a3 = c0 = c1 = c2 = 0; }
+    __device__ __forceinline__ void mac(uint64_t x, uint64_t y) {
+        asm("{\n\t.reg .u32 x0,x1,y0,y1;\n\t"
+            "mov.b64 {x0,x1}, %7;\n\tmov.b64 {y0,y1}, %8;\n\t"
+            "mad.lo.cc.u32 %0, x0, y0, %0;\n\tmadc.hi.cc.u32 %1, x0, y0, %1;\n\t"
+            "madc.lo.cc.u32 %2, x1, y1, %2;\n\tmadc.hi.u32 %3, x1, y1, %3;\n\t"
+            "mad.lo.cc.u32 %4, x0, y1, %4;\n\tmadc.hi.cc.u32 %5, x0, y1, %5;\n\taddc.u32 %6, %6, 0;\n\t"
+            "mad.lo.cc.u32 %4, x1, y0, %4;\n\tmadc.hi.cc.u32 %5, x1, y0, %5;\n\taddc.u32 %6, %6, 0;\n\t}"
+            : "+r"(a0), "+r"(a1), "+r"(a2), "+r"(a3), "+r"(c0), "+r"(c1), "+r"(c2)
+            : "l"(x), "l"(y));
+    }
+    __device__ __forceinline__ void add(uint64_t x) {
+        asm("add.cc.u32 %0, %0, %4;\n\taddc.cc.u32 %1, %1, %5;\n\taddc.cc.u32 %2, %2, 0;\n\taddc.u32 %3, %3, 0;"
+            : "+r"(a0), "+r"(a1), "+r"(a2), "+r"(a3)
+            : "r"((uint32_t)x), "r"((uint32_t)(x >> 32)));
+    }
+    // fold C into A: (a3:a2:a1:a0) += (c2:c1:c0) << 32
+    __device__ __forceinline__ void fold() {
+        asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+            : "+r"(a1), "+r"(a2), "+r"(a3)
+            : "r"(c0), "r"(c1), "r"(c2));
+        c0 = c1 = c2 = 0;
+    }
+    __device__ __forceinline__ uint64_t lo64() { fold(); return ((uint64_t)a1 << 32) | a0; }
+    __device__ __forceinline__ uint64_t hi64() { fold(); return ((uint64_t)a3 << 32) | a2; }
+    __device__ __forceinline__ void set(uint64_t lo, uint64_t hi) {
+        a0 = (uint32_t)lo; a1 = (uint32_t)(lo >> 32); a2 = (uint32_t)hi; a3 = (uint32_t)(hi >> 32);
+        c0 = c1 = c2 = 0;
+    }
+};
+
 // 128-bit accumulator for lazy multiply-add chains (four 32-bit words).
 struct Acc {
     uint32_t w0, w1, w2, w3;

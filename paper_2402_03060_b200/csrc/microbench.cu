@@ -132,6 +132,28 @@ __global__ void k_fp64mac_peak(double *out, int iters, double seed, double q, do
     if (s == 1.2345) out[0] = s;
 }
 
+__global__ void k_macs_peak(uint64_t *out, int iters, uint64_t seed) {  // split accumulator (AccS)
+    AccS acc[8];
+    uint64_t x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        acc[i].zero();
+        x[i] = (seed + threadIdx.x * 8 + i) & ((1ull << 60) - 1);
+    }
+    const uint64_t w = (0x0FEDCBA987654321ull + blockIdx.x) & ((1ull << 60) - 1);
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            acc[i].mac(x[i], w);
+            x[i] ^= acc[i].a0;
+        }
+    }
+    uint64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s ^= acc[i].lo64() ^ acc[i].hi64();
+    if (s == 0x1234567812345678ull) out[0] = s;
+}
+
 // both pipes: half the chains on IMAD (128-bit integer MAC), half on FP64
 __global__ void k_mixed_peak(uint64_t *out, int iters, uint64_t seed, double q, double qinv) {
     Acc acc[4];
@@ -204,6 +226,8 @@ void bench_peaks(const Ctx &c, double *rates) {
     rates[5] = lanes * iters * 8 / (ms * 1e-3);
     ms = time_ms([&] { k_mixed_peak<<<blocks, threads>>>(out, iters, 7ull, q40, 1.0 / q40); });
     rates[6] = lanes * iters * 8 / (ms * 1e-3);
+    ms = time_ms([&] { k_macs_peak<<<blocks, threads>>>(out, iters, 7ull); });
+    rates[7] = lanes * iters * 8 / (ms * 1e-3);
     UH_CHECK(cudaGetLastError());
     cudaFree(out);
 }

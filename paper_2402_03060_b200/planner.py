@@ -421,6 +421,46 @@ def lenet1(seed: int = 0, w_sigma: float = 0.1, b_sigma: float = 0.01) -> ModelS
                         lambda *s: rng.normal(0.0, b_sigma, size=s))
 
 
+def config1_net(seed: int = 0) -> ModelSpec:
+    """BASELINE config 1: Conv 1->4 3x3 -> x^2 -> Flatten -> FC 2704->10 (conv w N(0,0.1^2),
+    b N(0,0.01^2), FC w N(0,0.05^2)).  Needs depth 4 under the reference's rules."""
+    rng = np.random.default_rng(seed)
+    conv = Conv2d(1, 4, 3, 1, rng.normal(0, 0.1, (4, 1, 3, 3)), rng.normal(0, 0.01, 4))
+    fc_ = FC(2704, 10, rng.normal(0, 0.05, (10, 2704)), rng.normal(0, 0.01, 10))
+    return ModelSpec("config1", 1, 28, 28, (conv, Square(), Flatten(), fc_))
+
+
+def cifar_net(seed: int = 0) -> ModelSpec:
+    """BASELINE config 4 made realisable: Conv 3->16 3x3 -> x^2 -> pool 2 ->
+    Conv 16->32 4x4 -> x^2 -> pool 2 -> Flatten -> FC 1152->10 (w N(0,0.05^2), b N(0,0.01^2)),
+    one ciphertext per input channel as in the reference's layout."""
+    rng = np.random.default_rng(seed)
+    w = lambda *s: rng.normal(0, 0.05, s)  # noqa: E731
+    b = lambda *s: rng.normal(0, 0.01, s)  # noqa: E731
+    c1 = Conv2d(3, 16, 3, 1, w(16, 3, 3, 3), b(16))
+    c2 = Conv2d(16, 32, 4, 1, w(32, 16, 4, 4), b(32))
+    f = FC(1152, 10, w(10, 1152), b(10))
+    return ModelSpec("cifar", 3, 32, 32, (c1, Square(), AvgPool2d(2), c2, Square(), AvgPool2d(2), Flatten(), f))
+
+
+def lr_model(seed: int = 0) -> ModelSpec:
+    """BASELINE config 5 (LR) on the reference layers: (1,1,784) -> Flatten -> FC 784->10, w N(0,0.05^2)."""
+    rng = np.random.default_rng(seed)
+    return ModelSpec("lr", 1, 1, 784, (Flatten(), FC(784, 10, rng.normal(0, 0.05, (10, 784)),
+                                                       rng.normal(0, 0.01, 10))))
+
+
+def svm_model(seed: int = 0, n_sv: int = 256) -> ModelSpec:
+    """BASELINE config 5 (polynomial-kernel SVM, (gamma <x, sv> + 1)^2, gamma = 1/784) on the
+    reference layers: Flatten -> FC 784->n_sv (w = gamma*sv, b = 1) -> Square -> FC n_sv->1
+    (w = dual coefficients N(0,1), b N(0,0.1^2))."""
+    rng = np.random.default_rng(seed)
+    sv = rng.uniform(0, 1, (n_sv, 784))
+    k = FC(784, n_sv, sv / 784.0, np.ones(n_sv))
+    out = FC(n_sv, 1, rng.normal(0, 1, (1, n_sv)), rng.normal(0, 0.1, 1))
+    return ModelSpec("svm", 1, 1, 784, (Flatten(), k, Square(), out))
+
+
 # -- packing (packing.py:28-126) ---------------------------------------------------------------
 
 

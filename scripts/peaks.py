@@ -11,7 +11,7 @@ from paper_2402_03060_b200.he_backend import GpuBackend  # noqa: E402
 from paper_2402_03060_b200.params import HEParams  # noqa: E402
 
 NAMES = ["IMAD", "MAC128 (engine, IMAD.WIDE chain)", "mulmod (reduced)", "MAC128 (plain-C form)",
-         "Shoup lazy", "FP64 exact modMAC (q<2^50)", "mixed IMAD+FP64 MAC"]
+         "Shoup lazy", "FP64 exact modMAC (q<2^50)", "mixed IMAD+FP64 MAC", "MAC128 split accumulator (AccS)"]
 
 if __name__ == "__main__":
     be = GpuBackend(HEParams(poly_degree=1 << 12, depth=2, scale_bits=40))
