@@ -211,6 +211,222 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined variant: the next chunk's operands (hoisted digits at the rotated
+// offsets, c0, and the Galois-key rows) are staged into shared memory with
+// cp.async while the current chunk is multiply-accumulated, so phase A reads
+// shared memory instead of waiting on L2/HBM.  Warp g of the chunk owns item
+// group (term qc = g / 8, ciphertext bt = g % 8) for both copy and compute.
+__device__ __forceinline__ void cp8(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NW> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NW)); }
+
+template <int PPW, int W>
+__global__ void __launch_bounds__(W * 32, 1)
+    k_hoisted_mac_cp(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
+                     const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
+                     const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
+                     const int32_t *__restrict__ shifts, int B, int I, int T, int O, int diag, int L, int sp,
+                     int logn, const Mod *__restrict__ mods) {
+    extern __shared__ uint64_t dyn[];
+    __shared__ uint64_t sv[2][kTChunk][kTBatch][2][32];
+    __shared__ const uint64_t *s_key[kMaxTerms];
+    __shared__ uint32_t s_shift[kMaxTerms];
+    __shared__ uint32_t s_kstride[kMaxTerms];
+    const int LP = L + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b0 = blockIdx.x * kTBatch;
+    const uint32_t n = blockIdx.y * 32 + lane;
+    const int k = blockIdx.z;
+    const uint32_t N = 1u << logn, half = N >> 1;
+    const Mod m = mods[limb_mod(k, L, 0, sp)];
+    const bool qlimb = k < L;
+    const uint64_t P = mods[sp].q;
+    const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
+    const int Q = diag ? I : I * T;
+    const int npairs = O * kTBatch;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        s_key[t] = keys[t];
+        s_shift[t] = (uint32_t)shifts[t];
+        s_kstride[t] = (uint32_t)key_limbs[t] << logn;
+    }
+    // stage layout (uint64 words): D [kTChunk][kTBatch][L][32], C [kTChunk][kTBatch][32], K [kTChunk][2L][32]
+    const int szD = kTChunk * kTBatch * L * 32, szC = kTChunk * kTBatch * 32, szK = kTChunk * 2 * L * 32;
+    const int stage = szD + szC + szK;
+    __syncthreads();
+
+    const uint32_t dstride = (uint32_t)LP << logn;
+    // (input, tap) of a term q, from the running (i0, t0) of q0
+    auto term_it = [&](int i0, int t0, int qc, int &i, int &t) {
+        if (diag) {
+            i = t = 0;  // set by caller
+        } else {
+            i = i0;
+            t = t0 + qc;
+            while (t >= T) {
+                t -= T;
+                i++;
+            }
+        }
+    };
+    auto issue = [&](int q0, int i0, int t0, int s) {
+        uint64_t *sD = dyn + s * stage, *sC = sD + szD, *sK = sC + szC;
+        for (int g = warp; g < kTChunk * kTBatch; g += W) {
+            const int qc = g / kTBatch, bt = g % kTBatch, q = q0 + qc, b = b0 + bt;
+            if (q >= Q || b >= B) continue;
+            int i, t;
+            term_it(i0, t0, qc, i, t);
+            if (diag) i = t = q;
+            const uint32_t ib = (uint32_t)(i * B + b);
+            const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
+            const uint32_t r = s_shift[t];
+            const uint32_t src = r ? rot_index(n, half, r) : n;
+            uint64_t *dD = sD + ((qc * kTBatch + bt) * L) * 32 + lane;
+            if (qlimb) cp8(sC + (qc * kTBatch + bt) * 32 + lane, c0 + src);
+            if (r == 0) {
+                if (qlimb) cp8(dD, c0 + ((uint32_t)xls << logn) + n);  // c1, unrotated
+            } else {
+                const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
+                for (int j = 0; j < L; j++) cp8(dD + j * 32, Di + j * dstride);
+            }
+        }
+        for (int row = warp; row < kTChunk * 2 * L; row += W) {
+            const int qc = row / (2 * L), jc = row % (2 * L), q = q0 + qc;
+            if (q >= Q) continue;
+            int i, t;
+            term_it(i0, t0, qc, i, t);
+            if (diag) t = q;
+            if (s_shift[t] == 0) continue;
+            const uint32_t ks = s_kstride[t];
+            const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + n;
+            cp8(sK + row * 32 + lane, k0 + jc * ks);
+        }
+    };
+
+    Acc acc[PPW][2];
+#pragma unroll
+    for (int j = 0; j < PPW; j++) {
+        acc[j][0].zero();
+        acc[j][1].zero();
+    }
+    int since_fold = 0;
+    int buf = 0;
+    constexpr int PB = PPW == 4 ? 2 : PPW, PO = PPW / PB, WB = kTBatch / PB;
+    const int o_a = (warp / WB) * PO, b_a = (warp % WB) * PB;
+    const bool warp_active = o_a < O && warp * PPW < npairs;
+    const uint32_t mask_row = ((uint32_t)k << logn) + n;
+    int i0 = 0, t0 = 0;
+    issue(0, 0, 0, 0);
+    cp_commit();
+    int st = 0;
+    for (int q0 = 0; q0 < Q; q0 += kTChunk) {
+        // next chunk's (i0, t0)
+        int i1 = i0, t1 = t0 + kTChunk;
+        while (t1 >= T) {
+            t1 -= T;
+            i1++;
+        }
+        if (q0 + kTChunk < Q) issue(q0 + kTChunk, i1, t1, st ^ 1);
+        cp_commit();
+        uint64_t mpre[kTChunk][PO];
+#pragma unroll
+        for (int qc = 0; qc < kTChunk; qc++)
+#pragma unroll
+            for (int d = 0; d < PO; d++)
+                mpre[qc][d] = (masks && warp_active && o_a + d < O && q0 + qc < Q)
+                                  ? masks[(((uint32_t)(o_a + d) * Q + q0 + qc) * dstride) + mask_row]
+                                  : 0;
+        cp_wait<1>();
+        __syncthreads();
+        // ---- phase A from shared memory ----
+        const uint64_t *sD = dyn + st * stage, *sC = sD + szD, *sK = sC + szC;
+        for (int g = warp; g < kTChunk * kTBatch; g += W) {
+            const int qc = g / kTBatch, bt = g % kTBatch, q = q0 + qc, b = b0 + bt;
+            uint64_t v0 = 0, v1 = 0;
+            if (q < Q && b < B) {
+                int i, t;
+                term_it(i0, t0, qc, i, t);
+                if (diag) t = q;
+                const uint32_t r = s_shift[t];
+                const uint64_t *dD = sD + ((qc * kTBatch + bt) * L) * 32 + lane;
+                if (r == 0) {
+                    if (qlimb) {
+                        v0 = mulmod(Pk, sC[(qc * kTBatch + bt) * 32 + lane], m);
+                        v1 = mulmod(Pk, dD[0], m);
+                    }
+                } else {
+                    const uint64_t *kK = sK + (qc * 2 * L) * 32 + lane;
+                    Acc a0, a1;
+                    a0.zero();
+                    a1.zero();
+#pragma unroll 4
+                    for (int j = 0; j < L; j++) {
+                        const uint64_t d = dD[j * 32];
+                        a0.mac(d, kK[(2 * j) * 32]);
+                        a1.mac(d, kK[(2 * j + 1) * 32]);
+                    }
+                    if (qlimb) a0.mac(Pk, sC[(qc * kTBatch + bt) * 32 + lane]);
+                    v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
+                    v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
+                }
+            }
+            sv[buf][qc][bt][0][lane] = v0;
+            sv[buf][qc][bt][1][lane] = v1;
+        }
+        __syncthreads();
+        // ---- phase B ----
+        const int qn = min(kTChunk, Q - q0);
+#pragma unroll
+        for (int qc = 0; qc < kTChunk; qc++) {
+            if (qc >= qn) break;
+            if (warp_active) {
+#pragma unroll
+                for (int db = 0; db < PB; db++) {
+                    const int bt = b_a + db;
+                    const uint64_t v0 = sv[buf][qc][bt][0][lane], v1 = sv[buf][qc][bt][1][lane];
+#pragma unroll
+                    for (int d = 0; d < PO; d++) {
+                        const int j = d * PB + db;
+                        if (masks) {
+                            acc[j][0].mac(mpre[qc][d], v0);
+                            acc[j][1].mac(mpre[qc][d], v1);
+                        } else {
+                            acc[j][0].add(v0);
+                            acc[j][1].add(v1);
+                        }
+                    }
+                }
+            }
+            if (++since_fold == kFold) {
+                since_fold = 0;
+#pragma unroll
+                for (int j = 0; j < PPW; j++)
+                    for (int cc = 0; cc < 2; cc++) {
+                        uint64_t rr = reduce128_lazy(acc[j][cc].hi64(), acc[j][cc].lo64(), m);
+                        acc[j][cc].set(rr, 0);
+                    }
+            }
+        }
+        buf ^= 1;
+        st ^= 1;
+        i0 = i1;
+        t0 = t1;
+    }
+    cp_wait<0>();
+#pragma unroll
+    for (int j = 0; j < PPW; j++) {
+        const int o = o_a + j / PB, b = b0 + b_a + j % PB;
+        if (warp_active && o < O && b < B) {
+            uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
+            dst[0] = acc[j][0].reduce(m);
+            dst[dstride] = acc[j][1].reduce(m);
+        }
+    }
+}
+
 }  // namespace
 
 void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D, const uint64_t *masks,
@@ -233,10 +449,32 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
         const char *e = getenv("UH_HOIST_CFG");
         return e && std::string(e) == "narrow";
     }();
+    // cp.async-pipelined variant: measured faster where phase A (key products over many
+    // digits) dominates -- the 24-warp, 2-pair configuration (e.g. LeNet conv1 at level 7);
+    // UH_HOIST_ASYNC=1 / 0 forces it on / off everywhere.
+    static const int async_mode = [] {
+        const char *e = getenv("UH_HOIST_ASYNC");
+        return e ? (std::string(e) == "0" ? 0 : 1) : -1;
+    }();
     auto go = [&](auto ppw_tag, auto w_tag) {
         constexpr int PP = decltype(ppw_tag)::value, WW = decltype(w_tag)::value;
-        k_hoisted_mac<PP, WW><<<grid, WW * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O,
-                                                      diag, L, c.sp(), (int)c.logn, c.d_mods);
+        const bool async = async_mode >= 0 ? async_mode == 1 : (WW == 24 && PP == 2);
+        if (async) {
+            // two cp.async stages: D [3][8][L][32] + C [3][8][32] + K [3][2L][32] words each
+            const size_t smem = 2 * (size_t)(kTChunk * kTBatch * L * 32 + kTChunk * kTBatch * 32 +
+                                             kTChunk * 2 * L * 32) * sizeof(uint64_t);
+            static size_t configured = 0;  // opt in to > 48 KB dynamic shared memory (up to 192 KB at L = 12)
+            if (smem > configured) {
+                UH_CHECK(cudaFuncSetAttribute(k_hoisted_mac_cp<PP, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem));
+                configured = smem;
+            }
+            k_hoisted_mac_cp<PP, WW><<<grid, WW * 32, smem, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B,
+                                                                 I, T, O, diag, L, c.sp(), (int)c.logn, c.d_mods);
+        } else {
+            k_hoisted_mac<PP, WW><<<grid, WW * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T,
+                                                          O, diag, L, c.sp(), (int)c.logn, c.d_mods);
+        }
     };
     using std::integral_constant;
     if (O <= 12) {
