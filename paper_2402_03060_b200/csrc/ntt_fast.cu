@@ -116,6 +116,23 @@ __device__ __forceinline__ uint64_t load_in(const LimbInfo &li, size_t idx, cons
     return li.qsrc ? centred_to(x, li.qsrc, m) : x;
 }
 
+// Compile-time load transform of pass 1: 0 plain, 1 centred lift (ModUp / ModDown / rescale),
+// 2 CRT pair (fused ModDown + rescale).  The centred lift is branch-free; the magnitude
+// needs a reduction only when the source modulus exceeds twice the target (a 60-bit
+// digit into a 40-bit limb), which is uniform per limb (`red`).
+template <int LM>
+__device__ __forceinline__ uint64_t load_t(const LimbInfo &li, size_t idx, const Mod &m, bool red) {
+    if (LM == 2) return crt2_to(li.src[idx], li.src2[idx], li, m);
+    const uint64_t x = li.src[idx];
+    if (LM == 0) return x;
+    const uint64_t p = li.qsrc;
+    const bool neg = x > ((p - 1) >> 1);
+    uint64_t v = neg ? p - x : x;
+    if (red) v = csub(barrett_lite(v, m), m.q);
+    const uint64_t nv = v ? m.q - v : 0;
+    return neg ? nv : v;
+}
+
 // Harvey CT butterfly: x, y in [0, 4q) -> [0, 4q)
 __device__ __forceinline__ void ct(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q) {
     uint64_t q2 = 2 * q;
@@ -181,7 +198,7 @@ struct P1 {
     static constexpr int GC = R1 * 32 / kThreads;  // contiguous groups per thread
 };
 
-template <int A>
+template <int A, int LM>
 __global__ void __launch_bounds__(kThreads) k_fwd_p1(NttJob J, uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ twd) {
@@ -193,13 +210,14 @@ __global__ void __launch_bounds__(kThreads) k_fwd_p1(NttJob J, uint64_t *__restr
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
     const uint64_t q = m.q;
+    const bool red = LM == 1 && ((li.qsrc - 1) >> 1) >= q;
     const ulonglong2 *T = twd + ((size_t)li.mod << logn);
 #pragma unroll
     for (int g = 0; g < C::GS; g++) {
         const int r0 = wq + 8 * g;  // < S1
         uint64_t v[C::R1];
 #pragma unroll
-        for (int x = 0; x < C::R1; x++) v[x] = load_in(li, (size_t)(r0 + C::S1 * x) * n2 + col, m);
+        for (int x = 0; x < C::R1; x++) v[x] = load_t<LM>(li, (size_t)(r0 + C::S1 * x) * n2 + col, m, red);
         fwd_strided<C::R1>(v, T, 1, 0, q);
 #pragma unroll
         for (int x = 0; x < C::R1; x++) sm[(r0 + C::S1 * x) * 32 + lane] = v[x];
@@ -394,7 +412,12 @@ template <int A, int B>
 void run_fwd(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
     Scratch tmp((size_t)limbs * c.n * 8, s);
     dim3 g1((1u << B) / 32, limbs), g2((1u << A) / P2<B>::G, limbs);
-    k_fwd_p1<A><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2);
+    if (J.mode == NTT_PLAIN)
+        k_fwd_p1<A, 0><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2);
+    else if (J.mode == NTT_DIVIDE2)
+        k_fwd_p1<A, 2><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2);
+    else
+        k_fwd_p1<A, 1><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2);
     UH_LAUNCH_CHECK();
     k_fwd_p2<B><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2, c.d_bsel,
                                         c.d_csl);
