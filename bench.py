@@ -285,12 +285,23 @@ def main():
         lev, (tms, work, cnt) = top
         achieved = work / (tms / 1e3) / 1e12
         peak = rates[1] / 1e12
-        roofline = {"bound": "int32-imad (64-bit modular MAC)", "kernel": "k_conv_mac (conv2, hoisted fused)",
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "conv2_traffic.json")  # from the committed ncu --set full capture
+        if os.path.exists(tpath):
+            t = json.load(open(tpath))
+            if t.get("batch") == B:
+                traffic = t["dram_bytes_per_launch"]
+        roofline = {"bound": "int32-imad (64-bit modular MAC; no tensor cores: modular integer work)",
+                    "kernel": f"k_hoisted_mac (LeNet conv2, level {lev}: hoisted key switch + weight MAC)",
                     "achieved": achieved, "peak": peak, "unit": "T modMAC/s", "frac": achieved / peak,
-                    "traffic": None, "launch_ms": tms / cnt, "algorithmic_macs_per_launch": work / cnt,
+                    "traffic": traffic, "launch_ms": tms / cnt, "algorithmic_macs_per_launch": work / cnt,
                     "share_of_step": tms / ms, "conv_mac_share_of_step": conv_ms / ms,
-                    "peak_source": "measured on this GPU: uh_bench_peaks (register-resident 128-bit MAC loop)",
-                    "peaks_measured": {"imad_per_s": rates[0], "mac128_per_s": rates[1], "mulmod_per_s": rates[2]}}
+                    "peak_source": "measured on this GPU: uh_bench_peaks (register-resident 128-bit MAC loop, "
+                                   "4 IMAD.WIDE.U32 per MAC)",
+                    "peaks_measured": {"imad_per_s": rates[0], "mac128_per_s": rates[1], "mulmod_per_s": rates[2],
+                                       "shoup_per_s": rates[4], "fp64_modmac_per_s": rates[5]},
+                    "hbm_peak_gbs": 6540.2,
+                    "hbm_achieved_gbs": (traffic / (tms / cnt / 1e3) / 1e9) if traffic else None}
 
     # ---- e2e through the public API from host images ----
     e2e = None

@@ -33,7 +33,9 @@ def main():
     args = ap.parse_args()
     rows = load(args.csv)
     skip = tuple(args.skip_prefix.split(","))
-    rows = [r for r in rows if not short(r["Kernel Name"]).startswith(skip)]
+    rows = [r for r in rows if not short(r["Kernel Name"]).startswith(skip)
+            and not short(r["Kernel Name"]).split("<")[0].endswith("_peak")
+            and not short(r["Kernel Name"]).startswith(("at::", "regular_fft", "vector_fft"))]
     if args.last:
         rows = rows[-args.last:]
     agg = {}
