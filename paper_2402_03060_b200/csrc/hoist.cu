@@ -42,6 +42,43 @@ __device__ __forceinline__ uint64_t reduce128_lazy(uint64_t hi, uint64_t lo, con
 
 constexpr int kMaxL = 12;  // phase-A digit loop fully unrolled (predicated) up to this many limbs
 
+// Phase-A key-switch dot product of one rotated term:
+//   a0 += sum_j D_j * K[j][0],  a1 += sum_j D_j * K[j][1]   (j < L digits)
+// Loads are issued in groups of G digits (3G independent 64-bit loads in flight)
+// before any of the group's products: a per-digit load->use chain would
+// serialise L round trips to L2 (ncu: long-scoreboard on the first MAC).
+#ifndef UH_KS_GROUP_FOR
+#define UH_KS_GROUP_FOR(PPW, W) ((PPW) * (W) >= 96 || ((W) == 8 && (PPW) == 2) ? 2 : 4)
+#endif
+#ifndef UH_WS_GROUP
+#define UH_WS_GROUP 4
+#endif
+template <int G>
+__device__ __forceinline__ void ks_dot(Acc &a0, Acc &a1, const uint64_t *Di, uint32_t dstride,
+                                       const uint64_t *k0, uint32_t ks, int L) {
+#pragma unroll
+    for (int j0 = 0; j0 < kMaxL; j0 += G) {
+        if (j0 < L) {
+            uint64_t d[G], x[G], y[G];
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                const int j = j0 + g;
+                const bool ok = j < L;
+                d[g] = ok ? __ldg(Di + j * dstride) : 0;
+                x[g] = ok ? __ldg(k0 + (2 * j) * ks) : 0;
+                y[g] = ok ? __ldg(k0 + (2 * j + 1) * ks) : 0;
+            }
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+                if (j0 + g < L) {
+                    a0.mac(d[g], x[g]);
+                    a1.mac(d[g], y[g]);
+                }
+            }
+        }
+    }
+}
+
 // 8-warp CTAs are capped at 64 registers (4 CTAs / SM), 24-warp CTAs at 85 (1 CTA / SM).
 // All element offsets are 32-bit (the host checks every operand has < 2^32 elements).
 constexpr int kMaxTerms = 512;  // per-term metadata staged in shared memory
@@ -82,6 +119,8 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
         acc[j][0].zero();
         acc[j][1].zero();
     }
+    // phase-A load group: bounded by the registers left next to the PPW accumulators
+    constexpr int kKsGroup = UH_KS_GROUP_FOR(PPW, W);
     int since_fold = 0;
     int buf = 0;
     constexpr int ITEMS = kTChunk * kTBatch / W;  // phase-A items per thread (1, 2 or 3)
@@ -141,14 +180,7 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
                     Acc a0, a1;
                     a0.zero();
                     a1.zero();
-#pragma unroll
-                    for (int j = 0; j < kMaxL; j++) {  // fully unrolled: all digit/key loads in flight
-                        if (j < L) {
-                            const uint64_t d = Di[j * dstride];
-                            a0.mac(d, k0[(2 * j) * ks]);
-                            a1.mac(d, k0[(2 * j + 1) * ks]);
-                        }
-                    }
+                    ks_dot<kKsGroup>(a0, a1, Di, dstride, k0, ks, L);
                     if (qlimb) a0.mac(Pk, c0[src]);
                     v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
                     v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
@@ -312,6 +344,8 @@ __global__ void __launch_bounds__(W * 32, 1)
         acc[j][0].zero();
         acc[j][1].zero();
     }
+    // phase-A load group: bounded by the registers left next to the PPW accumulators
+    constexpr int kKsGroup = UH_KS_GROUP_FOR(PPW, W);
     int since_fold = 0;
     int buf = 0;
     constexpr int PB = PPW == 4 ? 2 : PPW, PO = PPW / PB, WB = kTBatch / PB;
@@ -427,6 +461,165 @@ __global__ void __launch_bounds__(W * 32, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised variant for wide masked layers (9..12 outputs, e.g. LeNet
+// conv2): 8 producer warps form the rotated key-switched terms (phase A) of
+// chunk c+1 while 16 consumer warps multiply-accumulate chunk c (phase B);
+// double-buffered shared-memory terms, named-barrier full/empty handshake
+// (no CTA-wide barrier in the steady state).  Consumer warp w owns 3 outputs x
+// 2 ciphertexts.
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n)); }
+
+constexpr int kWSProd = 8, kWSCons = 16, kWSPO = 3, kWSPB = 2;
+
+__global__ void __launch_bounds__((kWSProd + kWSCons) * 32, 1)
+    k_hoisted_ws(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
+                 const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
+                 const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
+                 const int32_t *__restrict__ shifts, int B, int I, int T, int O, int L, int sp, int logn,
+                 const Mod *__restrict__ mods) {
+    constexpr int NT = (kWSProd + kWSCons) * 32;
+    __shared__ uint64_t sv[2][kTChunk][kTBatch][2][32];
+    __shared__ const uint64_t *s_key[kMaxTerms];
+    __shared__ uint32_t s_shift[kMaxTerms];
+    __shared__ uint32_t s_kstride[kMaxTerms];
+    const int LP = L + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b0 = blockIdx.x * kTBatch;
+    const uint32_t n = blockIdx.y * 32 + lane;
+    const int k = blockIdx.z;
+    const uint32_t N = 1u << logn, half = N >> 1;
+    const Mod m = mods[limb_mod(k, L, 0, sp)];
+    const bool qlimb = k < L;
+    const uint64_t P = mods[sp].q;
+    const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
+    const int Q = I * T;
+    const int nchunks = (Q + kTChunk - 1) / kTChunk;
+    for (int t = threadIdx.x; t < T; t += NT) {
+        s_key[t] = keys[t];
+        s_shift[t] = (uint32_t)shifts[t];
+        s_kstride[t] = (uint32_t)key_limbs[t] << logn;
+    }
+    __syncthreads();
+    const uint32_t dstride = (uint32_t)LP << logn;
+
+    if (warp < kWSProd) {
+        // ---------------- producers ----------------
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 48;\n" ::);
+        int i0 = 0, t0 = 0;
+        for (int c = 0; c < nchunks; c++) {
+            const int buf = c & 1, q0 = c * kTChunk;
+            if (c >= 2) bar_sync(3 + buf, NT);  // consumers released this buffer
+#pragma unroll
+            for (int gi = 0; gi < kTChunk * kTBatch / kWSProd; gi++) {
+                const int g = warp + kWSProd * gi;
+                const int qc = g / kTBatch, bt = g % kTBatch, q = q0 + qc, b = b0 + bt;
+                uint64_t v0 = 0, v1 = 0;
+                if (q < Q && b < B) {
+                    int i = i0, t = t0 + qc;
+                    while (t >= T) {
+                        t -= T;
+                        i++;
+                    }
+                    const uint32_t ib = (uint32_t)(i * B + b);
+                    const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
+                    const uint32_t r = s_shift[t];
+                    if (r == 0) {
+                        if (qlimb) {
+                            v0 = mulmod(Pk, c0[n], m);
+                            v1 = mulmod(Pk, c0[((uint32_t)xls << logn) + n], m);
+                        }
+                    } else {
+                        const uint32_t src = rot_index(n, half, r);
+                        const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
+                        const uint32_t ks = s_kstride[t];
+                        const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + n;
+                        Acc a0, a1;
+                        a0.zero();
+                        a1.zero();
+                        ks_dot<UH_WS_GROUP>(a0, a1, Di, dstride, k0, ks, L);
+                        if (qlimb) a0.mac(Pk, c0[src]);
+                        v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
+                        v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
+                    }
+                }
+                sv[buf][qc][bt][0][lane] = v0;
+                sv[buf][qc][bt][1][lane] = v1;
+            }
+            __threadfence_block();
+            bar_arrive(1 + buf, NT);  // buffer full
+            t0 += kTChunk;
+            while (t0 >= T) {
+                t0 -= T;
+                i0++;
+            }
+        }
+        return;
+    }
+    // ---------------- consumers ----------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 96;\n" ::);
+    const int cw = warp - kWSProd;                       // 0..15
+    const int o_a = (cw / (kTBatch / kWSPB)) * kWSPO;    // 0, 3, 6, 9
+    const int b_a = (cw % (kTBatch / kWSPB)) * kWSPB;    // 0, 2, 4, 6
+    const uint32_t mask_row = ((uint32_t)k << logn) + n;
+    Acc acc[kWSPO * kWSPB][2];
+#pragma unroll
+    for (int j = 0; j < kWSPO * kWSPB; j++) {
+        acc[j][0].zero();
+        acc[j][1].zero();
+    }
+    int since_fold = 0;
+    const uint32_t qstride = (uint32_t)Q * dstride;  // between outputs of the mask bank
+    const uint64_t *mp = masks + (uint32_t)o_a * qstride + mask_row;
+    for (int c = 0; c < nchunks; c++) {
+        const int buf = c & 1, q0 = c * kTChunk;
+        uint64_t mpre[kTChunk][kWSPO];
+#pragma unroll
+        for (int qc = 0; qc < kTChunk; qc++)
+#pragma unroll
+            for (int d = 0; d < kWSPO; d++)
+                mpre[qc][d] = (o_a + d < O && q0 + qc < Q) ? mp[qc * dstride + d * qstride] : 0;
+        mp += kTChunk * dstride;
+        bar_sync(1 + buf, NT);  // wait until the producers filled this buffer
+        const int qn = min(kTChunk, Q - q0);
+#pragma unroll
+        for (int qc = 0; qc < kTChunk; qc++) {
+            if (qc >= qn) break;
+#pragma unroll
+            for (int db = 0; db < kWSPB; db++) {
+                const int bt = b_a + db;
+                const uint64_t v0 = sv[buf][qc][bt][0][lane], v1 = sv[buf][qc][bt][1][lane];
+#pragma unroll
+                for (int d = 0; d < kWSPO; d++) {
+                    const int j = d * kWSPB + db;
+                    acc[j][0].mac(mpre[qc][d], v0);
+                    acc[j][1].mac(mpre[qc][d], v1);
+                }
+            }
+            if (++since_fold == kFold) {
+                since_fold = 0;
+#pragma unroll
+                for (int j = 0; j < kWSPO * kWSPB; j++)
+                    for (int cc = 0; cc < 2; cc++) {
+                        uint64_t rr = reduce128_lazy(acc[j][cc].hi64(), acc[j][cc].lo64(), m);
+                        acc[j][cc].set(rr, 0);
+                    }
+            }
+        }
+        if (c + 2 < nchunks) bar_arrive(3 + buf, NT);  // buffer free for chunk c + 2
+    }
+#pragma unroll
+    for (int j = 0; j < kWSPO * kWSPB; j++) {
+        const int o = o_a + j / kWSPB, b = b0 + b_a + j % kWSPB;
+        if (o < O && b < B) {
+            uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
+            dst[0] = acc[j][0].reduce(m);
+            dst[dstride] = acc[j][1].reduce(m);
+        }
+    }
+}
+
 }  // namespace
 
 void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D, const uint64_t *masks,
@@ -477,6 +670,18 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
         }
     };
     using std::integral_constant;
+    // warp-specialised producer/consumer kernel for wide masked dense layers: opt-in
+    // (UH_HOIST_WS=1); measured slower than the 24-warp kernel on LeNet conv2 (B200, N=2^15)
+    static const bool ws_on = [] {
+        const char *e = getenv("UH_HOIST_WS");
+        return e && std::string(e) == "1";
+    }();
+    if (ws_on && masks && !diag && O > 8 && O <= 12) {
+        k_hoisted_ws<<<grid, (kWSProd + kWSCons) * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I,
+                                                                T, O, L, c.sp(), (int)c.logn, c.d_mods);
+        UH_LAUNCH_CHECK();
+        return;
+    }
     if (O <= 12) {
         // measured (B200, N=2^15): 24 warps win when phase B is heavy (O >= 3), 8-warp CTAs when it is not
         if (narrow || O <= 2) {

@@ -110,12 +110,6 @@ __device__ __forceinline__ uint64_t crt2_to(uint64_t a, uint64_t b, const LimbIn
     return neg ? submod(t, li.qpk, m.q) : t;
 }
 
-__device__ __forceinline__ uint64_t load_in(const LimbInfo &li, size_t idx, const Mod &m) {
-    if (li.mode == NTT_DIVIDE2) return crt2_to(li.src[idx], li.src2[idx], li, m);
-    uint64_t x = li.src[idx];
-    return li.qsrc ? centred_to(x, li.qsrc, m) : x;
-}
-
 // Compile-time load transform of pass 1: 0 plain, 1 centred lift (ModUp / ModDown / rescale),
 // 2 CRT pair (fused ModDown + rescale).  The centred lift is branch-free; the magnitude
 // needs a reduction only when the source modulus exceeds twice the target (a 60-bit
@@ -307,7 +301,7 @@ __device__ __forceinline__ size_t cta_slot(int i, int logn) {
     return ((size_t)h << (logn - 1)) + js + (i % C::G) + (size_t)(n1 / 2) * (i / C::G);
 }
 
-template <int B>
+template <int B, int EM>
 __global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ twd,
@@ -348,16 +342,31 @@ __global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *_
         for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = reduce4q(v[z], q);
     }
     __syncthreads();
-    // coalesced slot-order epilogue
-    for (int i = tid; i < 4096; i += kThreads) {
-        const size_t s = cta_slot<B>(i, logn);
-        const uint64_t y = sm[C::at(i % C::G, csl[s])];
-        if (J.mode == NTT_DIVIDE)
-            li.dst[s] = csub(shoup_lazy(submod(li.in[s], y, q), li.w, li.ws, q), q);
-        else if (J.mode == NTT_DIVIDE2)
-            li.dst[s] = shoup(shoup(submod(li.in[s], y, q), li.w, li.ws, q), li.w2, li.ws2, q);
-        else
-            li.dst[s] = y;
+    // coalesced slot-order epilogue: a thread's 16 slot-table (and DIVIDE input) loads are
+    // issued together, then the shared-memory gathers and the stores
+    constexpr int E = EM ? 8 : 16;  // loads in flight per round (register budget)
+#pragma unroll
+    for (int e0 = 0; e0 < 4096 / kThreads; e0 += E) {
+        int cs[E];
+        uint64_t a[E];
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const size_t s = cta_slot<B>(tid + kThreads * (e0 + e), logn);
+            cs[e] = __ldg(csl + s);
+            if (EM != 0) a[e] = li.in[s];
+        }
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const int i = tid + kThreads * (e0 + e);
+            const size_t s = cta_slot<B>(i, logn);
+            const uint64_t y = sm[C::at(i % C::G, cs[e])];
+            if (EM == 1)
+                li.dst[s] = csub(shoup_lazy(submod(a[e], y, q), li.w, li.ws, q), q);
+            else if (EM == 2)
+                li.dst[s] = shoup(shoup(submod(a[e], y, q), li.w, li.ws, q), li.w2, li.ws2, q);
+            else
+                li.dst[s] = y;
+        }
     }
 }
 
@@ -376,10 +385,20 @@ __global__ void __launch_bounds__(kThreads) k_inv_pa(NttJob J, uint64_t *__restr
     const Mod m = mods[li.mod];
     const uint64_t q = m.q;
     const ulonglong2 *T = itwd + ((size_t)li.mod << logn);
-    // coalesced slot-order gather into the blocks' shared-memory tiles
-    for (int i = tid; i < 4096; i += kThreads) {
-        const size_t s = cta_slot<B>(i, logn);
-        sm[C::at(i % C::G, csl[s])] = load_in(li, s, m);
+    // coalesced slot-order gather into the blocks' shared-memory tiles (plain limbs: the only
+    // inverse mode); all of a thread's loads are issued before the shared-memory stores
+    {
+        constexpr int E = 4096 / kThreads;
+        int cs[E];
+        uint64_t a[E];
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            const size_t s = cta_slot<B>(tid + kThreads * e, logn);
+            cs[e] = __ldg(csl + s);
+            a[e] = li.src[s];
+        }
+#pragma unroll
+        for (int e = 0; e < E; e++) sm[C::at((tid + kThreads * e) % C::G, cs[e])] = a[e];
     }
     __syncthreads();
 #pragma unroll
@@ -419,13 +438,21 @@ void run_fwd(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
     else
         k_fwd_p1<A, 1><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2);
     UH_LAUNCH_CHECK();
-    k_fwd_p2<B><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2, c.d_bsel,
-                                        c.d_csl);
+    if (J.mode == NTT_DIVIDE)
+        k_fwd_p2<B, 1><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2, c.d_bsel,
+                                               c.d_csl);
+    else if (J.mode == NTT_DIVIDE2)
+        k_fwd_p2<B, 2><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2, c.d_bsel,
+                                               c.d_csl);
+    else
+        k_fwd_p2<B, 0><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2, c.d_bsel,
+                                               c.d_csl);
     UH_LAUNCH_CHECK();
 }
 
 template <int A, int B>
 void run_inv(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
+    if (J.mode != NTT_PLAIN) throw std::invalid_argument("inverse NTT: plain limbs only");
     Scratch tmp((size_t)limbs * c.n * 8, s);
     dim3 g1((1u << B) / 32, limbs), g2((1u << A) / P2<B>::G, limbs);
     k_inv_pa<B><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_bsel,
