@@ -128,7 +128,7 @@ __device__ __forceinline__ uint64_t load_t(const LimbInfo &li, size_t idx, const
 }
 
 // Harvey CT butterfly: x, y in [0, 4q) -> [0, 4q)
-__device__ __forceinline__ void ct(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q) {
+__device__ __forceinline__ void bf_ct(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q) {
     uint64_t q2 = 2 * q;
     uint64_t u = x >= q2 ? x - q2 : x;
     uint64_t t = shoup_lazy(y, w.x, w.y, q);
@@ -136,39 +136,105 @@ __device__ __forceinline__ void ct(uint64_t &x, uint64_t &y, ulonglong2 w, uint6
     y = u - t + q2;
 }
 // Harvey GS butterfly: x, y in [0, 2q) -> [0, 2q)
-__device__ __forceinline__ void gs(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q) {
+__device__ __forceinline__ void bf_gs(uint64_t &x, uint64_t &y, ulonglong2 w, uint64_t q) {
     uint64_t q2 = 2 * q;
     uint64_t s = x + y;
     uint64_t d = x - y + q2;
     x = s >= q2 ? s - q2 : s;
     y = shoup_lazy(d, w.x, w.y, q);
 }
+
+// ---- FP64-pipe arithmetic for limbs with q < 2^42 ----
+// Values are signed integers held exactly in doubles (|v| < 2^50).  Twiddles are
+// (w, w / q) pairs.  y * w mod q (centred, |r| <= 0.51 q) is exact:
+//   p = fl(y w), e = y w - p (one fma, exact), k = rint(y * (w / q)) (|k q - y w| <= 0.51 q),
+//   r = (p - k q) + e, where p - k q is an integer below 2^53 (one fma, exact).
+// A CT butterfly is 8 FP64 operations and no integer work; the 64-bit Shoup
+// butterfly costs ~14 IMAD-pipe slots.  Magnitudes: forward 15 stages from [0, q)
+// stay below 9q; inverse butterflies double the sum output, so the inverse reduces
+// once between its passes (<= 2^8 q, then <= 2^7 q / 2).
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: fma(x, y, kMagic) - kMagic = rint(x * y)
+constexpr double kTwo52 = 4503599627370496.0;
+__device__ __forceinline__ double fmm(double y, double2 w, double q) {
+    const double p = y * w.x;
+    const double e = fma(y, w.x, -p);
+    const double k = fma(y, w.y, kMagic) - kMagic;
+    return fma(-k, q, p) + e;
+}
+__device__ __forceinline__ void bf_ct(double &x, double &y, double2 w, double q) {
+    const double t = fmm(y, w, q);
+    const double u = x;
+    x = u + t;
+    y = u - t;
+}
+__device__ __forceinline__ void bf_gs(double &x, double &y, double2 w, double q) {
+    const double s = x + y, d = x - y;
+    x = s;
+    y = fmm(d, w, q);
+}
+__device__ __forceinline__ double u2d(uint64_t x) {  // exact for x < 2^52
+    return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - kTwo52;
+}
+__device__ __forceinline__ double fred(double v, double q, double qinv) {  // centred: |result| <= q / 2 (+ tiny)
+    const double k = fma(v, qinv, kMagic) - kMagic;
+    return fma(-k, q, v);
+}
+__device__ __forceinline__ uint64_t d2u_canon(double v, double q, double qinv) {  // -> [0, q)
+    double r = fred(v, q, qinv);
+    r = r < 0 ? r + q : r;
+    return (uint64_t)__double_as_longlong(r + kTwo52) ^ 0x4330000000000000ull;
+}
 __device__ __forceinline__ uint64_t reduce4q(uint64_t x, uint64_t q) {
     x = x >= 2 * q ? x - 2 * q : x;
     return x >= q ? x - q : x;
 }
 __device__ __forceinline__ ulonglong2 tw(const ulonglong2 *__restrict__ t, int i) { return __ldg(t + i); }
+__device__ __forceinline__ double2 tw(const double2 *__restrict__ t, int i) { return __ldg(t + i); }
+
+// value type of a limb's arithmetic: 64-bit integers (Shoup) or FP64
+template <bool FP> struct Arith;
+template <> struct Arith<false> {
+    using V = uint64_t;
+    using W = ulonglong2;
+    uint64_t q;
+    __device__ Arith(uint64_t q_) : q(q_) {}
+    __device__ static V in(uint64_t x) { return x; }           // canonical residue -> V
+    __device__ static V raw_in(uint64_t x) { return x; }       // stored word -> V
+    __device__ static uint64_t raw(V v) { return v; }          // V -> stored word
+    __device__ uint64_t canon(V v) const { return reduce4q(v, q); }
+    __device__ uint64_t qv() const { return q; }
+};
+template <> struct Arith<true> {
+    using V = double;
+    using W = double2;
+    double q, qinv;
+    __device__ Arith(uint64_t q_) : q((double)q_), qinv(1.0 / (double)q_) {}
+    __device__ static V in(uint64_t x) { return u2d(x); }
+    __device__ static V raw_in(uint64_t x) { return __longlong_as_double((long long)x); }
+    __device__ static uint64_t raw(V v) { return (uint64_t)__double_as_longlong(v); }
+    __device__ uint64_t canon(V v) const { return d2u_canon(v, q, qinv); }
+    __device__ double qv() const { return q; }
+};
+__device__ __forceinline__ bool fp_limb(uint64_t q) { return (q >> 42) == 0; }
 
 // forward radix network on R register values (elements base + S*x), stages with
 // distance dx = R/2 .. 1; twiddle index = m0 * (1 << s) + off(s) + x / (2 dx)
-template <int R>
-__device__ __forceinline__ void fwd_strided(uint64_t (&v)[R], const ulonglong2 *__restrict__ T, int m0, int moff,
-                                            uint64_t q) {
+template <int R, typename V, typename W, typename Q>
+__device__ __forceinline__ void fwd_strided(V (&v)[R], const W *__restrict__ T, int m0, int moff, Q q) {
     int m = m0, off = moff;
 #pragma unroll
     for (int dx = R / 2; dx >= 1; dx >>= 1) {
 #pragma unroll
         for (int x = 0; x < R; x++) {
             if (x & dx) continue;
-            ct(v[x], v[x + dx], tw(T, m + off + x / (2 * dx)), q);
+            bf_ct(v[x], v[x + dx], tw(T, m + off + x / (2 * dx)), q);
         }
         m <<= 1;
         off <<= 1;
     }
 }
-template <int R>
-__device__ __forceinline__ void inv_strided(uint64_t (&v)[R], const ulonglong2 *__restrict__ T, int mlast,
-                                            int offlast, uint64_t q) {
+template <int R, typename V, typename W, typename Q>
+__device__ __forceinline__ void inv_strided(V (&v)[R], const W *__restrict__ T, int mlast, int offlast, Q q) {
     // mirror of fwd_strided: distances 1 .. R/2, m halves each stage
     int m = mlast, off = offlast;
 #pragma unroll
@@ -176,12 +242,20 @@ __device__ __forceinline__ void inv_strided(uint64_t (&v)[R], const ulonglong2 *
 #pragma unroll
         for (int x = 0; x < R; x++) {
             if (x & dx) continue;
-            gs(v[x], v[x + dx], tw(T, m + off + x / (2 * dx)), q);
+            bf_gs(v[x], v[x + dx], tw(T, m + off + x / (2 * dx)), q);
         }
         m >>= 1;
         off >>= 1;
     }
 }
+
+struct Tw {  // both twiddle tables of one limb's modulus
+    const ulonglong2 *i;
+    const double2 *f;
+};
+template <bool FP> __device__ __forceinline__ const typename Arith<FP>::W *pick(const Tw &t);
+template <> __device__ __forceinline__ const ulonglong2 *pick<false>(const Tw &t) { return t.i; }
+template <> __device__ __forceinline__ const double2 *pick<true>(const Tw &t) { return t.f; }
 
 // ---------------- pass 1 (columns), N1 = 2^A ----------------
 template <int A>
@@ -192,84 +266,118 @@ struct P1 {
     static constexpr int GC = R1 * 32 / kThreads;  // contiguous groups per thread
 };
 
+template <int A, int LM, bool FP>
+__device__ __forceinline__ void fwd_p1_body(uint64_t *sm, const LimbInfo &li, const Mod &m, bool red,
+                                            const Tw &tws, uint64_t *out, int n2, int col, int lane, int wq) {
+    using C = P1<A>;
+    using AR = Arith<FP>;
+    using V = typename AR::V;
+    const AR ar(m.q);
+    const auto *T = pick<FP>(tws);
+#pragma unroll
+    for (int g = 0; g < C::GS; g++) {
+        const int r0 = wq + 8 * g;  // < S1
+        V v[C::R1];
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) v[x] = AR::in(load_t<LM>(li, (size_t)(r0 + C::S1 * x) * n2 + col, m, red));
+        fwd_strided<C::R1>(v, T, 1, 0, ar.qv());
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) sm[(r0 + C::S1 * x) * 32 + lane] = AR::raw(v[x]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < C::GC; g++) {
+        const int grp = wq + 8 * g;  // < R1
+        const int r0 = grp * C::R2;
+        V v[C::R2];
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) v[z] = AR::raw_in(sm[(r0 + z) * 32 + lane]);
+        // stages m = R1 .. N1/2 on contiguous rows r0 + z: twiddle m + (r0 + z) / (2t)
+        fwd_strided<C::R2>(v, T, C::R1, grp, ar.qv());
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) out[(size_t)(r0 + z) * n2 + col] = AR::raw(v[z]);
+    }
+}
+
 template <int A, int LM>
 __global__ void __launch_bounds__(kThreads) k_fwd_p1(NttJob J, uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
-                                                    const ulonglong2 *__restrict__ twd) {
-    using C = P1<A>;
-    __shared__ uint64_t sm[C::N1 * 32];
+                                                    const ulonglong2 *__restrict__ twd,
+                                                    const double2 *__restrict__ twf) {
+    __shared__ uint64_t sm[P1<A>::N1 * 32];
     const int f = blockIdx.y, lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const int n2 = 1 << (logn - A);
     const int col = blockIdx.x * 32 + lane;
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
-    const uint64_t q = m.q;
-    const bool red = LM == 1 && ((li.qsrc - 1) >> 1) >= q;
-    const ulonglong2 *T = twd + ((size_t)li.mod << logn);
-#pragma unroll
-    for (int g = 0; g < C::GS; g++) {
-        const int r0 = wq + 8 * g;  // < S1
-        uint64_t v[C::R1];
-#pragma unroll
-        for (int x = 0; x < C::R1; x++) v[x] = load_t<LM>(li, (size_t)(r0 + C::S1 * x) * n2 + col, m, red);
-        fwd_strided<C::R1>(v, T, 1, 0, q);
-#pragma unroll
-        for (int x = 0; x < C::R1; x++) sm[(r0 + C::S1 * x) * 32 + lane] = v[x];
-    }
-    __syncthreads();
+    const bool red = LM == 1 && ((li.qsrc - 1) >> 1) >= m.q;
+    const Tw tws{twd + ((size_t)li.mod << logn), twf + ((size_t)li.mod << logn)};
     uint64_t *out = tmp + ((size_t)f << logn);
+    if (fp_limb(m.q))
+        fwd_p1_body<A, LM, true>(sm, li, m, red, tws, out, n2, col, lane, wq);
+    else
+        fwd_p1_body<A, LM, false>(sm, li, m, red, tws, out, n2, col, lane, wq);
+}
+
+template <int A, bool FP>
+__device__ __forceinline__ void inv_pb_body(uint64_t *sm, const LimbInfo &li, const Mod &m, const Tw &tws,
+                                            const uint64_t *in, int n2, int col, int lane, int wq) {
+    using C = P1<A>;
+    using AR = Arith<FP>;
+    using V = typename AR::V;
+    const AR ar(m.q);
+    const auto *T = pick<FP>(tws);
 #pragma unroll
     for (int g = 0; g < C::GC; g++) {
-        const int grp = wq + 8 * g;  // < R1
+        const int grp = wq + 8 * g;
         const int r0 = grp * C::R2;
-        uint64_t v[C::R2];
+        V v[C::R2];
 #pragma unroll
-        for (int z = 0; z < C::R2; z++) v[z] = sm[(r0 + z) * 32 + lane];
-        // stages m = R1 .. N1/2 on contiguous rows r0 + z: twiddle m + (r0 + z) / (2t)
-        fwd_strided<C::R2>(v, T, C::R1, grp, q);
+        for (int z = 0; z < C::R2; z++) v[z] = AR::raw_in(in[(size_t)(r0 + z) * n2 + col]);
+        // mirror of the forward contiguous stages: last stage m = N1/2 with offset grp * (R2/2)
+        inv_strided<C::R2>(v, T, C::N1 / 2, grp * (C::R2 / 2), ar.qv());
 #pragma unroll
-        for (int z = 0; z < C::R2; z++) out[(size_t)(r0 + z) * n2 + col] = v[z];
+        for (int z = 0; z < C::R2; z++) sm[(r0 + z) * 32 + lane] = AR::raw(v[z]);
+    }
+    __syncthreads();
+    double2 nf;
+    if (FP) nf = make_double2((double)m.ninv, (double)m.ninv / (double)m.q);
+#pragma unroll
+    for (int g = 0; g < C::GS; g++) {
+        const int r0 = wq + 8 * g;
+        V v[C::R1];
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(sm[(r0 + C::S1 * x) * 32 + lane]);
+        inv_strided<C::R1>(v, T, C::R1 / 2, 0, ar.qv());
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) {
+            uint64_t r;
+            if constexpr (FP)
+                r = ar.canon(fmm(v[x], nf, ar.q));
+            else
+                r = csub(shoup_lazy(v[x], m.ninv, m.ninvs, m.q), m.q);
+            li.dst[(size_t)(r0 + C::S1 * x) * n2 + col] = r;
+        }
     }
 }
 
 template <int A>
 __global__ void __launch_bounds__(kThreads) k_inv_pb(NttJob J, const uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
-                                                    const ulonglong2 *__restrict__ itwd) {
-    using C = P1<A>;
-    __shared__ uint64_t sm[C::N1 * 32];
+                                                    const ulonglong2 *__restrict__ itwd,
+                                                    const double2 *__restrict__ itwf) {
+    __shared__ uint64_t sm[P1<A>::N1 * 32];
     const int f = blockIdx.y, lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const int n2 = 1 << (logn - A);
     const int col = blockIdx.x * 32 + lane;
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
-    const uint64_t q = m.q;
-    const ulonglong2 *T = itwd + ((size_t)li.mod << logn);
+    const Tw tws{itwd + ((size_t)li.mod << logn), itwf + ((size_t)li.mod << logn)};
     const uint64_t *in = tmp + ((size_t)f << logn);
-#pragma unroll
-    for (int g = 0; g < C::GC; g++) {
-        const int grp = wq + 8 * g;
-        const int r0 = grp * C::R2;
-        uint64_t v[C::R2];
-#pragma unroll
-        for (int z = 0; z < C::R2; z++) v[z] = in[(size_t)(r0 + z) * n2 + col];
-        // mirror of the forward contiguous stages: last stage m = N1/2 with offset grp * (R2/2)
-        inv_strided<C::R2>(v, T, C::N1 / 2, grp * (C::R2 / 2), q);
-#pragma unroll
-        for (int z = 0; z < C::R2; z++) sm[(r0 + z) * 32 + lane] = v[z];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int g = 0; g < C::GS; g++) {
-        const int r0 = wq + 8 * g;
-        uint64_t v[C::R1];
-#pragma unroll
-        for (int x = 0; x < C::R1; x++) v[x] = sm[(r0 + C::S1 * x) * 32 + lane];
-        inv_strided<C::R1>(v, T, C::R1 / 2, 0, q);
-#pragma unroll
-        for (int x = 0; x < C::R1; x++)
-            li.dst[(size_t)(r0 + C::S1 * x) * n2 + col] = csub(shoup_lazy(v[x], m.ninv, m.ninvs, q), q);
-    }
+    if (fp_limb(m.q))
+        inv_pb_body<A, true>(sm, li, m, tws, in, n2, col, lane, wq);
+    else
+        inv_pb_body<A, false>(sm, li, m, tws, in, n2, col, lane, wq);
 }
 
 // ---------------- pass 2 (contiguous blocks), N2 = 2^B ----------------
@@ -301,10 +409,47 @@ __device__ __forceinline__ size_t cta_slot(int i, int logn) {
     return ((size_t)h << (logn - 1)) + js + (i % C::G) + (size_t)(n1 / 2) * (i / C::G);
 }
 
+// pass 2 forward stages: tmp (pass-1 output) -> canonical residues in shared memory
+template <int B, bool FP>
+__device__ __forceinline__ void fwd_p2_body(uint64_t *sm, const Mod &m, const Tw &tws, const uint64_t *in,
+                                            const int *sel, int n1, int tid) {
+    using C = P2<B>;
+    using AR = Arith<FP>;
+    using V = typename AR::V;
+    const AR ar(m.q);
+    const auto *T = pick<FP>(tws);
+    {
+        const int g = tid / C::S, c0 = tid % C::S, blk = sel[g];
+        V v[C::R1];
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(in[(size_t)blk * C::N2 + c0 + C::S * x]);
+        // local stages m' = 1..8: global twiddle index m' * (n1 + blk) + x / (2 dx)
+        fwd_strided<C::R1>(v, T, n1 + blk, 0, ar.qv());
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) sm[C::at(g, c0 + C::S * x)] = AR::raw(v[x]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int gi = 0; gi < C::GC; gi++) {
+        const int grp = tid + kThreads * gi;
+        const int per = C::N2 / C::R2;
+        const int g = grp / per, c = (grp % per) * C::R2, blk = sel[g];
+        V v[C::R2];
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) v[z] = AR::raw_in(sm[C::at(g, c + z)]);
+        // local stages m' = 16 .. N2/2 on contiguous c + z
+        fwd_strided<C::R2>(v, T, 16 * (n1 + blk), (c / C::R2), ar.qv());
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = ar.canon(v[z]);
+    }
+    __syncthreads();
+}
+
 template <int B, int EM>
 __global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ twd,
+                                                    const double2 *__restrict__ twf,
                                                     const int32_t *__restrict__ bsel,
                                                     const int32_t *__restrict__ csl) {
     using C = P2<B>;
@@ -315,33 +460,12 @@ __global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *_
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
     const uint64_t q = m.q;
-    const ulonglong2 *T = twd + ((size_t)li.mod << logn);
+    const Tw tws{twd + ((size_t)li.mod << logn), twf + ((size_t)li.mod << logn)};
     const uint64_t *in = tmp + ((size_t)f << logn);
-    {
-        const int g = tid / C::S, c0 = tid % C::S, blk = sel[g];
-        uint64_t v[C::R1];
-#pragma unroll
-        for (int x = 0; x < C::R1; x++) v[x] = in[(size_t)blk * C::N2 + c0 + C::S * x];
-        // local stages m' = 1..8: global twiddle index m' * (n1 + blk) + x / (2 dx)
-        fwd_strided<C::R1>(v, T, n1 + blk, 0, q);
-#pragma unroll
-        for (int x = 0; x < C::R1; x++) sm[C::at(g, c0 + C::S * x)] = v[x];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int gi = 0; gi < C::GC; gi++) {
-        const int grp = tid + kThreads * gi;
-        const int per = C::N2 / C::R2;
-        const int g = grp / per, c = (grp % per) * C::R2, blk = sel[g];
-        uint64_t v[C::R2];
-#pragma unroll
-        for (int z = 0; z < C::R2; z++) v[z] = sm[C::at(g, c + z)];
-        // local stages m' = 16 .. N2/2 on contiguous c + z
-        fwd_strided<C::R2>(v, T, 16 * (n1 + blk), (c / C::R2) , q);
-#pragma unroll
-        for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = reduce4q(v[z], q);
-    }
-    __syncthreads();
+    if (fp_limb(q))
+        fwd_p2_body<B, true>(sm, m, tws, in, sel, n1, tid);
+    else
+        fwd_p2_body<B, false>(sm, m, tws, in, sel, n1, tid);
     // coalesced slot-order epilogue: a thread's 16 slot-table (and DIVIDE input) loads are
     // issued together, then the shared-memory gathers and the stores
     constexpr int E = EM ? 8 : 16;  // loads in flight per round (register budget)
@@ -370,10 +494,49 @@ __global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *_
     }
 }
 
+// inverse pass A stages: canonical residues in shared memory -> tmp (pass-B input)
+template <int B, bool FP>
+__device__ __forceinline__ void inv_pa_body(uint64_t *sm, const Mod &m, const Tw &tws, uint64_t *out,
+                                            const int *sel, int n1, int tid) {
+    using C = P2<B>;
+    using AR = Arith<FP>;
+    using V = typename AR::V;
+    const AR ar(m.q);
+    const auto *T = pick<FP>(tws);
+#pragma unroll
+    for (int gi = 0; gi < C::GC; gi++) {
+        const int grp = tid + kThreads * gi;
+        const int per = C::N2 / C::R2;
+        const int g = grp / per, c = (grp % per) * C::R2, blk = sel[g];
+        V v[C::R2];
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) v[z] = AR::in(sm[C::at(g, c + z)]);
+        // mirror of the forward contiguous stages: last local stage m' = N2/2
+        inv_strided<C::R2>(v, T, (C::N2 / 2) * (n1 + blk), (c / C::R2) * (C::R2 / 2), ar.qv());
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = AR::raw(v[z]);
+    }
+    __syncthreads();
+    {
+        const int g = tid / C::S, c0 = tid % C::S, blk = sel[g];
+        V v[C::R1];
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(sm[C::at(g, c0 + C::S * x)]);
+        inv_strided<C::R1>(v, T, 8 * (n1 + blk), 0, ar.qv());
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) {
+            V r = v[x];
+            if constexpr (FP) r = fred(r, ar.q, ar.qinv);  // bound the growth before pass B
+            out[(size_t)blk * C::N2 + c0 + C::S * x] = AR::raw(r);
+        }
+    }
+}
+
 template <int B>
 __global__ void __launch_bounds__(kThreads) k_inv_pa(NttJob J, uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ itwd,
+                                                    const double2 *__restrict__ itwf,
                                                     const int32_t *__restrict__ bsel,
                                                     const int32_t *__restrict__ csl) {
     using C = P2<B>;
@@ -383,8 +546,7 @@ __global__ void __launch_bounds__(kThreads) k_inv_pa(NttJob J, uint64_t *__restr
     const int *sel = bsel + blockIdx.x * C::G;
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
-    const uint64_t q = m.q;
-    const ulonglong2 *T = itwd + ((size_t)li.mod << logn);
+    const Tw tws{itwd + ((size_t)li.mod << logn), itwf + ((size_t)li.mod << logn)};
     // coalesced slot-order gather into the blocks' shared-memory tiles (plain limbs: the only
     // inverse mode); all of a thread's loads are issued before the shared-memory stores
     {
@@ -401,52 +563,32 @@ __global__ void __launch_bounds__(kThreads) k_inv_pa(NttJob J, uint64_t *__restr
         for (int e = 0; e < E; e++) sm[C::at((tid + kThreads * e) % C::G, cs[e])] = a[e];
     }
     __syncthreads();
-#pragma unroll
-    for (int gi = 0; gi < C::GC; gi++) {
-        const int grp = tid + kThreads * gi;
-        const int per = C::N2 / C::R2;
-        const int g = grp / per, c = (grp % per) * C::R2, blk = sel[g];
-        uint64_t v[C::R2];
-#pragma unroll
-        for (int z = 0; z < C::R2; z++) v[z] = sm[C::at(g, c + z)];
-        // mirror of the forward contiguous stages: last local stage m' = N2/2
-        inv_strided<C::R2>(v, T, (C::N2 / 2) * (n1 + blk), (c / C::R2) * (C::R2 / 2), q);
-#pragma unroll
-        for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = v[z];
-    }
-    __syncthreads();
-    {
-        const int g = tid / C::S, c0 = tid % C::S, blk = sel[g];
-        uint64_t v[C::R1];
-#pragma unroll
-        for (int x = 0; x < C::R1; x++) v[x] = sm[C::at(g, c0 + C::S * x)];
-        inv_strided<C::R1>(v, T, 8 * (n1 + blk), 0, q);
-        uint64_t *out = tmp + ((size_t)f << logn);
-#pragma unroll
-        for (int x = 0; x < C::R1; x++) out[(size_t)blk * C::N2 + c0 + C::S * x] = v[x];
-    }
+    uint64_t *out = tmp + ((size_t)f << logn);
+    if (fp_limb(m.q))
+        inv_pa_body<B, true>(sm, m, tws, out, sel, n1, tid);
+    else
+        inv_pa_body<B, false>(sm, m, tws, out, sel, n1, tid);
 }
 
 template <int A, int B>
 void run_fwd(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
     Scratch tmp((size_t)limbs * c.n * 8, s);
     dim3 g1((1u << B) / 32, limbs), g2((1u << A) / P2<B>::G, limbs);
+    uint64_t *t = tmp.as<uint64_t>();
+    const int ln = (int)c.logn;
     if (J.mode == NTT_PLAIN)
-        k_fwd_p1<A, 0><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2);
+        k_fwd_p1<A, 0><<<g1, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf);
     else if (J.mode == NTT_DIVIDE2)
-        k_fwd_p1<A, 2><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2);
+        k_fwd_p1<A, 2><<<g1, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf);
     else
-        k_fwd_p1<A, 1><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2);
+        k_fwd_p1<A, 1><<<g1, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf);
     UH_LAUNCH_CHECK();
     if (J.mode == NTT_DIVIDE)
-        k_fwd_p2<B, 1><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2, c.d_bsel,
-                                               c.d_csl);
+        k_fwd_p2<B, 1><<<g2, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf, c.d_bsel, c.d_csl);
     else if (J.mode == NTT_DIVIDE2)
-        k_fwd_p2<B, 2><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2, c.d_bsel,
-                                               c.d_csl);
+        k_fwd_p2<B, 2><<<g2, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf, c.d_bsel, c.d_csl);
     else
-        k_fwd_p2<B, 0><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2, c.d_bsel,
-                                               c.d_csl);
+        k_fwd_p2<B, 0><<<g2, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf, c.d_bsel, c.d_csl);
     UH_LAUNCH_CHECK();
 }
 
@@ -455,10 +597,10 @@ void run_inv(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
     if (J.mode != NTT_PLAIN) throw std::invalid_argument("inverse NTT: plain limbs only");
     Scratch tmp((size_t)limbs * c.n * 8, s);
     dim3 g1((1u << B) / 32, limbs), g2((1u << A) / P2<B>::G, limbs);
-    k_inv_pa<B><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_bsel,
+    k_inv_pa<B><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwf, c.d_bsel,
                                         c.d_csl);
     UH_LAUNCH_CHECK();
-    k_inv_pb<A><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2);
+    k_inv_pb<A><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwf);
     UH_LAUNCH_CHECK();
 }
 
