@@ -138,6 +138,7 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
         }
     std::vector<ulonglong2> tw2((size_t)count * n), itw2((size_t)count * n);
     std::vector<double2> twf((size_t)count * n, make_double2(0, 0)), itwf((size_t)count * n, make_double2(0, 0));
+    std::vector<double> twd((size_t)count * n, 0.0), itwd((size_t)count * n, 0.0);
     for (size_t i = 0; i < tw2.size(); i++) {
         tw2[i] = make_ulonglong2(tw[i], tws[i]);
         itw2[i] = make_ulonglong2(itw[i], itws[i]);
@@ -145,6 +146,8 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
         if ((q >> 42) == 0) {  // FP64-pipe NTT limbs (ntt_fast.cu, fp_limb)
             twf[i] = make_double2((double)tw[i], (double)tw[i] / (double)q);
             itwf[i] = make_double2((double)itw[i], (double)itw[i] / (double)q);
+            twd[i] = (double)tw[i];
+            itwd[i] = (double)itw[i];
         }
     }
     if (c->n1) {
@@ -161,6 +164,8 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
     c->d_itw2 = upload(itw2);
     c->d_twf = upload(twf);
     c->d_itwf = upload(itwf);
+    c->d_twd = upload(twd);
+    c->d_itwd = upload(itwd);
     c->d_mods = upload(mods);
     c->d_psi = upload(tw);
     c->d_psis = upload(tws);
@@ -177,7 +182,7 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
 void ctx_destroy(Ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    for (void *p : {(void *)c->d_pmod, (void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_twf, (void *)c->d_itwf, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
+    for (void *p : {(void *)c->d_pmod, (void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_twf, (void *)c->d_itwf, (void *)c->d_twd, (void *)c->d_itwd, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
                     (void *)c->d_ipsi, (void *)c->d_ipsis,
                     (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_pos, (void *)c->d_neg})
         if (p) cudaFree(p);

@@ -217,24 +217,40 @@ template <> struct Arith<true> {
 };
 __device__ __forceinline__ bool fp_limb(uint64_t q) { return (q >> 42) == 0; }
 
+// Twiddle accessors: (local stage m', index j) -> twiddle of global index m' * f + j.
+template <typename W>
+struct TwG {  // global table (read-only path)
+    const W *__restrict__ T;
+    int f;
+    __device__ W operator()(int m, int j) const { return tw(T, m * f + j); }
+};
+struct TwS {  // FP64 limbs: w staged in shared memory at [m' + j] (m' + j < 256), w / q formed on the fly
+    const double *t;
+    double qinv;
+    __device__ double2 operator()(int m, int j) const {
+        const double w = t[m + j];
+        return make_double2(w, w * qinv);
+    }
+};
+
 // forward radix network on R register values (elements base + S*x), stages with
-// distance dx = R/2 .. 1; twiddle index = m0 * (1 << s) + off(s) + x / (2 dx)
-template <int R, typename V, typename W, typename Q>
-__device__ __forceinline__ void fwd_strided(V (&v)[R], const W *__restrict__ T, int m0, int moff, Q q) {
+// distance dx = R/2 .. 1; twiddle (m, off(s) + x / (2 dx)), m = m0 * (1 << s)
+template <int R, typename V, typename TA, typename Q>
+__device__ __forceinline__ void fwd_strided(V (&v)[R], const TA &ta, int m0, int moff, Q q) {
     int m = m0, off = moff;
 #pragma unroll
     for (int dx = R / 2; dx >= 1; dx >>= 1) {
 #pragma unroll
         for (int x = 0; x < R; x++) {
             if (x & dx) continue;
-            bf_ct(v[x], v[x + dx], tw(T, m + off + x / (2 * dx)), q);
+            bf_ct(v[x], v[x + dx], ta(m, off + x / (2 * dx)), q);
         }
         m <<= 1;
         off <<= 1;
     }
 }
-template <int R, typename V, typename W, typename Q>
-__device__ __forceinline__ void inv_strided(V (&v)[R], const W *__restrict__ T, int mlast, int offlast, Q q) {
+template <int R, typename V, typename TA, typename Q>
+__device__ __forceinline__ void inv_strided(V (&v)[R], const TA &ta, int mlast, int offlast, Q q) {
     // mirror of fwd_strided: distances 1 .. R/2, m halves each stage
     int m = mlast, off = offlast;
 #pragma unroll
@@ -242,7 +258,7 @@ __device__ __forceinline__ void inv_strided(V (&v)[R], const W *__restrict__ T, 
 #pragma unroll
         for (int x = 0; x < R; x++) {
             if (x & dx) continue;
-            bf_gs(v[x], v[x + dx], tw(T, m + off + x / (2 * dx)), q);
+            bf_gs(v[x], v[x + dx], ta(m, off + x / (2 * dx)), q);
         }
         m >>= 1;
         off >>= 1;
@@ -280,7 +296,7 @@ __device__ __forceinline__ void fwd_p1_body(uint64_t *sm, const LimbInfo &li, co
         V v[C::R1];
 #pragma unroll
         for (int x = 0; x < C::R1; x++) v[x] = AR::in(load_t<LM>(li, (size_t)(r0 + C::S1 * x) * n2 + col, m, red));
-        fwd_strided<C::R1>(v, T, 1, 0, ar.qv());
+        fwd_strided<C::R1>(v, TwG<typename AR::W>{T, 1}, 1, 0, ar.qv());
 #pragma unroll
         for (int x = 0; x < C::R1; x++) sm[(r0 + C::S1 * x) * 32 + lane] = AR::raw(v[x]);
     }
@@ -293,7 +309,7 @@ __device__ __forceinline__ void fwd_p1_body(uint64_t *sm, const LimbInfo &li, co
 #pragma unroll
         for (int z = 0; z < C::R2; z++) v[z] = AR::raw_in(sm[(r0 + z) * 32 + lane]);
         // stages m = R1 .. N1/2 on contiguous rows r0 + z: twiddle m + (r0 + z) / (2t)
-        fwd_strided<C::R2>(v, T, C::R1, grp, ar.qv());
+        fwd_strided<C::R2>(v, TwG<typename AR::W>{T, 1}, C::R1, grp, ar.qv());
 #pragma unroll
         for (int z = 0; z < C::R2; z++) out[(size_t)(r0 + z) * n2 + col] = AR::raw(v[z]);
     }
@@ -305,14 +321,14 @@ __global__ void __launch_bounds__(kThreads) k_fwd_p1(NttJob J, uint64_t *__restr
                                                     const ulonglong2 *__restrict__ twd,
                                                     const double2 *__restrict__ twf) {
     __shared__ uint64_t sm[P1<A>::N1 * 32];
-    const int f = blockIdx.y, lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int f = J.f0 + blockIdx.y, lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const int n2 = 1 << (logn - A);
     const int col = blockIdx.x * 32 + lane;
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
     const bool red = LM == 1 && ((li.qsrc - 1) >> 1) >= m.q;
     const Tw tws{twd + ((size_t)li.mod << logn), twf + ((size_t)li.mod << logn)};
-    uint64_t *out = tmp + ((size_t)f << logn);
+    uint64_t *out = tmp + ((size_t)blockIdx.y << logn);
     if (fp_limb(m.q))
         fwd_p1_body<A, LM, true>(sm, li, m, red, tws, out, n2, col, lane, wq);
     else
@@ -335,7 +351,7 @@ __device__ __forceinline__ void inv_pb_body(uint64_t *sm, const LimbInfo &li, co
 #pragma unroll
         for (int z = 0; z < C::R2; z++) v[z] = AR::raw_in(in[(size_t)(r0 + z) * n2 + col]);
         // mirror of the forward contiguous stages: last stage m = N1/2 with offset grp * (R2/2)
-        inv_strided<C::R2>(v, T, C::N1 / 2, grp * (C::R2 / 2), ar.qv());
+        inv_strided<C::R2>(v, TwG<typename AR::W>{T, 1}, C::N1 / 2, grp * (C::R2 / 2), ar.qv());
 #pragma unroll
         for (int z = 0; z < C::R2; z++) sm[(r0 + z) * 32 + lane] = AR::raw(v[z]);
     }
@@ -348,7 +364,7 @@ __device__ __forceinline__ void inv_pb_body(uint64_t *sm, const LimbInfo &li, co
         V v[C::R1];
 #pragma unroll
         for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(sm[(r0 + C::S1 * x) * 32 + lane]);
-        inv_strided<C::R1>(v, T, C::R1 / 2, 0, ar.qv());
+        inv_strided<C::R1>(v, TwG<typename AR::W>{T, 1}, C::R1 / 2, 0, ar.qv());
 #pragma unroll
         for (int x = 0; x < C::R1; x++) {
             uint64_t r;
@@ -367,13 +383,13 @@ __global__ void __launch_bounds__(kThreads) k_inv_pb(NttJob J, const uint64_t *_
                                                     const ulonglong2 *__restrict__ itwd,
                                                     const double2 *__restrict__ itwf) {
     __shared__ uint64_t sm[P1<A>::N1 * 32];
-    const int f = blockIdx.y, lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int f = J.f0 + blockIdx.y, lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const int n2 = 1 << (logn - A);
     const int col = blockIdx.x * 32 + lane;
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
     const Tw tws{itwd + ((size_t)li.mod << logn), itwf + ((size_t)li.mod << logn)};
-    const uint64_t *in = tmp + ((size_t)f << logn);
+    const uint64_t *in = tmp + ((size_t)blockIdx.y << logn);
     if (fp_limb(m.q))
         inv_pb_body<A, true>(sm, li, m, tws, in, n2, col, lane, wq);
     else
@@ -409,22 +425,44 @@ __device__ __forceinline__ size_t cta_slot(int i, int logn) {
     return ((size_t)h << (logn - 1)) + js + (i % C::G) + (size_t)(n1 / 2) * (i / C::G);
 }
 
+// FP64 limbs: stage the pass-2 twiddles of the CTA's G blocks in shared memory (w only,
+// coalesced runs: stage m' of block blk uses T[m' (n1 + blk) + j], j < m'), so the
+// butterflies read them at shared-memory latency instead of L2 latency.
+template <int B>
+__device__ __forceinline__ void stage_twiddles(double *tws, const double *__restrict__ Tw, const int *sel, int n1,
+                                               int tid) {
+    using C = P2<B>;
+    static_assert(kThreads % C::N2 == 0, "a thread keeps one in-block index r");
+    const int r = tid & (C::N2 - 1);  // the same for all of this thread's entries
+    if (r == 0) return;
+    const int mp = 1 << (31 - __clz(r)), j = r - mp;
+    const double *src = Tw + j;
+#pragma unroll
+    for (int g = tid >> B; g < C::G; g += kThreads / C::N2) tws[(g << B) + r] = __ldg(src + (size_t)mp * (n1 + sel[g]));
+}
+
 // pass 2 forward stages: tmp (pass-1 output) -> canonical residues in shared memory
 template <int B, bool FP>
-__device__ __forceinline__ void fwd_p2_body(uint64_t *sm, const Mod &m, const Tw &tws, const uint64_t *in,
-                                            const int *sel, int n1, int tid) {
+__device__ __forceinline__ void fwd_p2_body(uint64_t *sm, const double *tws, const Mod &m, const Tw &tw2,
+                                            const uint64_t *in, const int *sel, int n1, int tid) {
     using C = P2<B>;
     using AR = Arith<FP>;
     using V = typename AR::V;
     const AR ar(m.q);
-    const auto *T = pick<FP>(tws);
+    const auto *T = pick<FP>(tw2);
+    auto acc = [&](int g, int blk) {
+        if constexpr (FP)
+            return TwS{tws + g * C::N2, ar.qinv};
+        else
+            return TwG<ulonglong2>{T, n1 + blk};
+    };
     {
         const int g = tid / C::S, c0 = tid % C::S, blk = sel[g];
         V v[C::R1];
 #pragma unroll
         for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(in[(size_t)blk * C::N2 + c0 + C::S * x]);
         // local stages m' = 1..8: global twiddle index m' * (n1 + blk) + x / (2 dx)
-        fwd_strided<C::R1>(v, T, n1 + blk, 0, ar.qv());
+        fwd_strided<C::R1>(v, acc(g, blk), 1, 0, ar.qv());
 #pragma unroll
         for (int x = 0; x < C::R1; x++) sm[C::at(g, c0 + C::S * x)] = AR::raw(v[x]);
     }
@@ -438,34 +476,44 @@ __device__ __forceinline__ void fwd_p2_body(uint64_t *sm, const Mod &m, const Tw
 #pragma unroll
         for (int z = 0; z < C::R2; z++) v[z] = AR::raw_in(sm[C::at(g, c + z)]);
         // local stages m' = 16 .. N2/2 on contiguous c + z
-        fwd_strided<C::R2>(v, T, 16 * (n1 + blk), (c / C::R2), ar.qv());
+        fwd_strided<C::R2>(v, acc(g, blk), 16, (c / C::R2), ar.qv());
 #pragma unroll
         for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = ar.canon(v[z]);
     }
     __syncthreads();
 }
 
+template <int B>
+constexpr size_t p2_smem() {  // data tiles + FP64 twiddle stage
+    return (size_t)(P2<B>::G * P2<B>::PAD + P2<B>::G * P2<B>::N2) * 8;
+}
+
 template <int B, int EM>
 __global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ twd,
-                                                    const double2 *__restrict__ twf,
+                                                    const double *__restrict__ twdd,
                                                     const int32_t *__restrict__ bsel,
                                                     const int32_t *__restrict__ csl) {
     using C = P2<B>;
-    __shared__ uint64_t sm[C::G * C::PAD];
-    const int f = blockIdx.y, tid = threadIdx.x;
+    extern __shared__ uint64_t dsm[];
+    uint64_t *sm = dsm;
+    double *tws = reinterpret_cast<double *>(dsm + C::G * C::PAD);
+    const int f = J.f0 + blockIdx.y, tid = threadIdx.x;
     const int n1 = 1 << (logn - B);
     const int *sel = bsel + blockIdx.x * C::G;
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
     const uint64_t q = m.q;
-    const Tw tws{twd + ((size_t)li.mod << logn), twf + ((size_t)li.mod << logn)};
-    const uint64_t *in = tmp + ((size_t)f << logn);
-    if (fp_limb(q))
-        fwd_p2_body<B, true>(sm, m, tws, in, sel, n1, tid);
-    else
-        fwd_p2_body<B, false>(sm, m, tws, in, sel, n1, tid);
+    const Tw tw2{twd + ((size_t)li.mod << logn), nullptr};
+    const uint64_t *in = tmp + ((size_t)blockIdx.y << logn);
+    if (fp_limb(q)) {
+        stage_twiddles<B>(tws, twdd + ((size_t)li.mod << logn), sel, n1, tid);
+        __syncthreads();
+        fwd_p2_body<B, true>(sm, tws, m, tw2, in, sel, n1, tid);
+    } else {
+        fwd_p2_body<B, false>(sm, tws, m, tw2, in, sel, n1, tid);
+    }
     // coalesced slot-order epilogue: a thread's 16 slot-table (and DIVIDE input) loads are
     // issued together, then the shared-memory gathers and the stores
     constexpr int E = EM ? 8 : 16;  // loads in flight per round (register budget)
@@ -496,13 +544,19 @@ __global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *_
 
 // inverse pass A stages: canonical residues in shared memory -> tmp (pass-B input)
 template <int B, bool FP>
-__device__ __forceinline__ void inv_pa_body(uint64_t *sm, const Mod &m, const Tw &tws, uint64_t *out,
-                                            const int *sel, int n1, int tid) {
+__device__ __forceinline__ void inv_pa_body(uint64_t *sm, const double *tws, const Mod &m, const Tw &tw2,
+                                            uint64_t *out, const int *sel, int n1, int tid) {
     using C = P2<B>;
     using AR = Arith<FP>;
     using V = typename AR::V;
     const AR ar(m.q);
-    const auto *T = pick<FP>(tws);
+    const auto *T = pick<FP>(tw2);
+    auto acc = [&](int g, int blk) {
+        if constexpr (FP)
+            return TwS{tws + g * C::N2, ar.qinv};
+        else
+            return TwG<ulonglong2>{T, n1 + blk};
+    };
 #pragma unroll
     for (int gi = 0; gi < C::GC; gi++) {
         const int grp = tid + kThreads * gi;
@@ -512,7 +566,7 @@ __device__ __forceinline__ void inv_pa_body(uint64_t *sm, const Mod &m, const Tw
 #pragma unroll
         for (int z = 0; z < C::R2; z++) v[z] = AR::in(sm[C::at(g, c + z)]);
         // mirror of the forward contiguous stages: last local stage m' = N2/2
-        inv_strided<C::R2>(v, T, (C::N2 / 2) * (n1 + blk), (c / C::R2) * (C::R2 / 2), ar.qv());
+        inv_strided<C::R2>(v, acc(g, blk), C::N2 / 2, (c / C::R2) * (C::R2 / 2), ar.qv());
 #pragma unroll
         for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = AR::raw(v[z]);
     }
@@ -522,7 +576,7 @@ __device__ __forceinline__ void inv_pa_body(uint64_t *sm, const Mod &m, const Tw
         V v[C::R1];
 #pragma unroll
         for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(sm[C::at(g, c0 + C::S * x)]);
-        inv_strided<C::R1>(v, T, 8 * (n1 + blk), 0, ar.qv());
+        inv_strided<C::R1>(v, acc(g, blk), 8, 0, ar.qv());
 #pragma unroll
         for (int x = 0; x < C::R1; x++) {
             V r = v[x];
@@ -536,17 +590,21 @@ template <int B>
 __global__ void __launch_bounds__(kThreads) k_inv_pa(NttJob J, uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ itwd,
-                                                    const double2 *__restrict__ itwf,
+                                                    const double *__restrict__ itwdd,
                                                     const int32_t *__restrict__ bsel,
                                                     const int32_t *__restrict__ csl) {
     using C = P2<B>;
-    __shared__ uint64_t sm[C::G * C::PAD];
-    const int f = blockIdx.y, tid = threadIdx.x;
+    extern __shared__ uint64_t dsm[];
+    uint64_t *sm = dsm;
+    double *tws = reinterpret_cast<double *>(dsm + C::G * C::PAD);
+    const int f = J.f0 + blockIdx.y, tid = threadIdx.x;
     const int n1 = 1 << (logn - B);
     const int *sel = bsel + blockIdx.x * C::G;
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
-    const Tw tws{itwd + ((size_t)li.mod << logn), itwf + ((size_t)li.mod << logn)};
+    const Tw tw2{itwd + ((size_t)li.mod << logn), nullptr};
+    const bool fp = fp_limb(m.q);
+    if (fp) stage_twiddles<B>(tws, itwdd + ((size_t)li.mod << logn), sel, n1, tid);
     // coalesced slot-order gather into the blocks' shared-memory tiles (plain limbs: the only
     // inverse mode); all of a thread's loads are issued before the shared-memory stores
     {
@@ -563,45 +621,86 @@ __global__ void __launch_bounds__(kThreads) k_inv_pa(NttJob J, uint64_t *__restr
         for (int e = 0; e < E; e++) sm[C::at((tid + kThreads * e) % C::G, cs[e])] = a[e];
     }
     __syncthreads();
-    uint64_t *out = tmp + ((size_t)f << logn);
-    if (fp_limb(m.q))
-        inv_pa_body<B, true>(sm, m, tws, out, sel, n1, tid);
+    uint64_t *out = tmp + ((size_t)blockIdx.y << logn);
+    if (fp)
+        inv_pa_body<B, true>(sm, tws, m, tw2, out, sel, n1, tid);
     else
-        inv_pa_body<B, false>(sm, m, tws, out, sel, n1, tid);
+        inv_pa_body<B, false>(sm, tws, m, tw2, out, sel, n1, tid);
+}
+
+template <auto K>
+void p2_attr(size_t smem) {  // opt in to > 48 KB dynamic shared memory, once per kernel instance
+    static bool done = false;
+    if (!done) {
+        UH_CHECK(cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        done = true;
+    }
+}
+
+// Limbs are transformed in chunks whose pass-1 -> pass-2 intermediate (one reused
+// scratch buffer) stays resident in the 126 MB L2, so the intermediate never
+// round-trips through HBM.
+inline int ntt_chunk(const Ctx &c, int limbs) {
+    static const int env = [] {
+        const char *e = getenv("UH_NTT_CHUNK_MB");
+        return e ? atoi(e) : 0;  // measured: chunking starves the grid (B200), off by default
+    }();
+    if (env <= 0) return limbs;
+    const int ch = (int)(((size_t)env << 20) / (c.n * 8));
+    return std::max(1, std::min(limbs, ch));
 }
 
 template <int A, int B>
-void run_fwd(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
-    Scratch tmp((size_t)limbs * c.n * 8, s);
-    dim3 g1((1u << B) / 32, limbs), g2((1u << A) / P2<B>::G, limbs);
+void run_fwd(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
+    const int ch = ntt_chunk(c, limbs);
+    Scratch tmp((size_t)ch * c.n * 8, s);
     uint64_t *t = tmp.as<uint64_t>();
     const int ln = (int)c.logn;
-    if (J.mode == NTT_PLAIN)
-        k_fwd_p1<A, 0><<<g1, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf);
-    else if (J.mode == NTT_DIVIDE2)
-        k_fwd_p1<A, 2><<<g1, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf);
-    else
-        k_fwd_p1<A, 1><<<g1, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf);
-    UH_LAUNCH_CHECK();
-    if (J.mode == NTT_DIVIDE)
-        k_fwd_p2<B, 1><<<g2, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf, c.d_bsel, c.d_csl);
-    else if (J.mode == NTT_DIVIDE2)
-        k_fwd_p2<B, 2><<<g2, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf, c.d_bsel, c.d_csl);
-    else
-        k_fwd_p2<B, 0><<<g2, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf, c.d_bsel, c.d_csl);
-    UH_LAUNCH_CHECK();
+    constexpr size_t sm2 = p2_smem<B>();
+    for (int f0 = 0; f0 < limbs; f0 += ch) {
+        NttJob J = J0;
+        J.f0 = f0;
+        const int nl = std::min(ch, limbs - f0);
+        dim3 g1((1u << B) / 32, nl), g2((1u << A) / P2<B>::G, nl);
+        if (J.mode == NTT_PLAIN)
+            k_fwd_p1<A, 0><<<g1, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf);
+        else if (J.mode == NTT_DIVIDE2)
+            k_fwd_p1<A, 2><<<g1, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf);
+        else
+            k_fwd_p1<A, 1><<<g1, kThreads, 0, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twf);
+        UH_LAUNCH_CHECK();
+        if (J.mode == NTT_DIVIDE) {
+            p2_attr<k_fwd_p2<B, 1>>(sm2);
+            k_fwd_p2<B, 1><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_bsel, c.d_csl);
+        } else if (J.mode == NTT_DIVIDE2) {
+            p2_attr<k_fwd_p2<B, 2>>(sm2);
+            k_fwd_p2<B, 2><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_bsel, c.d_csl);
+        } else {
+            p2_attr<k_fwd_p2<B, 0>>(sm2);
+            k_fwd_p2<B, 0><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_bsel, c.d_csl);
+        }
+        UH_LAUNCH_CHECK();
+    }
 }
 
 template <int A, int B>
-void run_inv(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
-    if (J.mode != NTT_PLAIN) throw std::invalid_argument("inverse NTT: plain limbs only");
-    Scratch tmp((size_t)limbs * c.n * 8, s);
-    dim3 g1((1u << B) / 32, limbs), g2((1u << A) / P2<B>::G, limbs);
-    k_inv_pa<B><<<g2, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwf, c.d_bsel,
-                                        c.d_csl);
-    UH_LAUNCH_CHECK();
-    k_inv_pb<A><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwf);
-    UH_LAUNCH_CHECK();
+void run_inv(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
+    if (J0.mode != NTT_PLAIN) throw std::invalid_argument("inverse NTT: plain limbs only");
+    const int ch = ntt_chunk(c, limbs);
+    Scratch tmp((size_t)ch * c.n * 8, s);
+    constexpr size_t sm2 = p2_smem<B>();
+    p2_attr<k_inv_pa<B>>(sm2);
+    for (int f0 = 0; f0 < limbs; f0 += ch) {
+        NttJob J = J0;
+        J.f0 = f0;
+        const int nl = std::min(ch, limbs - f0);
+        dim3 g1((1u << B) / 32, nl), g2((1u << A) / P2<B>::G, nl);
+        k_inv_pa<B><<<g2, kThreads, sm2, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwd,
+                                              c.d_bsel, c.d_csl);
+        UH_LAUNCH_CHECK();
+        k_inv_pb<A><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwf);
+        UH_LAUNCH_CHECK();
+    }
 }
 
 }  // namespace

@@ -20,6 +20,7 @@ enum NttMode : int { NTT_PLAIN = 0, NTT_MODUP = 1, NTT_DIVIDE = 2, NTT_DIVIDE2 =
 //          dst[p][k] = (in[p][k] - y) * q_top^-1 * P^-1.
 struct NttJob {
     int mode = NTT_PLAIN;
+    int f0 = 0;  // first limb of this launch (chunked launches)
     int nl = 1, nq = 1, base = 0, sp = 0;
     const uint64_t *src = nullptr;
     int src_ps = 1;
