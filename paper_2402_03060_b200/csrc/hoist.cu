@@ -19,6 +19,7 @@
 // CTA: W warps; lane <-> coefficient n (coalesced 256-byte rows of every
 // operand); grid = (B/TB tiles fastest, N/32 coefficient tiles, L+1 limbs),
 // so CTAs sharing the same masks/keys run back to back and hit L2.
+#include <type_traits>
 #include "ops.cuh"
 
 namespace uh {
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
                   const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
                   const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
                   const int32_t *__restrict__ shifts, int B, int I, int T, int O, int diag, int L, int sp, int logn,
-                  const Mod *__restrict__ mods) {
+                  const Mod *__restrict__ mods, int z0 = 0, int zstep = 1) {
     __shared__ uint64_t sv[2][kTChunk][kTBatch][2][32];
     __shared__ const uint64_t *s_key[kMaxTerms];
     __shared__ uint32_t s_shift[kMaxTerms];
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b0 = blockIdx.x * kTBatch;
     const uint32_t n = blockIdx.y * 32 + lane;
-    const int k = blockIdx.z;
+    const int k = z0 + blockIdx.z * zstep;
     const uint32_t N = 1u << logn, half = N >> 1;
     const Mod m = mods[limb_mod(k, L, 0, sp)];
     const bool qlimb = k < L;
@@ -244,6 +245,190 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
 }
 
 // ---------------------------------------------------------------------------
+// FP64-pipe phase B for masked dense layers on limbs with q < 2^41.
+// Operands split at 21 bits (a = a1 2^21 + a0, a0 < 2^21, a1 < 2^20) make every
+// partial product an integer below 2^42, so three FP64 accumulators per
+// (output, ciphertext, component)
+//   S2 += a1 b1,   S1 += a1 b0 + a0 b1,   S0 += a0 b0
+// stay exact for up to 2^11 terms: 4 DFMA per multiply-accumulate instead of
+// ~11 IMAD-pipe slots for the 128-bit integer MAC, on an otherwise idle pipe.
+// The weight masks are split on load; the phase-A terms are split once when
+// they are staged in shared memory (dynamic, 2 x the integer staging).  Phase A
+// (key products) stays on the integer pipe.  Limbs k = z0 + blockIdx.z * zstep.
+constexpr double kTwo52d = 4503599627370496.0;
+__device__ __forceinline__ double lo21(uint64_t x) {  // exact double of x mod 2^21
+    return __longlong_as_double((long long)((x & 0x1FFFFFull) | 0x4330000000000000ull)) - kTwo52d;
+}
+__device__ __forceinline__ double hi21(uint64_t x) {  // exact double of x >> 21 (x < 2^52)
+    return __longlong_as_double((long long)((x >> 21) | 0x4330000000000000ull)) - kTwo52d;
+}
+__device__ __forceinline__ uint64_t d2u_exact(double v) {  // 0 <= v < 2^52, integer-valued
+    return (uint64_t)__double_as_longlong(v + kTwo52d) ^ 0x4330000000000000ull;
+}
+struct AccF {
+    double s0, s1, s2;
+    __device__ __forceinline__ void zero() { s0 = s1 = s2 = 0.0; }
+    __device__ __forceinline__ void mac(double a0, double a1, double b0, double b1) {
+        s2 = fma(a1, b1, s2);
+        s1 = fma(a1, b0, s1);
+        s1 = fma(a0, b1, s1);
+        s0 = fma(a0, b0, s0);
+    }
+    // (S2 2^42 + S1 2^21 + S0) mod q; c21 = 2^21 mod q, c42 = 2^42 mod q
+    __device__ __forceinline__ uint64_t reduce(const Mod &m, uint64_t c21, uint64_t c42) const {
+        const uint64_t u2 = d2u_exact(s2), u1 = d2u_exact(s1), u0 = d2u_exact(s0);
+        uint64_t r = mulmod(csub(barrett_lite(u2, m), m.q), c42, m);
+        r = addmod(r, mulmod(csub(barrett_lite(u1, m), m.q), c21, m), m.q);
+        return addmod(r, csub(barrett_lite(u0, m), m.q), m.q);
+    }
+};
+constexpr int kFpMaxTerms = 2048;  // exactness bound of the split accumulators
+
+template <int PPW, int W>
+__global__ void __launch_bounds__(W * 32, 1)
+    k_hoisted_fp(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
+                 const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
+                 const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
+                 const int32_t *__restrict__ shifts, int B, int I, int T, int O, int L, int sp, int logn,
+                 const Mod *__restrict__ mods, int z0, int zstep) {
+    extern __shared__ double svf[];  // [2][kTChunk][kTBatch][2 comps][2 halves][32]
+    __shared__ const uint64_t *s_key[kMaxTerms];
+    __shared__ uint32_t s_shift[kMaxTerms];
+    __shared__ uint32_t s_kstride[kMaxTerms];
+    auto SV = [&](int buf, int qc, int bt, int c, int h) -> double * {
+        return svf + ((((buf * kTChunk + qc) * kTBatch + bt) * 2 + c) * 2 + h) * 32;
+    };
+    const int LP = L + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b0 = blockIdx.x * kTBatch;
+    const uint32_t n = blockIdx.y * 32 + lane;
+    const int k = z0 + blockIdx.z * zstep;
+    const uint32_t N = 1u << logn, half = N >> 1;
+    const Mod m = mods[limb_mod(k, L, 0, sp)];
+    const bool qlimb = k < L;
+    const uint64_t P = mods[sp].q;
+    const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
+    const int Q = I * T;
+    const int npairs = O * kTBatch;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        s_key[t] = keys[t];
+        s_shift[t] = (uint32_t)shifts[t];
+        s_kstride[t] = (uint32_t)key_limbs[t] << logn;
+    }
+    __syncthreads();
+    AccF acc[PPW][2];
+#pragma unroll
+    for (int j = 0; j < PPW; j++) {
+        acc[j][0].zero();
+        acc[j][1].zero();
+    }
+    int buf = 0;
+    constexpr int ITEMS = kTChunk * kTBatch / W;
+    static_assert(ITEMS * W == kTChunk * kTBatch, "phase-A items must tile the chunk");
+    constexpr int PB = PPW == 4 ? 2 : PPW, PO = PPW / PB, WB = kTBatch / PB;
+    const int o_a = (warp / WB) * PO, b_a = (warp % WB) * PB;
+    const bool warp_active = o_a < O && warp * PPW < npairs;
+    const uint32_t dstride = (uint32_t)LP << logn;
+    const uint32_t mask_row = ((uint32_t)k << logn) + n;
+    int i0 = 0, t0 = 0;
+    for (int q0 = 0; q0 < Q; q0 += kTChunk) {
+        uint64_t mpre[kTChunk][PO];
+#pragma unroll
+        for (int qc = 0; qc < kTChunk; qc++)
+#pragma unroll
+            for (int d = 0; d < PO; d++)
+                mpre[qc][d] = (warp_active && o_a + d < O && q0 + qc < Q)
+                                  ? masks[(((uint32_t)(o_a + d) * Q + q0 + qc) * dstride) + mask_row]
+                                  : 0;
+        // ---- phase A (integer pipe), terms staged split into 21-bit halves ----
+#pragma unroll
+        for (int ii = 0; ii < ITEMS; ii++) {
+            const int it = threadIdx.x + ii * W * 32;
+            const int ln = it & 31, rest = it >> 5;
+            const int bt = rest % kTBatch, qc = rest / kTBatch;
+            const int q = q0 + qc, b = b0 + bt;
+            uint64_t v0 = 0, v1 = 0;
+            if (q < Q && b < B) {
+                int i = i0, t = t0 + qc;
+                while (t >= T) {
+                    t -= T;
+                    i++;
+                }
+                const uint32_t nn = blockIdx.y * 32 + ln;
+                const uint32_t ib = (uint32_t)(i * B + b);
+                const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
+                const uint32_t r = s_shift[t];
+                if (r == 0) {
+                    if (qlimb) {
+                        v0 = mulmod(Pk, c0[nn], m);
+                        v1 = mulmod(Pk, c0[((uint32_t)xls << logn) + nn], m);
+                    }
+                } else {
+                    const uint32_t src = rot_index(nn, half, r);
+                    const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
+                    const uint32_t ks = s_kstride[t];
+                    const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + nn;
+                    Acc a0, a1;
+                    a0.zero();
+                    a1.zero();
+                    ks_dot<UH_KS_GROUP_FOR(PPW, W)>(a0, a1, Di, dstride, k0, ks, L);
+                    if (qlimb) a0.mac(Pk, c0[src]);
+                    v0 = a0.reduce(m);
+                    v1 = a1.reduce(m);
+                }
+            }
+            SV(buf, qc, bt, 0, 0)[ln] = lo21(v0);
+            SV(buf, qc, bt, 0, 1)[ln] = hi21(v0);
+            SV(buf, qc, bt, 1, 0)[ln] = lo21(v1);
+            SV(buf, qc, bt, 1, 1)[ln] = hi21(v1);
+        }
+        __syncthreads();
+        // ---- phase B (FP64 pipe) ----
+        const int qn = min(kTChunk, Q - q0);
+#pragma unroll
+        for (int qc = 0; qc < kTChunk; qc++) {
+            if (qc >= qn) break;
+            if (warp_active) {
+                double ml[PO], mh[PO];
+#pragma unroll
+                for (int d = 0; d < PO; d++) {
+                    ml[d] = lo21(mpre[qc][d]);
+                    mh[d] = hi21(mpre[qc][d]);
+                }
+#pragma unroll
+                for (int db = 0; db < PB; db++) {
+                    const int bt = b_a + db;
+                    const double v0l = SV(buf, qc, bt, 0, 0)[lane], v0h = SV(buf, qc, bt, 0, 1)[lane];
+                    const double v1l = SV(buf, qc, bt, 1, 0)[lane], v1h = SV(buf, qc, bt, 1, 1)[lane];
+#pragma unroll
+                    for (int d = 0; d < PO; d++) {
+                        const int j = d * PB + db;
+                        acc[j][0].mac(ml[d], mh[d], v0l, v0h);
+                        acc[j][1].mac(ml[d], mh[d], v1l, v1h);
+                    }
+                }
+            }
+        }
+        buf ^= 1;
+        t0 += kTChunk;
+        while (t0 >= T) {
+            t0 -= T;
+            i0++;
+        }
+    }
+    const uint64_t c21 = (1ull << 21) % m.q, c42 = mulmod(c21, c21, m);
+#pragma unroll
+    for (int j = 0; j < PPW; j++) {
+        const int o = o_a + j / PB, b = b0 + b_a + j % PB;
+        if (warp_active && o < O && b < B) {
+            uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
+            dst[0] = acc[j][0].reduce(m, c21, c42);
+            dst[dstride] = acc[j][1].reduce(m, c21, c42);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Pipelined variant: the next chunk's operands (hoisted digits at the rotated
 // offsets, c0, and the Galois-key rows) are staged into shared memory with
 // cp.async while the current chunk is multiply-accumulated, so phase A reads
@@ -256,15 +441,17 @@ __device__ __forceinline__ void cp8(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int NW> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NW)); }
 
-template <int PPW, int W>
+// FPB: FP64-pipe phase B (split-operand accumulators, see AccF) for limbs with q < 2^41;
+// the rotated terms are then staged split in dynamic shared memory after the cp.async stages.
+template <int PPW, int W, bool FPB = false>
 __global__ void __launch_bounds__(W * 32, 1)
     k_hoisted_mac_cp(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
                      const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
                      const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
                      const int32_t *__restrict__ shifts, int B, int I, int T, int O, int diag, int L, int sp,
-                     int logn, const Mod *__restrict__ mods) {
+                     int logn, const Mod *__restrict__ mods, int z0 = 0, int zstep = 1) {
     extern __shared__ uint64_t dyn[];
-    __shared__ uint64_t sv[2][kTChunk][kTBatch][2][32];
+    __shared__ uint64_t sv[FPB ? 1 : 2][kTChunk][kTBatch][2][32];
     __shared__ const uint64_t *s_key[kMaxTerms];
     __shared__ uint32_t s_shift[kMaxTerms];
     __shared__ uint32_t s_kstride[kMaxTerms];
@@ -272,7 +459,7 @@ __global__ void __launch_bounds__(W * 32, 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b0 = blockIdx.x * kTBatch;
     const uint32_t n = blockIdx.y * 32 + lane;
-    const int k = blockIdx.z;
+    const int k = z0 + blockIdx.z * zstep;
     const uint32_t N = 1u << logn, half = N >> 1;
     const Mod m = mods[limb_mod(k, L, 0, sp)];
     const bool qlimb = k < L;
@@ -288,6 +475,10 @@ __global__ void __launch_bounds__(W * 32, 1)
     // stage layout (uint64 words): D [kTChunk][kTBatch][L][32], C [kTChunk][kTBatch][32], K [kTChunk][2L][32]
     const int szD = kTChunk * kTBatch * L * 32, szC = kTChunk * kTBatch * 32, szK = kTChunk * 2 * L * 32;
     const int stage = szD + szC + szK;
+    double *svf = reinterpret_cast<double *>(dyn + 2 * stage);  // FPB: [2][kTChunk][kTBatch][2][2][32]
+    auto SVF = [&](int bb, int qc, int bt, int c, int h) -> double * {
+        return svf + ((((bb * kTChunk + qc) * kTBatch + bt) * 2 + c) * 2 + h) * 32;
+    };
     __syncthreads();
 
     const uint32_t dstride = (uint32_t)LP << logn;
@@ -338,7 +529,8 @@ __global__ void __launch_bounds__(W * 32, 1)
         }
     };
 
-    Acc acc[PPW][2];
+    using AccT = std::conditional_t<FPB, AccF, Acc>;
+    AccT acc[PPW][2];
 #pragma unroll
     for (int j = 0; j < PPW; j++) {
         acc[j][0].zero();
@@ -396,19 +588,31 @@ __global__ void __launch_bounds__(W * 32, 1)
                     Acc a0, a1;
                     a0.zero();
                     a1.zero();
-#pragma unroll 4
+#pragma unroll (FPB ? 2 : 4)
                     for (int j = 0; j < L; j++) {
                         const uint64_t d = dD[j * 32];
                         a0.mac(d, kK[(2 * j) * 32]);
                         a1.mac(d, kK[(2 * j + 1) * 32]);
                     }
                     if (qlimb) a0.mac(Pk, sC[(qc * kTBatch + bt) * 32 + lane]);
-                    v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
-                    v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
+                    if constexpr (FPB) {
+                        v0 = a0.reduce(m);
+                        v1 = a1.reduce(m);
+                    } else {
+                        v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
+                        v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
+                    }
                 }
             }
-            sv[buf][qc][bt][0][lane] = v0;
-            sv[buf][qc][bt][1][lane] = v1;
+            if constexpr (FPB) {
+                SVF(buf, qc, bt, 0, 0)[lane] = lo21(v0);
+                SVF(buf, qc, bt, 0, 1)[lane] = hi21(v0);
+                SVF(buf, qc, bt, 1, 0)[lane] = lo21(v1);
+                SVF(buf, qc, bt, 1, 1)[lane] = hi21(v1);
+            } else {
+                sv[buf][qc][bt][0][lane] = v0;
+                sv[buf][qc][bt][1][lane] = v1;
+            }
         }
         __syncthreads();
         // ---- phase B ----
@@ -416,7 +620,29 @@ __global__ void __launch_bounds__(W * 32, 1)
 #pragma unroll
         for (int qc = 0; qc < kTChunk; qc++) {
             if (qc >= qn) break;
-            if (warp_active) {
+            if constexpr (FPB) {  // masks required on this path
+                if (warp_active) {
+                    double ml[PO], mh[PO];
+#pragma unroll
+                    for (int d = 0; d < PO; d++) {
+                        ml[d] = lo21(mpre[qc][d]);
+                        mh[d] = hi21(mpre[qc][d]);
+                    }
+#pragma unroll
+                    for (int db = 0; db < PB; db++) {
+                        const int bt = b_a + db;
+                        const double v0l = SVF(buf, qc, bt, 0, 0)[lane], v0h = SVF(buf, qc, bt, 0, 1)[lane];
+                        const double v1l = SVF(buf, qc, bt, 1, 0)[lane], v1h = SVF(buf, qc, bt, 1, 1)[lane];
+#pragma unroll
+                        for (int d = 0; d < PO; d++) {
+                            const int j = d * PB + db;
+                            acc[j][0].mac(ml[d], mh[d], v0l, v0h);
+                            acc[j][1].mac(ml[d], mh[d], v1l, v1h);
+                        }
+                    }
+                }
+                continue;
+            } else if (warp_active) {
 #pragma unroll
                 for (int db = 0; db < PB; db++) {
                     const int bt = b_a + db;
@@ -434,14 +660,16 @@ __global__ void __launch_bounds__(W * 32, 1)
                     }
                 }
             }
-            if (++since_fold == kFold) {
-                since_fold = 0;
+            if constexpr (!FPB) {
+                if (++since_fold == kFold) {
+                    since_fold = 0;
 #pragma unroll
-                for (int j = 0; j < PPW; j++)
-                    for (int cc = 0; cc < 2; cc++) {
-                        uint64_t rr = reduce128_lazy(acc[j][cc].hi64(), acc[j][cc].lo64(), m);
-                        acc[j][cc].set(rr, 0);
-                    }
+                    for (int j = 0; j < PPW; j++)
+                        for (int cc = 0; cc < 2; cc++) {
+                            uint64_t rr = reduce128_lazy(acc[j][cc].hi64(), acc[j][cc].lo64(), m);
+                            acc[j][cc].set(rr, 0);
+                        }
+                }
             }
         }
         buf ^= 1;
@@ -450,13 +678,23 @@ __global__ void __launch_bounds__(W * 32, 1)
         t0 = t1;
     }
     cp_wait<0>();
+    uint64_t c21 = 0, c42 = 0;
+    if constexpr (FPB) {
+        c21 = (1ull << 21) % m.q;
+        c42 = mulmod(c21, c21, m);
+    }
 #pragma unroll
     for (int j = 0; j < PPW; j++) {
         const int o = o_a + j / PB, b = b0 + b_a + j % PB;
         if (warp_active && o < O && b < B) {
             uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
-            dst[0] = acc[j][0].reduce(m);
-            dst[dstride] = acc[j][1].reduce(m);
+            if constexpr (FPB) {
+                dst[0] = acc[j][0].reduce(m, c21, c42);
+                dst[dstride] = acc[j][1].reduce(m, c21, c42);
+            } else {
+                dst[0] = acc[j][0].reduce(m);
+                dst[dstride] = acc[j][1].reduce(m);
+            }
         }
     }
 }
@@ -681,6 +919,53 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
                                                                 T, O, L, c.sp(), (int)c.logn, c.d_mods);
         UH_LAUNCH_CHECK();
         return;
+    }
+    // FP64-pipe phase B (k_hoisted_mac_cp<.., true>) for wide masked dense layers: the limbs with
+    // q < 2^41 run there, the others (q_0, P: 60-bit) through the integer kernel.  Opt-in
+    // (UH_HOIST_FP=1): measured slower on LeNet conv2 (B200, B=64: 89.9 vs 78.8 ms) -- the
+    // kernel is latency-bound in phase A, and the split accumulators cost registers.
+    static const bool fp_on = [] {
+        const char *e = getenv("UH_HOIST_FP");
+        return e && std::string(e) == "1";
+    }();
+    const int Qt = diag ? I : I * T;
+    if (fp_on && masks && !diag && O >= 3 && O <= 12 && Qt <= kFpMaxTerms && L >= 3 && L <= 8) {
+        bool mid_fp = true;  // limbs 1 .. L-1 (q_1 .. q_{L-1})
+        for (int kk = 1; kk < L; kk++) mid_fp = mid_fp && (c.h_q[kk] >> 41) == 0;
+        if (mid_fp) {
+            const int ppw = pairs > 48 ? 4 : (pairs > 24 ? 2 : 1);
+            // FP64 phase B runs inside the cp.async-pipelined kernel (k_hoisted_mac_cp<.., true>)
+            const size_t stage = (size_t)(kTChunk * kTBatch * L * 32 + kTChunk * kTBatch * 32 + kTChunk * 2 * L * 32) * 8;
+            const size_t smem_fp = 2 * stage + (size_t)2 * kTChunk * kTBatch * 2 * 2 * 32 * sizeof(double);
+            auto run = [&](auto ppw_tag, int z0, int zstep, int nz, bool fp) {
+                constexpr int PP = decltype(ppw_tag)::value;
+                dim3 g(grid.x, grid.y, nz);
+                if (fp) {
+                    static size_t configured = 0;
+                    if (smem_fp > configured) {
+                        UH_CHECK(cudaFuncSetAttribute(k_hoisted_mac_cp<PP, 24, true>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fp));
+                        configured = smem_fp;
+                    }
+                    k_hoisted_mac_cp<PP, 24, true><<<g, 24 * 32, smem_fp, s>>>(
+                        acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, diag, L, c.sp(), (int)c.logn,
+                        c.d_mods, z0, zstep);
+                } else {
+                    k_hoisted_mac<PP, 24><<<g, 24 * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I,
+                                                               T, O, diag, L, c.sp(), (int)c.logn, c.d_mods, z0,
+                                                               zstep);
+                }
+                UH_LAUNCH_CHECK();
+            };
+            auto both = [&](auto tag) {
+                run(tag, 1, 1, L - 1, true);   // q_1 .. q_{L-1}
+                run(tag, 0, L, 2, false);      // q_0 and P
+            };
+            if (ppw == 1) both(integral_constant<int, 1>());
+            else if (ppw == 2) both(integral_constant<int, 2>());
+            else both(integral_constant<int, 4>());
+            return;
+        }
     }
     if (O <= 12) {
         // measured (B200, N=2^15): 24 warps win when phase B is heavy (O >= 3), 8-warp CTAs when it is not
