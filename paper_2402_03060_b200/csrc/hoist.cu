@@ -858,6 +858,120 @@ __global__ void __launch_bounds__((kWSProd + kWSCons) * 32, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Direct variant for narrow layers (O <= 2: pooling rotation sums, flatten and
+// FC stages): one thread per (ciphertext, limb, coefficient) walks all terms
+// with everything in registers -- no shared-memory staging, no barriers.
+// Without masks (rotation sums) the key products of every term accumulate into
+// one 128-bit accumulator per component and are reduced once; with masks each
+// term is reduced and multiply-accumulated into the O output accumulators.
+// Warp w of the CTA serves ciphertext 8 * blockIdx.y + w at the same 32
+// coefficients, so key and mask rows are shared through L1; the coefficient
+// tile is the fastest grid dimension (rotated digit reads of neighbouring
+// tiles hit L2).
+template <int OM, bool MASKS>
+__global__ void __launch_bounds__(256, 4)
+    k_hoisted_direct(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
+                     const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
+                     const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
+                     const int32_t *__restrict__ shifts, int B, int I, int T, int O, int diag, int L, int sp,
+                     int logn, const Mod *__restrict__ mods) {
+    __shared__ const uint64_t *s_key[kMaxTerms];
+    __shared__ uint32_t s_shift[kMaxTerms];
+    __shared__ uint32_t s_kstride[kMaxTerms];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b = blockIdx.y * 8 + warp;
+    const uint32_t n = blockIdx.x * 32 + lane;
+    const int k = blockIdx.z;
+    const uint32_t N = 1u << logn, half = N >> 1;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        s_key[t] = keys[t];
+        s_shift[t] = (uint32_t)shifts[t];
+        s_kstride[t] = (uint32_t)key_limbs[t] << logn;
+    }
+    __syncthreads();
+    if (b >= B) return;
+    const int LP = L + 1;
+    const Mod m = mods[limb_mod(k, L, 0, sp)];
+    const bool qlimb = k < L;
+    const uint64_t P = mods[sp].q;
+    const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
+    const int Q = diag ? I : I * T;
+    const uint32_t dstride = (uint32_t)LP << logn;
+    const uint32_t mask_row = ((uint32_t)k << logn) + n;
+    Acc acc[OM][2];
+#pragma unroll
+    for (int o = 0; o < OM; o++) {
+        acc[o][0].zero();
+        acc[o][1].zero();
+    }
+    int i = 0, t = 0, since = 0;
+    for (int q = 0; q < Q; q++) {
+        if (diag) i = t = q;
+        const uint32_t ib = (uint32_t)(i * B + b);
+        const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
+        const uint32_t r = s_shift[t];
+        uint64_t mk[OM];
+        if (MASKS) {
+#pragma unroll
+            for (int o = 0; o < OM; o++)
+                mk[o] = o < O ? __ldg(masks + ((uint32_t)o * Q + q) * dstride + mask_row) : 0;
+        }
+        Acc a0, a1;
+        a0.zero();
+        a1.zero();
+        if (r == 0) {
+            if (qlimb) {
+                a0.mac(Pk, __ldg(c0 + n));
+                a1.mac(Pk, __ldg(c0 + ((uint32_t)xls << logn) + n));
+            }
+        } else {
+            const uint32_t src = rot_index(n, half, r);
+            const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
+            const uint32_t ks = s_kstride[t];
+            const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + n;
+            ks_dot<4>(a0, a1, Di, dstride, k0, ks, L);
+            if (qlimb) a0.mac(Pk, __ldg(c0 + src));
+        }
+        if (MASKS) {
+            const uint64_t v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
+            const uint64_t v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
+#pragma unroll
+            for (int o = 0; o < OM; o++) {
+                acc[o][0].mac(mk[o], v0);
+                acc[o][1].mac(mk[o], v1);
+            }
+            if (++since == kFold) {
+                since = 0;
+#pragma unroll
+                for (int o = 0; o < OM; o++)
+                    for (int cc = 0; cc < 2; cc++) {
+                        const uint64_t rr = reduce128_lazy(acc[o][cc].hi64(), acc[o][cc].lo64(), m);
+                        acc[o][cc].set(rr, 0);
+                    }
+            }
+        } else {
+            // fold the term's 128-bit sums (each < (L + 1) q^2 < 2^125) into the running residue
+            const uint64_t v0 = reduce128_lazy(a0.hi64(), a0.lo64(), m);
+            const uint64_t v1 = reduce128_lazy(a1.hi64(), a1.lo64(), m);
+            acc[0][0].add(v0);
+            acc[0][1].add(v1);
+        }
+        if (!diag && ++t == T) {
+            t = 0;
+            i++;
+        }
+    }
+#pragma unroll
+    for (int o = 0; o < OM; o++) {
+        if (o < O) {
+            uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
+            dst[0] = acc[o][0].reduce(m);
+            dst[dstride] = acc[o][1].reduce(m);
+        }
+    }
+}
+
 }  // namespace
 
 void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D, const uint64_t *masks,
@@ -917,6 +1031,38 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
     if (ws_on && masks && !diag && O > 8 && O <= 12) {
         k_hoisted_ws<<<grid, (kWSProd + kWSCons) * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I,
                                                                 T, O, L, c.sp(), (int)c.logn, c.d_mods);
+        UH_LAUNCH_CHECK();
+        return;
+    }
+    // narrow layers (O <= 2): direct register-only kernel (UH_HOIST_DIRECT=0 disables)
+    static const bool direct_on = [] {
+        const char *e = getenv("UH_HOIST_DIRECT");
+        return !(e && std::string(e) == "0");
+    }();
+    if (direct_on && O <= 2) {
+        dim3 gd((unsigned)(c.n / 32), (B + 7) / 8, L + 1);
+        if (gd.y > 65535) throw std::invalid_argument("hoisted kernel: batch too large for one launch");
+        if (masks) {
+            if (O == 1)
+                k_hoisted_direct<1, true><<<gd, 256, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T,
+                                                              O, diag, L, c.sp(), (int)c.logn, c.d_mods);
+            else
+                k_hoisted_direct<2, true><<<gd, 256, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T,
+                                                              O, diag, L, c.sp(), (int)c.logn, c.d_mods);
+        } else {
+            if (O != 1) {
+                // identical unmasked outputs: compute one, copy the rest
+                k_hoisted_direct<1, false><<<gd, 256, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I,
+                                                               T, 1, diag, L, c.sp(), (int)c.logn, c.d_mods);
+                UH_LAUNCH_CHECK();
+                const size_t one = (size_t)B * 2 * (L + 1) * c.n;
+                for (int o = 1; o < O; o++)
+                    UH_CHECK(cudaMemcpyAsync(acc + o * one, acc, one * 8, cudaMemcpyDeviceToDevice, s));
+                return;
+            }
+            k_hoisted_direct<1, false><<<gd, 256, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, 1,
+                                                           diag, L, c.sp(), (int)c.logn, c.d_mods);
+        }
         UH_LAUNCH_CHECK();
         return;
     }
