@@ -1066,50 +1066,54 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
         UH_LAUNCH_CHECK();
         return;
     }
-    // FP64-pipe phase B (k_hoisted_mac_cp<.., true>) for wide masked dense layers: the limbs with
-    // q < 2^41 run there, the others (q_0, P: 60-bit) through the integer kernel.  Opt-in
-    // (UH_HOIST_FP=1): measured slower on LeNet conv2 (B200, B=64: 89.9 vs 78.8 ms) -- the
-    // kernel is latency-bound in phase A, and the split accumulators cost registers.
+    // FP64-pipe phase B (k_hoisted_fp) for wide masked dense layers.  The limbs with q < 2^41 run
+    // there in groups of <= 6 outputs (2 pairs per warp: the split accumulators fit the register
+    // budget; each group repeats phase A on the integer pipe, while phase B moves to the FP64
+    // pipe); q_0 and P (60-bit) run through the integer kernel.  Opt-in (UH_HOIST_FP=1): measured
+    // slower on LeNet-1 at B=64 (conv2 96.8 vs 79.5 ms, conv1 24.1 vs 23.9 ms) -- these kernels are
+    // latency-bound in phase A, not bound by the IMAD pipe that the FP64 phase B relieves.
     static const bool fp_on = [] {
         const char *e = getenv("UH_HOIST_FP");
         return e && std::string(e) == "1";
     }();
     const int Qt = diag ? I : I * T;
-    if (fp_on && masks && !diag && O >= 3 && O <= 12 && Qt <= kFpMaxTerms && L >= 3 && L <= 8) {
+    if (fp_on && masks && !diag && O >= 3 && O <= 12 && Qt <= kFpMaxTerms && L >= 2) {
         bool mid_fp = true;  // limbs 1 .. L-1 (q_1 .. q_{L-1})
         for (int kk = 1; kk < L; kk++) mid_fp = mid_fp && (c.h_q[kk] >> 41) == 0;
         if (mid_fp) {
-            const int ppw = pairs > 48 ? 4 : (pairs > 24 ? 2 : 1);
-            // FP64 phase B runs inside the cp.async-pipelined kernel (k_hoisted_mac_cp<.., true>)
-            const size_t stage = (size_t)(kTChunk * kTBatch * L * 32 + kTChunk * kTBatch * 32 + kTChunk * 2 * L * 32) * 8;
-            const size_t smem_fp = 2 * stage + (size_t)2 * kTChunk * kTBatch * 2 * 2 * 32 * sizeof(double);
-            auto run = [&](auto ppw_tag, int z0, int zstep, int nz, bool fp) {
-                constexpr int PP = decltype(ppw_tag)::value;
-                dim3 g(grid.x, grid.y, nz);
-                if (fp) {
-                    static size_t configured = 0;
-                    if (smem_fp > configured) {
-                        UH_CHECK(cudaFuncSetAttribute(k_hoisted_mac_cp<PP, 24, true>,
-                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fp));
-                        configured = smem_fp;
+            const size_t smem = (size_t)2 * kTChunk * kTBatch * 2 * 2 * 32 * sizeof(double);
+            const size_t ostride = (size_t)B * 2 * (L + 1) * c.n, mstride = (size_t)Qt * (L + 1) * c.n;
+            for (int o0 = 0; o0 < O; o0 += 6) {
+                const int og = std::min(6, O - o0);
+                dim3 g(grid.x, grid.y, L - 1);
+                auto fp = [&](auto ppw_tag) {
+                    constexpr int PP = decltype(ppw_tag)::value;
+                    static bool attr = false;
+                    if (!attr) {
+                        UH_CHECK(cudaFuncSetAttribute(k_hoisted_fp<PP, 24>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                        attr = true;
                     }
-                    k_hoisted_mac_cp<PP, 24, true><<<g, 24 * 32, smem_fp, s>>>(
-                        acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, diag, L, c.sp(), (int)c.logn,
-                        c.d_mods, z0, zstep);
-                } else {
-                    k_hoisted_mac<PP, 24><<<g, 24 * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I,
-                                                               T, O, diag, L, c.sp(), (int)c.logn, c.d_mods, z0,
-                                                               zstep);
-                }
+                    k_hoisted_fp<PP, 24><<<g, 24 * 32, smem, s>>>(acc + o0 * ostride, X, xls, D, masks + o0 * mstride,
+                                                                  keys, key_limbs, shifts, B, I, T, og, L, c.sp(),
+                                                                  (int)c.logn, c.d_mods, 1, 1);
+                };
+                if (og * kTBatch > 24) fp(integral_constant<int, 2>());
+                else fp(integral_constant<int, 1>());
                 UH_LAUNCH_CHECK();
-            };
-            auto both = [&](auto tag) {
-                run(tag, 1, 1, L - 1, true);   // q_1 .. q_{L-1}
-                run(tag, 0, L, 2, false);      // q_0 and P
-            };
-            if (ppw == 1) both(integral_constant<int, 1>());
-            else if (ppw == 2) both(integral_constant<int, 2>());
-            else both(integral_constant<int, 4>());
+            }
+            dim3 g2(grid.x, grid.y, 2);  // q_0 and P
+            const int ppw = pairs > 48 ? 4 : (pairs > 24 ? 2 : 1);
+            if (ppw == 4)
+                k_hoisted_mac<4, 24><<<g2, 24 * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O,
+                                                           diag, L, c.sp(), (int)c.logn, c.d_mods, 0, L);
+            else if (ppw == 2)
+                k_hoisted_mac<2, 24><<<g2, 24 * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O,
+                                                           diag, L, c.sp(), (int)c.logn, c.d_mods, 0, L);
+            else
+                k_hoisted_mac<1, 24><<<g2, 24 * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O,
+                                                           diag, L, c.sp(), (int)c.logn, c.d_mods, 0, L);
+            UH_LAUNCH_CHECK();
             return;
         }
     }
