@@ -137,13 +137,55 @@ struct AccS {
     }
 };
 
-// 128-bit accumulator for lazy multiply-add chains (four 32-bit words).
+// 128-bit accumulator for lazy multiply-add chains.
+#ifndef UH_ACC32
+// Two 64-bit halves: the register allocator keeps each half in an aligned register
+// pair, so the in-place IMAD.WIDE.U32 accumulations need no register shuffles.
+__device__ __forceinline__ void mac128p(uint64_t &lo, uint64_t &hi, uint64_t x, uint64_t y) {
+    asm("{\n\t.reg .u32 x0,x1,y0,y1,l0,l1,h0,h1,t0,t1,t2;\n\t"
+        "mov.b64 {x0,x1}, %2;\n\tmov.b64 {y0,y1}, %3;\n\t"
+        "mov.b64 {l0,l1}, %0;\n\tmov.b64 {h0,h1}, %1;\n\t"
+        "mad.lo.cc.u32 l0, x0, y0, l0;\n\tmadc.hi.cc.u32 l1, x0, y0, l1;\n\t"
+        "madc.lo.cc.u32 h0, x1, y1, h0;\n\tmadc.hi.u32 h1, x1, y1, h1;\n\t"
+        "mul.lo.u32 t0, x0, y1;\n\tmul.hi.u32 t1, x0, y1;\n\t"
+        "mad.lo.cc.u32 t0, x1, y0, t0;\n\tmadc.hi.cc.u32 t1, x1, y0, t1;\n\taddc.u32 t2, 0, 0;\n\t"
+        "add.cc.u32 l1, l1, t0;\n\taddc.cc.u32 h0, h0, t1;\n\taddc.u32 h1, h1, t2;\n\t"
+        "mov.b64 %0, {l0,l1};\n\tmov.b64 %1, {h0,h1};\n\t}"
+        : "+l"(lo), "+l"(hi)
+        : "l"(x), "l"(y));
+}
+struct Acc {
+    uint64_t lo, hi;
+    __device__ __forceinline__ void zero() { lo = hi = 0; }
+    __device__ __forceinline__ void mac(uint64_t a, uint64_t b) { mac128p(lo, hi, a, b); }
+    __device__ __forceinline__ uint64_t lo64() const { return lo; }
+    __device__ __forceinline__ uint64_t hi64() const { return hi; }
+    __device__ __forceinline__ uint32_t hi32lo() const { return (uint32_t)hi; }  // bits 64..95
+    __device__ __forceinline__ void set(uint64_t l, uint64_t h) { lo = l; hi = h; }
+    __device__ __forceinline__ void mac_c(uint64_t a, uint64_t b) {  // plain-C reference form
+        uint64_t pl = a * b, ph = mulhi(a, b);
+        lo += pl;
+        hi += ph + (lo < pl);
+    }
+    __device__ __forceinline__ void add(uint64_t a) {
+        asm("{\n\t.reg .u32 a0,a1,l0,l1,h0,h1;\n\t"
+            "mov.b64 {a0,a1}, %2;\n\tmov.b64 {l0,l1}, %0;\n\tmov.b64 {h0,h1}, %1;\n\t"
+            "add.cc.u32 l0, l0, a0;\n\taddc.cc.u32 l1, l1, a1;\n\taddc.cc.u32 h0, h0, 0;\n\taddc.u32 h1, h1, 0;\n\t"
+            "mov.b64 %0, {l0,l1};\n\tmov.b64 %1, {h0,h1};\n\t}"
+            : "+l"(lo), "+l"(hi)
+            : "l"(a));
+    }
+    __device__ __forceinline__ uint64_t reduce(const Mod &m) const { return reduce128(hi, lo, m); }
+};
+#else
+// four 32-bit words (previous form, UH_ACC32)
 struct Acc {
     uint32_t w0, w1, w2, w3;
     __device__ __forceinline__ void zero() { w0 = w1 = w2 = w3 = 0; }
     __device__ __forceinline__ void mac(uint64_t a, uint64_t b) { mac128x4(w0, w1, w2, w3, a, b); }
     __device__ __forceinline__ uint64_t lo64() const { return ((uint64_t)w1 << 32) | w0; }
     __device__ __forceinline__ uint64_t hi64() const { return ((uint64_t)w3 << 32) | w2; }
+    __device__ __forceinline__ uint32_t hi32lo() const { return w2; }
     __device__ __forceinline__ void set(uint64_t lo, uint64_t hi) {
         w0 = (uint32_t)lo; w1 = (uint32_t)(lo >> 32); w2 = (uint32_t)hi; w3 = (uint32_t)(hi >> 32);
     }
@@ -161,6 +203,7 @@ struct Acc {
     }
     __device__ __forceinline__ uint64_t reduce(const Mod &m) const { return reduce128(hi64(), lo64(), m); }
 };
+#endif
 
 // Centred lift of x in [0, p) reduced into q: x > (p-1)/2 represents x - p.
 __device__ __forceinline__ uint64_t centred_to(uint64_t x, uint64_t p, const Mod &mq) {

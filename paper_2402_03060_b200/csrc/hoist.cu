@@ -40,6 +40,18 @@ __device__ __forceinline__ uint32_t rot_index(uint32_t n, uint32_t half, uint32_
 __device__ __forceinline__ uint64_t reduce128_lazy(uint64_t hi, uint64_t lo, const Mod &m) {
     return shoup_lazy(hi, m.r64, m.r64s, m.q) + barrett_lite(lo, m);
 }
+// A phase-A key sum for a limb with q < 2^41 is below 25 * 2^82 < 2^87, so its high word
+// is below 2^23 and (hi * (2^64 mod q) + lo) folds it to a 64-bit value congruent mod q
+// with one 32x64 product -- no full reduction (the phase-B accumulators absorb values < 2^64).
+__device__ __forceinline__ uint64_t fold64_small(const Acc &a, const Mod &m) {
+    const uint64_t lo = a.lo64(), p = (uint64_t)a.hi32lo() * m.r64;
+    const uint64_t v = lo + p;
+    return v < p ? v + m.r64 : v;  // a wrap past 2^64 is worth 2^64 mod q
+}
+// phase-A term value: lazily reduced into [0, 2q) (60-bit limbs) or folded below 2^64 (q < 2^41)
+__device__ __forceinline__ uint64_t term_value(const Acc &a, const Mod &m, bool smallq) {
+    return smallq ? fold64_small(a, m) : csub(reduce128_lazy(a.hi64(), a.lo64(), m), 2 * m.q);
+}
 
 constexpr int kMaxL = 12;  // phase-A digit loop fully unrolled (predicated) up to this many limbs
 
@@ -103,6 +115,7 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
     const uint32_t N = 1u << logn, half = N >> 1;
     const Mod m = mods[limb_mod(k, L, 0, sp)];
     const bool qlimb = k < L;
+    const bool smallq = (m.q >> 41) == 0 && L <= kMaxL;
     const uint64_t P = mods[sp].q;
     const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
     const int Q = diag ? I : I * T;
@@ -183,8 +196,8 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
                     a1.zero();
                     ks_dot<kKsGroup>(a0, a1, Di, dstride, k0, ks, L);
                     if (qlimb) a0.mac(Pk, c0[src]);
-                    v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
-                    v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
+                    v0 = term_value(a0, m, smallq);
+                    v1 = term_value(a1, m, smallq);
                 }
             }
             sv[buf][qc][bt][0][ln] = v0;
@@ -465,6 +478,7 @@ __global__ void __launch_bounds__(W * 32, 1)
     const bool qlimb = k < L;
     const uint64_t P = mods[sp].q;
     const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
+    const bool smallq = (m.q >> 41) == 0 && L <= kMaxL;
     const int Q = diag ? I : I * T;
     const int npairs = O * kTBatch;
     for (int t = threadIdx.x; t < T; t += blockDim.x) {
@@ -599,8 +613,8 @@ __global__ void __launch_bounds__(W * 32, 1)
                         v0 = a0.reduce(m);
                         v1 = a1.reduce(m);
                     } else {
-                        v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
-                        v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
+                        v0 = term_value(a0, m, smallq);
+                        v1 = term_value(a1, m, smallq);
                     }
                 }
             }
@@ -894,6 +908,7 @@ __global__ void __launch_bounds__(256, 4)
     const int LP = L + 1;
     const Mod m = mods[limb_mod(k, L, 0, sp)];
     const bool qlimb = k < L;
+    const bool smallq = (m.q >> 41) == 0 && L <= kMaxL;
     const uint64_t P = mods[sp].q;
     const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
     const int Q = diag ? I : I * T;
@@ -934,8 +949,8 @@ __global__ void __launch_bounds__(256, 4)
             if (qlimb) a0.mac(Pk, __ldg(c0 + src));
         }
         if (MASKS) {
-            const uint64_t v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
-            const uint64_t v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
+            const uint64_t v0 = term_value(a0, m, smallq);
+            const uint64_t v1 = term_value(a1, m, smallq);
 #pragma unroll
             for (int o = 0; o < OM; o++) {
                 acc[o][0].mac(mk[o], v0);
@@ -951,9 +966,9 @@ __global__ void __launch_bounds__(256, 4)
                     }
             }
         } else {
-            // fold the term's 128-bit sums (each < (L + 1) q^2 < 2^125) into the running residue
-            const uint64_t v0 = reduce128_lazy(a0.hi64(), a0.lo64(), m);
-            const uint64_t v1 = reduce128_lazy(a1.hi64(), a1.lo64(), m);
+            // fold the term's 128-bit sums (each < (2L + 1) q^2 < 2^125) into the running sum
+            const uint64_t v0 = smallq ? fold64_small(a0, m) : reduce128_lazy(a0.hi64(), a0.lo64(), m);
+            const uint64_t v1 = smallq ? fold64_small(a1, m) : reduce128_lazy(a1.hi64(), a1.lo64(), m);
             acc[0][0].add(v0);
             acc[0][1].add(v1);
         }
