@@ -13,7 +13,8 @@ import os
 from .errors import DeviceError
 
 LIB_NAME = "libunihenn_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", LIB_NAME)
+LIB_PATH = os.environ.get("UH_LIB_PATH") or os.path.join(  # override: A/B builds of compile-time variants
+    os.path.dirname(os.path.abspath(__file__)), "_build", LIB_NAME)
 
 _c_u32, _c_u64, _c_i64, _c_int, _c_dbl, _vp = (ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int,
                                                ctypes.c_double, ctypes.c_void_p)
