@@ -10,6 +10,7 @@ from .counter import OpCounter, diff_snapshots
 from .errors import (CapacityExceeded, DeviceError, FootprintOverflow, LevelExhausted, NonDivisibleDims,
                      NotFlattened, OversizedInput, PaddingUnsupported, ParseError, ScaleMismatch, ShapeMismatch,
                      SlotCnnError, SlotMismatch, TargetAboveCurrent, UnknownModel)
+from .keyio import EvalKeys, load_eval_keys, save_eval_keys
 from .params import DEFAULT_PARAMS, HEParams, rns_chain
 from .planner import (FC, RELU_COEFFS, ApproxReLU, AvgPool2d, Conv1d, Conv2d, Flatten, LayerTrace, ModelSpec,
                       PackPlan, Square, ValidationReport, batch_pack, batch_unpack, builtin, builtin_names,

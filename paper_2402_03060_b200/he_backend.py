@@ -167,6 +167,32 @@ class GpuBackend:
             self._rk = key
         return self._rk
 
+    def export_keys(self, path: str) -> None:
+        """Write every evaluation key generated so far (keyio container; no secret material)."""
+        from . import keyio
+
+        torch.cuda.synchronize(self.device)
+        u64 = lambda t: t.cpu().numpy().view(np.uint64)  # noqa: E731
+        keys = keyio.EvalKeys(self.n, list(self.chain.moduli), self.params.scale_bits, self.depth, self.params.seed,
+                              galois={r: u64(k) for r, k in self._gk.items()},
+                              relin=None if self._rk is None else u64(self._rk))
+        keyio.save_eval_keys(path, keys)
+
+    def import_keys(self, path: str) -> int:
+        """Load evaluation keys written by :meth:`export_keys` for this parameter set.
+
+        Imported keys replace lazily generated ones; returns how many were loaded.
+        """
+        from . import keyio
+
+        keys = keyio.load_eval_keys(path, self.n, self.chain.moduli)
+        dev = lambda a: torch.from_numpy(a.view(np.int64)).to(self.device)  # noqa: E731
+        for r, a in keys.galois.items():
+            self._gk[r % self.params.num_slots] = dev(a)
+        if keys.relin is not None:
+            self._rk = dev(keys.relin)
+        return len(keys.galois) + (keys.relin is not None)
+
     def prepare_keys(self, offsets, level: int, relin_level: int | None = None) -> None:
         """Generate every Galois key in ``offsets`` (and the relin key) up front."""
         for r in offsets:

@@ -12,8 +12,9 @@
 
 import numpy as np
 import pytest
+import torch
 
-from paper_2402_03060_b200.errors import LevelExhausted, OversizedInput, SlotMismatch
+from paper_2402_03060_b200.errors import LevelExhausted, OversizedInput, ParseError, SlotMismatch
 from paper_2402_03060_b200.he_backend import GpuBackend
 from paper_2402_03060_b200.params import HEParams
 
@@ -107,3 +108,28 @@ def test_homomorphism_and_counter():
     assert be2.counter.by_level == {("pt_mult", 4): 1, ("rotation", 3): 1, ("add", 3): 1, ("ct_mult", 3): 1}
     want = (2 * np.roll(np.array([1.0, 2.0, 0.0, 0.0]), -1)) ** 2  # rotate, double, square
     assert np.max(np.abs(be2.decrypt(c) - want)) < 1e-5
+
+
+def test_eval_key_export_import(tmp_path):
+    """Keys exported by one backend serve another with the same parameters (keyio container)."""
+    p = HEParams(poly_degree=64, depth=3, scale_bits=40, seed=5)
+    a = GpuBackend(p)
+    a.prepare_keys([1, 3], level=3, relin_level=3)
+    path = str(tmp_path / "evk.bin")
+    a.export_keys(path)
+    b = GpuBackend(p)
+    assert b.import_keys(path) == 3
+    for r in (1, 3):
+        assert b._gk[r].shape == (4, 2, 5, 64) and torch.equal(b._gk[r].cpu(), a._gk[r].cpu())
+    loaded = b._gk[1]
+    x = np.linspace(-1, 1, p.num_slots)
+    c = b.encrypt(b.encode(x))
+    assert np.max(np.abs(b.decrypt(b.rotate(c, 1)) - np.roll(x, -1))) < TOL
+    assert b._gk[1] is loaded  # served by the imported key, not regenerated
+    rk = b._rk
+    sq = b.mul_cipher(c, c)
+    assert np.max(np.abs(b.decrypt(sq) - x * x)) < 1e-5
+    assert b._rk is rk
+    other = GpuBackend(HEParams(poly_degree=128, depth=3, scale_bits=40, seed=5))
+    with pytest.raises(ParseError):
+        other.import_keys(path)
