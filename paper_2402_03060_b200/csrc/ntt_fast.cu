@@ -282,7 +282,7 @@ struct P1 {
     static constexpr int GC = R1 * 32 / kThreads;  // contiguous groups per thread
 };
 
-template <int A, int LM, bool FP>
+template <int A, int LM, bool FP, bool OUT_SM = false>
 __device__ __forceinline__ void fwd_p1_body(uint64_t *sm, const LimbInfo &li, const Mod &m, bool red,
                                             const Tw &tws, uint64_t *out, int n2, int col, int lane, int wq) {
     using C = P1<A>;
@@ -311,7 +311,12 @@ __device__ __forceinline__ void fwd_p1_body(uint64_t *sm, const LimbInfo &li, co
         // stages m = R1 .. N1/2 on contiguous rows r0 + z: twiddle m + (r0 + z) / (2t)
         fwd_strided<C::R2>(v, TwG<typename AR::W>{T, 1}, C::R1, grp, ar.qv());
 #pragma unroll
-        for (int z = 0; z < C::R2; z++) out[(size_t)(r0 + z) * n2 + col] = AR::raw(v[z]);
+        for (int z = 0; z < C::R2; z++) {
+            if constexpr (OUT_SM)  // cluster-fused NTT: the column tile stays in this CTA's shared memory
+                sm[(r0 + z) * 32 + lane] = AR::raw(v[z]);
+            else
+                out[(size_t)(r0 + z) * n2 + col] = AR::raw(v[z]);
+        }
     }
 }
 
@@ -441,26 +446,38 @@ __device__ __forceinline__ void stage_twiddles(double *tws, const double *__rest
     for (int g = tid >> B; g < C::G; g += kThreads / C::N2) tws[(g << B) + r] = __ldg(src + (size_t)mp * (n1 + sel[g]));
 }
 
+// pass-2 input: the pass-1 intermediate in global memory (two-pass NTT)
+template <int B>
+struct InGlobal {
+    const uint64_t *in;
+    __device__ uint64_t operator()(int blk, int c) const { return in[(size_t)blk * P2<B>::N2 + c]; }
+    __device__ void done() const {}
+};
+template <int B, int EM>
+__device__ __forceinline__ void fwd_p2_epilogue(const uint64_t *sm, const LimbInfo &li, uint64_t q,
+                                                const int32_t *__restrict__ csl, int logn, int tid);
+
 // pass 2 forward stages: tmp (pass-1 output) -> canonical residues in shared memory
-template <int B, bool FP>
+template <int B, bool FP, class IN, bool STAGED = true>
 __device__ __forceinline__ void fwd_p2_body(uint64_t *sm, const double *tws, const Mod &m, const Tw &tw2,
-                                            const uint64_t *in, const int *sel, int n1, int tid) {
+                                            const IN &in, const int *sel, int n1, int tid) {
     using C = P2<B>;
     using AR = Arith<FP>;
     using V = typename AR::V;
     const AR ar(m.q);
     const auto *T = pick<FP>(tw2);
     auto acc = [&](int g, int blk) {
-        if constexpr (FP)
+        if constexpr (FP && STAGED)
             return TwS{tws + g * C::N2, ar.qinv};
         else
-            return TwG<ulonglong2>{T, n1 + blk};
+            return TwG<typename AR::W>{T, n1 + blk};
     };
     {
         const int g = tid / C::S, c0 = tid % C::S, blk = sel[g];
         V v[C::R1];
 #pragma unroll
-        for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(in[(size_t)blk * C::N2 + c0 + C::S * x]);
+        for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(in(blk, c0 + C::S * x));
+        in.done();
         // local stages m' = 1..8: global twiddle index m' * (n1 + blk) + x / (2 dx)
         fwd_strided<C::R1>(v, acc(g, blk), 1, 0, ar.qv());
 #pragma unroll
@@ -506,7 +523,7 @@ __global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *_
     const Mod m = mods[li.mod];
     const uint64_t q = m.q;
     const Tw tw2{twd + ((size_t)li.mod << logn), nullptr};
-    const uint64_t *in = tmp + ((size_t)blockIdx.y << logn);
+    const InGlobal<B> in{tmp + ((size_t)blockIdx.y << logn)};
     if (fp_limb(q)) {
         stage_twiddles<B>(tws, twdd + ((size_t)li.mod << logn), sel, n1, tid);
         __syncthreads();
@@ -514,8 +531,15 @@ __global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *_
     } else {
         fwd_p2_body<B, false>(sm, tws, m, tw2, in, sel, n1, tid);
     }
-    // coalesced slot-order epilogue: a thread's 16 slot-table (and DIVIDE input) loads are
-    // issued together, then the shared-memory gathers and the stores
+    fwd_p2_epilogue<B, EM>(sm, li, q, csl, logn, tid);
+}
+
+// coalesced slot-order epilogue: a thread's 16 slot-table (and DIVIDE input) loads are
+// issued together, then the shared-memory gathers and the stores
+template <int B, int EM>
+__device__ __forceinline__ void fwd_p2_epilogue(const uint64_t *sm, const LimbInfo &li, uint64_t q,
+                                                const int32_t *__restrict__ csl, int logn, int tid) {
+    using C = P2<B>;
     constexpr int E = EM ? 8 : 16;  // loads in flight per round (register budget)
 #pragma unroll
     for (int e0 = 0; e0 < 4096 / kThreads; e0 += E) {
@@ -540,6 +564,82 @@ __global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *_
                 li.dst[s] = y;
         }
     }
+}
+
+// ---------------- cluster-fused forward NTT (one kernel, no global intermediate) ----------------
+// A thread-block cluster of NC = N2 / 32 CTAs owns one limb.  CTA `rank` runs pass 1 on the
+// 32 columns [32 rank, 32 rank + 32) and keeps its N1 x 32 tile in shared memory; after a
+// cluster barrier, pass 2 of CTA `rank` (blocks bsel[rank * G ..]) gathers each of its rows
+// from the NC tiles through distributed shared memory (DSMEM) -- the N1 x N2 transpose
+// happens on-chip, so the limb is read from HBM once and written once.
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::); }
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::);
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::); }
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+// 64-bit load from the shared memory of CTA `rank` of the cluster at the same offset as `local`
+__device__ __forceinline__ uint64_t dsmem_ld(const uint64_t *local, uint32_t rank) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(local), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(a), "r"(rank));
+    uint64_t v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];\n" : "=l"(v) : "r"(ra) : "memory");
+    return v;
+}
+template <int B>
+struct InCluster {  // row blk, column c of the limb -> CTA c / 32 of the cluster, tile row blk
+    const uint64_t *tile;
+    __device__ uint64_t operator()(int blk, int c) const { return dsmem_ld(tile + blk * 32 + (c & 31), c >> 5); }
+    // this CTA's remote reads are consumed (values in registers): no ordering to release
+    __device__ void done() const { cluster_arrive_relaxed(); }
+};
+
+template <int A, int B>
+constexpr size_t fused_smem() {  // column tile + pass-2 tiles (twiddles from L2: 3 CTAs / SM)
+    return (size_t)(P1<A>::N1 * 32 + P2<B>::G * P2<B>::PAD) * 8;
+}
+
+template <int A, int B, int LM, int EM>
+__global__ void __launch_bounds__(kThreads) k_fwd_fused(NttJob J, int logn, const Mod *__restrict__ mods,
+                                                       const ulonglong2 *__restrict__ twd,
+                                                       const double2 *__restrict__ twf,
+                                                       const double *__restrict__ twdd,
+                                                       const int32_t *__restrict__ bsel,
+                                                       const int32_t *__restrict__ csl) {
+    using C2 = P2<B>;
+    static_assert((1 << B) / 32 == (1 << A) / C2::G, "pass-1 and pass-2 CTA counts per limb must agree");
+    extern __shared__ uint64_t dsm[];
+    uint64_t *tile = dsm;                                   // [N1][32]
+    uint64_t *sm2 = dsm + P1<A>::N1 * 32;                   // [G][PAD]
+    const uint32_t rank = cluster_rank();
+    const int f = J.f0 + blockIdx.y, tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    const int n2 = 1 << (logn - A), n1 = 1 << (logn - B);
+    const LimbInfo li = limb_info(J, f, logn, mods);
+    const Mod m = mods[li.mod];
+    const uint64_t q = m.q;
+    const bool red = LM == 1 && ((li.qsrc - 1) >> 1) >= q;
+    const Tw tw1{twd + ((size_t)li.mod << logn), twf + ((size_t)li.mod << logn)};
+    const int *sel = bsel + rank * C2::G;
+    const bool fp = fp_limb(q);
+    // pass 1 on this CTA's 32 columns, result left in `tile`
+    if (fp)
+        fwd_p1_body<A, LM, true, true>(tile, li, m, red, tw1, nullptr, n2, rank * 32 + lane, lane, wq);
+    else
+        fwd_p1_body<A, LM, false, true>(tile, li, m, red, tw1, nullptr, n2, rank * 32 + lane, lane, wq);
+    // every tile of the cluster complete and visible (also orders the twiddle stage)
+    cluster_arrive();
+    cluster_wait();
+    const InCluster<B> in{tile};
+    if (fp)
+        fwd_p2_body<B, true, InCluster<B>, false>(sm2, nullptr, m, tw1, in, sel, n1, tid);
+    else
+        fwd_p2_body<B, false, InCluster<B>, false>(sm2, nullptr, m, tw1, in, sel, n1, tid);
+    fwd_p2_epilogue<B, EM>(sm2, li, q, csl, logn, tid);
+    cluster_wait();  // no CTA leaves while others may still read its tile
 }
 
 // inverse pass A stages: canonical residues in shared memory -> tmp (pass-B input)
@@ -650,8 +750,69 @@ inline int ntt_chunk(const Ctx &c, int limbs) {
     return std::max(1, std::min(limbs, ch));
 }
 
+template <auto K>
+void fused_attr(size_t smem) {
+    static bool done = false;
+    if (!done) {
+        UH_CHECK(cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        UH_CHECK(cudaFuncSetAttribute(K, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        done = true;
+    }
+}
+
+template <int A, int B, int LM, int EM>
+void launch_fused(const Ctx &c, const NttJob &J, int nl, cudaStream_t s) {
+    constexpr size_t smem = fused_smem<A, B>();
+    constexpr unsigned ncta = (1u << B) / 32;
+    fused_attr<k_fwd_fused<A, B, LM, EM>>(smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncta, nl, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ncta;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    UH_CHECK(cudaLaunchKernelEx(&cfg, k_fwd_fused<A, B, LM, EM>, J, (int)c.logn, (const Mod *)c.d_mods,
+                                (const ulonglong2 *)c.d_tw2, (const double2 *)c.d_twf, (const double *)c.d_twd,
+                                (const int32_t *)c.d_bsel, (const int32_t *)c.d_csl));
+    UH_LAUNCH_CHECK();
+}
+
+// Opt-in (UH_NTT_FUSED=1): measured slower than the two passes on B200 at N = 2^15
+// (0.41 vs 0.35 us per limb, 512 limbs): with one limb per 8-CTA cluster, the cluster
+// barriers and DSMEM gather latency are exposed, while the two-pass grids keep ~4k
+// independent CTAs in flight and the intermediate largely stays in L2.
+inline bool fused_ntt_on() {
+    static const bool on = [] {
+        const char *e = getenv("UH_NTT_FUSED");
+        return e && std::string(e) == "1";
+    }();
+    return on;
+}
+
 template <int A, int B>
 void run_fwd(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
+    if constexpr ((1 << B) / 32 == (1 << A) / P2<B>::G) {
+        if (fused_ntt_on()) {
+            for (int f0 = 0; f0 < limbs; f0 += 65535) {
+                NttJob J = J0;
+                J.f0 = f0;
+                const int nl = std::min(65535, limbs - f0);
+                const int lm = J.mode == NTT_PLAIN ? 0 : J.mode == NTT_DIVIDE2 ? 2 : 1;
+                const int em = J.mode == NTT_DIVIDE ? 1 : J.mode == NTT_DIVIDE2 ? 2 : 0;
+                if (lm == 0) launch_fused<A, B, 0, 0>(c, J, nl, s);
+                else if (lm == 2) launch_fused<A, B, 2, 2>(c, J, nl, s);
+                else if (em == 1) launch_fused<A, B, 1, 1>(c, J, nl, s);
+                else launch_fused<A, B, 1, 0>(c, J, nl, s);
+            }
+            return;
+        }
+    }
     const int ch = ntt_chunk(c, limbs);
     Scratch tmp((size_t)ch * c.n * 8, s);
     uint64_t *t = tmp.as<uint64_t>();
