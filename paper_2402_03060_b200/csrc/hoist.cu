@@ -60,8 +60,12 @@ constexpr int kMaxL = 12;  // phase-A digit loop fully unrolled (predicated) up 
 // Loads are issued in groups of G digits (3G independent 64-bit loads in flight)
 // before any of the group's products: a per-digit load->use chain would
 // serialise L round trips to L2 (ncu: long-scoreboard on the first MAC).
+#ifndef UH_KS_GROUP_WIDE
+#define UH_KS_GROUP_WIDE 2
+#endif
 #ifndef UH_KS_GROUP_FOR
-#define UH_KS_GROUP_FOR(PPW, W) ((PPW) * (W) >= 96 || ((W) == 8 && (PPW) == 2) ? 2 : 4)
+#define UH_KS_GROUP_FOR(PPW, W) \
+    ((PPW) * (W) >= 96 || ((PPW) >= 4 && (W) != 8) ? UH_KS_GROUP_WIDE : ((W) == 8 && (PPW) == 2) ? 2 : 4)
 #endif
 #ifndef UH_WS_GROUP
 #define UH_WS_GROUP 4
@@ -96,20 +100,22 @@ __device__ __forceinline__ void ks_dot(Acc &a0, Acc &a1, const uint64_t *Di, uin
 // All element offsets are 32-bit (the host checks every operand has < 2^32 elements).
 constexpr int kMaxTerms = 512;  // per-term metadata staged in shared memory
 
-template <int PPW, int W>
-__global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
+// TB: ciphertexts per CTA tile (8; 4 lets two 12-warp CTAs share an SM, so one CTA's
+// phase-A latency overlaps the other's phase B without any intra-CTA coupling)
+template <int PPW, int W, int TB = kTBatch>
+__global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : (TB < 8 && W * 2 == TB * 6 ? 24 / W : 1))
     k_hoisted_mac(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
                   const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
                   const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
                   const int32_t *__restrict__ shifts, int B, int I, int T, int O, int diag, int L, int sp, int logn,
                   const Mod *__restrict__ mods, int z0 = 0, int zstep = 1) {
-    __shared__ uint64_t sv[2][kTChunk][kTBatch][2][32];
+    __shared__ uint64_t sv[2][kTChunk][TB][2][32];
     __shared__ const uint64_t *s_key[kMaxTerms];
     __shared__ uint32_t s_shift[kMaxTerms];
     __shared__ uint32_t s_kstride[kMaxTerms];  // key limbs << logn: one key component
     const int LP = L + 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int b0 = blockIdx.x * kTBatch;
+    const int b0 = blockIdx.x * TB;
     const uint32_t n = blockIdx.y * 32 + lane;
     const int k = z0 + blockIdx.z * zstep;
     const uint32_t N = 1u << logn, half = N >> 1;
@@ -119,7 +125,7 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
     const uint64_t P = mods[sp].q;
     const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
     const int Q = diag ? I : I * T;
-    const int npairs = O * kTBatch;
+    const int npairs = O * TB;
     for (int t = threadIdx.x; t < T; t += blockDim.x) {
         s_key[t] = keys[t];
         s_shift[t] = (uint32_t)shifts[t];
@@ -137,11 +143,11 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
     constexpr int kKsGroup = UH_KS_GROUP_FOR(PPW, W);
     int since_fold = 0;
     int buf = 0;
-    constexpr int ITEMS = kTChunk * kTBatch / W;  // phase-A items per thread (1, 2 or 3)
-    static_assert(ITEMS * W == kTChunk * kTBatch, "phase-A items must tile the chunk");
+    constexpr int ITEMS = kTChunk * TB / W;  // phase-A items per thread (1, 2 or 3)
+    static_assert(ITEMS * W == kTChunk * TB, "phase-A items must tile the chunk");
     // a warp's PPW (output, ciphertext) pairs form a PO x PB block: each shared-memory v is
     // loaded once for PO outputs and each mask once for PB ciphertexts
-    constexpr int PB = PPW == 4 ? 2 : PPW, PO = PPW / PB, WB = kTBatch / PB;
+    constexpr int PB = (PPW == 4 ? 2 : PPW) < TB ? (PPW == 4 ? 2 : PPW) : TB, PO = PPW / PB, WB = TB / PB;
     const int o_a = (warp / WB) * PO, b_a = (warp % WB) * PB;
     const bool warp_active = o_a < O && warp * PPW < npairs;
     const uint32_t dstride = (uint32_t)LP << logn;  // between digits of one D block
@@ -162,7 +168,7 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : 1)
         for (int ii = 0; ii < ITEMS; ii++) {
             const int it = threadIdx.x + ii * W * 32;
             const int ln = it & 31, rest = it >> 5;
-            const int bt = rest % kTBatch, qc = rest / kTBatch;
+            const int bt = rest % TB, qc = rest / TB;
             const int q = q0 + qc, b = b0 + bt;
             uint64_t v0 = 0, v1 = 0;
             if (q < Q && b < B) {
@@ -1144,7 +1150,32 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
             const int ppw = pairs > 48 ? 4 : (pairs > 24 ? 2 : 1);
             if (ppw == 1) go(integral_constant<int, 1>(), integral_constant<int, 24>());
             else if (ppw == 2) go(integral_constant<int, 2>(), integral_constant<int, 24>());
-            else go(integral_constant<int, 4>(), integral_constant<int, 24>());
+            else {
+                // ciphertexts per CTA tile for the widest layers (UH_HOIST_TB): 2 (default: four
+                // 6-warp CTAs per SM, so one CTA's phase-A latency overlaps the others' phase B
+                // with no barrier coupling between them), 4 (two 12-warp CTAs), 1 (eight 3-warp
+                // CTAs) or 8 (one 24-warp CTA).  Measured LeNet conv2 at B = 64 (B200):
+                // 62.4 / 66.5 / 81.4 / 72.2 ms.
+                static const int tbw = [] {
+                    const char *e = getenv("UH_HOIST_TB");
+                    return e ? atoi(e) : 2;
+                }();
+                if (tbw == 4 && O > 6) {
+                    dim3 g4((B + 3) / 4, grid.y, grid.z);
+                    k_hoisted_mac<4, 12, 4><<<g4, 12 * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I,
+                                                                  T, O, diag, L, c.sp(), (int)c.logn, c.d_mods);
+                } else if (tbw == 1 && O > 6) {
+                    dim3 g1((unsigned)B, grid.y, grid.z);
+                    k_hoisted_mac<4, 3, 1><<<g1, 3 * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I,
+                                                                T, O, diag, L, c.sp(), (int)c.logn, c.d_mods);
+                } else if (tbw == 2 && O > 6) {
+                    dim3 g2((B + 1) / 2, grid.y, grid.z);
+                    k_hoisted_mac<4, 6, 2><<<g2, 6 * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I,
+                                                                T, O, diag, L, c.sp(), (int)c.logn, c.d_mods);
+                } else {
+                    go(integral_constant<int, 4>(), integral_constant<int, 24>());
+                }
+            }
         }
     } else {
         // very wide layers: split the outputs in groups of 12 (12 warps x 8 pairs)
