@@ -21,6 +21,10 @@
 //                  mod q_k and the epilogue writes (in[p][k] - y) * q_top^-1.
 #include "ntt_fast.cuh"
 
+#ifndef UH_NTT_MINB
+#define UH_NTT_MINB 4  // min resident CTAs per SM requested from ptxas (register cap: 64)
+#endif
+
 namespace uh {
 namespace {
 
@@ -321,7 +325,7 @@ __device__ __forceinline__ void fwd_p1_body(uint64_t *sm, const LimbInfo &li, co
 }
 
 template <int A, int LM>
-__global__ void __launch_bounds__(kThreads) k_fwd_p1(NttJob J, uint64_t *__restrict__ tmp, int logn,
+__global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p1(NttJob J, uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ twd,
                                                     const double2 *__restrict__ twf) {
@@ -383,7 +387,7 @@ __device__ __forceinline__ void inv_pb_body(uint64_t *sm, const LimbInfo &li, co
 }
 
 template <int A>
-__global__ void __launch_bounds__(kThreads) k_inv_pb(NttJob J, const uint64_t *__restrict__ tmp, int logn,
+__global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pb(NttJob J, const uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ itwd,
                                                     const double2 *__restrict__ itwf) {
@@ -506,7 +510,7 @@ constexpr size_t p2_smem() {  // data tiles + FP64 twiddle stage
 }
 
 template <int B, int EM>
-__global__ void __launch_bounds__(kThreads) k_fwd_p2(NttJob J, const uint64_t *__restrict__ tmp, int logn,
+__global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p2(NttJob J, const uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ twd,
                                                     const double *__restrict__ twdd,
@@ -604,7 +608,7 @@ constexpr size_t fused_smem() {  // column tile + pass-2 tiles (twiddles from L2
 }
 
 template <int A, int B, int LM, int EM>
-__global__ void __launch_bounds__(kThreads) k_fwd_fused(NttJob J, int logn, const Mod *__restrict__ mods,
+__global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_fused(NttJob J, int logn, const Mod *__restrict__ mods,
                                                        const ulonglong2 *__restrict__ twd,
                                                        const double2 *__restrict__ twf,
                                                        const double *__restrict__ twdd,
@@ -687,7 +691,7 @@ __device__ __forceinline__ void inv_pa_body(uint64_t *sm, const double *tws, con
 }
 
 template <int B>
-__global__ void __launch_bounds__(kThreads) k_inv_pa(NttJob J, uint64_t *__restrict__ tmp, int logn,
+__global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ itwd,
                                                     const double *__restrict__ itwdd,
