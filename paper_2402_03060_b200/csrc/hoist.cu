@@ -556,8 +556,6 @@ __global__ void __launch_bounds__(W * 32, 1)
         acc[j][0].zero();
         acc[j][1].zero();
     }
-    // phase-A load group: bounded by the registers left next to the PPW accumulators
-    constexpr int kKsGroup = UH_KS_GROUP_FOR(PPW, W);
     int since_fold = 0;
     int buf = 0;
     constexpr int PB = PPW == 4 ? 2 : PPW, PO = PPW / PB, WB = kTBatch / PB;

@@ -155,6 +155,66 @@ __global__ void k_key_inner(uint64_t *u, const uint64_t *D, const uint64_t *key,
     }
 }
 
+// Key-switch inner product, one thread per coefficient: grid (N / 256, L + 1 limbs, polys);
+// digit and key loads issued in groups of 4 (independent loads in flight, no division in
+// the index math).  With `t` (relinearisation) the epilogue also adds (P mod q_k) * t[p][c][k]
+// for the q-limbs, i.e. u + P * (d0, d1) in the QP basis, saving a pass over u.
+__global__ void __launch_bounds__(256) k_key_inner2(uint64_t *__restrict__ u, const uint64_t *__restrict__ D,
+                                                     const uint64_t *__restrict__ key, int key_limbs, int L, int sp,
+                                                     uint32_t r, int logn, const Mod *__restrict__ mods,
+                                                     const uint64_t *__restrict__ t,
+                                                     const ulonglong2 *__restrict__ pmod) {
+    const int LP = L + 1;
+    const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    const size_t p = blockIdx.z;
+    const uint32_t half = 1u << (logn - 1);
+    const Mod m = mods[limb_mod(k, L, 0, sp)];
+    const int kk = k < L ? k : key_limbs - 1;
+    const uint32_t src = rot_index(n, half, r);
+    const uint64_t *Dp = D + (((p * L) * LP + k) << logn) + src;
+    const size_t dstr = (size_t)LP << logn, kstr = (size_t)key_limbs << logn;
+    const uint64_t *K0 = key + ((size_t)kk << logn) + n;
+    // relinearisation addend, loaded up front (its latency overlaps the digit loads)
+    uint64_t t0 = 0, t1 = 0;
+    const bool addp = t && k < L;
+    if (addp) {
+        t0 = __ldg(t + (((p * 2 + 0) * L + k) << logn) + n);
+        t1 = __ldg(t + (((p * 2 + 1) * L + k) << logn) + n);
+    }
+    Acc a0, a1;
+    a0.zero();
+    a1.zero();
+#ifndef UH_KI_G
+#define UH_KI_G 4
+#endif
+    constexpr int G = UH_KI_G;
+    for (int j0 = 0; j0 < L; j0 += G) {
+        uint64_t d[G], x[G], y[G];
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            const int j = j0 + g;
+            const bool ok = j < L;
+            d[g] = ok ? __ldg(Dp + j * dstr) : 0;
+            x[g] = ok ? __ldg(K0 + (2 * j) * kstr) : 0;
+            y[g] = ok ? __ldg(K0 + (2 * j + 1) * kstr) : 0;
+        }
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            a0.mac(d[g], x[g]);
+            a1.mac(d[g], y[g]);
+        }
+    }
+    uint64_t v0 = a0.reduce(m), v1 = a1.reduce(m);
+    if (addp) {
+        const ulonglong2 pk = pmod[k];
+        v0 = addmod(v0, shoup(t0, pk.x, pk.y, m.q), m.q);
+        v1 = addmod(v1, shoup(t1, pk.x, pk.y, m.q), m.q);
+    }
+    u[(((p * 2 + 0) * LP + k) << logn) + n] = v0;
+    u[(((p * 2 + 1) * LP + k) << logn) + n] = v1;
+}
+
 // out c0 = rot(in c0) + ks0, c1 = ks1
 __global__ void k_rot_finish(uint64_t *out, const uint64_t *in, const uint64_t *ks, int B, int L, int out_ls,
                              int in_ls, uint32_t r, int logn, const Mod *__restrict__ mods) {
@@ -200,6 +260,22 @@ __global__ void k_tensor(uint64_t *T, uint64_t *D2, const uint64_t *a, const uin
     }
 }
 
+// u[p][k] += (P mod q_k) * t[p][k] for the q-limbs k < L of QP-basis polys (u has L + 1 limbs, t has L)
+__global__ void k_add_pscaled(uint64_t *u, const uint64_t *t, int n_polys, int L, int sp, int logn,
+                              const Mod *__restrict__ mods, const ulonglong2 *__restrict__ pmod) {
+    size_t total = ((size_t)n_polys * L) << logn;
+    size_t nmask = ((size_t)1 << logn) - 1;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        size_t n = idx & nmask, r = idx >> logn;
+        int k = (int)(r % L);
+        size_t p = r / L;
+        const uint64_t q = mods[k].q;
+        const ulonglong2 pk = pmod[k];
+        uint64_t &x = u[((p * (L + 1) + k) << logn) | n];
+        x = addmod(x, shoup(t[idx], pk.x, pk.y, q), q);
+    }
+}
 }  // namespace
 
 void elementwise(const Ctx &c, int op, uint64_t *out, const uint64_t *a, const uint64_t *b, int n_polys, int b_polys,
@@ -340,14 +416,35 @@ void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level
     ntt_forward(c, D, n_polys * L, L + 1, L, 0, L + 1, s);
 }
 
-void key_inner(const Ctx &c, uint64_t *u, const uint64_t *D, const uint64_t *key, int key_limbs, int n_polys,
-               int level, int64_t r, cudaStream_t s) {
+static void key_inner_impl(const Ctx &c, uint64_t *u, const uint64_t *D, const uint64_t *key, int key_limbs,
+                           int n_polys, int level, int64_t r, const uint64_t *t, cudaStream_t s) {
     int L = level + 1;
     int64_t half = c.n / 2;
     uint32_t rr = (uint32_t)(((r % half) + half) % half);
+    if (c.n >= 256) {
+        for (int p0 = 0; p0 < n_polys; p0 += 65535) {
+            const int np = std::min(65535, n_polys - p0);
+            dim3 g((unsigned)(c.n / 256), L + 1, np);
+            k_key_inner2<<<g, 256, 0, s>>>(u + (size_t)p0 * 2 * (L + 1) * c.n, D + (size_t)p0 * L * (L + 1) * c.n,
+                                           key, key_limbs, L, c.sp(), rr, (int)c.logn, c.d_mods,
+                                           t ? t + (size_t)p0 * 2 * L * c.n : nullptr, c.d_pmod);
+            UH_LAUNCH_CHECK();
+        }
+        return;
+    }
     size_t total = (size_t)n_polys * (L + 1) * c.n;
     k_key_inner<<<grid_for(total), kTB, 0, s>>>(u, D, key, key_limbs, n_polys, L, c.sp(), rr, (int)c.logn, c.d_mods);
     UH_LAUNCH_CHECK();
+    if (t) {
+        k_add_pscaled<<<grid_for((size_t)n_polys * 2 * L * c.n), kTB, 0, s>>>(u, t, 2 * n_polys, L, c.sp(),
+                                                                              (int)c.logn, c.d_mods, c.d_pmod);
+        UH_LAUNCH_CHECK();
+    }
+}
+
+void key_inner(const Ctx &c, uint64_t *u, const uint64_t *D, const uint64_t *key, int key_limbs, int n_polys,
+               int level, int64_t r, cudaStream_t s) {
+    key_inner_impl(c, u, D, key, key_limbs, n_polys, level, r, nullptr, s);
 }
 
 void keyswitch(const Ctx &c, uint64_t *out, const uint64_t *d, int n_polys, int level, int d_ps, const uint64_t *key,
@@ -395,24 +492,6 @@ void ct_mul_relin_rescale(const Ctx &c, uint64_t *out, const uint64_t *a, const 
     divide_top(c, out, T.as<uint64_t>(), 2 * B, level, level, out_ls, L, s);
 }
 
-namespace {
-// u[p][k] += (P mod q_k) * t[p][k] for the q-limbs k < L of QP-basis polys (u has L + 1 limbs, t has L)
-__global__ void k_add_pscaled(uint64_t *u, const uint64_t *t, int n_polys, int L, int sp, int logn,
-                              const Mod *__restrict__ mods, const ulonglong2 *__restrict__ pmod) {
-    size_t total = ((size_t)n_polys * L) << logn;
-    size_t nmask = ((size_t)1 << logn) - 1;
-    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (size_t)gridDim.x * blockDim.x) {
-        size_t n = idx & nmask, r = idx >> logn;
-        int k = (int)(r % L);
-        size_t p = r / L;
-        const uint64_t q = mods[k].q;
-        const ulonglong2 pk = pmod[k];
-        uint64_t &x = u[((p * (L + 1) + k) << logn) | n];
-        x = addmod(x, shoup(t[idx], pk.x, pk.y, q), q);
-    }
-}
-}  // namespace
 
 void ct_mul_relin_rescale_fused(const Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *b, int B, int level,
                                 int out_ls, int a_ls, int b_ls, const uint64_t *rk, int rk_limbs, cudaStream_t s) {
@@ -424,11 +503,8 @@ void ct_mul_relin_rescale_fused(const Ctx &c, uint64_t *out, const uint64_t *a, 
     UH_LAUNCH_CHECK();
     Scratch D((size_t)B * L * (L + 1) * N * 8, s), u((size_t)B * 2 * (L + 1) * N * 8, s);
     modup(c, D.as<uint64_t>(), D2.as<uint64_t>(), B, level, L, s);
-    key_inner(c, u.as<uint64_t>(), D.as<uint64_t>(), rk, rk_limbs, B, level, 0, s);
-    // u + P * (d0, d1): the relinearised product times P, in the QP basis
-    k_add_pscaled<<<grid_for((size_t)B * 2 * L * N), kTB, 0, s>>>(u.as<uint64_t>(), T.as<uint64_t>(), 2 * B, L,
-                                                                   c.sp(), (int)c.logn, c.d_mods, c.d_pmod);
-    UH_LAUNCH_CHECK();
+    // u = <D, rk> + P * (d0, d1): the relinearised product times P, in the QP basis
+    key_inner_impl(c, u.as<uint64_t>(), D.as<uint64_t>(), rk, rk_limbs, B, level, 0, T.as<uint64_t>(), s);
     divide_top2(c, out, u.as<uint64_t>(), 2 * B, level, out_ls, L + 1, s);
 }
 
