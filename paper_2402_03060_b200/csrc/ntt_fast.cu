@@ -21,6 +21,9 @@
 //                  mod q_k and the epilogue writes (in[p][k] - y) * q_top^-1.
 #include "ntt_fast.cuh"
 
+#ifndef UH_NTT_STAGE
+#define UH_NTT_STAGE 0  // 1: pass-2 FP64 twiddles staged in shared memory (measured slower at 4 CTAs/SM)
+#endif
 #ifndef UH_NTT_MINB
 #define UH_NTT_MINB 4  // min resident CTAs per SM requested from ptxas (register cap: 64)
 #endif
@@ -506,7 +509,7 @@ __device__ __forceinline__ void fwd_p2_body(uint64_t *sm, const double *tws, con
 
 template <int B>
 constexpr size_t p2_smem() {  // data tiles + FP64 twiddle stage
-    return (size_t)(P2<B>::G * P2<B>::PAD + P2<B>::G * P2<B>::N2) * 8;
+    return (size_t)(P2<B>::G * P2<B>::PAD + (UH_NTT_STAGE ? P2<B>::G * P2<B>::N2 : 0)) * 8;
 }
 
 template <int B, int EM>
@@ -514,6 +517,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p2(NttJob J, cons
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ twd,
                                                     const double *__restrict__ twdd,
+                                                    const double2 *__restrict__ twf,
                                                     const int32_t *__restrict__ bsel,
                                                     const int32_t *__restrict__ csl) {
     using C = P2<B>;
@@ -526,12 +530,14 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p2(NttJob J, cons
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
     const uint64_t q = m.q;
-    const Tw tw2{twd + ((size_t)li.mod << logn), nullptr};
+    const Tw tw2{twd + ((size_t)li.mod << logn), twf + ((size_t)li.mod << logn)};
     const InGlobal<B> in{tmp + ((size_t)blockIdx.y << logn)};
     if (fp_limb(q)) {
-        stage_twiddles<B>(tws, twdd + ((size_t)li.mod << logn), sel, n1, tid);
-        __syncthreads();
-        fwd_p2_body<B, true>(sm, tws, m, tw2, in, sel, n1, tid);
+        if constexpr (UH_NTT_STAGE) {
+            stage_twiddles<B>(tws, twdd + ((size_t)li.mod << logn), sel, n1, tid);
+            __syncthreads();
+        }
+        fwd_p2_body<B, true, InGlobal<B>, UH_NTT_STAGE>(sm, tws, m, tw2, in, sel, n1, tid);
     } else {
         fwd_p2_body<B, false>(sm, tws, m, tw2, in, sel, n1, tid);
     }
@@ -647,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_fused(NttJob J, i
 }
 
 // inverse pass A stages: canonical residues in shared memory -> tmp (pass-B input)
-template <int B, bool FP>
+template <int B, bool FP, bool STAGED = true>
 __device__ __forceinline__ void inv_pa_body(uint64_t *sm, const double *tws, const Mod &m, const Tw &tw2,
                                             uint64_t *out, const int *sel, int n1, int tid) {
     using C = P2<B>;
@@ -656,10 +662,10 @@ __device__ __forceinline__ void inv_pa_body(uint64_t *sm, const double *tws, con
     const AR ar(m.q);
     const auto *T = pick<FP>(tw2);
     auto acc = [&](int g, int blk) {
-        if constexpr (FP)
+        if constexpr (FP && STAGED)
             return TwS{tws + g * C::N2, ar.qinv};
         else
-            return TwG<ulonglong2>{T, n1 + blk};
+            return TwG<typename AR::W>{T, n1 + blk};
     };
 #pragma unroll
     for (int gi = 0; gi < C::GC; gi++) {
@@ -695,6 +701,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ itwd,
                                                     const double *__restrict__ itwdd,
+                                                    const double2 *__restrict__ itwf,
                                                     const int32_t *__restrict__ bsel,
                                                     const int32_t *__restrict__ csl) {
     using C = P2<B>;
@@ -706,9 +713,9 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint
     const int *sel = bsel + blockIdx.x * C::G;
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
-    const Tw tw2{itwd + ((size_t)li.mod << logn), nullptr};
+    const Tw tw2{itwd + ((size_t)li.mod << logn), itwf + ((size_t)li.mod << logn)};
     const bool fp = fp_limb(m.q);
-    if (fp) stage_twiddles<B>(tws, itwdd + ((size_t)li.mod << logn), sel, n1, tid);
+    if (UH_NTT_STAGE && fp) stage_twiddles<B>(tws, itwdd + ((size_t)li.mod << logn), sel, n1, tid);
     // coalesced slot-order gather into the blocks' shared-memory tiles (plain limbs: the only
     // inverse mode); all of a thread's loads are issued before the shared-memory stores
     {
@@ -727,7 +734,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint
     __syncthreads();
     uint64_t *out = tmp + ((size_t)blockIdx.y << logn);
     if (fp)
-        inv_pa_body<B, true>(sm, tws, m, tw2, out, sel, n1, tid);
+        inv_pa_body<B, true, UH_NTT_STAGE>(sm, tws, m, tw2, out, sel, n1, tid);
     else
         inv_pa_body<B, false>(sm, tws, m, tw2, out, sel, n1, tid);
 }
@@ -836,13 +843,13 @@ void run_fwd(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
         UH_LAUNCH_CHECK();
         if (J.mode == NTT_DIVIDE) {
             p2_attr<k_fwd_p2<B, 1>>(sm2);
-            k_fwd_p2<B, 1><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_bsel, c.d_csl);
+            k_fwd_p2<B, 1><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl);
         } else if (J.mode == NTT_DIVIDE2) {
             p2_attr<k_fwd_p2<B, 2>>(sm2);
-            k_fwd_p2<B, 2><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_bsel, c.d_csl);
+            k_fwd_p2<B, 2><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl);
         } else {
             p2_attr<k_fwd_p2<B, 0>>(sm2);
-            k_fwd_p2<B, 0><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_bsel, c.d_csl);
+            k_fwd_p2<B, 0><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl);
         }
         UH_LAUNCH_CHECK();
     }
@@ -861,7 +868,7 @@ void run_inv(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
         const int nl = std::min(ch, limbs - f0);
         dim3 g1((1u << B) / 32, nl), g2((1u << A) / P2<B>::G, nl);
         k_inv_pa<B><<<g2, kThreads, sm2, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwd,
-                                              c.d_bsel, c.d_csl);
+                                              c.d_itwf, c.d_bsel, c.d_csl);
         UH_LAUNCH_CHECK();
         k_inv_pb<A><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwf);
         UH_LAUNCH_CHECK();
