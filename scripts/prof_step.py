@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--oplevel", action="store_true")
     ap.add_argument("--logn", type=int, default=15)
+    ap.add_argument("--trace", action="store_true", help="print every engine call in order, per layer")
     args = ap.parse_args()
     params = HEParams(poly_degree=1 << args.logn, depth=9, scale_bits=40, seed=2)
     m = planner.lenet1(0)
@@ -39,12 +40,16 @@ def main():
     ct = be.encrypt(be.encode_batch(planes[0]))
     apply = schedule.apply_layer if args.oplevel else fused.apply_layer_fused
 
+    marks = []
+
     def step(layer_events=None):
         st = CipherState([ct], driver._input_layout(m, plan))
         st = schedule.drop_level(be, st, 7)
         for layer in m.layers:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
+            if _lib.PROFILE is not None:
+                marks.append((type(layer).__name__, len(_lib.PROFILE)))
             st = apply(be, st, layer)
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
@@ -76,6 +81,12 @@ def main():
     print("per C-ABI call:")
     for name, calls, ms in _lib.profile_summary(_lib.PROFILE):
         print(f"  {name:24s} {calls:6d} calls {ms:9.3f} ms  ({100 * ms / total:5.1f}%)")
+    if args.trace:
+        bounds = marks + [("end", len(_lib.PROFILE))]
+        for (name, a), (_, b) in zip(bounds[:-1], bounds[1:]):
+            print(f"-- {name}")
+            for cname, e0, e1 in _lib.PROFILE[a:b]:
+                print(f"     {cname:26s} {e0.elapsed_time(e1):8.3f} ms")
     _lib.PROFILE = None
 
 
