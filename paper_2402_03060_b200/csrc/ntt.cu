@@ -239,6 +239,7 @@ void ntt_forward(const Ctx &c, uint64_t *data, int n_polys, int nl, int nq, int 
         ntt_fast_forward(c, J, limbs, s);
         return;
     }
+    if (limbs > 65535) throw std::invalid_argument("NTT: more than 65535 limbs in one call at this ring degree");
     Scratch tmp((size_t)limbs * n * sizeof(uint64_t), s);
     int n1 = (int)c.n1, n2 = (int)c.n2, g = pass2_group(c);
     dim3 g1(n2 / kCols, limbs), g2(n1 / g, limbs);
@@ -273,6 +274,7 @@ void ntt_inverse(const Ctx &c, uint64_t *data, int n_polys, int nl, int nq, int 
         ntt_fast_inverse(c, J, limbs, s);
         return;
     }
+    if (limbs > 65535) throw std::invalid_argument("NTT: more than 65535 limbs in one call at this ring degree");
     Scratch tmp((size_t)limbs * n * sizeof(uint64_t), s);
     int n1 = (int)c.n1, n2 = (int)c.n2, g = pass2_group(c);
     dim3 g1(n2 / kCols, limbs), g2(n1 / g, limbs);

@@ -756,9 +756,9 @@ inline int ntt_chunk(const Ctx &c, int limbs) {
         const char *e = getenv("UH_NTT_CHUNK_MB");
         return e ? atoi(e) : 0;  // measured: chunking starves the grid (B200), off by default
     }();
-    if (env <= 0) return limbs;
+    if (env <= 0) return std::min(limbs, 65535);  // grid.y limit
     const int ch = (int)(((size_t)env << 20) / (c.n * 8));
-    return std::max(1, std::min(limbs, ch));
+    return std::max(1, std::min(std::min(limbs, ch), 65535));
 }
 
 template <auto K>
