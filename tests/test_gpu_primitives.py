@@ -59,6 +59,25 @@ def test_ntt_roundtrip_bit_exact(params):
     assert np.array_equal(host(t), x)
 
 
+def test_ntt_more_limbs_than_one_grid():
+    """A single call over more than 65535 limbs (the grid.y limit) is split into launches."""
+    params = HEParams(poly_degree=1 << 13, depth=3, scale_bits=40)
+    g, o = pair(params)
+    nq = params.depth + 1
+    polys = 65535 // (nq + 1) + 7  # > 65535 limbs in the QP basis
+    q = torch.tensor([int(o.moduli[m]) for m in list(range(nq)) + [o.sp]], dtype=torch.float64, device="cuda")
+    t = (torch.rand((polys, nq + 1, o.n), dtype=torch.float64, device="cuda") * q[None, :, None]).to(torch.int64)
+    tail = t[-3:].clone()
+    _lib.call("uh_ntt", g._ctx, vp(t), polys, nq + 1, nq, nq + 1, 0, stream())
+    _lib.call("uh_ntt", g._ctx, vp(tail), 3, nq + 1, nq, nq + 1, 0, stream())
+    assert torch.equal(t[-3:], tail)
+    mods = list(range(nq)) + [o.sp]
+    head = t[:2].clone()  # the head, back through the inverse, against the oracle
+    _lib.call("uh_ntt", g._ctx, vp(head), 2, nq + 1, nq, nq + 1, 1, stream())
+    back = host(head)
+    assert np.array_equal(np.stack([o.ntt(back[r], mods) for r in range(2)]), host(t[:2]))
+
+
 @pytest.mark.parametrize("params", [SMALL, C2], ids=lambda p: f"N{p.poly_degree}")
 def test_keys_bit_exact(params):
     g, o = pair(params)
