@@ -231,6 +231,7 @@ struct TwG {  // global table (read-only path)
     int f;
     __device__ W operator()(int m, int j) const { return tw(T, m * f + j); }
 };
+#if UH_NTT_STAGE
 struct TwS {  // FP64 limbs: w staged in shared memory at [m' + j] (m' + j < 256), w / q formed on the fly
     const double *t;
     double qinv;
@@ -239,6 +240,12 @@ struct TwS {  // FP64 limbs: w staged in shared memory at [m' + j] (m' + j < 256
         return make_double2(w, w * qinv);
     }
 };
+#else
+struct TwS {  // unused unless UH_NTT_STAGE
+    const double *t;
+    double qinv;
+};
+#endif
 
 // forward radix network on R register values (elements base + S*x), stages with
 // distance dx = R/2 .. 1; twiddle (m, off(s) + x / (2 dx)), m = m0 * (1 << s)
@@ -411,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pb(NttJob J, cons
 // ---------------- pass 2 (contiguous blocks), N2 = 2^B ----------------
 template <int B>
 struct P2 {
-    static constexpr int N2 = 1 << B, B1 = 4, B2 = B - 4;
+    static constexpr int N2 = 1 << B, B2 = B - 4;
     static constexpr int R1 = 16, S = N2 / 16, R2 = 1 << B2;
     static constexpr int G = 4096 / N2;                  // blocks per CTA
     static constexpr int GC = (4096 / R2) / kThreads;    // contiguous groups per thread
