@@ -24,6 +24,9 @@
 #ifndef UH_NTT_STAGE
 #define UH_NTT_STAGE 0  // 1: pass-2 FP64 twiddles staged in shared memory (measured slower at 4 CTAs/SM)
 #endif
+#ifndef UH_NTT_TW8
+#define UH_NTT_TW8 1  // pass-2 FP64 twiddles read as w only (8 B), w / q formed with one multiply
+#endif
 #ifndef UH_NTT_MINB
 #define UH_NTT_MINB 4  // min resident CTAs per SM requested from ptxas (register cap: 64)
 #endif
@@ -230,6 +233,15 @@ struct TwG {  // global table (read-only path)
     const W *__restrict__ T;
     int f;
     __device__ W operator()(int m, int j) const { return tw(T, m * f + j); }
+};
+struct TwGd {  // FP64 limbs, w-only global table: (w, w / q) with one multiply, half the bytes of TwG<double2>
+    const double *__restrict__ T;
+    int f;
+    double qinv;
+    __device__ double2 operator()(int m, int j) const {
+        const double w = __ldg(T + m * f + j);
+        return make_double2(w, w * qinv);
+    }
 };
 #if UH_NTT_STAGE
 struct TwS {  // FP64 limbs: w staged in shared memory at [m' + j] (m' + j < 256), w / q formed on the fly
@@ -483,6 +495,8 @@ __device__ __forceinline__ void fwd_p2_body(uint64_t *sm, const double *tws, con
     auto acc = [&](int g, int blk) {
         if constexpr (FP && STAGED)
             return TwS{tws + g * C::N2, ar.qinv};
+        else if constexpr (FP && UH_NTT_TW8)
+            return TwGd{tws, n1 + blk, ar.qinv};  // tws: the limb's w-only global table here
         else
             return TwG<typename AR::W>{T, n1 + blk};
     };
@@ -544,7 +558,8 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p2(NttJob J, cons
             stage_twiddles<B>(tws, twdd + ((size_t)li.mod << logn), sel, n1, tid);
             __syncthreads();
         }
-        fwd_p2_body<B, true, InGlobal<B>, UH_NTT_STAGE>(sm, tws, m, tw2, in, sel, n1, tid);
+        fwd_p2_body<B, true, InGlobal<B>, UH_NTT_STAGE>(
+            sm, UH_NTT_STAGE ? tws : twdd + ((size_t)li.mod << logn), m, tw2, in, sel, n1, tid);
     } else {
         fwd_p2_body<B, false>(sm, tws, m, tw2, in, sel, n1, tid);
     }
@@ -652,7 +667,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_fused(NttJob J, i
     cluster_wait();
     const InCluster<B> in{tile};
     if (fp)
-        fwd_p2_body<B, true, InCluster<B>, false>(sm2, nullptr, m, tw1, in, sel, n1, tid);
+        fwd_p2_body<B, true, InCluster<B>, false>(sm2, twdd + ((size_t)li.mod << logn), m, tw1, in, sel, n1, tid);
     else
         fwd_p2_body<B, false, InCluster<B>, false>(sm2, nullptr, m, tw1, in, sel, n1, tid);
     fwd_p2_epilogue<B, EM>(sm2, li, q, csl, logn, tid);
@@ -671,6 +686,8 @@ __device__ __forceinline__ void inv_pa_body(uint64_t *sm, const double *tws, con
     auto acc = [&](int g, int blk) {
         if constexpr (FP && STAGED)
             return TwS{tws + g * C::N2, ar.qinv};
+        else if constexpr (FP && UH_NTT_TW8)
+            return TwGd{tws, n1 + blk, ar.qinv};  // tws: the limb's w-only global table here
         else
             return TwG<typename AR::W>{T, n1 + blk};
     };
@@ -741,7 +758,8 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint
     __syncthreads();
     uint64_t *out = tmp + ((size_t)blockIdx.y << logn);
     if (fp)
-        inv_pa_body<B, true, UH_NTT_STAGE>(sm, tws, m, tw2, out, sel, n1, tid);
+        inv_pa_body<B, true, UH_NTT_STAGE>(sm, UH_NTT_STAGE ? tws : itwdd + ((size_t)li.mod << logn), m, tw2, out,
+                                           sel, n1, tid);
     else
         inv_pa_body<B, false>(sm, tws, m, tw2, out, sel, n1, tid);
 }
