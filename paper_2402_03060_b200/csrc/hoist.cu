@@ -887,8 +887,14 @@ __global__ void __launch_bounds__((kWSProd + kWSCons) * 32, 1)
 // coefficients, so key and mask rows are shared through L1; the coefficient
 // tile is the fastest grid dimension (rotated digit reads of neighbouring
 // tiles hit L2).
+#ifndef UH_DIRECT_MINB
+#define UH_DIRECT_MINB 4
+#endif
+#ifndef UH_DIRECT_G
+#define UH_DIRECT_G 4
+#endif
 template <int OM, bool MASKS>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, UH_DIRECT_MINB)
     k_hoisted_direct(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
                      const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
                      const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
@@ -949,7 +955,7 @@ __global__ void __launch_bounds__(256, 4)
             const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
             const uint32_t ks = s_kstride[t];
             const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + n;
-            ks_dot<4>(a0, a1, Di, dstride, k0, ks, L);
+            ks_dot<UH_DIRECT_G>(a0, a1, Di, dstride, k0, ks, L);
             if (qlimb) a0.mac(Pk, __ldg(c0 + src));
         }
         if (MASKS) {
