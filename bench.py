@@ -291,7 +291,10 @@ def main():
             t = json.load(open(tpath))
             if t.get("batch") == B:
                 traffic = t["dram_bytes_per_launch"]
-        roofline = {"bound": "int32-imad (64-bit modular MAC; no tensor cores: modular integer work)",
+        roofline = {"bound": "imad",
+                    "bound_note": "integer-pipe bound (64-bit modular MACs as IMAD.WIDE.U32 chains): neither the HBM "
+                                  "roofline (this kernel moves 9.2 GB at ~180 GB/s, see hbm_*) nor tensor cores apply "
+                                  "-- modular integer work with per-coefficient weight matrices",
                     "kernel": f"k_hoisted_mac (LeNet conv2, level {lev}: hoisted key switch + weight MAC)",
                     "achieved": achieved, "peak": peak, "unit": "T modMAC/s", "frac": achieved / peak,
                     "traffic": traffic, "launch_ms": tms / cnt, "algorithmic_macs_per_launch": work / cnt,
