@@ -893,8 +893,11 @@ __global__ void __launch_bounds__((kWSProd + kWSCons) * 32, 1)
 #ifndef UH_DIRECT_G
 #define UH_DIRECT_G 4
 #endif
+#ifndef UH_DIRECT_G4
+#define UH_DIRECT_G4 4  // load group of the 3..4-output direct kernel (4: a few spills, measured faster than 2)
+#endif
 template <int OM, bool MASKS>
-__global__ void __launch_bounds__(256, UH_DIRECT_MINB)
+__global__ void __launch_bounds__(256, OM > 2 ? 3 : UH_DIRECT_MINB)
     k_hoisted_direct(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
                      const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
                      const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
@@ -955,7 +958,7 @@ __global__ void __launch_bounds__(256, UH_DIRECT_MINB)
             const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
             const uint32_t ks = s_kstride[t];
             const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + n;
-            ks_dot<UH_DIRECT_G>(a0, a1, Di, dstride, k0, ks, L);
+            ks_dot<(OM > 2 ? UH_DIRECT_G4 : UH_DIRECT_G)>(a0, a1, Di, dstride, k0, ks, L);
             if (qlimb) a0.mac(Pk, __ldg(c0 + src));
         }
         if (MASKS) {
@@ -1064,6 +1067,19 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
         const char *e = getenv("UH_HOIST_DIRECT");
         return !(e && std::string(e) == "0");
     }();
+    // 3..4-output masked layers (e.g. LeNet conv1: phase-A heavy, 4 outputs) on the direct kernel:
+    // measured conv1 layer 17.2 vs 21.5 ms (cp.async 24-warp kernel) at B = 64.  UH_HOIST_DIRECT4=0 disables.
+    static const bool direct4 = [] {
+        const char *e = getenv("UH_HOIST_DIRECT4");
+        return !(e && std::string(e) == "0");
+    }();
+    if (direct4 && masks && O > 2 && O <= 4) {
+        dim3 gd((unsigned)(c.n / 32), (B + 7) / 8, L + 1);
+        k_hoisted_direct<4, true><<<gd, 256, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, diag,
+                                                      L, c.sp(), (int)c.logn, c.d_mods);
+        UH_LAUNCH_CHECK();
+        return;
+    }
     if (direct_on && O <= 2) {
         dim3 gd((unsigned)(c.n / 32), (B + 7) / 8, L + 1);
         if (gd.y > 65535) throw std::invalid_argument("hoisted kernel: batch too large for one launch");
