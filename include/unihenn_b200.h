@@ -152,10 +152,13 @@ int uh_conv_hoisted_mac(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, 
                         const int32_t *shifts, int B, int I, int T, int O, int level, void *stream);
 /* Generic hoisted rotation-MAC behind every fused layer: acc[O][B][2][level+2][N]
  * = sum over terms q of masks[o][q] * P * rot_{shifts[t]}(ct_i), terms dense
- * (q = i*T + t) or diagonal (diag != 0: q = i = t, I == T); masks may be NULL
- * (all ones, no rescale needed).  Used for conv, pool, the flatten stages
- * (masks pre-rotated: rot(m .* x) = rot(m) .* rot(x)), channel packing and the
- * FC diagonals / wrap fix / folds (layers.py:263-426). */
+ * (diag 0: q = i*T + t, T shared taps), diagonal (diag 1: q = i = t, I == T) or
+ * block-diagonal (diag 2: q = i*T + t' with per-term taps t = q, i.e. shifts /
+ * keys / key_limbs hold I*T entries; O <= 2); masks may be NULL (all ones, no
+ * rescale needed).  Used for conv, pool, the flatten stages (masks pre-rotated:
+ * rot(m .* x) = rot(m) .* rot(x)), the last flatten stage merged with the
+ * channel packing (block-diagonal), and the FC diagonals / wrap fix / folds
+ * (layers.py:263-426). */
 int uh_hoisted_mac(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D, const uint64_t *masks,
                    const uint64_t *const *keys, const int32_t *key_limbs, const int32_t *shifts, int B, int I, int T,
                    int O, int diag, int level, void *stream);

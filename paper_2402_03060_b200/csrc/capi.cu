@@ -310,7 +310,8 @@ __attribute__((visibility("default"))) int uh_hoisted_mac(uh_ctx *ctx, uint64_t 
         const uh::Ctx &c = C(ctx);
         check_level(c, level);
         need(B > 0 && I > 0 && T > 0 && O > 0 && xls >= level + 1, "bad shape");
-        need(!diag || I == T, "diagonal terms need I == T");
+        need(diag >= 0 && diag <= 2, "term mode must be 0 (dense), 1 (diagonal) or 2 (block-diagonal)");
+        need(diag != 1 || I == T, "diagonal terms need I == T");
         uh::hoisted_mac(c, acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, diag, level, S(stream));
     });
 }

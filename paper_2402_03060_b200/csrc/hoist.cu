@@ -911,7 +911,8 @@ __global__ void __launch_bounds__(256, OM > 2 ? 3 : UH_DIRECT_MINB)
     const uint32_t n = blockIdx.x * 32 + lane;
     const int k = blockIdx.z;
     const uint32_t N = 1u << logn, half = N >> 1;
-    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    const int NT = diag == 2 ? I * T : T;  // per-term metadata entries
+    for (int t = threadIdx.x; t < NT; t += blockDim.x) {
         s_key[t] = keys[t];
         s_shift[t] = (uint32_t)shifts[t];
         s_kstride[t] = (uint32_t)key_limbs[t] << logn;
@@ -924,7 +925,7 @@ __global__ void __launch_bounds__(256, OM > 2 ? 3 : UH_DIRECT_MINB)
     const bool smallq = (m.q >> 41) == 0 && L <= kMaxL;
     const uint64_t P = mods[sp].q;
     const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
-    const int Q = diag ? I : I * T;
+    const int Q = diag == 1 ? I : I * T;
     const uint32_t dstride = (uint32_t)LP << logn;
     const uint32_t mask_row = ((uint32_t)k << logn) + n;
     Acc acc[OM][2];
@@ -935,7 +936,12 @@ __global__ void __launch_bounds__(256, OM > 2 ? 3 : UH_DIRECT_MINB)
     }
     int i = 0, t = 0, since = 0;
     for (int q = 0; q < Q; q++) {
-        if (diag) i = t = q;
+        if (diag == 1) {
+            i = t = q;
+        } else if (diag == 2) {  // block-diagonal: input q / T with its own tap q
+            t = q;
+            i = q / T;
+        }
         const uint32_t ib = (uint32_t)(i * B + b);
         const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
         const uint32_t r = s_shift[t];
@@ -985,7 +991,7 @@ __global__ void __launch_bounds__(256, OM > 2 ? 3 : UH_DIRECT_MINB)
             acc[0][0].add(v0);
             acc[0][1].add(v1);
         }
-        if (!diag && ++t == T) {
+        if (diag == 0 && ++t == T) {
             t = 0;
             i++;
         }
@@ -1007,10 +1013,13 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
                  int O, int diag, int level, cudaStream_t s) {
     const int L = level + 1;
     if (L > kMaxL) throw std::invalid_argument("hoisted kernel supports up to 12 live limbs");
-    if (T > kMaxTerms) throw std::invalid_argument("hoisted kernel supports up to 512 taps");
+    if ((diag == 2 ? I * T : T) > kMaxTerms) throw std::invalid_argument("hoisted kernel supports up to 512 taps");
+    if (diag < 0 || diag > 2) throw std::invalid_argument("hoisted kernel: term mode must be 0, 1 or 2");
+    if (diag == 2 && O > 2)
+        throw std::invalid_argument("block-diagonal terms (per-input taps) are supported for up to 2 outputs");
     const double lim = 4294967295.0;  // 32-bit element offsets inside the kernel
     if ((double)I * B * 2 * xls * c.n > lim || (double)I * B * L * (L + 1) * c.n > lim ||
-        (double)O * B * 2 * (L + 1) * c.n > lim || (double)O * (diag ? I : I * T) * (L + 1) * c.n > lim)
+        (double)O * B * 2 * (L + 1) * c.n > lim || (double)O * (diag == 1 ? I : I * T) * (L + 1) * c.n > lim)
         throw std::invalid_argument("hoisted kernel operand exceeds 2^32 elements: split the batch");
     const int pairs = O * kTBatch;
     dim3 grid((B + kTBatch - 1) / kTBatch, (unsigned)(c.n / 32), L + 1);
@@ -1080,7 +1089,7 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
         UH_LAUNCH_CHECK();
         return;
     }
-    if (direct_on && O <= 2) {
+    if ((direct_on || diag == 2) && O <= 2) {
         dim3 gd((unsigned)(c.n / 32), (B + 7) / 8, L + 1);
         if (gd.y > 65535) throw std::invalid_argument("hoisted kernel: batch too large for one launch");
         if (masks) {

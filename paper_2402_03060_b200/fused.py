@@ -253,8 +253,11 @@ def square(backend, state: CipherState) -> CipherState:
 # reference's levels.
 
 
-def _hoist(backend, X, level, shifts, masks, O, diag, B):
-    """acc [O][B][2][level+2][N] of uh_hoisted_mac over stacked inputs X [I][B][2][level+1][N]."""
+def _hoist(backend, X, level, shifts, masks, O, diag, B, taps=None):
+    """acc [O][B][2][level+2][N] of uh_hoisted_mac over stacked inputs X [I][B][2][level+1][N].
+
+    diag: False (dense: every input x every shift), True (input i with shift i) or 2
+    (block-diagonal: input i with its own ``taps`` shifts, shifts[i * taps + t])."""
     L, LP, n = level + 1, level + 2, backend.n
     I = X.shape[0]
     st = backend._stream()
@@ -262,8 +265,10 @@ def _hoist(backend, X, level, shifts, masks, O, diag, B):
     backend._call("uh_modup", _vp(D), _vp(X.data_ptr() + L * n * 8), I * B, level, 2 * L, st)
     sh, ptrs, keys, limbs = _rotation_plan(backend, shifts, level)
     acc = backend._empty(O, B, 2, LP, n)
+    mode = 2 if diag == 2 else (1 if diag else 0)
+    T = taps if mode == 2 else len(shifts)
     backend._call("uh_hoisted_mac", _vp(acc), _vp(X), L, _vp(D), _vp(masks) if masks is not None else _vp(0),
-                  _vp(ptrs), _vp(limbs), _vp(sh), B, I, len(shifts), O, 1 if diag else 0, level, st)
+                  _vp(ptrs), _vp(limbs), _vp(sh), B, I, T, O, mode, level, st)
     del keys, D
     return acc
 
@@ -298,6 +303,22 @@ def _masked_rotation_stage(backend, X, level, B, plan, tag):
                  C * B)
     out = _finish(backend, acc, level, rescale=True)  # [1][C*B][2][level][N]
     return out.view(C, B, 2, level, backend.n)
+
+
+def _masked_rotation_pack(backend, X, level, B, plan, pack_shifts, tag):
+    """The last masked flatten stage fused with the channel packing (one level consumed):
+
+        sum_ch rot_{t_ch}( sum_r rot_{s_r}(m_r .* x_ch) ) = sum_{ch,r} rot_{t_ch+s_r}(m_r) .* rot_{t_ch+s_r}(x_ch)
+
+    one block-diagonal hoisted MAC over the C channels into a single output, so the packing
+    needs no ModUp of its own and only one ModDown + rescale per ciphertext is done instead of
+    C (rotation commutes with the slot-wise mask product)."""
+    C, R = X.shape[0], len(plan)
+    shifts = [t + s for t in pack_shifts for _, s in plan]
+    masks_np = np.stack([np.roll(m, -(t + s)) for t in pack_shifts for m, s in plan])
+    bank = _rows_bank(backend, tag + (level, tuple(pack_shifts)), masks_np, level, float(backend.modulus(level)))
+    acc = _hoist(backend, X, level, shifts, bank.view(1, C * R, level + 2, backend.n), 1, 2, B, taps=R)
+    return _finish(backend, acc, level, rescale=True)[0]  # [B][2][level][N]
 
 
 def flatten(backend, state: CipherState) -> CipherState:
@@ -355,6 +376,8 @@ def flatten(backend, state: CipherState) -> CipherState:
         masked_census(plan, level)
         X = _masked_rotation_stage(backend, X, level, B, plan, ("flat_r", lay))
         level -= 1
+    flat = w_in * h_in
+    packed = None
     if col_rm:
         plan = []
         for r in range(h_in):
@@ -362,10 +385,18 @@ def flatten(backend, state: CipherState) -> CipherState:
             region[r * span:r * span + w_in] = 1.0
             plan.append((schedule.tile_region(ns, lay, region), r * (span - w_in)))
         masked_census(plan, level)
-        X = _masked_rotation_stage(backend, X, level, B, plan, ("flat_c", lay))
+        if C > 1 and _merge_pack():
+            # channel packing fused into this stage (census of the packing recorded below as usual)
+            packed = _masked_rotation_pack(backend, X, level, B, plan, [-ch * flat for ch in range(C)],
+                                           ("flat_cp", lay))
+        else:
+            X = _masked_rotation_stage(backend, X, level, B, plan, ("flat_c", lay))
         level -= 1
-    flat = w_in * h_in
-    if C > 1:
+    if packed is not None:
+        cnt.record("rotation", level, C - 1)
+        cnt.record("add", level, C - 1)
+        out = packed
+    elif C > 1:
         cnt.record("rotation", level, C - 1)
         cnt.record("add", level, C - 1)
         X = X[:, :, :, :level + 1].contiguous() if X.shape[3] != level + 1 else X
@@ -376,6 +407,12 @@ def flatten(backend, state: CipherState) -> CipherState:
     new_lay = replace(lay, interval=1, w_in=flat * lay.channels, h_in=1, channels=1, pending_const=1.0,
                       gaps_zero=True)
     return CipherState([CipherVector(out, level, scale, backend)], new_lay)
+
+
+def _merge_pack() -> bool:
+    import os
+
+    return os.environ.get("UH_FLATTEN_MERGE", "1") != "0"
 
 
 def math_ceil(x):

@@ -68,3 +68,28 @@ def test_builtin_models_fused_vs_plaintext(name):
     for s, y in zip(samples, outs):
         ref = planner.reference_infer(m, s)
         assert np.max(np.abs(y - ref)) < 1e-5 * max(1.0, float(np.max(np.abs(ref))))
+
+
+def test_block_diagonal_hoisted_mac_equals_per_input_sums():
+    """uh_hoisted_mac term mode 2 (per-input taps) == the sum of dense single-input calls, residue for residue."""
+    import torch
+
+    p = HEParams(poly_degree=1 << 12, depth=3, scale_bits=40, seed=3)
+    be = GpuBackend(p)
+    level, B, C, R = 2, 3, 3, 2
+    rng = np.random.default_rng(7)
+    cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, p.num_slots)))) for _ in range(C)]
+    X = fused.stack_cts(be, cts, level)  # [C][B][2][L][N]
+    shifts = [int(s) for s in rng.integers(-40, 40, size=C * R)]
+    rows = rng.uniform(-1, 1, size=(C * R, p.num_slots))
+    bank = fused.encode_rows_qp(be, torch.from_numpy(rows).to(be.device), level, float(be.modulus(level)))
+    bank = bank.view(1, C * R, level + 2, be.n)
+    got = fused._hoist(be, X, level, shifts, bank, 1, 2, B, taps=R)[0]
+    want = None
+    for i in range(C):
+        part = fused._hoist(be, X[i:i + 1].contiguous(), level, shifts[i * R:(i + 1) * R],
+                            bank[:, i * R:(i + 1) * R].contiguous(), 1, False, B)[0]
+        want = part if want is None else want + part
+    mods = [be.modulus(k) for k in range(level + 1)] + [be.modulus(be.sp)]
+    q = torch.tensor(mods, dtype=torch.int64, device=be.device).view(1, 1, -1, 1)
+    assert torch.equal(got, torch.remainder(want, q))
