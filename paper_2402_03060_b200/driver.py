@@ -174,16 +174,37 @@ def infer_batch(m, planes, params, plan, backend, counts=None, cost_model=None, 
     if not report.ok:
         raise SlotCnnError("model failed validation: " + "; ".join(v["message"] for v in report.violations))
     cost = cost_model or CostModel()
-    cts = [backend.encrypt(backend.encode_batch(planes[ch])) for ch in range(m.channels)]
+    import torch
+
+    if isinstance(planes, torch.Tensor) and hasattr(backend, "encrypt_slots"):
+        cts = [backend.encrypt_slots(planes[ch]) for ch in range(m.channels)]  # async H2D (pinned host)
+    else:
+        cts = [backend.encrypt(backend.encode_batch(planes[ch])) for ch in range(m.channels)]
     state, rows, total = _run_layers(m, CipherState(cts, _input_layout(m, plan)), backend, cost,
                                      params.poly_degree, fused)
+    metrics = OpMetrics(rows, params.poly_degree, params.depth, total, m.channels)
+    if hasattr(backend, "decrypt_device"):
+        # decrypt and gather the output slots on the device; only the logits cross to the host
+        lay = state.layout
+        pos = valid_positions(lay)
+        idx = torch.from_numpy((np.asarray(plan.offsets)[:, None] + pos[None, :]).reshape(-1)).to(backend.device)
+        vals = torch.cat([backend.decrypt_device(ct)[:, idx].view(-1, len(plan.offsets), len(pos))
+                          for ct in state.cts], dim=2)
+        if lay.pending_const != 1.0:
+            vals = vals * lay.pending_const
+        host = vals.cpu().numpy()
+        outputs = []
+        for b in range(host.shape[0]):
+            cnt = plan.capacity if counts is None else counts[b]
+            outputs.append(list(host[b, :cnt]))
+        return outputs, metrics
     dec = [np.atleast_2d(backend.decrypt(ct)) for ct in state.cts]
     B = dec[0].shape[0]
     outputs = []
     for b in range(B):
         cnt = plan.capacity if counts is None else counts[b]
         outputs.append(_extract([d[b] for d in dec], state.layout, plan.offsets[:cnt]))
-    return outputs, OpMetrics(rows, params.poly_degree, params.depth, total, m.channels)
+    return outputs, metrics
 
 
 def verify_against_oracle(m, params, n_trials: int = 20, seed: int = 0, tol: float = 1e-3, alignment: int = 1,

@@ -260,13 +260,27 @@ class GpuBackend:
         """Fresh ciphertext(s) at the full level budget."""
         lev = self.depth
         pt = self.plain_device(plain, lev, self.scale0)
+        plain._dev.pop((lev, self.scale0), None)  # inputs are encrypted once; do not pin them
+        return self._encrypt_encoded(pt)
+
+    def _encrypt_encoded(self, pt: torch.Tensor) -> CipherVector:
+        lev = self.depth
         B = pt.shape[0]
         out = self._empty(B, 2, lev + 1, self.n)
         self._call("uh_encrypt", _ptr(out), _ptr(pt), _ptr(self.secret), B, lev, lev + 1, lev + 1,
                    self.params.seed, self._ct_id, self._stream())
         self._ct_id += B
-        plain._dev.pop((lev, self.scale0), None)  # inputs are encrypted once; do not pin them
         return CipherVector(out, lev, self.scale0, self)
+
+    def encrypt_slots(self, slots: torch.Tensor) -> CipherVector:
+        """Encode + encrypt a batch of slot rows given as a float64 tensor [B, <= num_slots]
+        (host -- ideally pinned, copied asynchronously -- or device): the batched client path."""
+        if slots.dim() != 2 or slots.shape[1] > self.params.num_slots:
+            raise OversizedInput(f"encrypt_slots expects [B, <= {self.params.num_slots}], got {tuple(slots.shape)}")
+        vals = slots.to(device=self.device, dtype=torch.float64, non_blocking=True)
+        if vals.shape[1] < self.params.num_slots:
+            vals = torch.nn.functional.pad(vals, (0, self.params.num_slots - vals.shape[1]))
+        return self._encrypt_encoded(self.encode_device(vals, self.depth, self.scale0))
 
     def decrypt_device(self, c: CipherVector) -> torch.Tensor:
         """Slot values [B, num_slots] as a float64 CUDA tensor."""
