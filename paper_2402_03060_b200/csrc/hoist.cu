@@ -19,7 +19,6 @@
 // CTA: W warps; lane <-> coefficient n (coalesced 256-byte rows of every
 // operand); grid = (B/TB tiles fastest, N/32 coefficient tiles, L+1 limbs),
 // so CTAs sharing the same masks/keys run back to back and hit L2.
-#include <type_traits>
 #include "ops.cuh"
 
 namespace uh {
@@ -264,190 +263,6 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : (TB < 8 && W 
 }
 
 // ---------------------------------------------------------------------------
-// FP64-pipe phase B for masked dense layers on limbs with q < 2^41.
-// Operands split at 21 bits (a = a1 2^21 + a0, a0 < 2^21, a1 < 2^20) make every
-// partial product an integer below 2^42, so three FP64 accumulators per
-// (output, ciphertext, component)
-//   S2 += a1 b1,   S1 += a1 b0 + a0 b1,   S0 += a0 b0
-// stay exact for up to 2^11 terms: 4 DFMA per multiply-accumulate instead of
-// ~11 IMAD-pipe slots for the 128-bit integer MAC, on an otherwise idle pipe.
-// The weight masks are split on load; the phase-A terms are split once when
-// they are staged in shared memory (dynamic, 2 x the integer staging).  Phase A
-// (key products) stays on the integer pipe.  Limbs k = z0 + blockIdx.z * zstep.
-constexpr double kTwo52d = 4503599627370496.0;
-__device__ __forceinline__ double lo21(uint64_t x) {  // exact double of x mod 2^21
-    return __longlong_as_double((long long)((x & 0x1FFFFFull) | 0x4330000000000000ull)) - kTwo52d;
-}
-__device__ __forceinline__ double hi21(uint64_t x) {  // exact double of x >> 21 (x < 2^52)
-    return __longlong_as_double((long long)((x >> 21) | 0x4330000000000000ull)) - kTwo52d;
-}
-__device__ __forceinline__ uint64_t d2u_exact(double v) {  // 0 <= v < 2^52, integer-valued
-    return (uint64_t)__double_as_longlong(v + kTwo52d) ^ 0x4330000000000000ull;
-}
-struct AccF {
-    double s0, s1, s2;
-    __device__ __forceinline__ void zero() { s0 = s1 = s2 = 0.0; }
-    __device__ __forceinline__ void mac(double a0, double a1, double b0, double b1) {
-        s2 = fma(a1, b1, s2);
-        s1 = fma(a1, b0, s1);
-        s1 = fma(a0, b1, s1);
-        s0 = fma(a0, b0, s0);
-    }
-    // (S2 2^42 + S1 2^21 + S0) mod q; c21 = 2^21 mod q, c42 = 2^42 mod q
-    __device__ __forceinline__ uint64_t reduce(const Mod &m, uint64_t c21, uint64_t c42) const {
-        const uint64_t u2 = d2u_exact(s2), u1 = d2u_exact(s1), u0 = d2u_exact(s0);
-        uint64_t r = mulmod(csub(barrett_lite(u2, m), m.q), c42, m);
-        r = addmod(r, mulmod(csub(barrett_lite(u1, m), m.q), c21, m), m.q);
-        return addmod(r, csub(barrett_lite(u0, m), m.q), m.q);
-    }
-};
-constexpr int kFpMaxTerms = 2048;  // exactness bound of the split accumulators
-
-template <int PPW, int W>
-__global__ void __launch_bounds__(W * 32, 1)
-    k_hoisted_fp(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
-                 const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
-                 const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
-                 const int32_t *__restrict__ shifts, int B, int I, int T, int O, int L, int sp, int logn,
-                 const Mod *__restrict__ mods, int z0, int zstep) {
-    extern __shared__ double svf[];  // [2][kTChunk][kTBatch][2 comps][2 halves][32]
-    __shared__ const uint64_t *s_key[kMaxTerms];
-    __shared__ uint32_t s_shift[kMaxTerms];
-    __shared__ uint32_t s_kstride[kMaxTerms];
-    auto SV = [&](int buf, int qc, int bt, int c, int h) -> double * {
-        return svf + ((((buf * kTChunk + qc) * kTBatch + bt) * 2 + c) * 2 + h) * 32;
-    };
-    const int LP = L + 1;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int b0 = blockIdx.x * kTBatch;
-    const uint32_t n = blockIdx.y * 32 + lane;
-    const int k = z0 + blockIdx.z * zstep;
-    const uint32_t N = 1u << logn, half = N >> 1;
-    const Mod m = mods[limb_mod(k, L, 0, sp)];
-    const bool qlimb = k < L;
-    const uint64_t P = mods[sp].q;
-    const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
-    const int Q = I * T;
-    const int npairs = O * kTBatch;
-    for (int t = threadIdx.x; t < T; t += blockDim.x) {
-        s_key[t] = keys[t];
-        s_shift[t] = (uint32_t)shifts[t];
-        s_kstride[t] = (uint32_t)key_limbs[t] << logn;
-    }
-    __syncthreads();
-    AccF acc[PPW][2];
-#pragma unroll
-    for (int j = 0; j < PPW; j++) {
-        acc[j][0].zero();
-        acc[j][1].zero();
-    }
-    int buf = 0;
-    constexpr int ITEMS = kTChunk * kTBatch / W;
-    static_assert(ITEMS * W == kTChunk * kTBatch, "phase-A items must tile the chunk");
-    constexpr int PB = PPW == 4 ? 2 : PPW, PO = PPW / PB, WB = kTBatch / PB;
-    const int o_a = (warp / WB) * PO, b_a = (warp % WB) * PB;
-    const bool warp_active = o_a < O && warp * PPW < npairs;
-    const uint32_t dstride = (uint32_t)LP << logn;
-    const uint32_t mask_row = ((uint32_t)k << logn) + n;
-    int i0 = 0, t0 = 0;
-    for (int q0 = 0; q0 < Q; q0 += kTChunk) {
-        uint64_t mpre[kTChunk][PO];
-#pragma unroll
-        for (int qc = 0; qc < kTChunk; qc++)
-#pragma unroll
-            for (int d = 0; d < PO; d++)
-                mpre[qc][d] = (warp_active && o_a + d < O && q0 + qc < Q)
-                                  ? masks[(((uint32_t)(o_a + d) * Q + q0 + qc) * dstride) + mask_row]
-                                  : 0;
-        // ---- phase A (integer pipe), terms staged split into 21-bit halves ----
-#pragma unroll
-        for (int ii = 0; ii < ITEMS; ii++) {
-            const int it = threadIdx.x + ii * W * 32;
-            const int ln = it & 31, rest = it >> 5;
-            const int bt = rest % kTBatch, qc = rest / kTBatch;
-            const int q = q0 + qc, b = b0 + bt;
-            uint64_t v0 = 0, v1 = 0;
-            if (q < Q && b < B) {
-                int i = i0, t = t0 + qc;
-                while (t >= T) {
-                    t -= T;
-                    i++;
-                }
-                const uint32_t nn = blockIdx.y * 32 + ln;
-                const uint32_t ib = (uint32_t)(i * B + b);
-                const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
-                const uint32_t r = s_shift[t];
-                if (r == 0) {
-                    if (qlimb) {
-                        v0 = mulmod(Pk, c0[nn], m);
-                        v1 = mulmod(Pk, c0[((uint32_t)xls << logn) + nn], m);
-                    }
-                } else {
-                    const uint32_t src = rot_index(nn, half, r);
-                    const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
-                    const uint32_t ks = s_kstride[t];
-                    const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + nn;
-                    Acc a0, a1;
-                    a0.zero();
-                    a1.zero();
-                    ks_dot<UH_KS_GROUP_FOR(PPW, W)>(a0, a1, Di, dstride, k0, ks, L);
-                    if (qlimb) a0.mac(Pk, c0[src]);
-                    v0 = a0.reduce(m);
-                    v1 = a1.reduce(m);
-                }
-            }
-            SV(buf, qc, bt, 0, 0)[ln] = lo21(v0);
-            SV(buf, qc, bt, 0, 1)[ln] = hi21(v0);
-            SV(buf, qc, bt, 1, 0)[ln] = lo21(v1);
-            SV(buf, qc, bt, 1, 1)[ln] = hi21(v1);
-        }
-        __syncthreads();
-        // ---- phase B (FP64 pipe) ----
-        const int qn = min(kTChunk, Q - q0);
-#pragma unroll
-        for (int qc = 0; qc < kTChunk; qc++) {
-            if (qc >= qn) break;
-            if (warp_active) {
-                double ml[PO], mh[PO];
-#pragma unroll
-                for (int d = 0; d < PO; d++) {
-                    ml[d] = lo21(mpre[qc][d]);
-                    mh[d] = hi21(mpre[qc][d]);
-                }
-#pragma unroll
-                for (int db = 0; db < PB; db++) {
-                    const int bt = b_a + db;
-                    const double v0l = SV(buf, qc, bt, 0, 0)[lane], v0h = SV(buf, qc, bt, 0, 1)[lane];
-                    const double v1l = SV(buf, qc, bt, 1, 0)[lane], v1h = SV(buf, qc, bt, 1, 1)[lane];
-#pragma unroll
-                    for (int d = 0; d < PO; d++) {
-                        const int j = d * PB + db;
-                        acc[j][0].mac(ml[d], mh[d], v0l, v0h);
-                        acc[j][1].mac(ml[d], mh[d], v1l, v1h);
-                    }
-                }
-            }
-        }
-        buf ^= 1;
-        t0 += kTChunk;
-        while (t0 >= T) {
-            t0 -= T;
-            i0++;
-        }
-    }
-    const uint64_t c21 = (1ull << 21) % m.q, c42 = mulmod(c21, c21, m);
-#pragma unroll
-    for (int j = 0; j < PPW; j++) {
-        const int o = o_a + j / PB, b = b0 + b_a + j % PB;
-        if (warp_active && o < O && b < B) {
-            uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
-            dst[0] = acc[j][0].reduce(m, c21, c42);
-            dst[dstride] = acc[j][1].reduce(m, c21, c42);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // Pipelined variant: the next chunk's operands (hoisted digits at the rotated
 // offsets, c0, and the Galois-key rows) are staged into shared memory with
 // cp.async while the current chunk is multiply-accumulated, so phase A reads
@@ -460,9 +275,7 @@ __device__ __forceinline__ void cp8(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int NW> __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NW)); }
 
-// FPB: FP64-pipe phase B (split-operand accumulators, see AccF) for limbs with q < 2^41;
-// the rotated terms are then staged split in dynamic shared memory after the cp.async stages.
-template <int PPW, int W, bool FPB = false>
+template <int PPW, int W>
 __global__ void __launch_bounds__(W * 32, 1)
     k_hoisted_mac_cp(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
                      const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
@@ -470,7 +283,7 @@ __global__ void __launch_bounds__(W * 32, 1)
                      const int32_t *__restrict__ shifts, int B, int I, int T, int O, int diag, int L, int sp,
                      int logn, const Mod *__restrict__ mods, int z0 = 0, int zstep = 1) {
     extern __shared__ uint64_t dyn[];
-    __shared__ uint64_t sv[FPB ? 1 : 2][kTChunk][kTBatch][2][32];
+    __shared__ uint64_t sv[2][kTChunk][kTBatch][2][32];
     __shared__ const uint64_t *s_key[kMaxTerms];
     __shared__ uint32_t s_shift[kMaxTerms];
     __shared__ uint32_t s_kstride[kMaxTerms];
@@ -495,10 +308,6 @@ __global__ void __launch_bounds__(W * 32, 1)
     // stage layout (uint64 words): D [kTChunk][kTBatch][L][32], C [kTChunk][kTBatch][32], K [kTChunk][2L][32]
     const int szD = kTChunk * kTBatch * L * 32, szC = kTChunk * kTBatch * 32, szK = kTChunk * 2 * L * 32;
     const int stage = szD + szC + szK;
-    double *svf = reinterpret_cast<double *>(dyn + 2 * stage);  // FPB: [2][kTChunk][kTBatch][2][2][32]
-    auto SVF = [&](int bb, int qc, int bt, int c, int h) -> double * {
-        return svf + ((((bb * kTChunk + qc) * kTBatch + bt) * 2 + c) * 2 + h) * 32;
-    };
     __syncthreads();
 
     const uint32_t dstride = (uint32_t)LP << logn;
@@ -549,8 +358,7 @@ __global__ void __launch_bounds__(W * 32, 1)
         }
     };
 
-    using AccT = std::conditional_t<FPB, AccF, Acc>;
-    AccT acc[PPW][2];
+    Acc acc[PPW][2];
 #pragma unroll
     for (int j = 0; j < PPW; j++) {
         acc[j][0].zero();
@@ -606,31 +414,19 @@ __global__ void __launch_bounds__(W * 32, 1)
                     Acc a0, a1;
                     a0.zero();
                     a1.zero();
-#pragma unroll (FPB ? 2 : 4)
+#pragma unroll 4
                     for (int j = 0; j < L; j++) {
                         const uint64_t d = dD[j * 32];
                         a0.mac(d, kK[(2 * j) * 32]);
                         a1.mac(d, kK[(2 * j + 1) * 32]);
                     }
                     if (qlimb) a0.mac(Pk, sC[(qc * kTBatch + bt) * 32 + lane]);
-                    if constexpr (FPB) {
-                        v0 = a0.reduce(m);
-                        v1 = a1.reduce(m);
-                    } else {
-                        v0 = term_value(a0, m, smallq);
-                        v1 = term_value(a1, m, smallq);
-                    }
+                    v0 = term_value(a0, m, smallq);
+                    v1 = term_value(a1, m, smallq);
                 }
             }
-            if constexpr (FPB) {
-                SVF(buf, qc, bt, 0, 0)[lane] = lo21(v0);
-                SVF(buf, qc, bt, 0, 1)[lane] = hi21(v0);
-                SVF(buf, qc, bt, 1, 0)[lane] = lo21(v1);
-                SVF(buf, qc, bt, 1, 1)[lane] = hi21(v1);
-            } else {
-                sv[buf][qc][bt][0][lane] = v0;
-                sv[buf][qc][bt][1][lane] = v1;
-            }
+            sv[buf][qc][bt][0][lane] = v0;
+            sv[buf][qc][bt][1][lane] = v1;
         }
         __syncthreads();
         // ---- phase B ----
@@ -638,29 +434,7 @@ __global__ void __launch_bounds__(W * 32, 1)
 #pragma unroll
         for (int qc = 0; qc < kTChunk; qc++) {
             if (qc >= qn) break;
-            if constexpr (FPB) {  // masks required on this path
-                if (warp_active) {
-                    double ml[PO], mh[PO];
-#pragma unroll
-                    for (int d = 0; d < PO; d++) {
-                        ml[d] = lo21(mpre[qc][d]);
-                        mh[d] = hi21(mpre[qc][d]);
-                    }
-#pragma unroll
-                    for (int db = 0; db < PB; db++) {
-                        const int bt = b_a + db;
-                        const double v0l = SVF(buf, qc, bt, 0, 0)[lane], v0h = SVF(buf, qc, bt, 0, 1)[lane];
-                        const double v1l = SVF(buf, qc, bt, 1, 0)[lane], v1h = SVF(buf, qc, bt, 1, 1)[lane];
-#pragma unroll
-                        for (int d = 0; d < PO; d++) {
-                            const int j = d * PB + db;
-                            acc[j][0].mac(ml[d], mh[d], v0l, v0h);
-                            acc[j][1].mac(ml[d], mh[d], v1l, v1h);
-                        }
-                    }
-                }
-                continue;
-            } else if (warp_active) {
+            if (warp_active) {
 #pragma unroll
                 for (int db = 0; db < PB; db++) {
                     const int bt = b_a + db;
@@ -678,16 +452,14 @@ __global__ void __launch_bounds__(W * 32, 1)
                     }
                 }
             }
-            if constexpr (!FPB) {
-                if (++since_fold == kFold) {
-                    since_fold = 0;
+            if (++since_fold == kFold) {
+                since_fold = 0;
 #pragma unroll
-                    for (int j = 0; j < PPW; j++)
-                        for (int cc = 0; cc < 2; cc++) {
-                            uint64_t rr = reduce128_lazy(acc[j][cc].hi64(), acc[j][cc].lo64(), m);
-                            acc[j][cc].set(rr, 0);
-                        }
-                }
+                for (int j = 0; j < PPW; j++)
+                    for (int cc = 0; cc < 2; cc++) {
+                        uint64_t rr = reduce128_lazy(acc[j][cc].hi64(), acc[j][cc].lo64(), m);
+                        acc[j][cc].set(rr, 0);
+                    }
             }
         }
         buf ^= 1;
@@ -696,183 +468,13 @@ __global__ void __launch_bounds__(W * 32, 1)
         t0 = t1;
     }
     cp_wait<0>();
-    uint64_t c21 = 0, c42 = 0;
-    if constexpr (FPB) {
-        c21 = (1ull << 21) % m.q;
-        c42 = mulmod(c21, c21, m);
-    }
 #pragma unroll
     for (int j = 0; j < PPW; j++) {
         const int o = o_a + j / PB, b = b0 + b_a + j % PB;
         if (warp_active && o < O && b < B) {
             uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
-            if constexpr (FPB) {
-                dst[0] = acc[j][0].reduce(m, c21, c42);
-                dst[dstride] = acc[j][1].reduce(m, c21, c42);
-            } else {
-                dst[0] = acc[j][0].reduce(m);
-                dst[dstride] = acc[j][1].reduce(m);
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Warp-specialised variant for wide masked layers (9..12 outputs, e.g. LeNet
-// conv2): 8 producer warps form the rotated key-switched terms (phase A) of
-// chunk c+1 while 16 consumer warps multiply-accumulate chunk c (phase B);
-// double-buffered shared-memory terms, named-barrier full/empty handshake
-// (no CTA-wide barrier in the steady state).  Consumer warp w owns 3 outputs x
-// 2 ciphertexts.
-__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
-__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n)); }
-
-constexpr int kWSProd = 8, kWSCons = 16, kWSPO = 3, kWSPB = 2;
-
-__global__ void __launch_bounds__((kWSProd + kWSCons) * 32, 1)
-    k_hoisted_ws(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, int xls,
-                 const uint64_t *__restrict__ D, const uint64_t *__restrict__ masks,
-                 const uint64_t *const *__restrict__ keys, const int32_t *__restrict__ key_limbs,
-                 const int32_t *__restrict__ shifts, int B, int I, int T, int O, int L, int sp, int logn,
-                 const Mod *__restrict__ mods) {
-    constexpr int NT = (kWSProd + kWSCons) * 32;
-    __shared__ uint64_t sv[2][kTChunk][kTBatch][2][32];
-    __shared__ const uint64_t *s_key[kMaxTerms];
-    __shared__ uint32_t s_shift[kMaxTerms];
-    __shared__ uint32_t s_kstride[kMaxTerms];
-    const int LP = L + 1;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int b0 = blockIdx.x * kTBatch;
-    const uint32_t n = blockIdx.y * 32 + lane;
-    const int k = blockIdx.z;
-    const uint32_t N = 1u << logn, half = N >> 1;
-    const Mod m = mods[limb_mod(k, L, 0, sp)];
-    const bool qlimb = k < L;
-    const uint64_t P = mods[sp].q;
-    const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
-    const int Q = I * T;
-    const int nchunks = (Q + kTChunk - 1) / kTChunk;
-    for (int t = threadIdx.x; t < T; t += NT) {
-        s_key[t] = keys[t];
-        s_shift[t] = (uint32_t)shifts[t];
-        s_kstride[t] = (uint32_t)key_limbs[t] << logn;
-    }
-    __syncthreads();
-    const uint32_t dstride = (uint32_t)LP << logn;
-
-    if (warp < kWSProd) {
-        // ---------------- producers ----------------
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 48;\n" ::);
-        int i0 = 0, t0 = 0;
-        for (int c = 0; c < nchunks; c++) {
-            const int buf = c & 1, q0 = c * kTChunk;
-            if (c >= 2) bar_sync(3 + buf, NT);  // consumers released this buffer
-#pragma unroll
-            for (int gi = 0; gi < kTChunk * kTBatch / kWSProd; gi++) {
-                const int g = warp + kWSProd * gi;
-                const int qc = g / kTBatch, bt = g % kTBatch, q = q0 + qc, b = b0 + bt;
-                uint64_t v0 = 0, v1 = 0;
-                if (q < Q && b < B) {
-                    int i = i0, t = t0 + qc;
-                    while (t >= T) {
-                        t -= T;
-                        i++;
-                    }
-                    const uint32_t ib = (uint32_t)(i * B + b);
-                    const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
-                    const uint32_t r = s_shift[t];
-                    if (r == 0) {
-                        if (qlimb) {
-                            v0 = mulmod(Pk, c0[n], m);
-                            v1 = mulmod(Pk, c0[((uint32_t)xls << logn) + n], m);
-                        }
-                    } else {
-                        const uint32_t src = rot_index(n, half, r);
-                        const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
-                        const uint32_t ks = s_kstride[t];
-                        const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + n;
-                        Acc a0, a1;
-                        a0.zero();
-                        a1.zero();
-                        ks_dot<UH_WS_GROUP>(a0, a1, Di, dstride, k0, ks, L);
-                        if (qlimb) a0.mac(Pk, c0[src]);
-                        v0 = csub(reduce128_lazy(a0.hi64(), a0.lo64(), m), 2 * m.q);
-                        v1 = csub(reduce128_lazy(a1.hi64(), a1.lo64(), m), 2 * m.q);
-                    }
-                }
-                sv[buf][qc][bt][0][lane] = v0;
-                sv[buf][qc][bt][1][lane] = v1;
-            }
-            __threadfence_block();
-            bar_arrive(1 + buf, NT);  // buffer full
-            t0 += kTChunk;
-            while (t0 >= T) {
-                t0 -= T;
-                i0++;
-            }
-        }
-        return;
-    }
-    // ---------------- consumers ----------------
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 96;\n" ::);
-    const int cw = warp - kWSProd;                       // 0..15
-    const int o_a = (cw / (kTBatch / kWSPB)) * kWSPO;    // 0, 3, 6, 9
-    const int b_a = (cw % (kTBatch / kWSPB)) * kWSPB;    // 0, 2, 4, 6
-    const uint32_t mask_row = ((uint32_t)k << logn) + n;
-    Acc acc[kWSPO * kWSPB][2];
-#pragma unroll
-    for (int j = 0; j < kWSPO * kWSPB; j++) {
-        acc[j][0].zero();
-        acc[j][1].zero();
-    }
-    int since_fold = 0;
-    const uint32_t qstride = (uint32_t)Q * dstride;  // between outputs of the mask bank
-    const uint64_t *mp = masks + (uint32_t)o_a * qstride + mask_row;
-    for (int c = 0; c < nchunks; c++) {
-        const int buf = c & 1, q0 = c * kTChunk;
-        uint64_t mpre[kTChunk][kWSPO];
-#pragma unroll
-        for (int qc = 0; qc < kTChunk; qc++)
-#pragma unroll
-            for (int d = 0; d < kWSPO; d++)
-                mpre[qc][d] = (o_a + d < O && q0 + qc < Q) ? mp[qc * dstride + d * qstride] : 0;
-        mp += kTChunk * dstride;
-        bar_sync(1 + buf, NT);  // wait until the producers filled this buffer
-        const int qn = min(kTChunk, Q - q0);
-#pragma unroll
-        for (int qc = 0; qc < kTChunk; qc++) {
-            if (qc >= qn) break;
-#pragma unroll
-            for (int db = 0; db < kWSPB; db++) {
-                const int bt = b_a + db;
-                const uint64_t v0 = sv[buf][qc][bt][0][lane], v1 = sv[buf][qc][bt][1][lane];
-#pragma unroll
-                for (int d = 0; d < kWSPO; d++) {
-                    const int j = d * kWSPB + db;
-                    acc[j][0].mac(mpre[qc][d], v0);
-                    acc[j][1].mac(mpre[qc][d], v1);
-                }
-            }
-            if (++since_fold == kFold) {
-                since_fold = 0;
-#pragma unroll
-                for (int j = 0; j < kWSPO * kWSPB; j++)
-                    for (int cc = 0; cc < 2; cc++) {
-                        uint64_t rr = reduce128_lazy(acc[j][cc].hi64(), acc[j][cc].lo64(), m);
-                        acc[j][cc].set(rr, 0);
-                    }
-            }
-        }
-        if (c + 2 < nchunks) bar_arrive(3 + buf, NT);  // buffer free for chunk c + 2
-    }
-#pragma unroll
-    for (int j = 0; j < kWSPO * kWSPB; j++) {
-        const int o = o_a + j / kWSPB, b = b0 + b_a + j % kWSPB;
-        if (o < O && b < B) {
-            uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
             dst[0] = acc[j][0].reduce(m);
-            dst[dstride] = acc[j][1].reduce(m);
-        }
+            dst[dstride] = acc[j][1].reduce(m);        }
     }
 }
 
@@ -1059,18 +661,6 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
         }
     };
     using std::integral_constant;
-    // warp-specialised producer/consumer kernel for wide masked dense layers: opt-in
-    // (UH_HOIST_WS=1); measured slower than the 24-warp kernel on LeNet conv2 (B200, N=2^15)
-    static const bool ws_on = [] {
-        const char *e = getenv("UH_HOIST_WS");
-        return e && std::string(e) == "1";
-    }();
-    if (ws_on && masks && !diag && O > 8 && O <= 12) {
-        k_hoisted_ws<<<grid, (kWSProd + kWSCons) * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I,
-                                                                T, O, L, c.sp(), (int)c.logn, c.d_mods);
-        UH_LAUNCH_CHECK();
-        return;
-    }
     // narrow layers (O <= 2): direct register-only kernel (UH_HOIST_DIRECT=0 disables)
     static const bool direct_on = [] {
         const char *e = getenv("UH_HOIST_DIRECT");
@@ -1115,57 +705,6 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
         }
         UH_LAUNCH_CHECK();
         return;
-    }
-    // FP64-pipe phase B (k_hoisted_fp) for wide masked dense layers.  The limbs with q < 2^41 run
-    // there in groups of <= 6 outputs (2 pairs per warp: the split accumulators fit the register
-    // budget; each group repeats phase A on the integer pipe, while phase B moves to the FP64
-    // pipe); q_0 and P (60-bit) run through the integer kernel.  Opt-in (UH_HOIST_FP=1): measured
-    // slower on LeNet-1 at B=64 (conv2 96.8 vs 79.5 ms, conv1 24.1 vs 23.9 ms) -- these kernels are
-    // latency-bound in phase A, not bound by the IMAD pipe that the FP64 phase B relieves.
-    static const bool fp_on = [] {
-        const char *e = getenv("UH_HOIST_FP");
-        return e && std::string(e) == "1";
-    }();
-    const int Qt = diag ? I : I * T;
-    if (fp_on && masks && !diag && O >= 3 && O <= 12 && Qt <= kFpMaxTerms && L >= 2) {
-        bool mid_fp = true;  // limbs 1 .. L-1 (q_1 .. q_{L-1})
-        for (int kk = 1; kk < L; kk++) mid_fp = mid_fp && (c.h_q[kk] >> 41) == 0;
-        if (mid_fp) {
-            const size_t smem = (size_t)2 * kTChunk * kTBatch * 2 * 2 * 32 * sizeof(double);
-            const size_t ostride = (size_t)B * 2 * (L + 1) * c.n, mstride = (size_t)Qt * (L + 1) * c.n;
-            for (int o0 = 0; o0 < O; o0 += 6) {
-                const int og = std::min(6, O - o0);
-                dim3 g(grid.x, grid.y, L - 1);
-                auto fp = [&](auto ppw_tag) {
-                    constexpr int PP = decltype(ppw_tag)::value;
-                    static bool attr = false;
-                    if (!attr) {
-                        UH_CHECK(cudaFuncSetAttribute(k_hoisted_fp<PP, 24>,
-                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                        attr = true;
-                    }
-                    k_hoisted_fp<PP, 24><<<g, 24 * 32, smem, s>>>(acc + o0 * ostride, X, xls, D, masks + o0 * mstride,
-                                                                  keys, key_limbs, shifts, B, I, T, og, L, c.sp(),
-                                                                  (int)c.logn, c.d_mods, 1, 1);
-                };
-                if (og * kTBatch > 24) fp(integral_constant<int, 2>());
-                else fp(integral_constant<int, 1>());
-                UH_LAUNCH_CHECK();
-            }
-            dim3 g2(grid.x, grid.y, 2);  // q_0 and P
-            const int ppw = pairs > 48 ? 4 : (pairs > 24 ? 2 : 1);
-            if (ppw == 4)
-                k_hoisted_mac<4, 24><<<g2, 24 * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O,
-                                                           diag, L, c.sp(), (int)c.logn, c.d_mods, 0, L);
-            else if (ppw == 2)
-                k_hoisted_mac<2, 24><<<g2, 24 * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O,
-                                                           diag, L, c.sp(), (int)c.logn, c.d_mods, 0, L);
-            else
-                k_hoisted_mac<1, 24><<<g2, 24 * 32, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O,
-                                                           diag, L, c.sp(), (int)c.logn, c.d_mods, 0, L);
-            UH_LAUNCH_CHECK();
-            return;
-        }
     }
     if (O <= 12) {
         // measured (B200, N=2^15): 24 warps win when phase B is heavy (O >= 3), 8-warp CTAs when it is not
