@@ -154,6 +154,18 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
         c->d_bsel = upload(bsel);
         c->d_csl = upload(csl);
     }
+    // (q_t * P)^-1 mod q_k: the fused ModDown + rescale epilogue (one Shoup product)
+    std::vector<uint64_t> inv2((size_t)count * count, 0), inv2s((size_t)count * count, 0);
+    for (uint32_t k = 0; k + 1 < count; k++)
+        for (uint32_t t = 0; t + 1 < count; t++) {
+            if (t == k) continue;
+            const uint64_t qk = moduli[k];
+            const uint64_t v = h_mulmod(h_inv(moduli[t] % qk, qk), h_inv(moduli[count - 1] % qk, qk), qk);
+            inv2[(size_t)k * count + t] = v;
+            inv2s[(size_t)k * count + t] = h_shoup(v, qk);
+        }
+    c->d_inv2 = upload(inv2);
+    c->d_inv2s = upload(inv2s);
     std::vector<ulonglong2> pmod(count);
     for (uint32_t i = 0; i < count; i++) {
         uint64_t pm = moduli[count - 1] % moduli[i];
@@ -167,6 +179,9 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
     c->d_twd = upload(twd);
     c->d_itwd = upload(itwd);
     c->d_mods = upload(mods);
+    c->h_mods = mods;
+    c->h_inv = inv;
+    c->h_invs = invs;
     c->d_psi = upload(tw);
     c->d_psis = upload(tws);
     c->d_ipsi = upload(itw);
@@ -184,7 +199,7 @@ void ctx_destroy(Ctx *c) {
     cudaSetDevice(c->device);
     for (void *p : {(void *)c->d_pmod, (void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_twf, (void *)c->d_itwf, (void *)c->d_twd, (void *)c->d_itwd, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
                     (void *)c->d_ipsi, (void *)c->d_ipsis,
-                    (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_pos, (void *)c->d_neg})
+                    (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_inv2, (void *)c->d_inv2s, (void *)c->d_pos, (void *)c->d_neg})
         if (p) cudaFree(p);
     delete c;
 }

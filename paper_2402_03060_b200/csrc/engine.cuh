@@ -15,6 +15,8 @@ struct Ctx {
     uint32_t n = 0, logn = 0, count = 0;  // count = depth + 2 moduli (q_0..q_depth, P)
     uint32_t n1 = 0, n2 = 0;              // two-pass NTT split, n = n1 * n2 (n1 = 0: one pass)
     std::vector<uint64_t> h_q;
+    std::vector<Mod> h_mods;                     // host copies of d_mods / d_inv / d_invs
+    std::vector<uint64_t> h_inv, h_invs;
     Mod *d_mods = nullptr;               // [count]
     uint64_t *d_psi = nullptr, *d_psis = nullptr;    // [count][n] psi^brv(i), Shoup companions
     uint64_t *d_ipsi = nullptr, *d_ipsis = nullptr;  // [count][n] psi^-brv(i)
@@ -25,6 +27,7 @@ struct Ctx {
     int32_t *d_bsel = nullptr;           // [n1] pass-2 block of CTA x, position g (ntt_fast.cu)
     int32_t *d_csl = nullptr;            // [n] element index inside its pass-2 block, per slot
     uint64_t *d_inv = nullptr, *d_invs = nullptr;  // [count][count]: q_j^-1 mod q_i at [i*count+j]
+    uint64_t *d_inv2 = nullptr, *d_inv2s = nullptr;  // [count][count]: (q_j * P)^-1 mod q_i at [i*count+j]
     ulonglong2 *d_pmod = nullptr;        // [count] (P mod q_i, Shoup companion)
     int32_t *d_pos = nullptr;            // [n/2] index (5^j mod 2N - 1)/2 : slot j -> odd exponent slot
     int32_t *d_neg = nullptr;            // [n/2] index (2N - 5^j - 1)/2

@@ -69,13 +69,10 @@ __device__ __forceinline__ LimbInfo limb_info(const NttJob &J, int f, int logn, 
         li.qsrc = 1;
         li.dst = J.dst + (((size_t)p * J.dst_ps + k) << logn);
         li.in = J.in + (((size_t)p * J.in_ps + k) << logn);
-        li.w = J.inv[(size_t)k * cnt + t];
-        li.ws = J.invs[(size_t)k * cnt + t];
-        li.w2 = J.inv[(size_t)k * cnt + sp];
-        li.ws2 = J.invs[(size_t)k * cnt + sp];
+        li.w = J.inv2[(size_t)k * cnt + t];  // (q_t P)^-1 mod q_k
+        li.ws = J.inv2s[(size_t)k * cnt + t];
         li.mt = mods[t];
         li.P = mods[sp].q;
-        li.pinv = make_ulonglong2(J.inv[(size_t)t * cnt + sp], J.invs[(size_t)t * cnt + sp]);
         li.pk = J.pmod[k];
         const uint64_t qtk = li.mt.q < m.q ? li.mt.q : csub(barrett_lite(li.mt.q, m), m.q);
         li.qpk = mulmod(qtk, li.pk.x, m);
@@ -107,13 +104,11 @@ __device__ __forceinline__ LimbInfo limb_info(const NttJob &J, int f, int logn, 
     return li;
 }
 
-// centred CRT lift of (a = x mod q_t, b = x mod P) in (-q_t P / 2, q_t P / 2), reduced into q_k
+// centred CRT lift reduced into q_k: a = y | neg << 63 (x = b + P y, y in [0, q_t), prepared
+// once per coefficient by ops.cu k_crt2_pre), b = x mod P
 __device__ __forceinline__ uint64_t crt2_to(uint64_t a, uint64_t b, const LimbInfo &li, const Mod &m) {
-    const uint64_t qt = li.mt.q;
-    const uint64_t bt = b < qt ? b : csub(barrett_lite(b, li.mt), qt);
-    const uint64_t y = shoup(submod(a, bt, qt), li.pinv.x, li.pinv.y, qt);  // x = b + P * y, y in [0, q_t)
-    const uint64_t h = (qt - 1) >> 1;
-    const bool neg = y > h || (y == h && b > (li.P - 1) / 2);
+    const bool neg = a >> 63;
+    const uint64_t y = a & 0x7FFFFFFFFFFFFFFFull;
     const uint64_t yk = y < m.q ? y : csub(barrett_lite(y, m), m.q);
     const uint64_t bk = b < m.q ? b : csub(barrett_lite(b, m), m.q);
     const uint64_t t = addmod(bk, shoup(yk, li.pk.x, li.pk.y, m.q), m.q);
@@ -591,7 +586,7 @@ __device__ __forceinline__ void fwd_p2_epilogue(const uint64_t *sm, const LimbIn
             if (EM == 1)
                 li.dst[s] = csub(shoup_lazy(submod(a[e], y, q), li.w, li.ws, q), q);
             else if (EM == 2)
-                li.dst[s] = shoup(shoup(submod(a[e], y, q), li.w, li.ws, q), li.w2, li.ws2, q);
+                li.dst[s] = shoup(submod(a[e], y, q), li.w, li.ws, q);
             else
                 li.dst[s] = y;
         }

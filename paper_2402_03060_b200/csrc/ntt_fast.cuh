@@ -14,10 +14,11 @@ enum NttMode : int { NTT_PLAIN = 0, NTT_MODUP = 1, NTT_DIVIDE = 2, NTT_DIVIDE2 =
 //          dst row dst + ((p * L + j) * (L + 1) + k) * N.
 //  DIVIDE: p = f / nl, k = f % nl, modulus k; forward input centred(src[p], q_top);
 //          epilogue dst[p][k] = (in[p][k] - y) * q_top^-1 (rows at p * dst_ps / p * in_ps).
-//  DIVIDE2 (fused ModDown + rescale, division by q_top * P): src rows [p][2] hold the
-//          coefficients of x mod q_top and x mod P; forward input = the centred CRT lift
-//          of (x mod q_top, x mod P) reduced into q_k; epilogue
-//          dst[p][k] = (in[p][k] - y) * q_top^-1 * P^-1.
+//  DIVIDE2 (fused ModDown + rescale, division by q_top * P): src rows [p][2] hold, per
+//          coefficient, y | neg << 63 and x mod P, where x = (x mod P) + P y is the CRT
+//          lift of (x mod q_top, x mod P) and neg marks its centred representative as
+//          negative (prepared by ops.cu k_crt2_pre); forward input = that centred value
+//          reduced into q_k; epilogue dst[p][k] = (in[p][k] - y) * (q_top P)^-1.
 struct NttJob {
     int mode = NTT_PLAIN;
     int f0 = 0;  // first limb of this launch (chunked launches)
@@ -31,6 +32,7 @@ struct NttJob {
     int in_ps = 1;
     int top_mod = 0, count = 0;
     const uint64_t *inv = nullptr, *invs = nullptr;
+    const uint64_t *inv2 = nullptr, *inv2s = nullptr;  // DIVIDE2: (q_top * P)^-1 mod q_k (Shoup pairs)
     const ulonglong2 *pmod = nullptr;  // DIVIDE2: (P mod q_i, Shoup companion) per modulus
 };
 

@@ -343,6 +343,27 @@ void divide_top(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, in
     UH_LAUNCH_CHECK();
 }
 
+namespace {
+// Per coefficient of the (x mod q_t, x mod P) rows: y = (a - b) P^-1 mod q_t, so x = b + P y,
+// and whether the centred representative of x (in (-q_t P / 2, q_t P / 2]) is negative;
+// stored in place of a as y | neg << 63.  Done once here instead of once per target limb
+// in the DIVIDE2 forward NTT.
+__global__ void k_crt2_pre(uint64_t *top, int n_polys, int logn, Mod mt, uint64_t P, ulonglong2 pinv) {
+    const size_t total = (size_t)n_polys << logn, nmask = ((size_t)1 << logn) - 1;
+    const uint64_t qt = mt.q, h = (qt - 1) >> 1, ph = (P - 1) / 2;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t p = idx >> logn, n = idx & nmask;
+        uint64_t *a = top + ((2 * p) << logn) + n;
+        const uint64_t b = a[(size_t)1 << logn];
+        const uint64_t bt = b < qt ? b : csub(barrett_lite(b, mt), qt);
+        const uint64_t y = shoup(submod(*a, bt, qt), pinv.x, pinv.y, qt);
+        const bool neg = y > h || (y == h && b > ph);
+        *a = y | ((uint64_t)neg << 63);
+    }
+}
+}  // namespace
+
 void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, int level, int out_ps, int in_ps,
                  cudaStream_t s) {
     if (!n_polys) return;
@@ -365,6 +386,14 @@ void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, i
     Ji.dst_ps = 2;
     ntt_fast_inverse(c, Ji, n_polys * 2, s);
     if (level == 0) return;
+    {
+        const int cnt = (int)c.count, sp = c.sp();
+        const Mod mt = c.h_mods[level];
+        const ulonglong2 pinv = make_ulonglong2(c.h_inv[(size_t)level * cnt + sp], c.h_invs[(size_t)level * cnt + sp]);
+        k_crt2_pre<<<grid_for((size_t)n_polys * N), kTB, 0, s>>>(top.as<uint64_t>(), n_polys, (int)c.logn, mt,
+                                                                 c.h_q[sp], pinv);
+        UH_LAUNCH_CHECK();
+    }
     NttJob Jf;
     Jf.mode = NTT_DIVIDE2;
     Jf.nl = level;
@@ -379,6 +408,8 @@ void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, i
     Jf.count = (int)c.count;
     Jf.inv = c.d_inv;
     Jf.invs = c.d_invs;
+    Jf.inv2 = c.d_inv2;
+    Jf.inv2s = c.d_inv2s;
     Jf.pmod = c.d_pmod;
     ntt_fast_forward(c, Jf, n_polys * level, s);
 }
