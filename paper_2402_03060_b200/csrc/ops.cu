@@ -69,6 +69,15 @@ __global__ void k_modup_diag(uint64_t *D, const uint64_t *in, int n_polys, int L
     }
 }
 
+// diagonal of the ModUp output: D[p][j][j] = in[p][j]; 16-byte vector copies, grid (N / 512, L, polys)
+__global__ void __launch_bounds__(256) k_modup_diag2(uint64_t *__restrict__ D, const uint64_t *__restrict__ in, int L,
+                                                     int in_ps, int logn) {
+    const size_t p = blockIdx.z, j = blockIdx.y;
+    const size_t n = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(in + ((p * in_ps + j) << logn) + n);
+    *reinterpret_cast<ulonglong2 *>(D + (((p * L + j) * (L + 1) + j) << logn) + n) = v;
+}
+
 __global__ void k_gather_limb(uint64_t *dst, const uint64_t *src, int n_polys, int limb, int src_ps, int logn) {
     size_t total = (size_t)n_polys << logn;
     size_t nmask = ((size_t)1 << logn) - 1;
@@ -435,7 +444,11 @@ void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level
         Jf.src = C.as<uint64_t>();
         Jf.dst = D;
         ntt_fast_forward(c, Jf, n_polys * L * L, s);
-        k_modup_diag<<<grid_for((size_t)n_polys * L * N), kTB, 0, s>>>(D, in, n_polys, L, in_ps, (int)c.logn);
+        if (N >= 512 && n_polys <= 65535) {
+            k_modup_diag2<<<dim3((unsigned)(N / 512), L, n_polys), 256, 0, s>>>(D, in, L, in_ps, (int)c.logn);
+        } else {
+            k_modup_diag<<<grid_for((size_t)n_polys * L * N), kTB, 0, s>>>(D, in, n_polys, L, in_ps, (int)c.logn);
+        }
         UH_LAUNCH_CHECK();
         return;
     }
