@@ -269,6 +269,26 @@ __global__ void k_tensor(uint64_t *T, uint64_t *D2, const uint64_t *a, const uin
     }
 }
 
+// k_tensor on a 3-D grid (N / 256, L, B): one thread per coefficient, limb-uniform modulus, no division
+__global__ void __launch_bounds__(256) k_tensor2(uint64_t *__restrict__ T, uint64_t *__restrict__ D2,
+                                                 const uint64_t *__restrict__ a, const uint64_t *__restrict__ b, int L,
+                                                 int a_ls, int b_ls, int logn, const Mod *__restrict__ mods) {
+    const size_t n = (size_t)blockIdx.x * blockDim.x + threadIdx.x, bb = blockIdx.z;
+    const int k = blockIdx.y;
+    const Mod m = mods[k];
+    const uint64_t a0 = __ldg(a + (((bb * 2) * a_ls + k) << logn) + n);
+    const uint64_t a1 = __ldg(a + (((bb * 2 + 1) * a_ls + k) << logn) + n);
+    const uint64_t b0 = __ldg(b + (((bb * 2) * b_ls + k) << logn) + n);
+    const uint64_t b1 = __ldg(b + (((bb * 2 + 1) * b_ls + k) << logn) + n);
+    Acc d1;
+    d1.zero();
+    d1.mac(a0, b1);
+    d1.mac(a1, b0);
+    T[(((bb * 2) * L + k) << logn) + n] = mulmod(a0, b0, m);
+    T[(((bb * 2 + 1) * L + k) << logn) + n] = d1.reduce(m);
+    D2[((bb * L + k) << logn) + n] = mulmod(a1, b1, m);
+}
+
 // u[p][k] += (P mod q_k) * t[p][k] for the q-limbs k < L of QP-basis polys (u has L + 1 limbs, t has L)
 __global__ void k_add_pscaled(uint64_t *u, const uint64_t *t, int n_polys, int L, int sp, int logn,
                               const Mod *__restrict__ mods, const ulonglong2 *__restrict__ pmod) {
@@ -528,8 +548,12 @@ void ct_mul_relin_rescale(const Ctx &c, uint64_t *out, const uint64_t *a, const 
     int L = level + 1;
     size_t N = c.n;
     Scratch T((size_t)B * 2 * L * N * 8, s), D2((size_t)B * L * N * 8, s), KS((size_t)B * 2 * L * N * 8, s);
-    k_tensor<<<grid_for((size_t)B * L * N), kTB, 0, s>>>(T.as<uint64_t>(), D2.as<uint64_t>(), a, b, B, L, a_ls, b_ls,
-                                                         (int)c.logn, c.d_mods);
+    if (N >= 256 && B <= 65535)
+        k_tensor2<<<dim3((unsigned)(N / 256), L, B), 256, 0, s>>>(T.as<uint64_t>(), D2.as<uint64_t>(), a, b, L, a_ls,
+                                                                  b_ls, (int)c.logn, c.d_mods);
+    else
+        k_tensor<<<grid_for((size_t)B * L * N), kTB, 0, s>>>(T.as<uint64_t>(), D2.as<uint64_t>(), a, b, B, L, a_ls,
+                                                             b_ls, (int)c.logn, c.d_mods);
     UH_LAUNCH_CHECK();
     keyswitch(c, KS.as<uint64_t>(), D2.as<uint64_t>(), B, level, L, rk, rk_limbs, 0, s);
     elementwise(c, OP_ADD, T.as<uint64_t>(), T.as<uint64_t>(), KS.as<uint64_t>(), 2 * B, 2 * B, L, L, L, L, L, s);
@@ -542,8 +566,12 @@ void ct_mul_relin_rescale_fused(const Ctx &c, uint64_t *out, const uint64_t *a, 
     int L = level + 1;
     size_t N = c.n;
     Scratch T((size_t)B * 2 * L * N * 8, s), D2((size_t)B * L * N * 8, s);
-    k_tensor<<<grid_for((size_t)B * L * N), kTB, 0, s>>>(T.as<uint64_t>(), D2.as<uint64_t>(), a, b, B, L, a_ls, b_ls,
-                                                         (int)c.logn, c.d_mods);
+    if (N >= 256 && B <= 65535)
+        k_tensor2<<<dim3((unsigned)(N / 256), L, B), 256, 0, s>>>(T.as<uint64_t>(), D2.as<uint64_t>(), a, b, L, a_ls,
+                                                                  b_ls, (int)c.logn, c.d_mods);
+    else
+        k_tensor<<<grid_for((size_t)B * L * N), kTB, 0, s>>>(T.as<uint64_t>(), D2.as<uint64_t>(), a, b, B, L, a_ls,
+                                                             b_ls, (int)c.logn, c.d_mods);
     UH_LAUNCH_CHECK();
     Scratch D((size_t)B * L * (L + 1) * N * 8, s), u((size_t)B * 2 * (L + 1) * N * 8, s);
     modup(c, D.as<uint64_t>(), D2.as<uint64_t>(), B, level, L, s);
