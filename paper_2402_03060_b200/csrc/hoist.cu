@@ -489,6 +489,9 @@ __global__ void __launch_bounds__(W * 32, 1)
 // coefficients, so key and mask rows are shared through L1; the coefficient
 // tile is the fastest grid dimension (rotated digit reads of neighbouring
 // tiles hit L2).
+#ifndef UH_DIRECT_CT_FAST
+#define UH_DIRECT_CT_FAST 1  // ciphertext groups fastest in the grid (measured: conv1 16.0 vs 16.8 ms)
+#endif
 #ifndef UH_DIRECT_MINB
 #define UH_DIRECT_MINB 4
 #endif
@@ -509,8 +512,13 @@ __global__ void __launch_bounds__(256, OM > 2 ? 3 : UH_DIRECT_MINB)
     __shared__ uint32_t s_shift[kMaxTerms];
     __shared__ uint32_t s_kstride[kMaxTerms];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#if UH_DIRECT_CT_FAST
+    const int b = blockIdx.x * 8 + warp;  // ciphertext groups fastest: CTAs sharing key rows run together
+    const uint32_t n = blockIdx.y * 32 + lane;
+#else
     const int b = blockIdx.y * 8 + warp;
     const uint32_t n = blockIdx.x * 32 + lane;
+#endif
     const int k = blockIdx.z;
     const uint32_t N = 1u << logn, half = N >> 1;
     const int NT = diag == 2 ? I * T : T;  // per-term metadata entries
@@ -673,15 +681,18 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
         return !(e && std::string(e) == "0");
     }();
     if (direct4 && masks && O > 2 && O <= 4) {
-        dim3 gd((unsigned)(c.n / 32), (B + 7) / 8, L + 1);
+        dim3 gd = UH_DIRECT_CT_FAST ? dim3((B + 7) / 8, (unsigned)(c.n / 32), L + 1)
+                                    : dim3((unsigned)(c.n / 32), (B + 7) / 8, L + 1);
         k_hoisted_direct<4, true><<<gd, 256, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, diag,
                                                       L, c.sp(), (int)c.logn, c.d_mods);
         UH_LAUNCH_CHECK();
         return;
     }
     if ((direct_on || diag == 2) && O <= 2) {
-        dim3 gd((unsigned)(c.n / 32), (B + 7) / 8, L + 1);
-        if (gd.y > 65535) throw std::invalid_argument("hoisted kernel: batch too large for one launch");
+        dim3 gd = UH_DIRECT_CT_FAST ? dim3((B + 7) / 8, (unsigned)(c.n / 32), L + 1)
+                                    : dim3((unsigned)(c.n / 32), (B + 7) / 8, L + 1);
+        if ((B + 7) / 8 > 65535 && !UH_DIRECT_CT_FAST)
+            throw std::invalid_argument("hoisted kernel: batch too large for one launch");
         if (masks) {
             if (O == 1)
                 k_hoisted_direct<1, true><<<gd, 256, 0, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T,
