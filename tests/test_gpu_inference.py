@@ -61,3 +61,40 @@ def test_batched_equals_solo_within_tolerance():
         for s, y in zip(group, outs[b]):
             assert np.max(np.abs(y - planner.reference_infer(m, s))) < 1e-5
     assert [r.level_after for r in metrics.per_layer] == M2_TRACE
+
+
+def test_pinned_tensor_client_path_matches_numpy_path():
+    """driver.infer_batch with pinned float64 planes (GpuBackend.encrypt_slots, async H2D) gives the
+    same logits as the numpy path (ciphertext ids continue, so the noise differs: compare to 1e-5)."""
+    import torch
+
+    params = HEParams(poly_degree=1 << 12, depth=7, scale_bits=40)
+    m = planner.lenet1(seed=3)
+    plan = planner.footprint(m, params)
+    groups = [_samples(m, plan.capacity, seed=20 + b) for b in range(2)]
+    planes = driver.pack_groups(m, groups, plan)
+    be = GpuBackend(params)
+    a, _ = driver.infer_batch(m, planes, params, plan, be, fused=True)
+    b, _ = driver.infer_batch(m, torch.from_numpy(np.ascontiguousarray(planes)).pin_memory(), params, plan, be,
+                              fused=True)
+    for ga, gb, group in zip(a, b, groups):
+        for ya, yb, s in zip(ga, gb, group):
+            ref = planner.reference_infer(m, s)
+            assert np.max(np.abs(ya - ref)) < 1e-5 and np.max(np.abs(yb - ref)) < 1e-5
+
+
+def test_encrypt_slots_rules():
+    import torch
+
+    from paper_2402_03060_b200.errors import OversizedInput
+
+    params = HEParams(poly_degree=64, depth=2, scale_bits=40)
+    be = GpuBackend(params)
+    x = torch.linspace(-1, 1, 10, dtype=torch.float64).view(1, 10)
+    c = be.encrypt_slots(x)
+    d = be.decrypt(c)
+    assert np.max(np.abs(d[:10] - x.numpy()[0])) < 1e-6 and np.max(np.abs(d[10:])) < 1e-6
+    with pytest.raises(OversizedInput):
+        be.encrypt_slots(torch.zeros((1, params.num_slots + 1), dtype=torch.float64))
+    with pytest.raises(OversizedInput):
+        be.encrypt_slots(torch.zeros(5, dtype=torch.float64))
