@@ -276,7 +276,7 @@ def main():
         d[2] += 1
     conv_ms = sum(v[0] for v in by_level.values())
     top = max(by_level.items(), key=lambda kv: kv[1][0]) if by_level else None
-    rates = np.zeros(8, dtype=np.float64)
+    rates = np.zeros(16, dtype=np.float64)
     import ctypes
 
     _lib.call("uh_bench_peaks", be._ctx, ctypes.c_void_p(rates.ctypes.data))

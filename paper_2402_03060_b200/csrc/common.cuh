@@ -101,6 +101,57 @@ __device__ __forceinline__ void mac128x4(uint32_t &a0, uint32_t &a1, uint32_t &a
         : "l"(x), "l"(y));
 }
 
+// Narrow-operand accumulator for limbs with q < 2^41: both factors below 2^42,
+// so their high 32-bit words x1, y1 are below 2^10.  The 128-bit sum is kept in
+// two 64-bit words, value = a + b * 2^32:
+//   a = sum x0*y0 mod 2^64,
+//   b = sum (x0*y1 + x1*y0) + 2^32 * sum (x1*y1 + carry out of a)
+//     (< 2^43 + 2^52 + 2^32 per term: exact for up to 2^11 terms between folds).
+// One multiply-accumulate is three IMAD.WIDE.U32 (one with carry-out) and one
+// IMAD.X into b's high word -- against four IMAD.WIDE.U32 plus a carry chain for
+// full 64-bit operands -- in the same four registers.
+struct AccN {
+    uint64_t a, b;
+    __device__ __forceinline__ void zero() { a = b = 0; }
+    __device__ __forceinline__ void mac(uint64_t x, uint64_t y) {
+        asm("{\n\t.reg .u32 x0,x1,y0,y1,a0,a1,b0,b1;\n\t"
+            "mov.b64 {x0,x1}, %2;\n\tmov.b64 {y0,y1}, %3;\n\tmov.b64 {a0,a1}, %0;\n\tmov.b64 {b0,b1}, %1;\n\t"
+            "mad.lo.cc.u32 a0, x0, y0, a0;\n\tmadc.hi.cc.u32 a1, x0, y0, a1;\n\tmadc.lo.u32 b1, x1, y1, b1;\n\t"
+            "mov.b64 %0, {a0,a1};\n\tmov.b64 %1, {b0,b1};\n\t"
+            "mad.wide.u32 %1, x0, y1, %1;\n\tmad.wide.u32 %1, x1, y0, %1;\n\t}"
+            : "+l"(a), "+l"(b)
+            : "l"(x), "l"(y));
+    }
+    __device__ __forceinline__ void add(uint64_t x) {  // any 64-bit addend
+        asm("{\n\t.reg .u32 x0,x1,a0,a1,b0,b1;\n\t"
+            "mov.b64 {x0,x1}, %2;\n\tmov.b64 {a0,a1}, %0;\n\tmov.b64 {b0,b1}, %1;\n\t"
+            "add.cc.u32 a0, a0, x0;\n\taddc.cc.u32 a1, a1, x1;\n\taddc.u32 b1, b1, 0;\n\t"
+            "mov.b64 %0, {a0,a1};\n\tmov.b64 %1, {b0,b1};\n\t}"
+            : "+l"(a), "+l"(b)
+            : "l"(x));
+    }
+    // the 128-bit value as (hi, lo)
+    __device__ __forceinline__ void value(uint64_t &hi, uint64_t &lo) const {
+        lo = a + (b << 32);
+        hi = (b >> 32) + (lo < a);
+    }
+    __device__ __forceinline__ uint64_t lo64() const { return a + (b << 32); }
+    __device__ __forceinline__ uint64_t hi64() const {
+        uint64_t h, l;
+        value(h, l);
+        return h;
+    }
+    __device__ __forceinline__ void set(uint64_t l, uint64_t h) {  // callers only set values below 2^96
+        a = l;
+        b = h << 32;
+    }
+    __device__ __forceinline__ uint64_t reduce(const Mod &m) const {
+        uint64_t h, l;
+        value(h, l);
+        return reduce128(h, l, m);
+    }
+};
+
 // Split accumulator: A = sum x0*y0 + (x1*y1 << 64) (a0..a3) and C = sum of the
 // cross products x0*y1 + x1*y0 (c0:c1, carries counted in c2); value = A + (C << 32).
 // Every IMAD.WIDE accumulates into an aligned register pair in place (no moves).
@@ -176,6 +227,7 @@ struct Acc {
             : "l"(a));
     }
     __device__ __forceinline__ uint64_t reduce(const Mod &m) const { return reduce128(hi, lo, m); }
+    __device__ __forceinline__ void value(uint64_t &h, uint64_t &l) const { h = hi; l = lo; }
 };
 #else
 // four 32-bit words (previous form, UH_ACC32)

@@ -19,6 +19,8 @@
 // CTA: W warps; lane <-> coefficient n (coalesced 256-byte rows of every
 // operand); grid = (B/TB tiles fastest, N/32 coefficient tiles, L+1 limbs),
 // so CTAs sharing the same masks/keys run back to back and hit L2.
+#include <type_traits>
+
 #include "ops.cuh"
 
 namespace uh {
@@ -42,15 +44,33 @@ __device__ __forceinline__ uint64_t reduce128_lazy(uint64_t hi, uint64_t lo, con
 // A phase-A key sum for a limb with q < 2^41 is below 25 * 2^82 < 2^87, so its high word
 // is below 2^23 and (hi * (2^64 mod q) + lo) folds it to a 64-bit value congruent mod q
 // with one 32x64 product -- no full reduction (the phase-B accumulators absorb values < 2^64).
-__device__ __forceinline__ uint64_t fold64_small(const Acc &a, const Mod &m) {
-    const uint64_t lo = a.lo64(), p = (uint64_t)a.hi32lo() * m.r64;
+__device__ __forceinline__ uint64_t fold64_small(uint64_t hi, uint64_t lo, const Mod &m) {
+    const uint64_t p = (uint64_t)(uint32_t)hi * m.r64;
     const uint64_t v = lo + p;
     return v < p ? v + m.r64 : v;  // a wrap past 2^64 is worth 2^64 mod q
 }
-// phase-A term value: lazily reduced into [0, 2q) (60-bit limbs) or folded below 2^64 (q < 2^41)
-__device__ __forceinline__ uint64_t term_value(const Acc &a, const Mod &m, bool smallq) {
-    return smallq ? fold64_small(a, m) : csub(reduce128_lazy(a.hi64(), a.lo64(), m), 2 * m.q);
+// phase-A term value: lazily reduced into [0, 2q) (60-bit limbs) or folded below 2^64 (q < 2^41);
+// with the narrow-operand accumulator (AccN) the value must itself stay a narrow operand: [0, 2q)
+template <class A>
+__device__ __forceinline__ uint64_t term_value(const A &a, const Mod &m, bool smallq) {
+    uint64_t h, l;
+    a.value(h, l);
+    if constexpr (std::is_same<A, AccN>::value) return barrett_lite(fold64_small(h, l, m), m);
+    return smallq ? fold64_small(h, l, m) : csub(reduce128_lazy(h, l, m), 2 * m.q);
 }
+// fold a lazily accumulated 128-bit sum back to one word in [0, 4q)
+template <class A>
+__device__ __forceinline__ void acc_fold(A &a, const Mod &m) {
+    uint64_t h, l;
+    a.value(h, l);
+    a.set(reduce128_lazy(h, l, m), 0);
+}
+// The accumulator type is chosen per limb (uniform per CTA): limbs with q < 2^41 take the
+// narrow-operand form (AccN, 3 IMAD.WIDE + 1 IMAD per multiply-add), the 60-bit limbs
+// (q_0, P) the full 128-bit one.
+#ifndef UH_NARROW_MAC
+#define UH_NARROW_MAC 1
+#endif
 
 constexpr int kMaxL = 12;  // phase-A digit loop fully unrolled (predicated) up to this many limbs
 
@@ -69,8 +89,8 @@ constexpr int kMaxL = 12;  // phase-A digit loop fully unrolled (predicated) up 
 #ifndef UH_WS_GROUP
 #define UH_WS_GROUP 4
 #endif
-template <int G>
-__device__ __forceinline__ void ks_dot(Acc &a0, Acc &a1, const uint64_t *Di, uint32_t dstride,
+template <int G, class A>
+__device__ __forceinline__ void ks_dot(A &a0, A &a1, const uint64_t *Di, uint32_t dstride,
                                        const uint64_t *k0, uint32_t ks, int L) {
 #pragma unroll
     for (int j0 = 0; j0 < kMaxL; j0 += G) {
@@ -132,134 +152,140 @@ __global__ void __launch_bounds__(W * 32, W == 8 && PPW <= 2 ? 4 : (TB < 8 && W 
     }
     __syncthreads();
 
-    Acc acc[PPW][2];
+    auto body = [&](auto acc_tag) {
+        using A = decltype(acc_tag);
+        A acc[PPW][2];
 #pragma unroll
-    for (int j = 0; j < PPW; j++) {
-        acc[j][0].zero();
-        acc[j][1].zero();
-    }
-    // phase-A load group: bounded by the registers left next to the PPW accumulators
-    constexpr int kKsGroup = UH_KS_GROUP_FOR(PPW, W);
-    int since_fold = 0;
-    int buf = 0;
-    constexpr int ITEMS = kTChunk * TB / W;  // phase-A items per thread (1, 2 or 3)
-    static_assert(ITEMS * W == kTChunk * TB, "phase-A items must tile the chunk");
-    // a warp's PPW (output, ciphertext) pairs form a PO x PB block: each shared-memory v is
-    // loaded once for PO outputs and each mask once for PB ciphertexts
-    constexpr int PB = (PPW == 4 ? 2 : PPW) < TB ? (PPW == 4 ? 2 : PPW) : TB, PO = PPW / PB, WB = TB / PB;
-    const int o_a = (warp / WB) * PO, b_a = (warp % WB) * PB;
-    const bool warp_active = o_a < O && warp * PPW < npairs;
-    const uint32_t dstride = (uint32_t)LP << logn;  // between digits of one D block
-    const uint32_t mask_row = ((uint32_t)k << logn) + n;
-    int i0 = 0, t0 = 0;  // (input, tap) of term q0, advanced incrementally (no runtime division)
-    for (int q0 = 0; q0 < Q; q0 += kTChunk) {
-        // prefetch this chunk's weight masks (consumed after the barrier, latency hidden by phase A)
-        uint64_t mpre[kTChunk][PO];
-#pragma unroll
-        for (int qc = 0; qc < kTChunk; qc++)
-#pragma unroll
-            for (int d = 0; d < PO; d++)
-                mpre[qc][d] = (masks && warp_active && o_a + d < O && q0 + qc < Q)
-                                  ? masks[(((uint32_t)(o_a + d) * Q + q0 + qc) * dstride) + mask_row]
-                                  : 0;
-        // ---- phase A: rotated, key-switched inputs of this chunk into shared memory ----
-#pragma unroll
-        for (int ii = 0; ii < ITEMS; ii++) {
-            const int it = threadIdx.x + ii * W * 32;
-            const int ln = it & 31, rest = it >> 5;
-            const int bt = rest % TB, qc = rest / TB;
-            const int q = q0 + qc, b = b0 + bt;
-            uint64_t v0 = 0, v1 = 0;
-            if (q < Q && b < B) {
-                int i, t;
-                if (diag) {
-                    i = t = q;
-                } else {
-                    i = i0;
-                    t = t0 + qc;
-                    while (t >= T) {
-                        t -= T;
-                        i++;
-                    }
-                }
-                const uint32_t nn = blockIdx.y * 32 + ln;
-                const uint32_t ib = (uint32_t)(i * B + b);
-                const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
-                const uint32_t r = s_shift[t];
-                if (r == 0) {
-                    if (qlimb) {
-                        v0 = mulmod(Pk, c0[nn], m);
-                        v1 = mulmod(Pk, c0[((uint32_t)xls << logn) + nn], m);
-                    }
-                } else {
-                    const uint32_t src = rot_index(nn, half, r);
-                    const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
-                    const uint32_t ks = s_kstride[t];
-                    const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + nn;
-                    Acc a0, a1;
-                    a0.zero();
-                    a1.zero();
-                    ks_dot<kKsGroup>(a0, a1, Di, dstride, k0, ks, L);
-                    if (qlimb) a0.mac(Pk, c0[src]);
-                    v0 = term_value(a0, m, smallq);
-                    v1 = term_value(a1, m, smallq);
-                }
-            }
-            sv[buf][qc][bt][0][ln] = v0;
-            sv[buf][qc][bt][1][ln] = v1;
+        for (int j = 0; j < PPW; j++) {
+            acc[j][0].zero();
+            acc[j][1].zero();
         }
-        __syncthreads();
-        // ---- phase B: multiply-accumulate into every (output, ciphertext) pair ----
-        const int qn = min(kTChunk, Q - q0);
+        // phase-A load group: bounded by the registers left next to the PPW accumulators
+        constexpr int kKsGroup = UH_KS_GROUP_FOR(PPW, W);
+        int since_fold = 0;
+        int buf = 0;
+        constexpr int ITEMS = kTChunk * TB / W;  // phase-A items per thread (1, 2 or 3)
+        static_assert(ITEMS * W == kTChunk * TB, "phase-A items must tile the chunk");
+        // a warp's PPW (output, ciphertext) pairs form a PO x PB block: each shared-memory v is
+        // loaded once for PO outputs and each mask once for PB ciphertexts
+        constexpr int PB = (PPW == 4 ? 2 : PPW) < TB ? (PPW == 4 ? 2 : PPW) : TB, PO = PPW / PB, WB = TB / PB;
+        const int o_a = (warp / WB) * PO, b_a = (warp % WB) * PB;
+        const bool warp_active = o_a < O && warp * PPW < npairs;
+        const uint32_t dstride = (uint32_t)LP << logn;  // between digits of one D block
+        const uint32_t mask_row = ((uint32_t)k << logn) + n;
+        int i0 = 0, t0 = 0;  // (input, tap) of term q0, advanced incrementally (no runtime division)
+        for (int q0 = 0; q0 < Q; q0 += kTChunk) {
+            // prefetch this chunk's weight masks (consumed after the barrier, latency hidden by phase A)
+            uint64_t mpre[kTChunk][PO];
 #pragma unroll
-        for (int qc = 0; qc < kTChunk; qc++) {
-            if (qc >= qn) break;
-            if (warp_active) {
+            for (int qc = 0; qc < kTChunk; qc++)
 #pragma unroll
-                for (int db = 0; db < PB; db++) {
-                    const int bt = b_a + db;
-                    const uint64_t v0 = sv[buf][qc][bt][0][lane], v1 = sv[buf][qc][bt][1][lane];
+                for (int d = 0; d < PO; d++)
+                    mpre[qc][d] = (masks && warp_active && o_a + d < O && q0 + qc < Q)
+                                      ? masks[(((uint32_t)(o_a + d) * Q + q0 + qc) * dstride) + mask_row]
+                                      : 0;
+            // ---- phase A: rotated, key-switched inputs of this chunk into shared memory ----
 #pragma unroll
-                    for (int d = 0; d < PO; d++) {
-                        const int j = d * PB + db;
-                        if (masks) {
-                            acc[j][0].mac(mpre[qc][d], v0);
-                            acc[j][1].mac(mpre[qc][d], v1);
-                        } else {
-                            acc[j][0].add(v0);
-                            acc[j][1].add(v1);
+            for (int ii = 0; ii < ITEMS; ii++) {
+                const int it = threadIdx.x + ii * W * 32;
+                const int ln = it & 31, rest = it >> 5;
+                const int bt = rest % TB, qc = rest / TB;
+                const int q = q0 + qc, b = b0 + bt;
+                uint64_t v0 = 0, v1 = 0;
+                if (q < Q && b < B) {
+                    int i, t;
+                    if (diag) {
+                        i = t = q;
+                    } else {
+                        i = i0;
+                        t = t0 + qc;
+                        while (t >= T) {
+                            t -= T;
+                            i++;
+                        }
+                    }
+                    const uint32_t nn = blockIdx.y * 32 + ln;
+                    const uint32_t ib = (uint32_t)(i * B + b);
+                    const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
+                    const uint32_t r = s_shift[t];
+                    if (r == 0) {
+                        if (qlimb) {
+                            v0 = mulmod(Pk, c0[nn], m);
+                            v1 = mulmod(Pk, c0[((uint32_t)xls << logn) + nn], m);
+                        }
+                    } else {
+                        const uint32_t src = rot_index(nn, half, r);
+                        const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
+                        const uint32_t ks = s_kstride[t];
+                        const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + nn;
+                        A a0, a1;
+                        a0.zero();
+                        a1.zero();
+                        ks_dot<kKsGroup>(a0, a1, Di, dstride, k0, ks, L);
+                        if (qlimb) a0.mac(Pk, c0[src]);
+                        v0 = term_value(a0, m, smallq);
+                        v1 = term_value(a1, m, smallq);
+                    }
+                }
+                sv[buf][qc][bt][0][ln] = v0;
+                sv[buf][qc][bt][1][ln] = v1;
+            }
+            __syncthreads();
+            // ---- phase B: multiply-accumulate into every (output, ciphertext) pair ----
+            const int qn = min(kTChunk, Q - q0);
+#pragma unroll
+            for (int qc = 0; qc < kTChunk; qc++) {
+                if (qc >= qn) break;
+                if (warp_active) {
+#pragma unroll
+                    for (int db = 0; db < PB; db++) {
+                        const int bt = b_a + db;
+                        const uint64_t v0 = sv[buf][qc][bt][0][lane], v1 = sv[buf][qc][bt][1][lane];
+#pragma unroll
+                        for (int d = 0; d < PO; d++) {
+                            const int j = d * PB + db;
+                            if (masks) {
+                                acc[j][0].mac(mpre[qc][d], v0);
+                                acc[j][1].mac(mpre[qc][d], v1);
+                            } else {
+                                acc[j][0].add(v0);
+                                acc[j][1].add(v1);
+                            }
                         }
                     }
                 }
-            }
-            if (++since_fold == kFold) {
-                since_fold = 0;
+                if (++since_fold == kFold) {
+                    since_fold = 0;
 #pragma unroll
-                for (int j = 0; j < PPW; j++)
-                    for (int cc = 0; cc < 2; cc++) {
-                        uint64_t rr = reduce128_lazy(acc[j][cc].hi64(), acc[j][cc].lo64(), m);
-                        acc[j][cc].set(rr, 0);
-                    }
+                    for (int j = 0; j < PPW; j++)
+                        for (int cc = 0; cc < 2; cc++) acc_fold(acc[j][cc], m);
+                }
+            }
+            buf ^= 1;  // the other buffer is free: every thread passed the barrier after using it
+            t0 += kTChunk;
+            while (t0 >= T) {
+                t0 -= T;
+                i0++;
             }
         }
-        buf ^= 1;  // the other buffer is free: every thread passed the barrier after using it
-        t0 += kTChunk;
-        while (t0 >= T) {
-            t0 -= T;
-            i0++;
-        }
-    }
 #pragma unroll
-    for (int j = 0; j < PPW; j++) {
-        const int o = o_a + j / PB, b = b0 + b_a + j % PB;
-        if (warp_active && o < O) {
-            if (b < B) {
-                uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
-                dst[0] = acc[j][0].reduce(m);
-                dst[dstride] = acc[j][1].reduce(m);
+        for (int j = 0; j < PPW; j++) {
+            const int o = o_a + j / PB, b = b0 + b_a + j % PB;
+            if (warp_active && o < O) {
+                if (b < B) {
+                    uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
+                    dst[0] = acc[j][0].reduce(m);
+                    dst[dstride] = acc[j][1].reduce(m);
+                }
             }
         }
-    }
+    };
+#if UH_NARROW_MAC
+    if (smallq)
+        body(AccN{});
+    else
+#endif
+        body(Acc{});
 }
 
 // ---------------------------------------------------------------------------
@@ -538,82 +564,91 @@ __global__ void __launch_bounds__(256, OM > 2 ? 3 : UH_DIRECT_MINB)
     const int Q = diag == 1 ? I : I * T;
     const uint32_t dstride = (uint32_t)LP << logn;
     const uint32_t mask_row = ((uint32_t)k << logn) + n;
-    Acc acc[OM][2];
+    auto body = [&](auto acc_tag) {
+        using A = decltype(acc_tag);
+        A acc[OM][2];
 #pragma unroll
-    for (int o = 0; o < OM; o++) {
-        acc[o][0].zero();
-        acc[o][1].zero();
-    }
-    int i = 0, t = 0, since = 0;
-    for (int q = 0; q < Q; q++) {
-        if (diag == 1) {
-            i = t = q;
-        } else if (diag == 2) {  // block-diagonal: input q / T with its own tap q
-            t = q;
-            i = q / T;
+        for (int o = 0; o < OM; o++) {
+            acc[o][0].zero();
+            acc[o][1].zero();
         }
-        const uint32_t ib = (uint32_t)(i * B + b);
-        const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
-        const uint32_t r = s_shift[t];
-        uint64_t mk[OM];
-        if (MASKS) {
-#pragma unroll
-            for (int o = 0; o < OM; o++)
-                mk[o] = o < O ? __ldg(masks + ((uint32_t)o * Q + q) * dstride + mask_row) : 0;
-        }
-        Acc a0, a1;
-        a0.zero();
-        a1.zero();
-        if (r == 0) {
-            if (qlimb) {
-                a0.mac(Pk, __ldg(c0 + n));
-                a1.mac(Pk, __ldg(c0 + ((uint32_t)xls << logn) + n));
+        int i = 0, t = 0, since = 0;
+        for (int q = 0; q < Q; q++) {
+            if (diag == 1) {
+                i = t = q;
+            } else if (diag == 2) {  // block-diagonal: input q / T with its own tap q
+                t = q;
+                i = q / T;
             }
-        } else {
-            const uint32_t src = rot_index(n, half, r);
-            const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
-            const uint32_t ks = s_kstride[t];
-            const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + n;
-            ks_dot<(OM > 2 ? UH_DIRECT_G4 : UH_DIRECT_G)>(a0, a1, Di, dstride, k0, ks, L);
-            if (qlimb) a0.mac(Pk, __ldg(c0 + src));
-        }
-        if (MASKS) {
-            const uint64_t v0 = term_value(a0, m, smallq);
-            const uint64_t v1 = term_value(a1, m, smallq);
-#pragma unroll
-            for (int o = 0; o < OM; o++) {
-                acc[o][0].mac(mk[o], v0);
-                acc[o][1].mac(mk[o], v1);
-            }
-            if (++since == kFold) {
-                since = 0;
+            const uint32_t ib = (uint32_t)(i * B + b);
+            const uint64_t *c0 = X + ((ib * 2 * (uint32_t)xls + (uint32_t)k) << logn);
+            const uint32_t r = s_shift[t];
+            uint64_t mk[OM];
+            if (MASKS) {
 #pragma unroll
                 for (int o = 0; o < OM; o++)
-                    for (int cc = 0; cc < 2; cc++) {
-                        const uint64_t rr = reduce128_lazy(acc[o][cc].hi64(), acc[o][cc].lo64(), m);
-                        acc[o][cc].set(rr, 0);
-                    }
+                    mk[o] = o < O ? __ldg(masks + ((uint32_t)o * Q + q) * dstride + mask_row) : 0;
             }
-        } else {
-            // fold the term's 128-bit sums (each < (2L + 1) q^2 < 2^125) into the running sum
-            const uint64_t v0 = smallq ? fold64_small(a0, m) : reduce128_lazy(a0.hi64(), a0.lo64(), m);
-            const uint64_t v1 = smallq ? fold64_small(a1, m) : reduce128_lazy(a1.hi64(), a1.lo64(), m);
-            acc[0][0].add(v0);
-            acc[0][1].add(v1);
-        }
-        if (diag == 0 && ++t == T) {
-            t = 0;
-            i++;
-        }
-    }
+            A a0, a1;
+            a0.zero();
+            a1.zero();
+            if (r == 0) {
+                if (qlimb) {
+                    a0.mac(Pk, __ldg(c0 + n));
+                    a1.mac(Pk, __ldg(c0 + ((uint32_t)xls << logn) + n));
+                }
+            } else {
+                const uint32_t src = rot_index(n, half, r);
+                const uint64_t *Di = D + (((ib * (uint32_t)L) * LP + k) << logn) + src;
+                const uint32_t ks = s_kstride[t];
+                const uint64_t *k0 = s_key[t] + (qlimb ? ((uint32_t)k << logn) : ks - N) + n;
+                ks_dot<(OM > 2 ? UH_DIRECT_G4 : UH_DIRECT_G)>(a0, a1, Di, dstride, k0, ks, L);
+                if (qlimb) a0.mac(Pk, __ldg(c0 + src));
+            }
+            if (MASKS) {
+                const uint64_t v0 = term_value(a0, m, smallq);
+                const uint64_t v1 = term_value(a1, m, smallq);
 #pragma unroll
-    for (int o = 0; o < OM; o++) {
-        if (o < O) {
-            uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
-            dst[0] = acc[o][0].reduce(m);
-            dst[dstride] = acc[o][1].reduce(m);
+                for (int o = 0; o < OM; o++) {
+                    acc[o][0].mac(mk[o], v0);
+                    acc[o][1].mac(mk[o], v1);
+                }
+                if (++since == kFold) {
+                    since = 0;
+#pragma unroll
+                    for (int o = 0; o < OM; o++)
+                        for (int cc = 0; cc < 2; cc++) acc_fold(acc[o][cc], m);
+                }
+            } else {
+                // fold the term's 128-bit sums (each < (2L + 1) q^2 < 2^125) into the running sum
+                uint64_t h0, l0, h1, l1;
+                a0.value(h0, l0);
+                a1.value(h1, l1);
+                const uint64_t v0 = smallq ? fold64_small(h0, l0, m) : reduce128_lazy(h0, l0, m);
+                const uint64_t v1 = smallq ? fold64_small(h1, l1, m) : reduce128_lazy(h1, l1, m);
+                acc[0][0].add(v0);
+                acc[0][1].add(v1);
+            }
+            if (diag == 0 && ++t == T) {
+                t = 0;
+                i++;
+            }
         }
-    }
+#pragma unroll
+        for (int o = 0; o < OM; o++) {
+            if (o < O) {
+                uint64_t *dst = acc_out + (((uint32_t)(o * B + b) * 2 * LP + k) << logn) + n;
+                dst[0] = acc[o][0].reduce(m);
+                dst[dstride] = acc[o][1].reduce(m);
+            }
+        }
+    };
+#if UH_NARROW_MAC
+    if (smallq)
+        body(AccN{});
+    else
+#endif
+        body(Acc{});
 }
 
 }  // namespace

@@ -183,6 +183,30 @@ __global__ void k_mixed_peak(uint64_t *out, int iters, uint64_t seed, double q, 
     if (s == 0x1234567812345678ull) out[0] = s;
 }
 
+// narrow-operand MAC (AccN, limbs with q < 2^41): both factors below 2^41
+__global__ void k_macn_peak(uint64_t *out, int iters, uint64_t seed) {
+    AccN acc[8];
+    uint64_t x[8];
+    constexpr uint64_t M41 = (1ull << 41) - 1;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        acc[i].zero();
+        x[i] = (seed + threadIdx.x * 8 + i) & M41;
+    }
+    const uint64_t w = (0x0FEDCBA987654321ull + blockIdx.x) & M41;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            acc[i].mac(x[i], w);
+            x[i] ^= acc[i].a & M41;  // one 3-input LOP3 (ALU pipe)
+        }
+    }
+    uint64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s ^= acc[i].lo64() ^ acc[i].hi64();
+    if (s == 0x1234567812345678ull) out[0] = s;
+}
+
 template <class F> double time_ms(F &&launch) {
     cudaEvent_t a, b;
     UH_CHECK(cudaEventCreate(&a));
@@ -228,6 +252,8 @@ void bench_peaks(const Ctx &c, double *rates) {
     rates[6] = lanes * iters * 8 / (ms * 1e-3);
     ms = time_ms([&] { k_macs_peak<<<blocks, threads>>>(out, iters, 7ull); });
     rates[7] = lanes * iters * 8 / (ms * 1e-3);
+    ms = time_ms([&] { k_macn_peak<<<blocks, threads>>>(out, iters, 7ull); });
+    rates[8] = lanes * iters * 8 / (ms * 1e-3);
     UH_CHECK(cudaGetLastError());
     cudaFree(out);
 }
