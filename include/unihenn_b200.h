@@ -164,6 +164,20 @@ int uh_conv_hoisted_mac(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, 
 int uh_hoisted_mac(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D, const uint64_t *masks,
                    const uint64_t *const *keys, const int32_t *key_limbs, const int32_t *shifts, int B, int I, int T,
                    int O, int diag, int level, void *stream);
+/* uh_hoisted_mac over a per-layer key bank instead of per-key pointers (every
+ * term mode; masks may be NULL): kbank is [NT][level+2][2*(level+1)][N] with NT
+ * = T (dense), I (diagonal) or I*T (block-diagonal) entries, one per entry of
+ * `shifts` (limb-major; row (k, 2j + c) = component c of digit j of the Galois
+ * key of that shift, limb k of q_0..q_level, P; any content for shift 0).
+ * Same result as uh_hoisted_mac / uh_conv_hoisted_mac / uh_rot_sum_hoisted
+ * (layers.conv / avgpool / flatten / fc, layers.py:134-426) bit for bit, with
+ * compile-time strides.  Supported when uh_hoisted_bank_supported(ctx, level, O)
+ * returns 1 (N = 2^15, level + 1 <= 10, 1 <= O <= 12); X must hold exactly
+ * level + 1 limbs (xls == level + 1). */
+int uh_hoisted_bank_supported(uh_ctx *ctx, int level, int O);
+int uh_hoisted_mac_bank(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D,
+                        const uint64_t *masks, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T,
+                        int O, int diag, int level, void *stream);
 /* Hoisted rotation sum (layers.avgpool, layers.py:213-218): out[C][B][2][level+2][N]
  * = sum_t P * rot_t(ct_c) in the QP basis; ModDown gives the pooled ciphertexts. */
 int uh_rot_sum_hoisted(uh_ctx *ctx, uint64_t *out, const uint64_t *X, int xls, const uint64_t *D,

@@ -316,6 +316,27 @@ __attribute__((visibility("default"))) int uh_hoisted_mac(uh_ctx *ctx, uint64_t 
     });
 }
 
+__attribute__((visibility("default"))) int uh_hoisted_bank_supported(uh_ctx *ctx, int level, int O) {
+    return ctx && uh::hoisted_bank_supported(C(ctx), level, O) ? 1 : 0;
+}
+
+__attribute__((visibility("default"))) int uh_hoisted_mac_bank(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls,
+                                                               const uint64_t *D, const uint64_t *masks,
+                                                               const uint64_t *kbank, const int32_t *shifts, int B,
+                                                               int I, int T, int O, int diag, int level,
+                                                               void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(B > 0 && I > 0 && T > 0 && O > 0 && xls == level + 1, "bad shape (xls must equal level + 1)");
+        need(diag >= 0 && diag <= 2, "term mode must be 0 (dense), 1 (diagonal) or 2 (block-diagonal)");
+        need(diag != 1 || I == T, "diagonal terms need I == T");
+        need(diag != 2 || O <= 4, "block-diagonal terms are supported for up to 4 outputs");
+        need(kbank != nullptr, "key bank is required");
+        uh::hoisted_mac_bank(c, acc, X, D, masks, kbank, shifts, B, I, T, O, diag, level, S(stream));
+    });
+}
+
 __attribute__((visibility("default"))) int uh_decode_coeffs(uh_ctx *ctx, double *slots, const double *coef,
                                                             int n_polys, double scale, void *stream) {
     return guard([&] { uh::decode_coeffs(C(ctx), slots, coef, n_polys, scale, S(stream)); });

@@ -85,6 +85,12 @@ void conv_hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, c
 void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D, const uint64_t *masks,
                  const uint64_t *const *keys, const int32_t *key_limbs, const int32_t *shifts, int B, int I, int T,
                  int O, int diag, int level, cudaStream_t s);
+// hoist_bank.cu -- the same hoisted MAC (every term mode, masks optional) over a per-layer key bank
+// kb[NT][L+1][2L][N] (limb-major, (digit, component) inner), compile-time strides (N = 2^15).
+bool hoisted_bank_supported(const Ctx &c, int level, int O);
+void hoisted_mac_bank(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
+                      const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, int diag, int level,
+                      cudaStream_t s);
 // microbench.cu: rates[0] = IMAD/s, rates[1] = 128-bit MAC/s, rates[2] = reduced mulmod/s
 void bench_peaks(const Ctx &c, double *rates);
 // pool: out[C][B][2][L+1][N] (QP basis) = sum_t P * rot_t(ct_c)

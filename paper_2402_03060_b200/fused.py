@@ -25,10 +25,12 @@ Weight masks are encoded once per (layer, level, layout) into a device
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
-from . import schedule
+from . import _lib, schedule
 from .planner import AvgPool2d, Conv1d, Conv2d, Square
 from .schedule import CipherState, conv_geometry, pool_layout, pool_shifts, position_mask, valid_positions
 
@@ -73,6 +75,38 @@ def _rotation_plan(backend, shifts, level):
                          device=backend.device)
     sh = torch.tensor(norm, dtype=torch.int32, device=backend.device)
     return sh, ptrs, keys, limbs
+
+
+def _key_bank_ok(backend, level: int, O: int) -> bool:
+    """Dense masked terms run on the key-bank kernel (hoist_bank.cu) where it is compiled for."""
+    if os.environ.get("UH_KEY_BANK", "1") == "0":
+        return False
+    return bool(_lib.load().uh_hoisted_bank_supported(backend._ctx, level, O))
+
+
+def key_bank(backend, shifts, level: int) -> torch.Tensor:
+    """Galois keys of ``shifts`` re-laid for the key-bank kernel: [T][level+2][2(level+1)][N].
+
+    Row (k, 2j + c) of tap t is component c of digit j of the key of shifts[t],
+    limb k of (q_0..q_level, P), truncated from whatever level the key was
+    generated at.  Cached per (shifts, level, key buffers)."""
+    half = backend.params.num_slots
+    norm = [s % half for s in shifts]
+    keys = [backend.galois_key(s, level) if s else None for s in norm]
+    ck = ("kbank", tuple(norm), level, tuple(k.data_ptr() if k is not None else 0 for k in keys))
+    banks = backend.__dict__.setdefault("_key_banks", {})
+    bank = banks.get(ck)
+    if bank is None:
+        L, LP, n = level + 1, level + 2, backend.n
+        bank = torch.zeros((len(norm), LP, 2 * L, n), dtype=torch.int64, device=backend.device)
+        for t, k in enumerate(keys):
+            if k is None:
+                continue
+            idx = torch.tensor(list(range(L)) + [k.shape[2] - 1], device=backend.device)
+            kk = k[:L].index_select(2, idx)  # [L][2][LP][N]
+            bank[t] = kk.permute(2, 0, 1, 3).reshape(LP, 2 * L, n)
+        banks[ck] = bank
+    return bank
 
 
 def _bank(backend, key, build):
@@ -162,8 +196,13 @@ def conv(backend, state: CipherState, layer) -> CipherState:
     if timer is not None:
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(torch.cuda.current_stream(backend.device))
-    backend._call("uh_conv_hoisted_mac", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ptrs), _vp(key_limbs), _vp(sh),
-                  B, I, T, O, level, st)
+    if _key_bank_ok(backend, level, O):
+        kb = key_bank(backend, shifts, level)
+        backend._call("uh_hoisted_mac_bank", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(kb), _vp(sh), B, I, T, O,
+                      0, level, st)
+    else:
+        backend._call("uh_conv_hoisted_mac", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ptrs), _vp(key_limbs),
+                      _vp(sh), B, I, T, O, level, st)
     if timer is not None:
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(torch.cuda.current_stream(backend.device))
@@ -204,10 +243,18 @@ def avgpool(backend, state: CipherState, layer: AvgPool2d) -> CipherState:
     st = backend._stream()
     D = backend._empty(C, B, L, LP, n)
     backend._call("uh_modup", _vp(D), _vp(X.data_ptr() + L * n * 8), C * B, level, 2 * L, st)
-    sh, ptrs, keys, key_limbs = _rotation_plan(backend, shifts, level)
     acc = backend._empty(C, B, 2, LP, n)
-    backend._call("uh_rot_sum_hoisted", _vp(acc), _vp(X), L, _vp(D), _vp(ptrs), _vp(key_limbs), _vp(sh), B, C, T, level,
-                  st)
+    keys = None
+    if _key_bank_ok(backend, level, 1):
+        # the C channels x B ciphertexts as one batch of one input, unmasked
+        kb = key_bank(backend, shifts, level)
+        sh = torch.tensor([s % backend.params.num_slots for s in shifts], dtype=torch.int32, device=backend.device)
+        backend._call("uh_hoisted_mac_bank", _vp(acc), _vp(X), L, _vp(D), _vp(0), _vp(kb), _vp(sh), C * B, 1, T, 1, 0,
+                      level, st)
+    else:
+        sh, ptrs, keys, key_limbs = _rotation_plan(backend, shifts, level)
+        backend._call("uh_rot_sum_hoisted", _vp(acc), _vp(X), L, _vp(D), _vp(ptrs), _vp(key_limbs), _vp(sh), B, C, T,
+                      level, st)
     del D
     out = backend._empty(C, B, 2, L, n)
     backend._call("uh_divide_top", _vp(out), _vp(acc), C * B * 2, L, backend.sp, L, LP, st)
@@ -263,10 +310,17 @@ def _hoist(backend, X, level, shifts, masks, O, diag, B, taps=None):
     st = backend._stream()
     D = backend._empty(I, B, L, LP, n)
     backend._call("uh_modup", _vp(D), _vp(X.data_ptr() + L * n * 8), I * B, level, 2 * L, st)
-    sh, ptrs, keys, limbs = _rotation_plan(backend, shifts, level)
     acc = backend._empty(O, B, 2, LP, n)
     mode = 2 if diag == 2 else (1 if diag else 0)
     T = taps if mode == 2 else len(shifts)
+    if _key_bank_ok(backend, level, O) and (mode != 2 or O <= 4):
+        kb = key_bank(backend, shifts, level)
+        sh = torch.tensor([s % backend.params.num_slots for s in shifts], dtype=torch.int32, device=backend.device)
+        backend._call("uh_hoisted_mac_bank", _vp(acc), _vp(X), L, _vp(D), _vp(masks) if masks is not None else _vp(0),
+                      _vp(kb), _vp(sh), B, I, T, O, mode, level, st)
+        del D
+        return acc
+    sh, ptrs, keys, limbs = _rotation_plan(backend, shifts, level)
     backend._call("uh_hoisted_mac", _vp(acc), _vp(X), L, _vp(D), _vp(masks) if masks is not None else _vp(0),
                   _vp(ptrs), _vp(limbs), _vp(sh), B, I, T, O, mode, level, st)
     del keys, D

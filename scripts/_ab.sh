@@ -1,4 +1,5 @@
-P="python scripts/prof_step.py --batch 64"
-UH_LIB_PATH=paper_2402_03060_b200/_build/variants/nonarrow.so $P > gpurun_out/prof_nonarrow.log 2>&1
-$P > gpurun_out/prof_narrow.log 2>&1 || exit 1
-ncu --set full --clock-control none --import-source on -k regex:k_hoisted -c 4 -o gpurun_out/narrow $P > gpurun_out/ncu_narrow.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_hoisted.py -x -q > gpurun_out/t_hoist.log 2>&1
+P="python scripts/prof_step.py --batch 64 --trace"
+$P > gpurun_out/prof_bank.log 2>&1
+UH_KEY_BANK=0 $P > gpurun_out/prof_nobank.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1

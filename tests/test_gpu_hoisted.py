@@ -112,3 +112,82 @@ def test_hoisted_diag_bit_exact_vs_oracle():
             for c in range(2):
                 want[0, b, c] = o.add(want[0, b, c], part[0, b, c], qp)
     assert np.array_equal(got, want)
+
+
+C2 = HEParams(poly_degree=1 << 15, depth=9, scale_bits=40, seed=6)  # BASELINE config-2 chain
+
+
+def _c2():
+    if "c2" not in _CACHE:
+        _CACHE["c2"] = (GpuBackend(C2), Oracle(C2))
+    return _CACHE["c2"]
+
+
+def _rand_masks(o, rng, O, Q, level):
+    masks = np.zeros((O, Q, level + 2, o.n), dtype=np.uint64)
+    for k, m in enumerate(o.qp_mods(level)):
+        masks[:, :, k] = rng.integers(0, int(o.moduli[m]), size=(O, Q, o.n), dtype=np.uint64)
+    return masks
+
+
+@pytest.mark.parametrize("O,level", [(12, 5), (5, 2), (1, 7)])
+def test_key_bank_kernel_bit_exact_vs_oracle(O, level, monkeypatch):
+    """The key-bank kernel (hoist_bank.cu, N = 2^15 only) on the BASELINE chain, residue for residue."""
+    monkeypatch.setenv("UH_KEY_BANK", "1")
+    be, o = _c2()
+    assert fused._key_bank_ok(be, level, O)
+    s = o.secret()
+    B, I = 3, 2
+    shifts = [0, 1, 28, -29, 16383]
+    rng = np.random.default_rng(20 + O)
+    cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, C2.num_slots)))) for _ in range(I)]
+    X = fused.stack_cts(be, cts, level)
+    masks = _rand_masks(o, rng, O, I * len(shifts), level)
+    got = fused._hoist(be, X, level, shifts, torch.from_numpy(masks.view(np.int64)).to(be.device), O, False, B)
+    want = _reference(o, s, X.cpu().numpy().view(np.uint64), level, shifts, masks, O, B)
+    assert np.array_equal(got.cpu().numpy().view(np.uint64), want)
+
+
+def test_key_bank_kernel_equals_generic_at_lenet_conv2_shape(monkeypatch):
+    """LeNet conv2 shape (4 inputs x 25 taps, 12 outputs, level 5): bank kernel == generic kernel, bit for bit."""
+    be, o = _c2()
+    level, B, I, O = 5, 5, 4, 12
+    shifts = [a + 28 * b for b in range(5) for a in range(5)]
+    rng = np.random.default_rng(9)
+    cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, C2.num_slots)))) for _ in range(I)]
+    X = fused.stack_cts(be, cts, level)
+    mdev = torch.from_numpy(_rand_masks(o, rng, O, I * len(shifts), level).view(np.int64)).to(be.device)
+    monkeypatch.setenv("UH_KEY_BANK", "1")
+    got = fused._hoist(be, X, level, shifts, mdev, O, False, B)
+    monkeypatch.setenv("UH_KEY_BANK", "0")
+    want = fused._hoist(be, X, level, shifts, mdev, O, False, B)
+    assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("O,with_masks,diag", [(1, True, 0), (2, True, 0), (3, True, 0), (4, True, 0),
+                                               (1, False, 0), (3, False, 0), (1, False, 1), (2, True, 2)])
+def test_key_bank_kernels_equal_generic_every_mode(O, with_masks, diag, monkeypatch):
+    """Register-only key-bank kernel (narrow layers, rotation sums, diagonal / block-diagonal terms) ==
+    the generic kernel (oracle-pinned above), bit for bit, at N = 2^15 on the BASELINE chain."""
+    be, o = _c2()
+    level, B = 3, 9  # B not a multiple of the 8-ciphertext CTA tile
+    if diag == 1:
+        I, shifts, taps, Q = 3, [0, 5, -11], None, 3
+    elif diag == 2:
+        I, shifts, taps = 2, [1, 29, -3, 0], 2
+        Q = 4
+    else:
+        I, shifts, taps = 2, [0, 1, 28, -29, 16383], None
+        Q = I * len(shifts)
+    rng = np.random.default_rng(40 + O + diag)
+    cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, C2.num_slots)))) for _ in range(I)]
+    X = fused.stack_cts(be, cts, level)
+    mdev = None
+    if with_masks:
+        mdev = torch.from_numpy(_rand_masks(o, rng, O, Q, level).view(np.int64)).to(be.device)
+    mode = 2 if diag == 2 else bool(diag)
+    monkeypatch.setenv("UH_KEY_BANK", "1")
+    got = fused._hoist(be, X, level, shifts, mdev, O, mode, B, taps=taps)
+    monkeypatch.setenv("UH_KEY_BANK", "0")
+    want = fused._hoist(be, X, level, shifts, mdev, O, mode, B, taps=taps)
+    assert torch.equal(got, want)
