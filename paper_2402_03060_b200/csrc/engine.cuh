@@ -23,6 +23,7 @@ struct Ctx {
     ulonglong2 *d_tw2 = nullptr, *d_itw2 = nullptr;  // [count][n] interleaved (w, w') pairs of the above
     double2 *d_twf = nullptr, *d_itwf = nullptr;     // [count][n] (w, w / q) for FP64-pipe limbs (q < 2^42), else 0
     double *d_twd = nullptr, *d_itwd = nullptr;       // [count][n] w as double (FP64-pipe limbs), else 0
+    double *d_twist = nullptr, *d_itwist = nullptr;   // [count][n] pass-2 block twists beta_X^(+-c) (FP64 limbs)
     int32_t *d_sob = nullptr;            // [n] slot-order index of bit-reversed NTT output k
     int32_t *d_bsel = nullptr;           // [n1] pass-2 block of CTA x, position g (ntt_fast.cu)
     int32_t *d_csl = nullptr;            // [n] element index inside its pass-2 block, per slot

@@ -34,7 +34,7 @@ constexpr int kChunk = 3;        // terms per shared-memory chunk
 constexpr int kFoldChunks = 18;  // 54 terms between folds of the 128-bit accumulators
 constexpr int kBankMaxTerms = 512;
 #ifndef UH_BANK_MINB
-#define UH_BANK_MINB 4  // resident CTAs per SM requested from ptxas (4: 80 registers)
+#define UH_BANK_MINB 3  // resident CTAs per SM requested from ptxas (3: 96 registers, no spills; measured 51.9 vs 52.8 ms at 4)
 #endif
 #ifndef UH_BANK_DIRECT_MINB
 #define UH_BANK_DIRECT_MINB 3
@@ -43,7 +43,7 @@ constexpr int kBankMaxTerms = 512;
 #define UH_BANK_DIRECT_G 2
 #endif
 #ifndef UH_BANK_G
-#define UH_BANK_G 2  // phase-A load group (digits)
+#define UH_BANK_G 6  // phase-A load group (digits): all of a term's loads in flight for L <= 6
 #endif
 
 __device__ __forceinline__ uint32_t rot_index_b(uint32_t n, uint32_t half, uint32_t r) {

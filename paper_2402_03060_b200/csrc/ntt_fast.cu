@@ -27,6 +27,9 @@
 #ifndef UH_NTT_TW8
 #define UH_NTT_TW8 1  // pass-2 FP64 twiddles read as w only (8 B), w / q formed with one multiply
 #endif
+#ifndef UH_NTT_TWIST
+#define UH_NTT_TWIST 0  // (opt-in, measured slower: 0.343 vs 0.313 us/limb) FP64 limbs: pass-2 blocks twisted by beta^c, shared twiddles W[0, N2/2) in shared memory
+#endif
 #ifndef UH_NTT_MINB
 #define UH_NTT_MINB 4  // min resident CTAs per SM requested from ptxas (register cap: 64)
 #endif
@@ -253,6 +256,11 @@ struct TwS {  // unused unless UH_NTT_STAGE
     double qinv;
 };
 #endif
+
+struct TwSh {  // twisted pass 2: every block uses the shared twiddles W[j] (staged as (w, w / q))
+    const double2 *t;
+    __device__ double2 operator()(int, int j) const { return t[j]; }
+};
 
 // forward radix network on R register values (elements base + S*x), stages with
 // distance dx = R/2 .. 1; twiddle (m, off(s) + x / (2 dx)), m = m0 * (1 << s)
@@ -523,9 +531,63 @@ __device__ __forceinline__ void fwd_p2_body(uint64_t *sm, const double *tws, con
     __syncthreads();
 }
 
+// Twisted pass 2 (FP64 limbs): block blk's CT network with twiddles W[(X << s) + g]
+// (X = N1 + blk) equals the same network with the shared twiddles W[g] applied to the
+// input scaled elementwise by beta_X^c (context.cu builds the twist table): one
+// coalesced twist load and one exact FP64 product per element replace the per-block
+// twiddle loads (the dominant L1 traffic of the untwisted pass), and the twist resets
+// the magnitudes to |v| <= 0.51 q.
+template <int B, class IN>
+__device__ __forceinline__ void fwd_p2_twist(uint64_t *sm, const double2 *sw, const double *__restrict__ twist,
+                                             const Mod &m, const IN &in, const int *sel, int tid) {
+    using C = P2<B>;
+    using AR = Arith<true>;
+    const AR ar(m.q);
+    const TwSh ta{sw};
+    {
+        const int g = tid / C::S, c0 = tid % C::S, blk = sel[g];
+        double v[C::R1];
+        const double *tb = twist + (size_t)blk * C::N2 + c0;
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(in(blk, c0 + C::S * x));
+        in.done();
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) {
+            const double t = __ldg(tb + C::S * x);
+            v[x] = fmm(v[x], make_double2(t, t * ar.qinv), ar.q);
+        }
+        fwd_strided<C::R1>(v, ta, 1, 0, ar.qv());
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) sm[C::at(g, c0 + C::S * x)] = AR::raw(v[x]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int gi = 0; gi < C::GC; gi++) {
+        const int grp = tid + kThreads * gi;
+        const int per = C::N2 / C::R2;
+        const int g = grp / per, c = (grp % per) * C::R2;
+        double v[C::R2];
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) v[z] = AR::raw_in(sm[C::at(g, c + z)]);
+        fwd_strided<C::R2>(v, ta, 16, (c / C::R2), ar.qv());
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = ar.canon(v[z]);
+    }
+    __syncthreads();
+}
+// shared twiddles W[0, N2/2) of the limb's prime as (w, w / q) in shared memory
 template <int B>
-constexpr size_t p2_smem() {  // data tiles + FP64 twiddle stage
-    return (size_t)(P2<B>::G * P2<B>::PAD + (UH_NTT_STAGE ? P2<B>::G * P2<B>::N2 : 0)) * 8;
+__device__ __forceinline__ void stage_shared_tw(double2 *sw, const double *__restrict__ T, double qinv, int tid) {
+    for (int j = tid; j < P2<B>::N2 / 2; j += kThreads) {
+        const double w = __ldg(T + j);
+        sw[j] = make_double2(w, w * qinv);
+    }
+}
+
+template <int B>
+constexpr size_t p2_smem() {  // data tiles + FP64 twiddle stage (per-block staged twiddles or the shared ones)
+    return (size_t)(P2<B>::G * P2<B>::PAD +
+                    (UH_NTT_STAGE ? P2<B>::G * P2<B>::N2 : (UH_NTT_TWIST ? P2<B>::N2 : 0))) * 8;
 }
 
 template <int B, int EM>
@@ -535,7 +597,8 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p2(NttJob J, cons
                                                     const double *__restrict__ twdd,
                                                     const double2 *__restrict__ twf,
                                                     const int32_t *__restrict__ bsel,
-                                                    const int32_t *__restrict__ csl) {
+                                                    const int32_t *__restrict__ csl,
+                                                    const double *__restrict__ twist) {
     using C = P2<B>;
     extern __shared__ uint64_t dsm[];
     uint64_t *sm = dsm;
@@ -549,6 +612,14 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p2(NttJob J, cons
     const Tw tw2{twd + ((size_t)li.mod << logn), twf + ((size_t)li.mod << logn)};
     const InGlobal<B> in{tmp + ((size_t)blockIdx.y << logn)};
     if (fp_limb(q)) {
+        if constexpr (UH_NTT_TWIST && !UH_NTT_STAGE) {
+            double2 *sw = reinterpret_cast<double2 *>(tws);
+            stage_shared_tw<B>(sw, twdd + ((size_t)li.mod << logn), 1.0 / (double)q, tid);
+            __syncthreads();
+            fwd_p2_twist<B>(sm, sw, twist + ((size_t)li.mod << logn), m, in, sel, tid);
+            fwd_p2_epilogue<B, EM>(sm, li, q, csl, logn, tid);
+            return;
+        }
         if constexpr (UH_NTT_STAGE) {
             stage_twiddles<B>(tws, twdd + ((size_t)li.mod << logn), sel, n1, tid);
             __syncthreads();
@@ -715,6 +786,43 @@ __device__ __forceinline__ void inv_pa_body(uint64_t *sm, const double *tws, con
     }
 }
 
+// twisted inverse pass A (FP64 limbs): the GS network with the shared inverse twiddles,
+// then element c of block blk scaled by beta_X^-c (exact FP64 product, centred result)
+template <int B>
+__device__ __forceinline__ void inv_pa_twist(uint64_t *sm, const double2 *sw, const double *__restrict__ itwist,
+                                             const Mod &m, uint64_t *out, const int *sel, int tid) {
+    using C = P2<B>;
+    using AR = Arith<true>;
+    const AR ar(m.q);
+    const TwSh ta{sw};
+#pragma unroll
+    for (int gi = 0; gi < C::GC; gi++) {
+        const int grp = tid + kThreads * gi;
+        const int per = C::N2 / C::R2;
+        const int g = grp / per, c = (grp % per) * C::R2;
+        double v[C::R2];
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) v[z] = AR::in(sm[C::at(g, c + z)]);
+        inv_strided<C::R2>(v, ta, C::N2 / 2, (c / C::R2) * (C::R2 / 2), ar.qv());
+#pragma unroll
+        for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = AR::raw(v[z]);
+    }
+    __syncthreads();
+    {
+        const int g = tid / C::S, c0 = tid % C::S, blk = sel[g];
+        double v[C::R1];
+        const double *tb = itwist + (size_t)blk * C::N2 + c0;
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(sm[C::at(g, c0 + C::S * x)]);
+        inv_strided<C::R1>(v, ta, 8, 0, ar.qv());
+#pragma unroll
+        for (int x = 0; x < C::R1; x++) {
+            const double t = __ldg(tb + C::S * x);
+            out[(size_t)blk * C::N2 + c0 + C::S * x] = AR::raw(fmm(v[x], make_double2(t, t * ar.qinv), ar.q));
+        }
+    }
+}
+
 template <int B>
 __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
@@ -722,7 +830,8 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint
                                                     const double *__restrict__ itwdd,
                                                     const double2 *__restrict__ itwf,
                                                     const int32_t *__restrict__ bsel,
-                                                    const int32_t *__restrict__ csl) {
+                                                    const int32_t *__restrict__ csl,
+                                                    const double *__restrict__ itwist) {
     using C = P2<B>;
     extern __shared__ uint64_t dsm[];
     uint64_t *sm = dsm;
@@ -735,6 +844,8 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint
     const Tw tw2{itwd + ((size_t)li.mod << logn), itwf + ((size_t)li.mod << logn)};
     const bool fp = fp_limb(m.q);
     if (UH_NTT_STAGE && fp) stage_twiddles<B>(tws, itwdd + ((size_t)li.mod << logn), sel, n1, tid);
+    if (UH_NTT_TWIST && !UH_NTT_STAGE && fp)
+        stage_shared_tw<B>(reinterpret_cast<double2 *>(tws), itwdd + ((size_t)li.mod << logn), 1.0 / (double)m.q, tid);
     // coalesced slot-order gather into the blocks' shared-memory tiles (plain limbs: the only
     // inverse mode); all of a thread's loads are issued before the shared-memory stores
     {
@@ -752,7 +863,9 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint
     }
     __syncthreads();
     uint64_t *out = tmp + ((size_t)blockIdx.y << logn);
-    if (fp)
+    if (UH_NTT_TWIST && !UH_NTT_STAGE && fp)
+        inv_pa_twist<B>(sm, reinterpret_cast<const double2 *>(tws), itwist + ((size_t)li.mod << logn), m, out, sel, tid);
+    else if (fp)
         inv_pa_body<B, true, UH_NTT_STAGE>(sm, UH_NTT_STAGE ? tws : itwdd + ((size_t)li.mod << logn), m, tw2, out,
                                            sel, n1, tid);
     else
@@ -863,13 +976,13 @@ void run_fwd(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
         UH_LAUNCH_CHECK();
         if (J.mode == NTT_DIVIDE) {
             p2_attr<k_fwd_p2<B, 1>>(sm2);
-            k_fwd_p2<B, 1><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl);
+            k_fwd_p2<B, 1><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl, c.d_twist);
         } else if (J.mode == NTT_DIVIDE2) {
             p2_attr<k_fwd_p2<B, 2>>(sm2);
-            k_fwd_p2<B, 2><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl);
+            k_fwd_p2<B, 2><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl, c.d_twist);
         } else {
             p2_attr<k_fwd_p2<B, 0>>(sm2);
-            k_fwd_p2<B, 0><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl);
+            k_fwd_p2<B, 0><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl, c.d_twist);
         }
         UH_LAUNCH_CHECK();
     }
@@ -888,7 +1001,7 @@ void run_inv(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
         const int nl = std::min(ch, limbs - f0);
         dim3 g1((1u << B) / 32, nl), g2((1u << A) / P2<B>::G, nl);
         k_inv_pa<B><<<g2, kThreads, sm2, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwd,
-                                              c.d_itwf, c.d_bsel, c.d_csl);
+                                              c.d_itwf, c.d_bsel, c.d_csl, c.d_itwist);
         UH_LAUNCH_CHECK();
         k_inv_pb<A><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwf);
         UH_LAUNCH_CHECK();

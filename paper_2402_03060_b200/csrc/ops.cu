@@ -224,6 +224,65 @@ __global__ void __launch_bounds__(256) k_key_inner2(uint64_t *__restrict__ u, co
     u[(((p * 2 + 1) * LP + k) << logn) + n] = v1;
 }
 
+// Same product with compile-time L and N (N = 2^15): no predicated digit groups, all 3L
+// operand loads in flight at once, and the narrow-operand accumulator (AccN) for limbs
+// with q < 2^41.  Grid (N / 256, L + 1, polys) as k_key_inner2.
+template <int L, int LOGN>
+__global__ void __launch_bounds__(256) k_key_inner_l(uint64_t *__restrict__ u, const uint64_t *__restrict__ D,
+                                                     const uint64_t *__restrict__ key, int key_limbs, int sp,
+                                                     uint32_t r, const Mod *__restrict__ mods,
+                                                     const uint64_t *__restrict__ t,
+                                                     const ulonglong2 *__restrict__ pmod) {
+    constexpr int LP = L + 1;
+    constexpr uint32_t half = 1u << (LOGN - 1);
+    const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    const uint32_t p = blockIdx.z;
+    const Mod m = mods[k < L ? k : sp];
+    const int kk = k < L ? k : key_limbs - 1;
+    const uint32_t src = rot_index(n, half, r);
+    const uint64_t *Dp = D + (((size_t)p * L * LP + k) << LOGN) + src;
+    const size_t kstr = (size_t)key_limbs << LOGN;
+    const uint64_t *K0 = key + ((size_t)kk << LOGN) + n;
+    const bool addp = t && k < L;
+    uint64_t t0 = 0, t1 = 0;
+    if (addp) {
+        t0 = __ldg(t + (((size_t)(p * 2 + 0) * L + k) << LOGN) + n);
+        t1 = __ldg(t + (((size_t)(p * 2 + 1) * L + k) << LOGN) + n);
+    }
+    uint64_t d[L], x[L], y[L];
+#pragma unroll
+    for (int j = 0; j < L; j++) {
+        d[j] = __ldg(Dp + ((size_t)j * LP << LOGN));
+        x[j] = __ldg(K0 + (2 * j) * kstr);
+        y[j] = __ldg(K0 + (2 * j + 1) * kstr);
+    }
+    auto dot = [&](auto tag, uint64_t &v0, uint64_t &v1) {
+        decltype(tag) a0, a1;
+        a0.zero();
+        a1.zero();
+#pragma unroll
+        for (int j = 0; j < L; j++) {
+            a0.mac(d[j], x[j]);
+            a1.mac(d[j], y[j]);
+        }
+        v0 = a0.reduce(m);
+        v1 = a1.reduce(m);
+    };
+    uint64_t v0, v1;
+    if ((m.q >> 41) == 0)
+        dot(AccN{}, v0, v1);
+    else
+        dot(Acc{}, v0, v1);
+    if (addp) {
+        const ulonglong2 pk = pmod[k];
+        v0 = addmod(v0, shoup(t0, pk.x, pk.y, m.q), m.q);
+        v1 = addmod(v1, shoup(t1, pk.x, pk.y, m.q), m.q);
+    }
+    u[(((size_t)(p * 2 + 0) * LP + k) << LOGN) + n] = v0;
+    u[(((size_t)(p * 2 + 1) * LP + k) << LOGN) + n] = v1;
+}
+
 // out c0 = rot(in c0) + ks0, c1 = ks1
 __global__ void k_rot_finish(uint64_t *out, const uint64_t *in, const uint64_t *ks, int B, int L, int out_ls,
                              int in_ls, uint32_t r, int logn, const Mod *__restrict__ mods) {
@@ -485,6 +544,29 @@ static void key_inner_impl(const Ctx &c, uint64_t *u, const uint64_t *D, const u
     int L = level + 1;
     int64_t half = c.n / 2;
     uint32_t rr = (uint32_t)(((r % half) + half) % half);
+#ifndef UH_KI_FIXED
+#define UH_KI_FIXED 1
+#endif
+    if (UH_KI_FIXED && c.logn == 15 && L <= 10) {
+        for (int p0 = 0; p0 < n_polys; p0 += 65535) {
+            const int np = std::min(65535, n_polys - p0);
+            dim3 g((unsigned)(c.n / 256), L + 1, np);
+            uint64_t *up = u + (size_t)p0 * 2 * (L + 1) * c.n;
+            const uint64_t *Dp = D + (size_t)p0 * L * (L + 1) * c.n;
+            const uint64_t *tp = t ? t + (size_t)p0 * 2 * L * c.n : nullptr;
+#define UH_KI_CASE(LL)                                                                                          \
+    case LL:                                                                                                    \
+        k_key_inner_l<LL, 15><<<g, 256, 0, s>>>(up, Dp, key, key_limbs, c.sp(), rr, c.d_mods, tp, c.d_pmod); \
+        break;
+            switch (L) {
+                UH_KI_CASE(1) UH_KI_CASE(2) UH_KI_CASE(3) UH_KI_CASE(4) UH_KI_CASE(5)
+                UH_KI_CASE(6) UH_KI_CASE(7) UH_KI_CASE(8) UH_KI_CASE(9) UH_KI_CASE(10)
+            }
+#undef UH_KI_CASE
+            UH_LAUNCH_CHECK();
+        }
+        return;
+    }
     if (c.n >= 256) {
         for (int p0 = 0; p0 < n_polys; p0 += 65535) {
             const int np = std::min(65535, n_polys - p0);
