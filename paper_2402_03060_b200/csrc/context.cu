@@ -217,6 +217,16 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
     c->d_invs = upload(invs);
     c->d_pos = upload(pos);
     c->d_neg = upload(neg);
+    if (n >= 8192 && n <= 65536) {
+        // half-limb forward NTT (ntt_fast.cu, k_fwd_half): output index k and its slot lie in the same half
+        std::vector<uint16_t> hpos(n);
+        for (uint32_t k = 0; k < n; k++) {
+            const uint32_t s = (uint32_t)sob[k];
+            if (s / half != k / half) throw std::logic_error("NTT half-output invariant violated");
+            hpos[s] = (uint16_t)(k % half);
+        }
+        c->d_hpos = upload(hpos);
+    }
     return c;
 }
 
@@ -225,8 +235,9 @@ void ctx_destroy(Ctx *c) {
     cudaSetDevice(c->device);
     for (void *p : {(void *)c->d_pmod, (void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_twf, (void *)c->d_itwf, (void *)c->d_twd, (void *)c->d_itwd, (void *)c->d_twist, (void *)c->d_itwist, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
                     (void *)c->d_ipsi, (void *)c->d_ipsis,
-                    (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_inv2, (void *)c->d_inv2s, (void *)c->d_pos, (void *)c->d_neg})
+                    (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_inv2, (void *)c->d_inv2s, (void *)c->d_pos, (void *)c->d_neg, (void *)c->d_hpos})
         if (p) cudaFree(p);
+    for (auto &e : c->ntt_sel) cudaFree(e.second);
     delete c;
 }
 

@@ -1,6 +1,7 @@
 // Internal host-side interface of the engine (not part of the C-ABI).
 #pragma once
 #include <atomic>
+#include <utility>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -32,6 +33,9 @@ struct Ctx {
     ulonglong2 *d_pmod = nullptr;        // [count] (P mod q_i, Shoup companion)
     int32_t *d_pos = nullptr;            // [n/2] index (5^j mod 2N - 1)/2 : slot j -> odd exponent slot
     int32_t *d_neg = nullptr;            // [n/2] index (2N - 5^j - 1)/2
+    uint16_t *d_hpos = nullptr;          // [n] slot h*n/2 + j -> index inside half h of the bit-reversed NTT output (ntt_fast.cu, k_fwd_half)
+    // per-job-shape limb selections of the forward NTT (FP64 limbs first, then the rest), one period each
+    std::vector<std::pair<uint64_t, int16_t *>> ntt_sel;
     int sp() const { return (int)count - 1; }
 };
 

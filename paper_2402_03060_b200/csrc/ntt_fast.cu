@@ -56,6 +56,12 @@ struct LimbInfo {
     Mod mt;               // the top modulus
 };
 
+__device__ __forceinline__ int job_limb(const NttJob &J, int i) {
+    if (!J.sel) return i;
+    const int p = i / J.sel_cnt;
+    return p * J.sel_T + (int)__ldg(J.sel + (i - p * J.sel_cnt));
+}
+
 __device__ __forceinline__ LimbInfo limb_info(const NttJob &J, int f, int logn, const Mod *__restrict__ mods) {
     LimbInfo li;
     li.mode = J.mode;
@@ -355,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p1(NttJob J, uint
                                                     const ulonglong2 *__restrict__ twd,
                                                     const double2 *__restrict__ twf) {
     __shared__ uint64_t sm[P1<A>::N1 * 32];
-    const int f = J.f0 + blockIdx.y, lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int f = job_limb(J, J.f0 + blockIdx.y), lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const int n2 = 1 << (logn - A);
     const int col = blockIdx.x * 32 + lane;
     const LimbInfo li = limb_info(J, f, logn, mods);
@@ -417,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pb(NttJob J, cons
                                                     const ulonglong2 *__restrict__ itwd,
                                                     const double2 *__restrict__ itwf) {
     __shared__ uint64_t sm[P1<A>::N1 * 32];
-    const int f = J.f0 + blockIdx.y, lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int f = job_limb(J, J.f0 + blockIdx.y), lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
     const int n2 = 1 << (logn - A);
     const int col = blockIdx.x * 32 + lane;
     const LimbInfo li = limb_info(J, f, logn, mods);
@@ -603,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p2(NttJob J, cons
     extern __shared__ uint64_t dsm[];
     uint64_t *sm = dsm;
     double *tws = reinterpret_cast<double *>(dsm + C::G * C::PAD);
-    const int f = J.f0 + blockIdx.y, tid = threadIdx.x;
+    const int f = job_limb(J, J.f0 + blockIdx.y), tid = threadIdx.x;
     const int n1 = 1 << (logn - B);
     const int *sel = bsel + blockIdx.x * C::G;
     const LimbInfo li = limb_info(J, f, logn, mods);
@@ -714,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_fused(NttJob J, i
     uint64_t *tile = dsm;                                   // [N1][32]
     uint64_t *sm2 = dsm + P1<A>::N1 * 32;                   // [G][PAD]
     const uint32_t rank = cluster_rank();
-    const int f = J.f0 + blockIdx.y, tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    const int f = job_limb(J, J.f0 + blockIdx.y), tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
     const int n2 = 1 << (logn - A), n1 = 1 << (logn - B);
     const LimbInfo li = limb_info(J, f, logn, mods);
     const Mod m = mods[li.mod];
@@ -836,7 +842,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint
     extern __shared__ uint64_t dsm[];
     uint64_t *sm = dsm;
     double *tws = reinterpret_cast<double *>(dsm + C::G * C::PAD);
-    const int f = J.f0 + blockIdx.y, tid = threadIdx.x;
+    const int f = job_limb(J, J.f0 + blockIdx.y), tid = threadIdx.x;
     const int n1 = 1 << (logn - B);
     const int *sel = bsel + blockIdx.x * C::G;
     const LimbInfo li = limb_info(J, f, logn, mods);
@@ -939,8 +945,348 @@ inline bool fused_ntt_on() {
     return on;
 }
 
+// ---------------- persistent cluster-pair forward NTT (N = 2^15, FP64 limbs, one HBM pass) ----------------
+// A 2-CTA cluster (one CTA per SM, 512 threads, 224 KB shared memory) walks a strided list of
+// limbs.  CTA h owns output half h (slots [h N/2, (h+1) N/2): output index k and its slot lie
+// in the same half, context.cu checks it) and stages the raw input half h with TMA bulk copies
+// (cp.async.bulk + mbarrier) -- the next limb's copy is in flight while this limb's last 10
+// stages run, so the load latency is off the critical path.
+//   phase B : CTA h takes columns [512 h, 512 h + 512) of the 2^15 = 32 x 1024 view; it reads
+//             x[e] (half 0) and x[e + N/2] (half 1) from the two CTAs' staging buffers (one of
+//             them over DSMEM), forms the first CT stage for both halves, runs local stages
+//             0..3 of each half (radix 16) and writes half 0's values into CTA 0's and half 1's
+//             into CTA 1's shared data area (again one of them over DSMEM);
+//   rounds 2, 3 : local stages 4..8 and 9..13 (radix 32) in this CTA's data area;
+//   output  : canonical residues gathered in slot order, coalesced stores (+ the DIVIDE epilogue).
+// The data area keeps 48-bit two's-complement integers (lo32 + hi16; FP64 values stay below
+// 9q < 2^44, no reduction between rounds) under an XOR swizzle e ^ ((e >> 5) & 31), which
+// makes all three access patterns bank-conflict free without padding.
+constexpr int kPT = 512;
+constexpr int kPH = 1 << 14;
+constexpr size_t kPStage = (size_t)kPH * 8, kPLo = (size_t)kPH * 4, kPHi = (size_t)kPH * 2;
+constexpr size_t kPSmem = kPStage + kPLo + kPHi + 16;
+__device__ __forceinline__ int psw(int e) { return e ^ ((e >> 5) & 31); }
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t cl_map(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t ld_cl64(uint32_t a) {
+    uint64_t v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+// store one FP64 value (|v| < 2^47, integer) as lo32 + hi16 at swizzled element e of a data area
+__device__ __forceinline__ void pput(uint32_t lo_a, uint32_t hi_a, bool remote, int e, double v) {
+    const long long b = __double_as_longlong(v + kMagic);
+    const int se = psw(e);
+    const uint32_t l = (uint32_t)b;
+    const uint16_t hh = (uint16_t)(b >> 32);
+    if (remote) {
+        asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(lo_a + 4 * se), "r"(l));
+        asm volatile("st.shared::cluster.u16 [%0], %1;" ::"r"(hi_a + 2 * se), "h"(hh));
+    } else {
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(lo_a + 4 * se), "r"(l));
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(hi_a + 2 * se), "h"(hh));
+    }
+}
+__device__ __forceinline__ double pget(const uint32_t *lo, const uint16_t *hi, int e) {
+    const int se = psw(e);
+    const long long b = ((long long)(int16_t)hi[se] << 32) | (long long)lo[se];
+    return __longlong_as_double(b + 0x4338000000000000LL) - kMagic;
+}
+__device__ __forceinline__ void pputl(uint32_t *lo, uint16_t *hi, int e, double v) {
+    const long long b = __double_as_longlong(v + kMagic);
+    const int se = psw(e);
+    lo[se] = (uint32_t)b;
+    hi[se] = (uint16_t)(b >> 32);
+}
+// load transform on a staged word: 0 plain, 1 centred lift (as load_t)
+template <int LM>
+__device__ __forceinline__ uint64_t xform(uint64_t x, uint64_t p, const Mod &m, bool red) {
+    if (LM == 0) return x;
+    const bool neg = x > ((p - 1) >> 1);
+    uint64_t v = neg ? p - x : x;
+    if (red) v = csub(barrett_lite(v, m), m.q);
+    const uint64_t nv = v ? m.q - v : 0;
+    return neg ? nv : v;
+}
+
+template <int LM, int EM>
+__global__ void __launch_bounds__(kPT, 1) k_fwd_pair(NttJob J, const Mod *__restrict__ mods,
+                                                     const double *__restrict__ twdd,
+                                                     const uint16_t *__restrict__ hpos, int nl) {
+    constexpr int LOGN = 15;
+    extern __shared__ __align__(128) unsigned char psm[];
+    uint64_t *stg = reinterpret_cast<uint64_t *>(psm);
+    uint32_t *lo = reinterpret_cast<uint32_t *>(psm + kPStage);
+    uint16_t *hi = reinterpret_cast<uint16_t *>(psm + kPStage + kPLo);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(psm + kPStage + kPLo + kPHi);
+    const int h = blockIdx.x, tid = threadIdx.x;
+    const uint32_t stg_l = su32(stg), lo_l = su32(lo), hi_l = su32(hi), bar_l = su32(bar);
+    const uint32_t stg_r = cl_map(stg_l, h ^ 1), lo_r = cl_map(lo_l, h ^ 1), hi_r = cl_map(hi_l, h ^ 1);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(bar_l));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int i) {  // thread 0: TMA bulk copy of raw input half h of launch limb i
+        const LimbInfo li = limb_info(J, job_limb(J, J.f0 + i), LOGN, mods);
+        const uint64_t *src = li.src + (size_t)h * kPH;
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar_l), "r"((uint32_t)kPStage)
+                     : "memory");
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 32768, [%2];" ::"r"(
+                    stg_l + 32768u * k),
+                "l"(src + 4096 * k), "r"(bar_l)
+                : "memory");
+    };
+    const int ncl = gridDim.y;
+    uint32_t parity = 0;
+    if (tid == 0 && (int)blockIdx.y < nl) issue(blockIdx.y);
+#pragma unroll 1
+    for (int i = blockIdx.y; i < nl; i += ncl) {
+        const LimbInfo li = limb_info(J, job_limb(J, J.f0 + i), LOGN, mods);
+        const Mod m = mods[li.mod];
+        const bool red = LM == 1 && ((li.qsrc - 1) >> 1) >= m.q;
+        const double q = (double)m.q, qinv = 1.0 / q;
+        const double *T = twdd + ((size_t)li.mod << LOGN);
+        {  // wait for this CTA's staging, then for the partner's (and for its previous output phase)
+            uint32_t ok = 0;
+            while (!ok)
+                asm volatile(
+                    "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                    : "=r"(ok)
+                    : "r"(bar_l), "r"(parity)
+                    : "memory");
+            parity ^= 1;
+        }
+        cl_sync();
+        // ---- phase B: first stage (both halves) + local stages 0..3 of each half on column c ----
+        {
+            const int c = 512 * h + tid;
+            const double w1 = __ldg(T + 1);
+            const double2 W1 = make_double2(w1, w1 * qinv);
+            // half 0 input lives in CTA 0's staging, half 1 in CTA 1's
+            double v0[16], v1[16];
+#pragma unroll
+            for (int t0 = 0; t0 < 16; t0 += 8) {
+                uint64_t r0[8], r1[8];
+#pragma unroll
+                for (int t = 0; t < 8; t++) {
+                    const int e = (t0 + t) * 1024 + c;
+                    const uint64_t mine = stg[e], other = ld_cl64(stg_r + 8u * e);
+                    r0[t] = h == 0 ? mine : other;
+                    r1[t] = h == 0 ? other : mine;
+                }
+#pragma unroll
+                for (int t = 0; t < 8; t++) {
+                    const double x = u2d(xform<LM>(r0[t], li.qsrc, m, red));
+                    const double y = fmm(u2d(xform<LM>(r1[t], li.qsrc, m, red)), W1, q);
+                    v0[t0 + t] = x + y;
+                    v1[t0 + t] = x - y;
+                }
+            }
+            fwd_strided<16>(v0, TwGd{T, 2, qinv}, 1, 0, q);
+#pragma unroll
+            for (int t = 0; t < 16; t++) pput(h == 0 ? lo_l : lo_r, h == 0 ? hi_l : hi_r, h != 0, t * 1024 + c, v0[t]);
+            fwd_strided<16>(v1, TwGd{T, 3, qinv}, 1, 0, q);
+#pragma unroll
+            for (int t = 0; t < 16; t++) pput(h == 1 ? lo_l : lo_r, h == 1 ? hi_l : hi_r, h != 1, t * 1024 + c, v1[t]);
+        }
+        cl_sync();  // both data areas complete; both staging buffers consumed
+        if (tid == 0 && i + ncl < nl) issue(i + ncl);
+        const TwGd ta{T, 2 + h, qinv};
+        {  // ---- round 2: local stages 4..8 on (t, c0) = (tid / 32, tid % 32) ----
+            const int t = tid >> 5, c0 = tid & 31;
+            double v[32];
+#pragma unroll
+            for (int u = 0; u < 32; u++) v[u] = pget(lo, hi, t * 1024 + u * 32 + c0);
+            fwd_strided<32>(v, ta, 16, t, q);
+#pragma unroll
+            for (int u = 0; u < 32; u++) pputl(lo, hi, t * 1024 + u * 32 + c0, v[u]);
+        }
+        __syncthreads();
+        {  // ---- round 3: local stages 9..13 on 32 contiguous elements; canonical residues ----
+            const int grp = tid;
+            double v[32];
+#pragma unroll
+            for (int z = 0; z < 32; z++) v[z] = pget(lo, hi, grp * 32 + z);
+            fwd_strided<32>(v, ta, 512, grp, q);
+#pragma unroll
+            for (int z = 0; z < 32; z++) {
+                const uint64_t r = d2u_canon(v[z], q, qinv);
+                const int se = psw(grp * 32 + z);
+                lo[se] = (uint32_t)r;
+                hi[se] = (uint16_t)(r >> 32);
+            }
+        }
+        __syncthreads();
+        {  // ---- output: slots h N/2 + j in order (coalesced), gathered from the bit-reversed half ----
+            const size_t sbase = (size_t)h << (LOGN - 1);
+            const uint16_t *hp = hpos + sbase;
+            const uint64_t qq = m.q;
+#pragma unroll 1
+            for (int i0 = 0; i0 < kPH / kPT; i0 += 16) {
+                int e[16];
+                uint64_t a[16];
+#pragma unroll
+                for (int k = 0; k < 16; k++) {
+                    const int j = tid + kPT * (i0 + k);
+                    e[k] = __ldg(hp + j);
+                    if (EM != 0) a[k] = li.in[sbase + j];
+                }
+#pragma unroll
+                for (int k = 0; k < 16; k++) {
+                    const int j = tid + kPT * (i0 + k);
+                    const int se = psw(e[k]);
+                    const uint64_t y = (uint64_t)lo[se] | ((uint64_t)hi[se] << 32);
+                    uint64_t r;
+                    if (EM == 1)
+                        r = csub(shoup_lazy(submod(a[k], y, qq), li.w, li.ws, qq), qq);
+                    else
+                        r = y;
+                    li.dst[sbase + j] = r;
+                }
+            }
+        }
+        // the next iteration's cluster barrier orders this output phase before the partner's
+        // phase-B writes into this data area
+    }
+}
+
+template <int LM, int EM>
+void launch_pair(const Ctx &c, const NttJob &J, int nl, cudaStream_t s) {
+    static bool done = false;
+    if (!done) {
+        UH_CHECK(cudaFuncSetAttribute(k_fwd_pair<LM, EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPSmem));
+        done = true;
+    }
+    static int sms = 0;
+    if (!sms) UH_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    const int ncl = std::max(1, std::min(nl, sms / 2));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2, ncl, 1);
+    cfg.blockDim = dim3(kPT, 1, 1);
+    cfg.dynamicSmemBytes = kPSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    UH_CHECK(cudaLaunchKernelEx(&cfg, k_fwd_pair<LM, EM>, J, (const Mod *)c.d_mods, (const double *)c.d_twd,
+                                (const uint16_t *)c.d_hpos, nl));
+    UH_LAUNCH_CHECK();
+}
+
+// Opt-in (UH_NTT_PAIR=1): measured slower than the two passes on B200 (forward, 512 limbs at
+// N = 2^15: 0.48 vs 0.31 us per limb; ModUp 0.39 vs 0.30).  ncu: FP64 pipe 31% active, issue
+// 30%, stalls on DSMEM / round-3 twiddle (L2) latency with 16 warps per SM and 128-register
+// threads; the two-pass grids keep 32 warps per SM with 16-value register tiles.  An earlier
+// non-persistent variant (two 99 KB CTAs per SM, each loading both input halves) measured
+// 0.40 us per limb.  Both are bit-exact (tests/test_gpu_primitives.py runs the NTT parity
+// cases with UH_NTT_PAIR=1 in a subprocess).
+inline bool pair_ntt_on() {
+    static const bool on = [] {
+        const char *e = getenv("UH_NTT_PAIR");
+        return e && std::string(e) == "1";
+    }();
+    return on;
+}
+
+// Limb selection of a forward job: FP64 limbs (half-limb kernel) and the rest (two-pass),
+// one period of the job's limb pattern each, cached per job shape in the context.
+struct LimbSplit {
+    const int16_t *d = nullptr;  // [nfp offsets][nint offsets]
+    int T = 0, nfp = 0, nint = 0;
+};
+inline LimbSplit limb_split(const Ctx &c, const NttJob &J) {
+    LimbSplit r;
+    std::vector<int> mod_of;
+    if (J.mode == NTT_MODUP) {
+        r.T = J.L * J.L;
+        for (int j = 0; j < J.L; j++)
+            for (int kk = 0; kk < J.L; kk++) {
+                const int k = kk + (kk >= j);
+                mod_of.push_back(k < J.L ? k : J.sp);
+            }
+    } else if (J.mode == NTT_PLAIN) {
+        r.T = J.nl;
+        for (int k = 0; k < J.nl; k++) mod_of.push_back(k < J.nq ? J.base + k : J.sp);
+    } else {
+        r.T = J.nl;
+        for (int k = 0; k < J.nl; k++) mod_of.push_back(k);
+    }
+    if (r.T <= 0 || r.T > 4096) return LimbSplit{};
+    std::vector<int16_t> fp, in;
+    for (int o = 0; o < r.T; o++) ((c.h_q[mod_of[o]] >> 42) == 0 ? fp : in).push_back((int16_t)o);
+    r.nfp = (int)fp.size();
+    r.nint = (int)in.size();
+    const uint64_t key = ((uint64_t)J.mode << 56) ^ ((uint64_t)J.L << 48) ^ ((uint64_t)J.nl << 32) ^
+                         ((uint64_t)J.nq << 16) ^ ((uint64_t)J.base << 8) ^ (uint64_t)J.sp;
+    auto &cache = const_cast<Ctx &>(c).ntt_sel;
+    for (auto &e : cache)
+        if (e.first == key) {
+            r.d = e.second;
+            return r;
+        }
+    std::vector<int16_t> all(fp);
+    all.insert(all.end(), in.begin(), in.end());
+    int16_t *d = nullptr;
+    UH_CHECK(cudaMalloc(&d, all.size() * sizeof(int16_t)));
+    UH_CHECK(cudaMemcpy(d, all.data(), all.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
+    cache.emplace_back(key, d);
+    r.d = d;
+    return r;
+}
+
+template <int A, int B>
+void run_fwd_two_pass(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s);
+
 template <int A, int B>
 void run_fwd(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
+    if (c.logn == 15 && c.d_hpos && pair_ntt_on() && !fused_ntt_on() && J0.mode != NTT_DIVIDE2) {
+        const LimbSplit sp = limb_split(c, J0);
+        if (sp.T > 0 && limbs % sp.T == 0) {
+            const int periods = limbs / sp.T;
+            if (sp.nfp) {
+                NttJob J = J0;
+                J.sel = sp.d;
+                J.sel_T = sp.T;
+                J.sel_cnt = sp.nfp;
+                const int n = periods * sp.nfp;
+                for (int f0 = 0; f0 < n; f0 += 65535) {
+                    J.f0 = f0;
+                    const int nl = std::min(65535, n - f0);
+                    if (J.mode == NTT_PLAIN) launch_pair<0, 0>(c, J, nl, s);
+                    else if (J.mode == NTT_DIVIDE) launch_pair<1, 1>(c, J, nl, s);
+                    else launch_pair<1, 0>(c, J, nl, s);
+                }
+            }
+            if (sp.nint) {
+                NttJob J = J0;
+                J.sel = sp.d + sp.nfp;
+                J.sel_T = sp.T;
+                J.sel_cnt = sp.nint;
+                run_fwd_two_pass<A, B>(c, J, periods * sp.nint, s);
+            }
+            return;
+        }
+    }
+    run_fwd_two_pass<A, B>(c, J0, limbs, s);
+}
+
+template <int A, int B>
+void run_fwd_two_pass(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
     if constexpr ((1 << B) / 32 == (1 << A) / P2<B>::G) {
         if (fused_ntt_on()) {
             for (int f0 = 0; f0 < limbs; f0 += 65535) {

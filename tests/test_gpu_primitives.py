@@ -266,3 +266,20 @@ def test_divide_top2_is_centred_division_by_q_level_times_p(params, level):
                 else:  # small-N fallback divides by P then q_level: within one unit
                     diff = (int(gotc[r, k, i]) - want) % qs[k]
                     assert diff in (0, 1, qs[k] - 1)
+
+
+def test_opt_in_pair_ntt_bit_exact():
+    """The opt-in persistent cluster-pair forward NTT (UH_NTT_PAIR=1, ntt_fast.cu k_fwd_pair:
+    TMA-staged halves, DSMEM first stage) gives the same residues as the oracle: NTT, ModUp /
+    key inner product / ModDown, rotation and rescale parity cases re-run in a subprocess
+    (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, UH_NTT_PAIR="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.abspath(__file__),
+                        "-k", "ntt_roundtrip or modup_keyinner or rotate_bit_exact or rescale_and_mul_plain"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
