@@ -47,6 +47,10 @@ def main():
         ms = timeit(lambda: _lib.call("uh_ntt", be._ctx, vp(x), polys, nl, nl, nl, inv, st))
         print(f"{'inverse' if inv else 'forward'} NTT: {limbs} limbs {ms:.3f} ms -> {1e3 * ms / limbs:.3f} us/limb, "
               f"{limbs * n * 16 / (ms * 1e-3) / 1e9:.0f} GB/s (r+w)")
+    # 60-bit limbs only (q_0: nl = nq = 1) vs the mixed 8-limb case above (1 x 60-bit + 7 x 40-bit)
+    x1 = torch.randint(0, 1 << 39, (limbs, 1, n), dtype=torch.int64, device="cuda")
+    ms = timeit(lambda: _lib.call("uh_ntt", be._ctx, vp(x1), limbs, 1, 1, 1, 0, st))
+    print(f"forward NTT, 60-bit q_0 limbs only: {limbs} limbs -> {1e3 * ms / limbs:.3f} us/limb")
     lev = 5
     L = lev + 1
     d = torch.randint(0, 1 << 39, (polys, L, n), dtype=torch.int64, device="cuda")
