@@ -37,7 +37,7 @@ constexpr int kBankMaxTerms = 512;
 #define UH_BANK_MINB 3  // resident CTAs per SM requested from ptxas (3: 96 registers, no spills; measured 51.9 vs 52.8 ms at 4)
 #endif
 #ifndef UH_BANK_DIRECT_MINB
-#define UH_BANK_DIRECT_MINB 3
+#define UH_BANK_DIRECT_MINB 4  // narrow layers (<= 2 outputs): 64 registers, no spills (flatten 22.2 vs 22.7 ms, pools -0.2 ms at B = 64)
 #endif
 #ifndef UH_BANK_DIRECT_G
 #define UH_BANK_DIRECT_G 2
@@ -245,8 +245,8 @@ __global__ void __launch_bounds__(W * 32, UH_BANK_MINB)
 // once into the per-term offset tables.  Warp w of the CTA serves ciphertext
 // 8 * blockIdx.x + w (ciphertext groups fastest in the grid: CTAs sharing the
 // same key and mask rows run together).
-template <int L, int LOGN, int OM, bool MASKS, int G>
-__global__ void __launch_bounds__(256, UH_BANK_DIRECT_MINB)
+template <int L, int LOGN, int OM, bool MASKS, int G, int MINB>
+__global__ void __launch_bounds__(256, MINB)
     k_direct_bank(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, const uint64_t *__restrict__ D,
                   const uint64_t *__restrict__ masks, const uint64_t *__restrict__ kbank,
                   const int32_t *__restrict__ shifts, int B, int I, int T, int O, int diag, int sp,
@@ -393,8 +393,13 @@ void launch_direct_bank(const Ctx &c, uint64_t *acc, const uint64_t *X, const ui
                         const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, int diag,
                         cudaStream_t s) {
     dim3 grid((unsigned)((B + 7) / 8), (unsigned)(c.n / 32), L + 1);
-    k_direct_bank<L, 15, OM, MASKS, UH_BANK_DIRECT_G><<<grid, 256, 0, s>>>(acc, X, D, masks, kbank, shifts, B, I, T,
-                                                                          O, diag, c.sp(), c.d_mods);
+    // 4-output layers (LeNet conv1): all of a term's digit / key loads in flight at 2 CTAs per SM
+    // (measured 13.5 vs 15.5 ms for conv1 at B = 64 with 3 CTAs and groups of 2); narrower
+    // layers are unchanged by either knob
+    constexpr int G = OM >= 4 ? 8 : UH_BANK_DIRECT_G;
+    constexpr int MINB = OM >= 4 ? 2 : UH_BANK_DIRECT_MINB;
+    k_direct_bank<L, 15, OM, MASKS, G, MINB><<<grid, 256, 0, s>>>(acc, X, D, masks, kbank, shifts, B, I, T, O, diag,
+                                                                  c.sp(), c.d_mods);
     UH_LAUNCH_CHECK();
 }
 
