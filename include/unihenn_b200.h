@@ -67,6 +67,12 @@ int uh_ntt(uh_ctx *ctx, uint64_t *data, int n_polys, int nl, int nq, int pstride
 int uh_elementwise(uh_ctx *ctx, int op, uint64_t *out, const uint64_t *a, const uint64_t *b, int n_polys,
                    int b_polys, int nl, int nq, int out_ps, int a_ps, int b_ps, void *stream);
 
+/* uh_elementwise with grouped broadcast: b poly index = (p / group) % b_polys
+ * (e.g. one bias plaintext per output channel over its B ciphertexts, one launch
+ * for all channels: layers.conv's bias add, layers.py:193-195). */
+int uh_elementwise_grouped(uh_ctx *ctx, int op, uint64_t *out, const uint64_t *a, const uint64_t *b, int n_polys,
+                           int b_polys, int group, int nl, int nq, int out_ps, int a_ps, int b_ps, void *stream);
+
 /* Divide by the modulus of the top limb with centred rounding (rescale when
  * top_mod = nl, ModDown when top_mod = P): in n_polys x (nl+1) -> out n_polys x nl. */
 int uh_divide_top(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int n_polys, int nl, int top_mod, int out_ps,

@@ -25,6 +25,8 @@ SIGNATURES = {
     "uh_ctx_destroy": [_vp],
     "uh_ntt": [_vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_elementwise": [_vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
+    "uh_elementwise_grouped": [_vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
+                               _c_int, _vp],
     "uh_divide_top": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_rescale": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_divide_top2": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp],

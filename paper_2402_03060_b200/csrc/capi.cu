@@ -103,6 +103,19 @@ __attribute__((visibility("default"))) int uh_elementwise(uh_ctx *ctx, int op, u
     });
 }
 
+__attribute__((visibility("default"))) int uh_elementwise_grouped(uh_ctx *ctx, int op, uint64_t *out, const uint64_t *a,
+                                                                  const uint64_t *b, int n_polys, int b_polys,
+                                                                  int group, int nl, int nq, int out_ps, int a_ps,
+                                                                  int b_ps, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        need(op >= 0 && op <= 5, "bad op");
+        need(b_polys >= 1 && group >= 1, "bad broadcast");
+        need(nq >= 0 && nq <= nl && nl - nq <= 1 && nq <= (int)c.count - 1, "bad basis");
+        uh::elementwise_grouped(c, op, out, a, b, n_polys, b_polys, group, nl, nq, out_ps, a_ps, b_ps, S(stream));
+    });
+}
+
 __attribute__((visibility("default"))) int uh_divide_top(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int n_polys,
                                                          int nl, int top_mod, int out_ps, int in_ps, void *stream) {
     return guard([&] {

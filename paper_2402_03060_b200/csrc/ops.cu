@@ -380,6 +380,15 @@ void elementwise(const Ctx &c, int op, uint64_t *out, const uint64_t *a, const u
     UH_LAUNCH_CHECK();
 }
 
+void elementwise_grouped(const Ctx &c, int op, uint64_t *out, const uint64_t *a, const uint64_t *b, int n_polys,
+                         int b_polys, int group, int nl, int nq, int out_ps, int a_ps, int b_ps, cudaStream_t s) {
+    size_t total = ((size_t)n_polys * nl) << c.logn;
+    if (!total) return;
+    k_elementwise<<<grid_for(total), kTB, 0, s>>>(op, out, a, b, n_polys, b_polys, group, nl, nq, c.sp(), out_ps, a_ps,
+                                                 b_ps, (int)c.logn, c.d_mods);
+    UH_LAUNCH_CHECK();
+}
+
 void divide_top(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, int nl, int top_mod, int out_ps,
                 int in_ps, cudaStream_t s) {
     if (!n_polys) return;

@@ -19,6 +19,8 @@ enum BinOp : int { OP_ADD = 0, OP_SUB = 1, OP_MUL = 2, OP_MAC = 3, OP_NEG = 4, O
 // out[p] = op(a[p], b[p % b_polys]) over nl limbs, moduli 0..nq-1 (+P).
 void elementwise(const Ctx &c, int op, uint64_t *out, const uint64_t *a, const uint64_t *b, int n_polys,
                  int b_polys, int nl, int nq, int out_ps, int a_ps, int b_ps, cudaStream_t s);
+void elementwise_grouped(const Ctx &c, int op, uint64_t *out, const uint64_t *a, const uint64_t *b, int n_polys,
+                         int b_polys, int group, int nl, int nq, int out_ps, int a_ps, int b_ps, cudaStream_t s);
 
 // Divide by the top limb's modulus with centred rounding:
 // in: n_polys x (nl + 1) limbs, limb nl has modulus `top_mod`, limbs 0..nl-1

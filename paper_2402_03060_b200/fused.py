@@ -216,10 +216,9 @@ def conv(backend, state: CipherState, layer) -> CipherState:
     del acc
     bias = bias_bank(backend, layer, out_lay, level - 1, scale)
     Lo = level
-    for o in range(O):
-        co = out[o]
-        backend._call("uh_elementwise", OP_ADD, _vp(co), _vp(co), _vp(bias[o]), B, 1, Lo, Lo, 2 * Lo, 2 * Lo, Lo,
-                      st)
+    # bias of output channel o onto c0 of its B ciphertexts, all channels in one launch
+    backend._call("uh_elementwise_grouped", OP_ADD, _vp(out), _vp(out), _vp(bias), O * B, O, B, Lo, Lo, 2 * Lo,
+                  2 * Lo, Lo, st)
     del keys
     return CipherState([CipherVector(out[o], level - 1, scale, backend) for o in range(O)], out_lay)
 
