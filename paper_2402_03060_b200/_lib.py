@@ -53,10 +53,14 @@ SIGNATURES = {
                        _vp],
     "uh_hoisted_mac_bank": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                             _vp],
+    "uh_imma_mask_bank": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp],
+    "uh_hoisted_mac_imma": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int,
+                            _vp],
 }
 EXTRA = {"uh_abi_version": ([], _c_int), "uh_last_error": ([], ctypes.c_char_p),
          "uh_launch_count": ([], ctypes.c_ulonglong), "uh_bench_peaks": ([_vp, _vp], _c_int),
-         "uh_hoisted_bank_supported": ([_vp, _c_int, _c_int], _c_int)}
+         "uh_hoisted_bank_supported": ([_vp, _c_int, _c_int], _c_int),
+         "uh_imma_supported": ([_vp, _c_int, _c_int, _c_int], _c_int)}
 
 
 def launch_count() -> int:

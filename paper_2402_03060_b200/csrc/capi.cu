@@ -350,6 +350,34 @@ __attribute__((visibility("default"))) int uh_hoisted_mac_bank(uh_ctx *ctx, uint
     });
 }
 
+__attribute__((visibility("default"))) int uh_imma_supported(uh_ctx *ctx, int level, int O, int Q) {
+    return ctx && uh::hoisted_imma_supported(C(ctx), level, O, Q) ? 1 : 0;
+}
+
+__attribute__((visibility("default"))) int uh_imma_mask_bank(uh_ctx *ctx, uint32_t *ib, const uint64_t *masks, int O,
+                                                             int Q, int level, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(uh::hoisted_imma_supported(c, level, O, Q), "IMMA mask bank: unsupported shape");
+        uh::imma_mask_bank(c, ib, masks, O, Q, level, S(stream));
+    });
+}
+
+__attribute__((visibility("default"))) int uh_hoisted_mac_imma(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls,
+                                                               const uint64_t *D, const uint64_t *masks,
+                                                               const uint32_t *ib, const uint64_t *kbank,
+                                                               const int32_t *shifts, int B, int I, int T, int O,
+                                                               int level, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(B > 0 && I > 0 && T > 0 && O > 0 && xls == level + 1, "bad shape (xls must equal level + 1)");
+        need(kbank != nullptr && ib != nullptr && masks != nullptr, "key bank, IMMA mask bank and masks are required");
+        uh::hoisted_mac_imma(c, acc, X, D, masks, ib, kbank, shifts, B, I, T, O, level, S(stream));
+    });
+}
+
 __attribute__((visibility("default"))) int uh_decode_coeffs(uh_ctx *ctx, double *slots, const double *coef,
                                                             int n_polys, double scale, void *stream) {
     return guard([&] { uh::decode_coeffs(C(ctx), slots, coef, n_polys, scale, S(stream)); });

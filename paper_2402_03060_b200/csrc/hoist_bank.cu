@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(W * 32, UH_BANK_MINB)
     k_hoisted_bank(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, const uint64_t *__restrict__ D,
                    const uint64_t *__restrict__ masks, const uint64_t *__restrict__ kbank,
                    const int32_t *__restrict__ shifts, int B, int I, int T, int O, int sp,
-                   const Mod *__restrict__ mods) {
+                   const Mod *__restrict__ mods, int wide_only) {
     constexpr int LP = L + 1;
     constexpr uint32_t N = 1u << LOGN, half = N >> 1;
     constexpr uint32_t ROW = (uint32_t)LP << LOGN;  // one limb block: digit / mask term / key stride
@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(W * 32, UH_BANK_MINB)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b0 = blockIdx.x * TB;
     const uint32_t n = blockIdx.y * 32 + lane;
-    const int k = blockIdx.z;
+    // wide_only: just the 60-bit limbs q_0 and P (the 40-bit ones run on hoist_imma.cu)
+    const int k = wide_only ? (blockIdx.z ? L : 0) : (int)blockIdx.z;
     const Mod m = mods[k < L ? k : sp];
     const bool qlimb = k < L;
     const uint64_t P = mods[sp].q;
@@ -422,15 +423,34 @@ void direct_bank_L(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_
 
 template <int L>
 void launch_bank(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
-                 const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
+                 const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s,
+                 int wide_only = 0) {
     constexpr int W = 6, TB = 2;
-    dim3 grid((unsigned)((B + TB - 1) / TB), (unsigned)(c.n / 32), L + 1);
+    dim3 grid((unsigned)((B + TB - 1) / TB), (unsigned)(c.n / 32), wide_only ? 2 : L + 1);
     k_hoisted_bank<L, 15, W, TB, UH_BANK_G><<<grid, W * 32, 0, s>>>(acc, X, D, masks, kbank, shifts, B, I, T, O, c.sp(),
-                                                          c.d_mods);
+                                                          c.d_mods, wide_only);
     UH_LAUNCH_CHECK();
 }
 
 }  // namespace
+
+// the tiled kernel over the 60-bit limbs (q_0, P) only -- hoist_imma.cu covers the rest
+void hoisted_mac_bank_wide(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
+                           const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, int level,
+                           cudaStream_t s) {
+    switch (level + 1) {
+        case 2: launch_bank<2>(c, acc, X, D, masks, kbank, shifts, B, I, T, O, s, 1); break;
+        case 3: launch_bank<3>(c, acc, X, D, masks, kbank, shifts, B, I, T, O, s, 1); break;
+        case 4: launch_bank<4>(c, acc, X, D, masks, kbank, shifts, B, I, T, O, s, 1); break;
+        case 5: launch_bank<5>(c, acc, X, D, masks, kbank, shifts, B, I, T, O, s, 1); break;
+        case 6: launch_bank<6>(c, acc, X, D, masks, kbank, shifts, B, I, T, O, s, 1); break;
+        case 7: launch_bank<7>(c, acc, X, D, masks, kbank, shifts, B, I, T, O, s, 1); break;
+        case 8: launch_bank<8>(c, acc, X, D, masks, kbank, shifts, B, I, T, O, s, 1); break;
+        case 9: launch_bank<9>(c, acc, X, D, masks, kbank, shifts, B, I, T, O, s, 1); break;
+        case 10: launch_bank<10>(c, acc, X, D, masks, kbank, shifts, B, I, T, O, s, 1); break;
+        default: throw std::invalid_argument("wide-limb hoisted kernel: 2 <= level + 1 <= 10");
+    }
+}
 
 bool hoisted_bank_supported(const Ctx &c, int level, int O) {
     return c.logn == 15 && level >= 0 && level + 1 <= 10 && O >= 1 && O <= 12;

@@ -1,0 +1,314 @@
+// Hoisted rotation-MAC with the weight-mask contraction on the tensor cores
+// (mma.sync m16n8k32 u8 -> IMMA.16832 on sm_100a).  Same result as
+// hoist_bank.cu's k_hoisted_bank, residue for residue:
+//
+//   acc[o][b] (QP basis) = sum over terms q = (i, t) of  M[o][q] (.) P * rot_{s_t}(ct_i[b])
+//
+// For a fixed coefficient n of a fixed limb k, phase B is a small integer GEMM
+//   acc[o][j] = sum_q M[o][q][n] * V[q][j][n]      (j = ciphertext x component)
+// whose A operand (the masks at n) is shared by every ciphertext.  Both factors
+// are residues below q_k < 2^40 (the 40-bit limbs of the chain), so they split
+// exactly into 5 bytes each, and
+//   acc = sum_{a,b < 5} 2^(8(a+b)) * sum_q M_a[o][q] V_b[q][j]
+// where each inner sum is a u8 x u8 dot product of length <= 128 (< 2^23 in
+// s32: exact).  Rows of the MMA are (output, mask byte a), columns (value byte
+// b, ciphertext, component); one m16n8k32 covers 3 outputs x 5 mask bytes by
+// 8 columns by 32 terms.  The epilogue recombines the 25 byte products of each
+// (output, column) in 128-bit integers and reduces mod q_k -- canonical, so the
+// output is bit-identical to the IMAD kernel's.
+//
+// CTA tile: 8 coefficients x 4 ciphertexts x one 40-bit limb, 256 threads.
+//   phase A : every (term, ciphertext, coefficient) item key-switches its term
+//             (hoisted digits x Galois-key bank, + P c0, as hoist_bank.cu) and
+//             writes the byte planes of the two results into shared memory, in
+//             the B-fragment layout ([coefficient][byte][column][term]);
+//   phase B : warp w takes (coefficient, m-tile) units; A fragments come from a
+//             pre-split mask bank (16-byte loads, fragment order), B fragments
+//             from shared memory; 4 k-steps x 5 n-tiles of IMMA per unit, then
+//             the byte recombination and the modular reduction per output.
+// The 60-bit limbs (q_0, P) keep the IMAD kernel (hoisted_mac_bank_wide).
+#include "ops.cuh"
+
+namespace uh {
+namespace {
+
+constexpr int kIC = 8;                      // coefficients per CTA
+constexpr int kICT = 4;                     // ciphertexts per CTA
+constexpr int kIJ = 2 * kICT;               // columns per value byte (ciphertext x component)
+constexpr int kIRow = 144;                  // bytes per (coefficient, byte, column) row: 128 terms + pad
+constexpr int kIPlane = 5 * kIJ * kIRow;    // 5760 bytes per coefficient
+constexpr int kICoef = kIPlane + 4;         // coefficient stride (bank-conflict-free phase-A stores)
+constexpr int kIMaxTerms = 128;             // 4 k-steps
+constexpr int kICStride = 42;               // C staging row stride (int32)
+constexpr size_t kISmem = (size_t)kIC * kICoef + 8 * 16 * kICStride * 4;  // B' planes + per-warp C staging
+
+__device__ __forceinline__ uint32_t rot_index_i(uint32_t n, uint32_t half, uint32_t r) {
+    uint32_t h = n >= half ? half : 0;
+    uint32_t j = n - h + r;
+    j = j >= half ? j - half : j;
+    return h + j;
+}
+__device__ __forceinline__ uint64_t fold64_i(uint64_t hi, uint64_t lo, const Mod &m) {
+    const uint64_t p = (uint64_t)(uint32_t)hi * m.r64;
+    const uint64_t v = lo + p;
+    return v < p ? v + m.r64 : v;
+}
+
+__device__ __forceinline__ void imma(int (&c)[4], const uint4 &a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+// mask bank [L-1 limbs 1..L-1][N][m-tile][k-step][lane][4 words]: the A fragments of the
+// per-coefficient (output x byte) x term matrices.  Row r of m-tile mt is output
+// 3 mt + r / 5, byte r % 5 (row 15 and outputs >= O are zero); k = term index.
+__global__ void k_imma_bank(uint32_t *__restrict__ ib, const uint64_t *__restrict__ masks, int O, int Q, int L,
+                            int logn, int nks) {
+    const uint32_t N = 1u << logn;
+    const size_t total = (size_t)(L - 1) * N * 4 * nks * 32;
+    const size_t ROW = (size_t)(L + 1) << logn;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const int lane = (int)(idx & 31);
+        const int ks = (int)((idx >> 5) % nks);
+        const size_t r0 = (idx >> 5) / nks;
+        const int mt = (int)(r0 & 3);
+        const size_t r1 = r0 >> 2;
+        const uint32_t n = (uint32_t)(r1 & (N - 1));
+        const int k = (int)(r1 >> logn) + 1;
+        const int g = lane >> 2, tig = lane & 3;
+        uint32_t w[4];
+#pragma unroll
+        for (int reg = 0; reg < 4; reg++) {
+            const int row = g + (reg & 1) * 8;
+            const int kb = ks * 32 + tig * 4 + (reg >> 1) * 16;
+            const int o = mt * 3 + row / 5, a = row % 5;
+            uint32_t v = 0;
+            if (row < 15 && o < O) {
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    const int q = kb + t;
+                    if (q < Q) {
+                        const uint64_t mv = masks[((size_t)o * Q + q) * ROW + ((size_t)k << logn) + n];
+                        v |= (uint32_t)((mv >> (8 * a)) & 0xFF) << (8 * t);
+                    }
+                }
+            }
+            w[reg] = v;
+        }
+        reinterpret_cast<uint4 *>(ib)[(((r1 * 4 + mt) * nks + ks) << 5) + lane] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+template <int L, int LOGN, int NKS>
+__global__ void __launch_bounds__(256, 3)
+    k_hoisted_imma(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, const uint64_t *__restrict__ D,
+                   const uint4 *__restrict__ ib, const uint64_t *__restrict__ kbank, const int32_t *__restrict__ shifts,
+                   int B, int I, int T, int O, int sp, const Mod *__restrict__ mods) {
+    constexpr int LP = L + 1;
+    constexpr uint32_t N = 1u << LOGN, half = N >> 1;
+    constexpr uint32_t ROW = (uint32_t)LP << LOGN;
+    extern __shared__ __align__(16) unsigned char ism[];
+    int *cst = reinterpret_cast<int *>(ism + (size_t)kIC * kICoef);
+    __shared__ uint32_t s_x[kIMaxTerms], s_d[kIMaxTerms], s_k[kIMaxTerms], s_r[kIMaxTerms];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b0 = blockIdx.x * kICT;
+    const uint32_t n0 = blockIdx.y * kIC;
+    const int k = 1 + blockIdx.z;  // 40-bit limbs q_1 .. q_{L-1}
+    const Mod m = mods[k];
+    const uint64_t P = mods[sp].q;
+    const uint64_t Pk = P < m.q ? P : csub(barrett_lite(P, m), m.q);
+    const int Q = I * T;
+    for (int q = tid; q < Q; q += blockDim.x) {
+        const int i = q / T, t = q - i * T;
+        s_x[q] = (uint32_t)i * (uint32_t)B * (2u * L << LOGN);
+        s_d[q] = (uint32_t)i * (uint32_t)B * ((uint32_t)L * LP << LOGN);
+        s_k[q] = (uint32_t)t * ((uint32_t)LP * 2 * L << LOGN);
+        s_r[q] = (uint32_t)shifts[t];
+    }
+    __syncthreads();
+
+    // ---- phase A: key-switched P * rot(ct) per (term, ciphertext, coefficient) -> byte planes ----
+    // one term per item (Q * 32 items over 256 threads: balanced to within one item per thread);
+    // lanes = (ciphertext, coefficient), so the byte stores of a warp hit 32 distinct banks
+    for (int it = tid; it < Q * 32; it += 256) {
+        const int q = it >> 5, ct = (it >> 3) & 3, cf = it & 7;
+        const int b = b0 + ct;
+        const uint32_t n = n0 + cf;
+        uint64_t v0 = 0, v1 = 0;
+        if (b < B) {
+            const uint32_t r = s_r[q];
+            const uint64_t *c0 = X + s_x[q] + (((uint32_t)b * 2 * L + k) << LOGN);
+            if (r == 0) {
+                v0 = mulmod(Pk, __ldg(c0 + n), m);
+                v1 = mulmod(Pk, __ldg(c0 + ((uint32_t)L << LOGN) + n), m);
+            } else {
+                const uint32_t src = rot_index_i(n, half, r);
+                const uint64_t *Dj = D + s_d[q] + (((uint32_t)b * L * LP + k) << LOGN) + src;
+                const uint64_t *K = kbank + s_k[q] + ((uint32_t)k * 2 * L << LOGN) + n;
+                uint64_t d[L], x[L], y[L];
+#pragma unroll
+                for (int j = 0; j < L; j++) {
+                    d[j] = __ldg(Dj + (uint32_t)j * ROW);
+                    x[j] = __ldg(K + ((uint32_t)(2 * j) << LOGN));
+                    y[j] = __ldg(K + ((uint32_t)(2 * j + 1) << LOGN));
+                }
+                const uint64_t cs = __ldg(c0 + src);
+                AccN a0, a1;
+                a0.zero();
+                a1.zero();
+#pragma unroll
+                for (int j = 0; j < L; j++) {
+                    a0.mac(d[j], x[j]);
+                    a1.mac(d[j], y[j]);
+                }
+                a0.mac(Pk, cs);
+                uint64_t h0, l0, h1, l1;
+                a0.value(h0, l0);
+                a1.value(h1, l1);
+                v0 = csub(barrett_lite(fold64_i(h0, l0, m), m), m.q);
+                v1 = csub(barrett_lite(fold64_i(h1, l1, m), m), m.q);
+            }
+        }
+        unsigned char *pl = ism + cf * kICoef + (2 * ct) * kIRow + q;
+#pragma unroll
+        for (int bb = 0; bb < 5; bb++) {
+            pl[bb * kIJ * kIRow] = (unsigned char)(v0 >> (8 * bb));
+            pl[bb * kIJ * kIRow + kIRow] = (unsigned char)(v1 >> (8 * bb));
+        }
+    }
+    // terms [Q, 32 NKS) of the B planes are never written: their A bytes are zero (integer
+    // products, so whatever the shared memory holds there contributes nothing)
+    __syncthreads();
+
+    // ---- phase B: IMMA per (coefficient, m-tile), byte recombination, reduction ----
+    const int gid = lane >> 2, tig = lane & 3;
+    int *cw = cst + warp * 16 * kICStride;
+    const int nmt = (O + 2) / 3;
+    for (int u = warp; u < kIC * 4; u += 8) {
+        const int cf = u >> 2, mt = u & 3;
+        if (mt >= nmt) continue;
+        const uint32_t n = n0 + cf;
+        const uint4 *af = ib + ((((size_t)(k - 1) * N + n) * 4 + mt) * NKS << 5) + lane;
+        uint4 A[NKS];
+#pragma unroll
+        for (int ks = 0; ks < NKS; ks++) A[ks] = __ldg(af + (ks << 5));
+        int C[5][4];
+#pragma unroll
+        for (int nb = 0; nb < 5; nb++) C[nb][0] = C[nb][1] = C[nb][2] = C[nb][3] = 0;
+        const unsigned char *bp = ism + cf * kICoef + gid * kIRow + tig * 4;
+#pragma unroll
+        for (int ks = 0; ks < NKS; ks++)
+#pragma unroll
+            for (int nb = 0; nb < 5; nb++) {
+                const unsigned char *p = bp + nb * kIJ * kIRow + ks * 32;
+                imma(C[nb], A[ks], *reinterpret_cast<const uint32_t *>(p),
+                     *reinterpret_cast<const uint32_t *>(p + 16));
+            }
+#pragma unroll
+        for (int nb = 0; nb < 5; nb++) {
+            const int col = nb * 8 + tig * 2;
+            *reinterpret_cast<int2 *>(cw + gid * kICStride + col) = make_int2(C[nb][0], C[nb][1]);
+            *reinterpret_cast<int2 *>(cw + (gid + 8) * kICStride + col) = make_int2(C[nb][2], C[nb][3]);
+        }
+        __syncwarp();
+        if (lane < 24) {
+            const int ol = lane >> 3, j = lane & 7;
+            const int o = mt * 3 + ol, b = b0 + (j >> 1);
+            if (o < O && b < B) {
+                uint64_t Ts[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int a = 0; a < 5; a++)
+#pragma unroll
+                    for (int nb = 0; nb < 5; nb++) Ts[a + nb] += (uint32_t)cw[(ol * 5 + a) * kICStride + nb * 8 + j];
+                // value = sum_s Ts[s] 2^(8 s) < 2^89: low part (s <= 4) and high part (s >= 5) * 2^40
+                const uint64_t lo = Ts[0] + (Ts[1] << 8) + (Ts[2] << 16) + (Ts[3] << 24) + (Ts[4] << 32);
+                const uint64_t hx = Ts[5] + (Ts[6] << 8) + (Ts[7] << 16) + (Ts[8] << 24);
+                const uint64_t l2 = lo + (hx << 40);
+                const uint64_t h2 = (hx >> 24) + (l2 < lo);
+                acc_out[((((uint32_t)o * B + b) * 2 + (j & 1)) * LP + k) * N + n] = reduce128(h2, l2, m);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+template <int L, int NKS>
+void launch_imma_k(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib,
+                   const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
+    static bool done = false;  // one opt-in per kernel instance
+    if (!done) {
+        UH_CHECK(cudaFuncSetAttribute(k_hoisted_imma<L, 15, NKS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kISmem));
+        done = true;
+    }
+    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / kIC), L - 1);
+    k_hoisted_imma<L, 15, NKS><<<grid, 256, kISmem, s>>>(acc, X, D, reinterpret_cast<const uint4 *>(ib), kbank, shifts,
+                                                        B, I, T, O, c.sp(), c.d_mods);
+    UH_LAUNCH_CHECK();
+}
+
+template <int L>
+void launch_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib,
+                 const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
+    const int nks = (I * T + 31) / 32;
+    if (nks <= 1) launch_imma_k<L, 1>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    else if (nks == 2) launch_imma_k<L, 2>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    else if (nks == 3) launch_imma_k<L, 3>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    else launch_imma_k<L, 4>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+}
+
+}  // namespace
+
+// Applicable when N = 2^15, the level has 40-bit limbs q_1..q_{L-1} (< 2^40) and 60-bit
+// q_0 and P, 5..12 dense masked outputs and at most 128 terms.
+bool hoisted_imma_supported(const Ctx &c, int level, int O, int Q) {
+    if (c.logn != 15 || level < 2 || level + 1 > 10 || O < 5 || O > 12 || Q < 1 || Q > kIMaxTerms) return false;
+    for (int k = 1; k <= level; k++)
+        if (c.h_q[k] >> 40) return false;
+    return (c.h_q[0] >> 40) && (c.h_q[c.count - 1] >> 40);
+}
+
+size_t imma_bank_words(const Ctx &c, int level, int Q) {
+    const int nks = (Q + 31) / 32;
+    return (size_t)level * c.n * 4 * nks * 32 * 4;
+}
+
+void imma_mask_bank(const Ctx &c, uint32_t *ib, const uint64_t *masks, int O, int Q, int level, cudaStream_t s) {
+    const int L = level + 1, nks = (Q + 31) / 32;
+    const size_t total = (size_t)(L - 1) * c.n * 4 * nks * 32;
+    k_imma_bank<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 32), 256, 0, s>>>(ib, masks, O, Q, L,
+                                                                                           (int)c.logn, nks);
+    UH_LAUNCH_CHECK();
+}
+
+void hoisted_mac_bank_wide(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
+                           const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, int level,
+                           cudaStream_t s);
+
+void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
+                      const uint32_t *ib, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O,
+                      int level, cudaStream_t s) {
+    if (!hoisted_imma_supported(c, level, O, I * T))
+        throw std::invalid_argument("IMMA hoisted kernel: needs N = 2^15, 40-bit q_1..q_level, 5 <= O <= 12, <= 128 terms");
+    const double lim = 4294967295.0;
+    const int L = level + 1;
+    if ((double)I * B * 2 * L * c.n > lim || (double)I * B * L * (L + 1) * c.n > lim ||
+        (double)O * B * 2 * (L + 1) * c.n > lim)
+        throw std::invalid_argument("IMMA hoisted kernel operand exceeds 2^32 elements: split the batch");
+    hoisted_mac_bank_wide(c, acc, X, D, masks, kbank, shifts, B, I, T, O, level, s);
+    switch (L) {
+        case 3: launch_imma<3>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
+        case 4: launch_imma<4>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
+        case 5: launch_imma<5>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
+        case 6: launch_imma<6>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
+        case 7: launch_imma<7>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
+        case 8: launch_imma<8>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
+        case 9: launch_imma<9>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
+        case 10: launch_imma<10>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
+        default: throw std::invalid_argument("IMMA hoisted kernel: 3 <= level + 1 <= 10");
+    }
+}
+
+}  // namespace uh

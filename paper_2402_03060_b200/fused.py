@@ -84,6 +84,31 @@ def _key_bank_ok(backend, level: int, O: int) -> bool:
     return bool(_lib.load().uh_hoisted_bank_supported(backend._ctx, level, O))
 
 
+def _imma_ok(backend, level: int, O: int, Q: int) -> bool:
+    """Dense 5..12-output layers: the mask contraction on the tensor cores (hoist_imma.cu)."""
+    if os.environ.get("UH_IMMA", "1") == "0" or not _key_bank_ok(backend, level, O):
+        return False
+    return bool(_lib.load().uh_imma_supported(backend._ctx, level, O, Q))
+
+
+def imma_bank(backend, masks: torch.Tensor, O: int, Q: int, level: int, cache: bool = True) -> torch.Tensor:
+    """The A-fragment byte-plane bank of a mask bank (uh_imma_mask_bank).
+
+    cache=True for masks from a persistent layer bank: the entry keeps the mask tensor
+    alive, so its address cannot be reused by another tensor while the entry exists."""
+    banks = backend.__dict__.setdefault("_imma_banks", {})
+    ck = (masks.data_ptr(), O, Q, level)
+    hit = banks.get(ck) if cache else None
+    if hit is not None and hit[0] is masks:
+        return hit[1]
+    nks = (Q + 31) // 32
+    ib = torch.empty((level, backend.n, 4, nks, 32, 4), dtype=torch.int32, device=backend.device)
+    backend._call("uh_imma_mask_bank", _vp(ib), _vp(masks), O, Q, level, backend._stream())
+    if cache:
+        banks[ck] = (masks, ib)
+    return ib
+
+
 def key_bank(backend, shifts, level: int) -> torch.Tensor:
     """Galois keys of ``shifts`` re-laid for the key-bank kernel: [T][level+2][2(level+1)][N].
 
@@ -196,7 +221,12 @@ def conv(backend, state: CipherState, layer) -> CipherState:
     if timer is not None:
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(torch.cuda.current_stream(backend.device))
-    if _key_bank_ok(backend, level, O):
+    if _imma_ok(backend, level, O, I * T):
+        kb = key_bank(backend, shifts, level)
+        ib = imma_bank(backend, masks, O, I * T, level)
+        backend._call("uh_hoisted_mac_imma", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ib), _vp(kb), _vp(sh), B, I,
+                      T, O, level, st)
+    elif _key_bank_ok(backend, level, O):
         kb = key_bank(backend, shifts, level)
         backend._call("uh_hoisted_mac_bank", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(kb), _vp(sh), B, I, T, O,
                       0, level, st)
@@ -312,6 +342,14 @@ def _hoist(backend, X, level, shifts, masks, O, diag, B, taps=None):
     acc = backend._empty(O, B, 2, LP, n)
     mode = 2 if diag == 2 else (1 if diag else 0)
     T = taps if mode == 2 else len(shifts)
+    if mode == 0 and masks is not None and _imma_ok(backend, level, O, I * T):
+        kb = key_bank(backend, shifts, level)
+        ib = imma_bank(backend, masks, O, I * T, level, cache=False)
+        sh = torch.tensor([s % backend.params.num_slots for s in shifts], dtype=torch.int32, device=backend.device)
+        backend._call("uh_hoisted_mac_imma", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ib), _vp(kb), _vp(sh), B, I,
+                      T, O, level, st)
+        del D
+        return acc
     if _key_bank_ok(backend, level, O) and (mode != 2 or O <= 4):
         kb = key_bank(backend, shifts, level)
         sh = torch.tensor([s % backend.params.num_slots for s in shifts], dtype=torch.int32, device=backend.device)

@@ -191,3 +191,26 @@ def test_key_bank_kernels_equal_generic_every_mode(O, with_masks, diag, monkeypa
     monkeypatch.setenv("UH_KEY_BANK", "0")
     want = fused._hoist(be, X, level, shifts, mdev, O, mode, B, taps=taps)
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("O,level,I,shifts,B", [
+    (12, 5, 4, [a + 28 * b for b in range(5) for a in range(5)], 5),   # LeNet conv2 shape, partial ct tile
+    (7, 3, 3, [0, 1, 28, -29, 16383, 57, -2, 3, 700], 4),              # partial m-tile, Q = 27 (not / 4)
+    (5, 2, 2, [0, 1, 28, -29, 16383], 3),                              # one k-step, 2 m-tiles
+    (9, 8, 1, [3, 0, -5], 9),                                          # high level, 3 terms, 3 ct tiles
+])
+def test_imma_kernel_equals_key_bank_kernel(O, level, I, shifts, B, monkeypatch):
+    """Tensor-core mask contraction (hoist_imma.cu: byte-split u8 IMMA on the 40-bit limbs, the IMAD
+    kernel on q_0 and P) == the key-bank IMAD kernel (oracle-pinned above), residue for residue, with
+    worst-case (uniform up to q - 1) masks."""
+    be, o = _c2()
+    rng = np.random.default_rng(70 + O + level)
+    cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, C2.num_slots)))) for _ in range(I)]
+    X = fused.stack_cts(be, cts, level)
+    mdev = torch.from_numpy(_rand_masks(o, rng, O, I * len(shifts), level).view(np.int64)).to(be.device)
+    monkeypatch.setenv("UH_IMMA", "1")
+    assert fused._imma_ok(be, level, O, I * len(shifts))
+    got = fused._hoist(be, X, level, shifts, mdev, O, False, B)
+    monkeypatch.setenv("UH_IMMA", "0")
+    want = fused._hoist(be, X, level, shifts, mdev, O, False, B)
+    assert torch.equal(got, want)
