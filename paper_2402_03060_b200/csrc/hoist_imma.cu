@@ -26,7 +26,8 @@
 //             pre-split mask bank (16-byte loads, fragment order), B fragments
 //             from shared memory; 4 k-steps x 5 n-tiles of IMMA per unit, then
 //             the byte recombination and the modular reduction per output.
-// The 60-bit limbs (q_0, P) keep the IMAD kernel (hoisted_mac_bank_wide).
+// The 60-bit limbs (q_0, P) keep the IMAD kernel (hoisted_mac_bank_wide) by default; the same
+// kernel with 8-byte operands (64 byte products, 2 outputs per m-tile) is opt-in.
 #include "ops.cuh"
 
 namespace uh {
@@ -36,11 +37,17 @@ constexpr int kIC = 8;                      // coefficients per CTA
 constexpr int kICT = 4;                     // ciphertexts per CTA
 constexpr int kIJ = 2 * kICT;               // columns per value byte (ciphertext x component)
 constexpr int kIRow = 144;                  // bytes per (coefficient, byte, column) row: 128 terms + pad
-constexpr int kIPlane = 5 * kIJ * kIRow;    // 5760 bytes per coefficient
-constexpr int kICoef = kIPlane + 4;         // coefficient stride (bank-conflict-free phase-A stores)
 constexpr int kIMaxTerms = 128;             // 4 k-steps
-constexpr int kICStride = 42;               // C staging row stride (int32)
-constexpr size_t kISmem = (size_t)kIC * kICoef + 8 * 16 * kICStride * 4;  // B' planes + per-warp C staging
+// Byte width W of the residues: 5 for the 40-bit limbs (3 outputs x 5 mask bytes per 16-row
+// m-tile, 4 m-tiles), 8 for the 60-bit limbs q_0 and P (2 outputs x 8 bytes, 6 m-tiles).
+template <int W> struct IW {
+    static constexpr int OPT = W == 5 ? 3 : 2;          // outputs per m-tile
+    static constexpr int MT = 12 / OPT;                 // m-tiles for 12 outputs
+    static constexpr int COEF = W * kIJ * kIRow + 4;    // coefficient stride of the B planes
+    static constexpr int CS = W * 8 + 2;                // C staging row stride (int32)
+    static constexpr size_t SMEM = (size_t)kIC * COEF + 8 * 16 * CS * 4;
+    static constexpr int MINB = W == 5 ? 3 : 2;         // resident CTAs per SM
+};
 
 __device__ __forceinline__ uint32_t rot_index_i(uint32_t n, uint32_t half, uint32_t r) {
     uint32_t h = n >= half ? half : 0;
@@ -53,6 +60,13 @@ __device__ __forceinline__ uint64_t fold64_i(uint64_t hi, uint64_t lo, const Mod
     const uint64_t v = lo + p;
     return v < p ? v + m.r64 : v;
 }
+// (hi:lo) += t << sh, 0 <= sh < 64
+__device__ __forceinline__ void add_shifted(uint64_t &hi, uint64_t &lo, uint64_t t, int sh) {
+    const uint64_t l = t << sh;
+    const uint64_t h = sh ? t >> (64 - sh) : 0;
+    lo += l;
+    hi += h + (lo < l);
+}
 
 __device__ __forceinline__ void imma(int (&c)[4], const uint4 &a, uint32_t b0, uint32_t b1) {
     asm volatile(
@@ -61,31 +75,36 @@ __device__ __forceinline__ void imma(int (&c)[4], const uint4 &a, uint32_t b0, u
         : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
 
-// mask bank [L-1 limbs 1..L-1][N][m-tile][k-step][lane][4 words]: the A fragments of the
-// per-coefficient (output x byte) x term matrices.  Row r of m-tile mt is output
-// 3 mt + r / 5, byte r % 5 (row 15 and outputs >= O are zero); k = term index.
+// A-fragment mask bank [limb slot][N][m-tile][k-step][lane][4 words]: per coefficient, the
+// (output x byte) x term matrix.  Row r of m-tile mt is output OPT mt + r / W, byte r % W
+// (rows past OPT W and outputs >= O are zero).  Limb slots: W = 5 -> limbs 1..L-1,
+// W = 8 -> limbs 0 and L (P).
+template <int W>
 __global__ void k_imma_bank(uint32_t *__restrict__ ib, const uint64_t *__restrict__ masks, int O, int Q, int L,
                             int logn, int nks) {
+    using C = IW<W>;
     const uint32_t N = 1u << logn;
-    const size_t total = (size_t)(L - 1) * N * 4 * nks * 32;
+    const int nslots = W == 5 ? L - 1 : 2;
+    const size_t total = (size_t)nslots * N * C::MT * nks * 32;
     const size_t ROW = (size_t)(L + 1) << logn;
     for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
         const int lane = (int)(idx & 31);
         const int ks = (int)((idx >> 5) % nks);
         const size_t r0 = (idx >> 5) / nks;
-        const int mt = (int)(r0 & 3);
-        const size_t r1 = r0 >> 2;
+        const int mt = (int)(r0 % C::MT);
+        const size_t r1 = r0 / C::MT;
         const uint32_t n = (uint32_t)(r1 & (N - 1));
-        const int k = (int)(r1 >> logn) + 1;
+        const int slot = (int)(r1 >> logn);
+        const int k = W == 5 ? slot + 1 : (slot ? L : 0);
         const int g = lane >> 2, tig = lane & 3;
         uint32_t w[4];
 #pragma unroll
         for (int reg = 0; reg < 4; reg++) {
             const int row = g + (reg & 1) * 8;
             const int kb = ks * 32 + tig * 4 + (reg >> 1) * 16;
-            const int o = mt * 3 + row / 5, a = row % 5;
+            const int o = mt * C::OPT + row / W, a = row % W;
             uint32_t v = 0;
-            if (row < 15 && o < O) {
+            if (row < C::OPT * W && o < O) {
 #pragma unroll
                 for (int t = 0; t < 4; t++) {
                     const int q = kb + t;
@@ -97,28 +116,31 @@ __global__ void k_imma_bank(uint32_t *__restrict__ ib, const uint64_t *__restric
             }
             w[reg] = v;
         }
-        reinterpret_cast<uint4 *>(ib)[(((r1 * 4 + mt) * nks + ks) << 5) + lane] = make_uint4(w[0], w[1], w[2], w[3]);
+        reinterpret_cast<uint4 *>(ib)[(((r1 * C::MT + mt) * nks + ks) << 5) + lane] = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
-template <int L, int LOGN, int NKS>
-__global__ void __launch_bounds__(256, 3)
+template <int L, int LOGN, int NKS, int W>
+__global__ void __launch_bounds__(256, IW<W>::MINB)
     k_hoisted_imma(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, const uint64_t *__restrict__ D,
                    const uint4 *__restrict__ ib, const uint64_t *__restrict__ kbank, const int32_t *__restrict__ shifts,
                    int B, int I, int T, int O, int sp, const Mod *__restrict__ mods) {
+    using C = IW<W>;
     constexpr int LP = L + 1;
     constexpr uint32_t N = 1u << LOGN, half = N >> 1;
     constexpr uint32_t ROW = (uint32_t)LP << LOGN;
     extern __shared__ __align__(16) unsigned char ism[];
-    int *cst = reinterpret_cast<int *>(ism + (size_t)kIC * kICoef);
+    int *cst = reinterpret_cast<int *>(ism + (size_t)kIC * C::COEF);
     __shared__ uint32_t s_x[kIMaxTerms], s_d[kIMaxTerms], s_k[kIMaxTerms], s_r[kIMaxTerms];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int b0 = blockIdx.x * kICT;
     const uint32_t n0 = blockIdx.y * kIC;
-    const int k = 1 + blockIdx.z;  // 40-bit limbs q_1 .. q_{L-1}
-    const Mod m = mods[k];
+    const int slot = blockIdx.z;
+    const int k = W == 5 ? 1 + slot : (slot ? L : 0);  // limb: q_1..q_{L-1}, or q_0 / P
+    const bool qlimb = k < L;
+    const Mod m = mods[qlimb ? k : sp];
     const uint64_t P = mods[sp].q;
-    const uint64_t Pk = P < m.q ? P : csub(barrett_lite(P, m), m.q);
+    const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
     const int Q = I * T;
     for (int q = tid; q < Q; q += blockDim.x) {
         const int i = q / T, t = q - i * T;
@@ -141,8 +163,10 @@ __global__ void __launch_bounds__(256, 3)
             const uint32_t r = s_r[q];
             const uint64_t *c0 = X + s_x[q] + (((uint32_t)b * 2 * L + k) << LOGN);
             if (r == 0) {
-                v0 = mulmod(Pk, __ldg(c0 + n), m);
-                v1 = mulmod(Pk, __ldg(c0 + ((uint32_t)L << LOGN) + n), m);
+                if (qlimb) {
+                    v0 = mulmod(Pk, __ldg(c0 + n), m);
+                    v1 = mulmod(Pk, __ldg(c0 + ((uint32_t)L << LOGN) + n), m);
+                }
             } else {
                 const uint32_t src = rot_index_i(n, half, r);
                 const uint64_t *Dj = D + s_d[q] + (((uint32_t)b * L * LP + k) << LOGN) + src;
@@ -154,26 +178,40 @@ __global__ void __launch_bounds__(256, 3)
                     x[j] = __ldg(K + ((uint32_t)(2 * j) << LOGN));
                     y[j] = __ldg(K + ((uint32_t)(2 * j + 1) << LOGN));
                 }
-                const uint64_t cs = __ldg(c0 + src);
-                AccN a0, a1;
-                a0.zero();
-                a1.zero();
+                if constexpr (W == 5) {
+                    const uint64_t cs = __ldg(c0 + src);
+                    AccN a0, a1;
+                    a0.zero();
+                    a1.zero();
 #pragma unroll
-                for (int j = 0; j < L; j++) {
-                    a0.mac(d[j], x[j]);
-                    a1.mac(d[j], y[j]);
+                    for (int j = 0; j < L; j++) {
+                        a0.mac(d[j], x[j]);
+                        a1.mac(d[j], y[j]);
+                    }
+                    a0.mac(Pk, cs);
+                    uint64_t h0, l0, h1, l1;
+                    a0.value(h0, l0);
+                    a1.value(h1, l1);
+                    v0 = csub(barrett_lite(fold64_i(h0, l0, m), m), m.q);
+                    v1 = csub(barrett_lite(fold64_i(h1, l1, m), m), m.q);
+                } else {
+                    Acc a0, a1;
+                    a0.zero();
+                    a1.zero();
+#pragma unroll
+                    for (int j = 0; j < L; j++) {
+                        a0.mac(d[j], x[j]);
+                        a1.mac(d[j], y[j]);
+                    }
+                    if (qlimb) a0.mac(Pk, __ldg(c0 + src));
+                    v0 = a0.reduce(m);
+                    v1 = a1.reduce(m);
                 }
-                a0.mac(Pk, cs);
-                uint64_t h0, l0, h1, l1;
-                a0.value(h0, l0);
-                a1.value(h1, l1);
-                v0 = csub(barrett_lite(fold64_i(h0, l0, m), m), m.q);
-                v1 = csub(barrett_lite(fold64_i(h1, l1, m), m), m.q);
             }
         }
-        unsigned char *pl = ism + cf * kICoef + (2 * ct) * kIRow + q;
+        unsigned char *pl = ism + cf * C::COEF + (2 * ct) * kIRow + q;
 #pragma unroll
-        for (int bb = 0; bb < 5; bb++) {
+        for (int bb = 0; bb < W; bb++) {
             pl[bb * kIJ * kIRow] = (unsigned char)(v0 >> (8 * bb));
             pl[bb * kIJ * kIRow + kIRow] = (unsigned char)(v1 >> (8 * bb));
         }
@@ -184,79 +222,93 @@ __global__ void __launch_bounds__(256, 3)
 
     // ---- phase B: IMMA per (coefficient, m-tile), byte recombination, reduction ----
     const int gid = lane >> 2, tig = lane & 3;
-    int *cw = cst + warp * 16 * kICStride;
-    const int nmt = (O + 2) / 3;
-    for (int u = warp; u < kIC * 4; u += 8) {
-        const int cf = u >> 2, mt = u & 3;
+    int *cw = cst + warp * 16 * C::CS;
+    const int nmt = (O + C::OPT - 1) / C::OPT;
+    for (int u = warp; u < kIC * C::MT; u += 8) {
+        const int cf = u / C::MT, mt = u % C::MT;
         if (mt >= nmt) continue;
         const uint32_t n = n0 + cf;
-        const uint4 *af = ib + ((((size_t)(k - 1) * N + n) * 4 + mt) * NKS << 5) + lane;
+        const uint4 *af = ib + ((((size_t)slot * N + n) * C::MT + mt) * NKS << 5) + lane;
         uint4 A[NKS];
 #pragma unroll
         for (int ks = 0; ks < NKS; ks++) A[ks] = __ldg(af + (ks << 5));
-        int C[5][4];
+        int Cr[W][4];
 #pragma unroll
-        for (int nb = 0; nb < 5; nb++) C[nb][0] = C[nb][1] = C[nb][2] = C[nb][3] = 0;
-        const unsigned char *bp = ism + cf * kICoef + gid * kIRow + tig * 4;
+        for (int nb = 0; nb < W; nb++) Cr[nb][0] = Cr[nb][1] = Cr[nb][2] = Cr[nb][3] = 0;
+        const unsigned char *bp = ism + cf * C::COEF + gid * kIRow + tig * 4;
 #pragma unroll
         for (int ks = 0; ks < NKS; ks++)
 #pragma unroll
-            for (int nb = 0; nb < 5; nb++) {
+            for (int nb = 0; nb < W; nb++) {
                 const unsigned char *p = bp + nb * kIJ * kIRow + ks * 32;
-                imma(C[nb], A[ks], *reinterpret_cast<const uint32_t *>(p),
+                imma(Cr[nb], A[ks], *reinterpret_cast<const uint32_t *>(p),
                      *reinterpret_cast<const uint32_t *>(p + 16));
             }
 #pragma unroll
-        for (int nb = 0; nb < 5; nb++) {
+        for (int nb = 0; nb < W; nb++) {
             const int col = nb * 8 + tig * 2;
-            *reinterpret_cast<int2 *>(cw + gid * kICStride + col) = make_int2(C[nb][0], C[nb][1]);
-            *reinterpret_cast<int2 *>(cw + (gid + 8) * kICStride + col) = make_int2(C[nb][2], C[nb][3]);
+            *reinterpret_cast<int2 *>(cw + gid * C::CS + col) = make_int2(Cr[nb][0], Cr[nb][1]);
+            *reinterpret_cast<int2 *>(cw + (gid + 8) * C::CS + col) = make_int2(Cr[nb][2], Cr[nb][3]);
         }
         __syncwarp();
-        if (lane < 24) {
+        if (lane < C::OPT * 8) {
             const int ol = lane >> 3, j = lane & 7;
-            const int o = mt * 3 + ol, b = b0 + (j >> 1);
+            const int o = mt * C::OPT + ol, b = b0 + (j >> 1);
             if (o < O && b < B) {
-                uint64_t Ts[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+                uint64_t Ts[2 * W - 1];
 #pragma unroll
-                for (int a = 0; a < 5; a++)
+                for (int s2 = 0; s2 < 2 * W - 1; s2++) Ts[s2] = 0;
 #pragma unroll
-                    for (int nb = 0; nb < 5; nb++) Ts[a + nb] += (uint32_t)cw[(ol * 5 + a) * kICStride + nb * 8 + j];
-                // value = sum_s Ts[s] 2^(8 s) < 2^89: low part (s <= 4) and high part (s >= 5) * 2^40
-                const uint64_t lo = Ts[0] + (Ts[1] << 8) + (Ts[2] << 16) + (Ts[3] << 24) + (Ts[4] << 32);
-                const uint64_t hx = Ts[5] + (Ts[6] << 8) + (Ts[7] << 16) + (Ts[8] << 24);
-                const uint64_t l2 = lo + (hx << 40);
-                const uint64_t h2 = (hx >> 24) + (l2 < lo);
-                acc_out[((((uint32_t)o * B + b) * 2 + (j & 1)) * LP + k) * N + n] = reduce128(h2, l2, m);
+                for (int a = 0; a < W; a++)
+#pragma unroll
+                    for (int nb = 0; nb < W; nb++) Ts[a + nb] += (uint32_t)cw[(ol * W + a) * C::CS + nb * 8 + j];
+                uint64_t r;
+                if constexpr (W == 5) {
+                    // value = sum_s Ts[s] 2^(8 s) < 2^89: low part (s <= 4) and high part (s >= 5) * 2^40
+                    const uint64_t lo = Ts[0] + (Ts[1] << 8) + (Ts[2] << 16) + (Ts[3] << 24) + (Ts[4] << 32);
+                    const uint64_t hx = Ts[5] + (Ts[6] << 8) + (Ts[7] << 16) + (Ts[8] << 24);
+                    const uint64_t l2 = lo + (hx << 40);
+                    const uint64_t h2 = (hx >> 24) + (l2 < lo);
+                    r = reduce128(h2, l2, m);
+                } else {
+                    // value = lo128 + hi128 * 2^64 (< 2^138): both halves < 2^83
+                    uint64_t lh = 0, ll = 0, hh = 0, hl = 0;
+#pragma unroll
+                    for (int s2 = 0; s2 < 8; s2++) add_shifted(lh, ll, Ts[s2], 8 * s2);
+#pragma unroll
+                    for (int s2 = 8; s2 < 15; s2++) add_shifted(hh, hl, Ts[s2], 8 * (s2 - 8));
+                    r = addmod(reduce128(lh, ll, m), mulmod(reduce128(hh, hl, m), m.r64, m), m.q);
+                }
+                acc_out[((((uint32_t)o * B + b) * 2 + (j & 1)) * LP + k) * N + n] = r;
             }
         }
         __syncwarp();
     }
 }
 
-template <int L, int NKS>
+template <int L, int NKS, int W>
 void launch_imma_k(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib,
                    const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
     static bool done = false;  // one opt-in per kernel instance
     if (!done) {
-        UH_CHECK(cudaFuncSetAttribute(k_hoisted_imma<L, 15, NKS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kISmem));
+        UH_CHECK(cudaFuncSetAttribute(k_hoisted_imma<L, 15, NKS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)IW<W>::SMEM));
         done = true;
     }
-    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / kIC), L - 1);
-    k_hoisted_imma<L, 15, NKS><<<grid, 256, kISmem, s>>>(acc, X, D, reinterpret_cast<const uint4 *>(ib), kbank, shifts,
-                                                        B, I, T, O, c.sp(), c.d_mods);
+    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / kIC), W == 5 ? L - 1 : 2);
+    k_hoisted_imma<L, 15, NKS, W><<<grid, 256, IW<W>::SMEM, s>>>(acc, X, D, reinterpret_cast<const uint4 *>(ib), kbank,
+                                                                shifts, B, I, T, O, c.sp(), c.d_mods);
     UH_LAUNCH_CHECK();
 }
 
-template <int L>
+template <int L, int W>
 void launch_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib,
                  const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
     const int nks = (I * T + 31) / 32;
-    if (nks <= 1) launch_imma_k<L, 1>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
-    else if (nks == 2) launch_imma_k<L, 2>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
-    else if (nks == 3) launch_imma_k<L, 3>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
-    else launch_imma_k<L, 4>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    if (nks <= 1) launch_imma_k<L, 1, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    else if (nks == 2) launch_imma_k<L, 2, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    else if (nks == 3) launch_imma_k<L, 3, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    else launch_imma_k<L, 4, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
 }
 
 }  // namespace
@@ -270,22 +322,37 @@ bool hoisted_imma_supported(const Ctx &c, int level, int O, int Q) {
     return (c.h_q[0] >> 40) && (c.h_q[c.count - 1] >> 40);
 }
 
+// words of the 40-bit-limb bank followed by the 60-bit-limb bank (uint32)
 size_t imma_bank_words(const Ctx &c, int level, int Q) {
     const int nks = (Q + 31) / 32;
-    return (size_t)level * c.n * 4 * nks * 32 * 4;
+    return ((size_t)level * IW<5>::MT + 2 * IW<8>::MT) * c.n * nks * 32 * 4;
 }
 
 void imma_mask_bank(const Ctx &c, uint32_t *ib, const uint64_t *masks, int O, int Q, int level, cudaStream_t s) {
     const int L = level + 1, nks = (Q + 31) / 32;
-    const size_t total = (size_t)(L - 1) * c.n * 4 * nks * 32;
-    k_imma_bank<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 32), 256, 0, s>>>(ib, masks, O, Q, L,
-                                                                                           (int)c.logn, nks);
+    const size_t t5 = (size_t)(L - 1) * c.n * IW<5>::MT * nks * 32, t8 = (size_t)2 * c.n * IW<8>::MT * nks * 32;
+    k_imma_bank<5><<<(unsigned)std::min<size_t>((t5 + 255) / 256, 148 * 32), 256, 0, s>>>(ib, masks, O, Q, L,
+                                                                                         (int)c.logn, nks);
+    UH_LAUNCH_CHECK();
+    k_imma_bank<8><<<(unsigned)std::min<size_t>((t8 + 255) / 256, 148 * 32), 256, 0, s>>>(ib + t5 * 4, masks, O, Q, L,
+                                                                                         (int)c.logn, nks);
     UH_LAUNCH_CHECK();
 }
 
 void hoisted_mac_bank_wide(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
                            const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, int level,
                            cudaStream_t s);
+
+// Opt-in (UH_IMMA_WIDE=1): the 8-byte IMMA path for q_0 and P as well.  Bit-exact, measured
+// slower than the IMAD kernel on those two limbs (LeNet conv2 at B = 64: 35.2 vs 33.0 ms for
+// the whole call; 64 byte products and 6 m-tiles per coefficient, two 107 KB CTAs per SM).
+static bool imma_wide_on() {
+    static const bool on = [] {
+        const char *e = getenv("UH_IMMA_WIDE");
+        return e && std::string(e) == "1";
+    }();
+    return on;
+}
 
 void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
                       const uint32_t *ib, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O,
@@ -297,18 +364,27 @@ void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint
     if ((double)I * B * 2 * L * c.n > lim || (double)I * B * L * (L + 1) * c.n > lim ||
         (double)O * B * 2 * (L + 1) * c.n > lim)
         throw std::invalid_argument("IMMA hoisted kernel operand exceeds 2^32 elements: split the batch");
-    hoisted_mac_bank_wide(c, acc, X, D, masks, kbank, shifts, B, I, T, O, level, s);
+    const int nks = (I * T + 31) / 32;
+    const uint32_t *ib8 = ib + (size_t)(L - 1) * c.n * IW<5>::MT * nks * 32 * 4;
+    const bool wide = imma_wide_on();
+    if (!wide) hoisted_mac_bank_wide(c, acc, X, D, masks, kbank, shifts, B, I, T, O, level, s);
+#define UH_IMMA_CASE(LL)                                                               \
+    case LL:                                                                           \
+        if (wide) launch_imma<LL, 8>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s); \
+        launch_imma<LL, 5>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);            \
+        break;
     switch (L) {
-        case 3: launch_imma<3>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
-        case 4: launch_imma<4>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
-        case 5: launch_imma<5>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
-        case 6: launch_imma<6>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
-        case 7: launch_imma<7>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
-        case 8: launch_imma<8>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
-        case 9: launch_imma<9>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
-        case 10: launch_imma<10>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); break;
+        UH_IMMA_CASE(3)
+        UH_IMMA_CASE(4)
+        UH_IMMA_CASE(5)
+        UH_IMMA_CASE(6)
+        UH_IMMA_CASE(7)
+        UH_IMMA_CASE(8)
+        UH_IMMA_CASE(9)
+        UH_IMMA_CASE(10)
         default: throw std::invalid_argument("IMMA hoisted kernel: 3 <= level + 1 <= 10");
     }
+#undef UH_IMMA_CASE
 }
 
 }  // namespace uh

@@ -102,7 +102,8 @@ def imma_bank(backend, masks: torch.Tensor, O: int, Q: int, level: int, cache: b
     if hit is not None and hit[0] is masks:
         return hit[1]
     nks = (Q + 31) // 32
-    ib = torch.empty((level, backend.n, 4, nks, 32, 4), dtype=torch.int32, device=backend.device)
+    # 40-bit limbs q_1..q_level: 4 m-tiles of 3 outputs x 5 bytes; q_0 and P: 6 m-tiles of 2 x 8 bytes
+    ib = torch.empty(((4 * level + 12) * backend.n * nks * 32 * 4,), dtype=torch.int32, device=backend.device)
     backend._call("uh_imma_mask_bank", _vp(ib), _vp(masks), O, Q, level, backend._stream())
     if cache:
         banks[ck] = (masks, ib)
