@@ -33,7 +33,9 @@
 namespace uh {
 namespace {
 
-constexpr int kIC = 8;                      // coefficients per CTA
+#ifndef UH_IMMA_CT2
+#define UH_IMMA_CT2 1  // phase A of the 40-bit limbs: two ciphertexts per item (shared key loads)
+#endif
 constexpr int kICT = 4;                     // ciphertexts per CTA
 constexpr int kIJ = 2 * kICT;               // columns per value byte (ciphertext x component)
 constexpr int kIRow = 144;                  // bytes per (coefficient, byte, column) row: 128 terms + pad
@@ -41,12 +43,13 @@ constexpr int kIMaxTerms = 128;             // 4 k-steps
 // Byte width W of the residues: 5 for the 40-bit limbs (3 outputs x 5 mask bytes per 16-row
 // m-tile, 4 m-tiles), 8 for the 60-bit limbs q_0 and P (2 outputs x 8 bytes, 6 m-tiles).
 template <int W> struct IW {
+    static constexpr int NC = W == 5 ? 8 : 4;           // coefficients per CTA (W = 8: 3 CTAs per SM)
     static constexpr int OPT = W == 5 ? 3 : 2;          // outputs per m-tile
     static constexpr int MT = 12 / OPT;                 // m-tiles for 12 outputs
     static constexpr int COEF = W * kIJ * kIRow + 4;    // coefficient stride of the B planes
     static constexpr int CS = W * 8 + 2;                // C staging row stride (int32)
-    static constexpr size_t SMEM = (size_t)kIC * COEF + 8 * 16 * CS * 4;
-    static constexpr int MINB = W == 5 ? 3 : 2;         // resident CTAs per SM
+    static constexpr size_t SMEM = (size_t)NC * COEF + 8 * 16 * CS * 4;
+    static constexpr int MINB = 3;                      // resident CTAs per SM
 };
 
 __device__ __forceinline__ uint32_t rot_index_i(uint32_t n, uint32_t half, uint32_t r) {
@@ -130,11 +133,11 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
     constexpr uint32_t N = 1u << LOGN, half = N >> 1;
     constexpr uint32_t ROW = (uint32_t)LP << LOGN;
     extern __shared__ __align__(16) unsigned char ism[];
-    int *cst = reinterpret_cast<int *>(ism + (size_t)kIC * C::COEF);
+    int *cst = reinterpret_cast<int *>(ism + (size_t)C::NC * C::COEF);
     __shared__ uint32_t s_x[kIMaxTerms], s_d[kIMaxTerms], s_k[kIMaxTerms], s_r[kIMaxTerms];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int b0 = blockIdx.x * kICT;
-    const uint32_t n0 = blockIdx.y * kIC;
+    const uint32_t n0 = blockIdx.y * C::NC;
     const int slot = blockIdx.z;
     const int k = W == 5 ? 1 + slot : (slot ? L : 0);  // limb: q_1..q_{L-1}, or q_0 / P
     const bool qlimb = k < L;
@@ -154,8 +157,80 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
     // ---- phase A: key-switched P * rot(ct) per (term, ciphertext, coefficient) -> byte planes ----
     // one term per item (Q * 32 items over 256 threads: balanced to within one item per thread);
     // lanes = (ciphertext, coefficient), so the byte stores of a warp hit 32 distinct banks
-    for (int it = tid; it < Q * 32; it += 256) {
-        const int q = it >> 5, ct = (it >> 3) & 3, cf = it & 7;
+#if UH_IMMA_CT2
+    if constexpr (W == 5) {
+        // two ciphertexts per item: the Galois-key rows (2L loads) serve both -- a third fewer
+        // loads through L1, which is the phase's limit (MIO throttle)
+        for (int it = tid; it < Q * 16; it += 256) {
+            const int q = it >> 4, cp = (it >> 3) & 1, cf = it & 7;
+            const int ba = b0 + 2 * cp;
+            const bool oka = ba < B, okb = ba + 1 < B;
+            const uint32_t n = n0 + cf;
+            uint64_t v[2][2] = {{0, 0}, {0, 0}};
+            const uint32_t r = s_r[q];
+            const uint64_t *c0a = X + s_x[q] + (((uint32_t)ba * 2 * L + k) << LOGN);
+            const uint64_t *c0b = c0a + ((uint32_t)(2 * L) << LOGN);
+            if (r == 0) {
+                if (oka) {
+                    v[0][0] = mulmod(Pk, __ldg(c0a + n), m);
+                    v[0][1] = mulmod(Pk, __ldg(c0a + ((uint32_t)L << LOGN) + n), m);
+                }
+                if (okb) {
+                    v[1][0] = mulmod(Pk, __ldg(c0b + n), m);
+                    v[1][1] = mulmod(Pk, __ldg(c0b + ((uint32_t)L << LOGN) + n), m);
+                }
+            } else if (oka) {
+                const uint32_t src = rot_index_i(n, half, r);
+                const uint64_t *Da = D + s_d[q] + (((uint32_t)ba * L * LP + k) << LOGN) + src;
+                const uint64_t *Db = Da + ((uint32_t)(L * LP) << LOGN);
+                const uint64_t *K = kbank + s_k[q] + ((uint32_t)k * 2 * L << LOGN) + n;
+                uint64_t da[L], db[L], x[L], y[L];
+#pragma unroll
+                for (int j = 0; j < L; j++) {
+                    x[j] = __ldg(K + ((uint32_t)(2 * j) << LOGN));
+                    y[j] = __ldg(K + ((uint32_t)(2 * j + 1) << LOGN));
+                    da[j] = __ldg(Da + (uint32_t)j * ROW);
+                    db[j] = okb ? __ldg(Db + (uint32_t)j * ROW) : 0;
+                }
+                const uint64_t csa = __ldg(c0a + src), csb = okb ? __ldg(c0b + src) : 0;
+                AccN a0, a1, e0, e1;
+                a0.zero();
+                a1.zero();
+                e0.zero();
+                e1.zero();
+#pragma unroll
+                for (int j = 0; j < L; j++) {
+                    a0.mac(da[j], x[j]);
+                    a1.mac(da[j], y[j]);
+                    e0.mac(db[j], x[j]);
+                    e1.mac(db[j], y[j]);
+                }
+                a0.mac(Pk, csa);
+                e0.mac(Pk, csb);
+                uint64_t h, l;
+                a0.value(h, l);
+                v[0][0] = csub(barrett_lite(fold64_i(h, l, m), m), m.q);
+                a1.value(h, l);
+                v[0][1] = csub(barrett_lite(fold64_i(h, l, m), m), m.q);
+                if (okb) {
+                    e0.value(h, l);
+                    v[1][0] = csub(barrett_lite(fold64_i(h, l, m), m), m.q);
+                    e1.value(h, l);
+                    v[1][1] = csub(barrett_lite(fold64_i(h, l, m), m), m.q);
+                }
+            }
+            unsigned char *pl = ism + cf * C::COEF + (4 * cp) * kIRow + q;
+#pragma unroll
+            for (int bb = 0; bb < W; bb++)
+#pragma unroll
+                for (int e = 0; e < 4; e++) pl[bb * kIJ * kIRow + e * kIRow] = (unsigned char)(v[e >> 1][e & 1] >> (8 * bb));
+        }
+    }
+    if constexpr (W != 5 || !UH_IMMA_CT2) {
+#endif
+    constexpr int LN = kICT * C::NC;  // lanes per term: (ciphertext, coefficient)
+    for (int it = tid; it < Q * LN; it += 256) {
+        const int q = it / LN, ct = (it / C::NC) & 3, cf = it % C::NC;
         const int b = b0 + ct;
         const uint32_t n = n0 + cf;
         uint64_t v0 = 0, v1 = 0;
@@ -216,6 +291,9 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
             pl[bb * kIJ * kIRow + kIRow] = (unsigned char)(v1 >> (8 * bb));
         }
     }
+#if UH_IMMA_CT2
+    }
+#endif
     // terms [Q, 32 NKS) of the B planes are never written: their A bytes are zero (integer
     // products, so whatever the shared memory holds there contributes nothing)
     __syncthreads();
@@ -224,7 +302,7 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
     const int gid = lane >> 2, tig = lane & 3;
     int *cw = cst + warp * 16 * C::CS;
     const int nmt = (O + C::OPT - 1) / C::OPT;
-    for (int u = warp; u < kIC * C::MT; u += 8) {
+    for (int u = warp; u < C::NC * C::MT; u += 8) {
         const int cf = u / C::MT, mt = u % C::MT;
         if (mt >= nmt) continue;
         const uint32_t n = n0 + cf;
@@ -295,7 +373,7 @@ void launch_imma_k(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_
                                       (int)IW<W>::SMEM));
         done = true;
     }
-    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / kIC), W == 5 ? L - 1 : 2);
+    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / IW<W>::NC), W == 5 ? L - 1 : 2);
     k_hoisted_imma<L, 15, NKS, W><<<grid, 256, IW<W>::SMEM, s>>>(acc, X, D, reinterpret_cast<const uint4 *>(ib), kbank,
                                                                 shifts, B, I, T, O, c.sp(), c.d_mods);
     UH_LAUNCH_CHECK();
