@@ -28,6 +28,8 @@
 //             the byte recombination and the modular reduction per output.
 // The 60-bit limbs (q_0, P) keep the IMAD kernel (hoisted_mac_bank_wide) by default; the same
 // kernel with 8-byte operands (64 byte products, 2 outputs per m-tile) is opt-in.
+#include <type_traits>
+
 #include "ops.cuh"
 
 namespace uh {
@@ -49,7 +51,7 @@ template <int W> struct IW {
     static constexpr int COEF = W * kIJ * kIRow + 4;    // coefficient stride of the B planes
     static constexpr int CS = W * 8 + 2;                // C staging row stride (int32)
     static constexpr size_t SMEM = (size_t)NC * COEF + 8 * 16 * CS * 4;
-    static constexpr int MINB = 3;                      // resident CTAs per SM
+    static constexpr int MINB = W == 5 ? 3 : 2;         // resident CTAs per SM (W = 8: 128 registers, no spills)
 };
 
 __device__ __forceinline__ uint32_t rot_index_i(uint32_t n, uint32_t half, uint32_t r) {
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
     const uint32_t n0 = blockIdx.y * C::NC;
     const int slot = blockIdx.z;
     const int k = W == 5 ? 1 + slot : (slot ? L : 0);  // limb: q_1..q_{L-1}, or q_0 / P
-    const bool qlimb = k < L;
+    const bool qlimb = W == 5 || k < L;  // the 40-bit slots are all q-limbs
     const Mod m = mods[qlimb ? k : sp];
     const uint64_t P = mods[sp].q;
     const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
@@ -158,11 +160,12 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
     // one term per item (Q * 32 items over 256 threads: balanced to within one item per thread);
     // lanes = (ciphertext, coefficient), so the byte stores of a warp hit 32 distinct banks
 #if UH_IMMA_CT2
-    if constexpr (W == 5) {
+    {
         // two ciphertexts per item: the Galois-key rows (2L loads) serve both -- a third fewer
         // loads through L1, which is the phase's limit (MIO throttle)
-        for (int it = tid; it < Q * 16; it += 256) {
-            const int q = it >> 4, cp = (it >> 3) & 1, cf = it & 7;
+        constexpr int LH = 2 * C::NC;  // lanes per term: (ciphertext pair, coefficient)
+        for (int it = tid; it < Q * LH; it += 256) {
+            const int q = it / LH, cp = (it / C::NC) & 1, cf = it % C::NC;
             const int ba = b0 + 2 * cp;
             const bool oka = ba < B, okb = ba + 1 < B;
             const uint32_t n = n0 + cf;
@@ -171,11 +174,11 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
             const uint64_t *c0a = X + s_x[q] + (((uint32_t)ba * 2 * L + k) << LOGN);
             const uint64_t *c0b = c0a + ((uint32_t)(2 * L) << LOGN);
             if (r == 0) {
-                if (oka) {
+                if (oka && qlimb) {
                     v[0][0] = mulmod(Pk, __ldg(c0a + n), m);
                     v[0][1] = mulmod(Pk, __ldg(c0a + ((uint32_t)L << LOGN) + n), m);
                 }
-                if (okb) {
+                if (okb && qlimb) {
                     v[1][0] = mulmod(Pk, __ldg(c0b + n), m);
                     v[1][1] = mulmod(Pk, __ldg(c0b + ((uint32_t)L << LOGN) + n), m);
                 }
@@ -192,8 +195,9 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
                     da[j] = __ldg(Da + (uint32_t)j * ROW);
                     db[j] = okb ? __ldg(Db + (uint32_t)j * ROW) : 0;
                 }
-                const uint64_t csa = __ldg(c0a + src), csb = okb ? __ldg(c0b + src) : 0;
-                AccN a0, a1, e0, e1;
+                const uint64_t csa = qlimb ? __ldg(c0a + src) : 0, csb = qlimb && okb ? __ldg(c0b + src) : 0;
+                using A = typename std::conditional<W == 5, AccN, Acc>::type;
+                A a0, a1, e0, e1;
                 a0.zero();
                 a1.zero();
                 e0.zero();
@@ -205,18 +209,24 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
                     e0.mac(db[j], x[j]);
                     e1.mac(db[j], y[j]);
                 }
-                a0.mac(Pk, csa);
-                e0.mac(Pk, csb);
-                uint64_t h, l;
-                a0.value(h, l);
-                v[0][0] = csub(barrett_lite(fold64_i(h, l, m), m), m.q);
-                a1.value(h, l);
-                v[0][1] = csub(barrett_lite(fold64_i(h, l, m), m), m.q);
+                if (qlimb) {
+                    a0.mac(Pk, csa);
+                    e0.mac(Pk, csb);
+                }
+                auto fin = [&](const A &acc) -> uint64_t {
+                    if constexpr (W == 5) {
+                        uint64_t h, l;
+                        acc.value(h, l);
+                        return csub(barrett_lite(fold64_i(h, l, m), m), m.q);
+                    } else {
+                        return acc.reduce(m);
+                    }
+                };
+                v[0][0] = fin(a0);
+                v[0][1] = fin(a1);
                 if (okb) {
-                    e0.value(h, l);
-                    v[1][0] = csub(barrett_lite(fold64_i(h, l, m), m), m.q);
-                    e1.value(h, l);
-                    v[1][1] = csub(barrett_lite(fold64_i(h, l, m), m), m.q);
+                    v[1][0] = fin(e0);
+                    v[1][1] = fin(e1);
                 }
             }
             unsigned char *pl = ism + cf * C::COEF + (4 * cp) * kIRow + q;
@@ -226,7 +236,7 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
                 for (int e = 0; e < 4; e++) pl[bb * kIJ * kIRow + e * kIRow] = (unsigned char)(v[e >> 1][e & 1] >> (8 * bb));
         }
     }
-    if constexpr (W != 5 || !UH_IMMA_CT2) {
+    if constexpr (!UH_IMMA_CT2) {
 #endif
     constexpr int LN = kICT * C::NC;  // lanes per term: (ciphertext, coefficient)
     for (int it = tid; it < Q * LN; it += 256) {
