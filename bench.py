@@ -292,10 +292,14 @@ def main():
             if t.get("batch") == B:
                 traffic = t["dram_bytes_per_launch"]
         roofline = {"bound": "imad",
-                    "bound_note": "integer-pipe bound (64-bit modular MACs as IMAD.WIDE.U32 chains): neither the HBM "
-                                  "roofline (this kernel moves 9.2 GB at ~180 GB/s, see hbm_*) nor tensor cores apply "
-                                  "-- modular integer work with per-coefficient weight matrices",
-                    "kernel": f"k_hoisted_mac (LeNet conv2, level {lev}: hoisted key switch + weight MAC)",
+                    "bound_note": "integer-pipe bound: the hoisted key-switch inner products (35% of the algorithmic "
+                                  "modMACs) and the 60-bit limbs q_0, P run as IMAD.WIDE.U32 chains; the weight-mask "
+                                  "contraction of the 40-bit limbs (the other 65% on 5 of 7 limbs) runs exactly on the "
+                                  "tensor cores as byte-split u8 IMMA (tensor pipe ~8% active), so frac is the speed "
+                                  "relative to an all-IMAD roofline.  Not HBM-bound (9 GB per launch at ~280 GB/s, "
+                                  "see hbm_*)",
+                    "kernel": f"LeNet conv2 hoisted MAC, level {lev}: k_hoisted_imma (q_1..q_{lev}: key inner "
+                              f"products on IMAD + mask contraction on IMMA) + k_hoisted_bank (q_0, P on IMAD)",
                     "achieved": achieved, "peak": peak, "unit": "T modMAC/s", "frac": achieved / peak,
                     "traffic": traffic, "launch_ms": tms / cnt, "algorithmic_macs_per_launch": work / cnt,
                     "share_of_step": tms / ms, "conv_mac_share_of_step": conv_ms / ms,
