@@ -35,6 +35,9 @@
 namespace uh {
 namespace {
 
+#ifndef UH_IMMA_MIN_O
+#define UH_IMMA_MIN_O 5  // narrower layers stay on the register-only IMAD kernel
+#endif
 #ifndef UH_IMMA_CT2
 #define UH_IMMA_CT2 1  // phase A of the 40-bit limbs: two ciphertexts per item (shared key loads)
 #endif
@@ -404,7 +407,7 @@ void launch_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t 
 // Applicable when N = 2^15, the level has 40-bit limbs q_1..q_{L-1} (< 2^40) and 60-bit
 // q_0 and P, 5..12 dense masked outputs and at most 128 terms.
 bool hoisted_imma_supported(const Ctx &c, int level, int O, int Q) {
-    if (c.logn != 15 || level < 2 || level + 1 > 10 || O < 5 || O > 12 || Q < 1 || Q > kIMaxTerms) return false;
+    if (c.logn != 15 || level < 2 || level + 1 > 10 || O < UH_IMMA_MIN_O || O > 12 || Q < 1 || Q > kIMaxTerms) return false;
     for (int k = 1; k <= level; k++)
         if (c.h_q[k] >> 40) return false;
     return (c.h_q[0] >> 40) && (c.h_q[c.count - 1] >> 40);

@@ -317,9 +317,19 @@ struct P1 {
     static constexpr int GC = R1 * 32 / kThreads;  // contiguous groups per thread
 };
 
+// centred lift of a canonical residue x mod p into q (as load_t<1>, from a register)
+__device__ __forceinline__ uint64_t lift_reg(uint64_t x, uint64_t p, const Mod &m, bool red) {
+    const bool neg = x > ((p - 1) >> 1);
+    uint64_t v = neg ? p - x : x;
+    if (red) v = csub(barrett_lite(v, m), m.q);
+    const uint64_t nv = v ? m.q - v : 0;
+    return neg ? nv : v;
+}
+
 template <int A, int LM, bool FP, bool OUT_SM = false>
 __device__ __forceinline__ void fwd_p1_body(uint64_t *sm, const LimbInfo &li, const Mod &m, bool red,
-                                            const Tw &tws, uint64_t *out, int n2, int col, int lane, int wq) {
+                                            const Tw &tws, uint64_t *out, int n2, int col, int lane, int wq,
+                                            const uint64_t *tile = nullptr) {
     using C = P1<A>;
     using AR = Arith<FP>;
     using V = typename AR::V;
@@ -330,7 +340,10 @@ __device__ __forceinline__ void fwd_p1_body(uint64_t *sm, const LimbInfo &li, co
         const int r0 = wq + 8 * g;  // < S1
         V v[C::R1];
 #pragma unroll
-        for (int x = 0; x < C::R1; x++) v[x] = AR::in(load_t<LM>(li, (size_t)(r0 + C::S1 * x) * n2 + col, m, red));
+        for (int x = 0; x < C::R1; x++)
+            v[x] = AR::in(tile ? lift_reg(tile[(r0 + C::S1 * x) * 32 + lane], li.qsrc, m, red)  // ModUp from a
+                                                                                                // coefficient tile
+                               : load_t<LM>(li, (size_t)(r0 + C::S1 * x) * n2 + col, m, red));
         fwd_strided<C::R1>(v, TwG<typename AR::W>{T, 1}, 1, 0, ar.qv());
 #pragma unroll
         for (int x = 0; x < C::R1; x++) sm[(r0 + C::S1 * x) * 32 + lane] = AR::raw(v[x]);
@@ -377,7 +390,8 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p1(NttJob J, uint
 
 template <int A, bool FP>
 __device__ __forceinline__ void inv_pb_body(uint64_t *sm, const LimbInfo &li, const Mod &m, const Tw &tws,
-                                            const uint64_t *in, int n2, int col, int lane, int wq) {
+                                            const uint64_t *in, int n2, int col, int lane, int wq,
+                                            uint64_t *tile = nullptr) {
     using C = P1<A>;
     using AR = Arith<FP>;
     using V = typename AR::V;
@@ -412,8 +426,59 @@ __device__ __forceinline__ void inv_pb_body(uint64_t *sm, const LimbInfo &li, co
                 r = ar.canon(fmm(v[x], nf, ar.q));
             else
                 r = csub(shoup_lazy(v[x], m.ninv, m.ninvs, m.q), m.q);
-            li.dst[(size_t)(r0 + C::S1 * x) * n2 + col] = r;
+            if (tile)
+                tile[(r0 + C::S1 * x) * 32 + lane] = r;
+            else
+                li.dst[(size_t)(r0 + C::S1 * x) * n2 + col] = r;
         }
+    }
+}
+
+#ifndef UH_MODUP_MINB
+#define UH_MODUP_MINB 3
+#endif
+// ModUp with the inverse NTT's last pass and the forward NTTs' first pass fused: CTA (column
+// block, poly p x digit j) finishes the inverse transform of digit j into a coefficient tile in
+// shared memory and runs forward pass 1 of every target limb k != j from that tile (centred
+// lift of q_j into q_k in the load) -- the coefficient-form digits never go through HBM, and
+// the L forward pass-1 loads of a digit become shared-memory reads.
+template <int A>
+__global__ void __launch_bounds__(kThreads, UH_MODUP_MINB) k_modup_pbp1(NttJob Ji, NttJob Jf, const uint64_t *__restrict__ ti,
+                                                       uint64_t *__restrict__ tf, int logn,
+                                                       const Mod *__restrict__ mods,
+                                                       const ulonglong2 *__restrict__ itwd,
+                                                       const double2 *__restrict__ itwf,
+                                                       const ulonglong2 *__restrict__ twd,
+                                                       const double2 *__restrict__ twf) {
+    extern __shared__ uint64_t msm[];
+    uint64_t *sm = msm, *tile = msm + P1<A>::N1 * 32;
+    const int pj = blockIdx.y, lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int n2 = 1 << (logn - A);
+    const int col = blockIdx.x * 32 + lane;
+    {
+        const LimbInfo li = limb_info(Ji, pj, logn, mods);
+        const Mod m = mods[li.mod];
+        const Tw tws{itwd + ((size_t)li.mod << logn), itwf + ((size_t)li.mod << logn)};
+        const uint64_t *in = ti + ((size_t)pj << logn);
+        if (fp_limb(m.q))
+            inv_pb_body<A, true>(sm, li, m, tws, in, n2, col, lane, wq, tile);
+        else
+            inv_pb_body<A, false>(sm, li, m, tws, in, n2, col, lane, wq, tile);
+    }
+    const int L = Jf.L;
+#pragma unroll 1
+    for (int kk = 0; kk < L; kk++) {
+        __syncthreads();  // tile complete / previous target done with the exchange buffer
+        const int f = pj * L + kk;
+        const LimbInfo li = limb_info(Jf, f, logn, mods);
+        const Mod m = mods[li.mod];
+        const bool red = ((li.qsrc - 1) >> 1) >= m.q;
+        const Tw tws{twd + ((size_t)li.mod << logn), twf + ((size_t)li.mod << logn)};
+        uint64_t *out = tf + ((size_t)f << logn);
+        if (fp_limb(m.q))
+            fwd_p1_body<A, 1, true>(sm, li, m, red, tws, out, n2, col, lane, wq, tile);
+        else
+            fwd_p1_body<A, 1, false>(sm, li, m, red, tws, out, n2, col, lane, wq, tile);
     }
 }
 
@@ -1357,6 +1422,46 @@ void run_inv(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
 }  // namespace
 
 bool ntt_fast_supported(const Ctx &c) { return c.logn >= 13 && c.logn <= 15; }
+
+#ifndef UH_MODUP_FUSED
+#define UH_MODUP_FUSED 0  // opt-in: bit-exact, measured slower (ModUp 0.310 vs 0.302 us/limb, step 124.3 vs 123.3 ms)
+#endif
+// ModUp of n_polys polys of L limbs (strided rows `in`, pstride in_ps) into D [p][j][L+1][N]
+// except the diagonal limbs: inverse pass A -> fused inverse pass B + forward pass 1 -> forward
+// pass 2.  Returns false (nothing launched) where the fused path does not apply.
+bool ntt_fast_modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int L, int in_ps, cudaStream_t s) {
+    if (!UH_MODUP_FUSED || c.logn != 15 || pair_ntt_on() || fused_ntt_on()) return false;
+    constexpr int A = 7, B = 8;
+    const long long npj = (long long)n_polys * L, nf = npj * L;
+    if (nf > 65535 || L < 2) return false;
+    NttJob Ji;
+    Ji.nl = L;
+    Ji.nq = L;
+    Ji.sp = c.sp();
+    Ji.src = in;
+    Ji.src_ps = in_ps;
+    NttJob Jf;
+    Jf.mode = NTT_MODUP;
+    Jf.L = L;
+    Jf.sp = c.sp();
+    Jf.dst = D;
+    Scratch ti((size_t)npj * c.n * 8, s), tf((size_t)nf * c.n * 8, s);
+    constexpr size_t sm2 = p2_smem<B>();
+    p2_attr<k_inv_pa<B>>(sm2);
+    k_inv_pa<B><<<dim3((1u << A) / P2<B>::G, (unsigned)npj), kThreads, sm2, s>>>(
+        Ji, ti.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwd, c.d_itwf, c.d_bsel, c.d_csl, c.d_itwist);
+    UH_LAUNCH_CHECK();
+    constexpr size_t sm1 = (size_t)2 * P1<A>::N1 * 32 * 8;
+    p2_attr<k_modup_pbp1<A>>(sm1);
+    k_modup_pbp1<A><<<dim3((1u << B) / 32, (unsigned)npj), kThreads, sm1, s>>>(
+        Ji, Jf, ti.as<uint64_t>(), tf.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwf, c.d_tw2, c.d_twf);
+    UH_LAUNCH_CHECK();
+    p2_attr<k_fwd_p2<B, 0>>(sm2);
+    k_fwd_p2<B, 0><<<dim3((1u << A) / P2<B>::G, (unsigned)nf), kThreads, sm2, s>>>(
+        Jf, tf.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl, c.d_twist);
+    UH_LAUNCH_CHECK();
+    return true;
+}
 
 void ntt_fast_forward(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s) {
     if (limbs <= 0) return;

@@ -42,5 +42,6 @@ struct NttJob {
 bool ntt_fast_supported(const Ctx &c);
 void ntt_fast_forward(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s);
 void ntt_fast_inverse(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s);
+bool ntt_fast_modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int L, int in_ps, cudaStream_t s);
 
 }  // namespace uh
