@@ -35,6 +35,9 @@
 namespace uh {
 namespace {
 
+#ifndef UH_IMMA_LDSM
+#define UH_IMMA_LDSM 0  // B fragments via ldmatrix (16-byte aligned planes): bit-exact, measured 31.9 vs 31.6 ms (the aligned planes cost phase-A store conflicts)
+#endif
 #ifndef UH_IMMA_MIN_O
 #define UH_IMMA_MIN_O 5  // narrower layers stay on the register-only IMAD kernel
 #endif
@@ -51,7 +54,7 @@ template <int W> struct IW {
     static constexpr int NC = W == 5 ? 8 : 4;           // coefficients per CTA (W = 8: 3 CTAs per SM)
     static constexpr int OPT = W == 5 ? 3 : 2;          // outputs per m-tile
     static constexpr int MT = 12 / OPT;                 // m-tiles for 12 outputs
-    static constexpr int COEF = W * kIJ * kIRow + 4;    // coefficient stride of the B planes
+    static constexpr int COEF = W * kIJ * kIRow + (UH_IMMA_LDSM ? 16 : 4);  // coefficient stride of the B planes
     static constexpr int CS = W * 8 + 2;                // C staging row stride (int32)
     static constexpr size_t SMEM = (size_t)NC * COEF + 8 * 16 * CS * 4;
     static constexpr int MINB = W == 5 ? 3 : 2;         // resident CTAs per SM (W = 8: 128 registers, no spills)
@@ -326,6 +329,32 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
         int Cr[W][4];
 #pragma unroll
         for (int nb = 0; nb < W; nb++) Cr[nb][0] = Cr[nb][1] = Cr[nb][2] = Cr[nb][3] = 0;
+#if UH_IMMA_LDSM
+        // B fragments with ldmatrix: x4 = (k 0-15, k 16-31) of two k-steps, lane l addresses row
+        // l % 8 of matrix l / 8 (16-byte rows: COEF is a multiple of 16)
+        {
+            const uint32_t lb = (uint32_t)__cvta_generic_to_shared(ism + cf * C::COEF + (lane & 7) * kIRow +
+                                                                   ((lane >> 3) & 1) * 16 + (lane >> 4) * 32);
+#pragma unroll
+            for (int nb = 0; nb < W; nb++) {
+#pragma unroll
+                for (int ks = 0; ks < NKS; ks += 2) {
+                    uint32_t r0, r1, r2, r3;
+                    const uint32_t a = lb + nb * kIJ * kIRow + ks * 32;
+                    if (ks + 1 < NKS) {
+                        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                                     : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(a));
+                        imma(Cr[nb], A[ks], r0, r1);
+                        imma(Cr[nb], A[ks + 1], r2, r3);
+                    } else {
+                        asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+                                     : "=r"(r0), "=r"(r1) : "r"(a));
+                        imma(Cr[nb], A[ks], r0, r1);
+                    }
+                }
+            }
+        }
+#else
         const unsigned char *bp = ism + cf * C::COEF + gid * kIRow + tig * 4;
 #pragma unroll
         for (int ks = 0; ks < NKS; ks++)
@@ -335,6 +364,7 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
                 imma(Cr[nb], A[ks], *reinterpret_cast<const uint32_t *>(p),
                      *reinterpret_cast<const uint32_t *>(p + 16));
             }
+#endif
 #pragma unroll
         for (int nb = 0; nb < W; nb++) {
             const int col = nb * 8 + tig * 2;
