@@ -42,11 +42,12 @@ int uh_abi_version(void);
 const char *uh_last_error(void);
 /* Number of engine kernel launches so far in this process (bench evidence). */
 unsigned long long uh_launch_count(void);
-/* Integer-pipe peaks measured on the context's device (HOST array of >= 9):
+/* Integer-pipe peaks measured on the context's device (HOST array of >= 16):
  * IMAD/s, lazy 128-bit multiply-accumulate/s (engine form), reduced 64-bit
  * mulmod/s, 128-bit MAC/s in plain-C form, lazy Shoup products/s, exact FP64
  * modMAC/s, mixed IMAD+FP64 MAC/s, split-accumulator MAC/s, narrow-operand
- * (q < 2^41) MAC/s. */
+ * (q < 2^41) MAC/s, u8 IMMA MAC/s (mma.sync m16n8k32), FP64 FMA/s: 11 entries
+ * (the caller's buffer holds at least 16). */
 int uh_bench_peaks(uh_ctx *ctx, double *rates);
 
 /* Parameter set -> device context.  Replaces HEParams' role as the space

@@ -148,6 +148,8 @@ class Oracle:
     """numpy-level access to the C oracle for one parameter set."""
 
     def __init__(self, params: HEParams):
+        if params.seed is None:
+            raise ValueError("the oracle reproduces seeded keys: give HEParams an explicit seed")
         self.params = params
         self.chain = rns_chain(params)
         self.n = params.poly_degree
@@ -316,11 +318,14 @@ class Oracle:
         s2 = self.mul(s_eval, s_eval, mods)
         return self.switching_key(s_eval, s2, RELIN_ID, level)
 
-    def encrypt_eval(self, m_eval: np.ndarray, s_eval: np.ndarray, level: int, ct_id: int) -> np.ndarray:
-        """Secret-key encryption: (c0, c1) = (-a*s + e + m, a)."""
+    def encrypt_eval(self, m_eval: np.ndarray, s_eval: np.ndarray, level: int, ct_id: int,
+                     enc_seed: int | None = None) -> np.ndarray:
+        """Secret-key encryption: (c0, c1) = (-a*s + e + m, a); the nonce stream is ``enc_seed``
+        (default: the parameter seed, the GPU backend's ``reproducible=True`` mode)."""
         mods = self.q_mods(level)
-        a = self.sample_uniform(stream(self.params.seed, TAG_ENC_A, ct_id, 0), mods)
-        e = self.sample_cbd(stream(self.params.seed, TAG_ENC_E, ct_id, 0))
+        es = self.params.seed if enc_seed is None else enc_seed
+        a = self.sample_uniform(stream(es, TAG_ENC_A, ct_id, 0), mods)
+        e = self.sample_cbd(stream(es, TAG_ENC_E, ct_id, 0))
         e_ev = self.ntt(self.from_signed(e, mods), mods)
         c0 = self.add(self.sub(e_ev, self.mul(a, s_eval[: level + 1], mods), mods), m_eval, mods)
         return np.stack([c0, a])
@@ -365,6 +370,11 @@ class OracleBackend:
         from paper_2402_03060_b200.errors import LevelExhausted, OversizedInput, SlotMismatch  # shared taxonomy
 
         self._errs = (LevelExhausted, OversizedInput, SlotMismatch)
+        if params.seed is None:  # unseeded parameters: a fresh secret, as the GPU backend does
+            import dataclasses
+            import os
+
+            params = dataclasses.replace(params, seed=int.from_bytes(os.urandom(8), "little"))
         self.params = params
         self.o = Oracle(params)
         self.n = params.poly_degree

@@ -5,7 +5,7 @@ float64 slot simulator: np.roll rotations, elementwise products, one level
 per multiplication, optional fixed-point quantisation) so the schedule and
 the decrypted-output parity can be checked on the GPU box, where the
 reference package is absent.  Pinned against the reference itself by
-tests/test_schedule_vs_reference.py and the golden vectors in tests/golden/.
+tests/test_schedule_and_golden.py and the golden vectors in tests/golden/.
 Batch-aware (values may be [B, slots]) so the batched driver and the
 multi-rank sharding can be exercised on CPU.
 """

@@ -298,7 +298,7 @@ __attribute__((visibility("default"))) int uh_conv_hoisted_mac(uh_ctx *ctx, uint
         const uh::Ctx &c = C(ctx);
         check_level(c, level);
         need(B > 0 && I > 0 && T > 0 && O > 0 && xls >= level + 1, "bad shape");
-        uh::conv_hoisted_mac(c, acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, level, S(stream));
+        uh::hoisted_mac(c, acc, X, xls, D, masks, keys, key_limbs, shifts, B, I, T, O, 0, level, S(stream));
     });
 }
 
@@ -310,7 +310,8 @@ __attribute__((visibility("default"))) int uh_rot_sum_hoisted(uh_ctx *ctx, uint6
         const uh::Ctx &c = C(ctx);
         check_level(c, level);
         need(B > 0 && C_ > 0 && T > 0 && xls >= level + 1, "bad shape");
-        uh::rot_sum_hoisted(c, out, X, xls, D, keys, key_limbs, shifts, B, C_, T, level, S(stream));
+        // channels ride the batch dimension, no masks: out[ch][b] = sum_t P * rot_t(ct[ch][b])
+        uh::hoisted_mac(c, out, X, xls, D, nullptr, keys, key_limbs, shifts, C_ * B, 1, T, 1, 0, level, S(stream));
     });
 }
 

@@ -41,7 +41,8 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
         if (moduli[i] >= (1ULL << 62) || moduli[i] % (2ULL * n) != 1)
             throw std::invalid_argument("every modulus must be < 2^62 and congruent to 1 mod 2N");
     }
-    UH_CHECK(cudaSetDevice(device));
+    // the caller's current device is restored on return (torch keeps its own notion of it)
+    DeviceGuard guard(device);
     // Scratch comes from the device's default stream-ordered pool; keep freed
     // blocks cached across synchronisations instead of returning them to the
     // driver (the default threshold 0 would re-map pages every step).
@@ -153,32 +154,6 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
     if (c->n1) {
         c->d_bsel = upload(bsel);
         c->d_csl = upload(csl);
-        // pass-2 twists (ntt_fast.cu): block blk of the N1 x N2 view is the twisted NTT whose
-        // stage-s twiddles factor as beta^(N2 / 2^(s+1)) * W[g], beta = psi^brv(N1 + blk) over
-        // log2(N1) + 1 bits; multiplying element c by beta^c first leaves the shared twiddles
-        // W[0 .. N2/2) for every block (and the inverse ends with beta^-c).
-        const uint32_t n1 = c->n1, n2 = c->n2;
-        uint32_t a1 = 0;
-        while ((1u << a1) < 2 * n1) a1++;
-        std::vector<double> twist((size_t)count * n, 0.0), itwist((size_t)count * n, 0.0);
-        for (uint32_t m = 0; m < count; m++) {
-            const uint64_t q = moduli[m];
-            if ((q >> 42) != 0) continue;  // integer-path limbs keep the per-block twiddles
-            const uint64_t ip = h_inv(psi[m], q);
-            for (uint32_t blk = 0; blk < n1; blk++) {
-                const uint32_t e = h_brv(n1 + blk, a1);
-                const uint64_t beta = h_pow(psi[m], e, q), ibeta = h_pow(ip, e, q);
-                uint64_t f = 1, fi = 1;
-                for (uint32_t cc = 0; cc < n2; cc++) {
-                    twist[(size_t)m * n + (size_t)blk * n2 + cc] = (double)f;
-                    itwist[(size_t)m * n + (size_t)blk * n2 + cc] = (double)fi;
-                    f = h_mulmod(f, beta, q);
-                    fi = h_mulmod(fi, ibeta, q);
-                }
-            }
-        }
-        c->d_twist = upload(twist);
-        c->d_itwist = upload(itwist);
     }
     // (q_t * P)^-1 mod q_k: the fused ModDown + rescale epilogue (one Shoup product)
     std::vector<uint64_t> inv2((size_t)count * count, 0), inv2s((size_t)count * count, 0);
@@ -217,27 +192,16 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
     c->d_invs = upload(invs);
     c->d_pos = upload(pos);
     c->d_neg = upload(neg);
-    if (n >= 8192 && n <= 65536) {
-        // half-limb forward NTT (ntt_fast.cu, k_fwd_half): output index k and its slot lie in the same half
-        std::vector<uint16_t> hpos(n);
-        for (uint32_t k = 0; k < n; k++) {
-            const uint32_t s = (uint32_t)sob[k];
-            if (s / half != k / half) throw std::logic_error("NTT half-output invariant violated");
-            hpos[s] = (uint16_t)(k % half);
-        }
-        c->d_hpos = upload(hpos);
-    }
     return c;
 }
 
 void ctx_destroy(Ctx *c) {
     if (!c) return;
-    cudaSetDevice(c->device);
-    for (void *p : {(void *)c->d_pmod, (void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_twf, (void *)c->d_itwf, (void *)c->d_twd, (void *)c->d_itwd, (void *)c->d_twist, (void *)c->d_itwist, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
+    DeviceGuard guard(c->device);
+    for (void *p : {(void *)c->d_pmod, (void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_twf, (void *)c->d_itwf, (void *)c->d_twd, (void *)c->d_itwd, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
                     (void *)c->d_ipsi, (void *)c->d_ipsis,
-                    (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_inv2, (void *)c->d_inv2s, (void *)c->d_pos, (void *)c->d_neg, (void *)c->d_hpos})
+                    (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_inv2, (void *)c->d_inv2s, (void *)c->d_pos, (void *)c->d_neg})
         if (p) cudaFree(p);
-    for (auto &e : c->ntt_sel) cudaFree(e.second);
     delete c;
 }
 

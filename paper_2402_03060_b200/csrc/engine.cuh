@@ -24,7 +24,6 @@ struct Ctx {
     ulonglong2 *d_tw2 = nullptr, *d_itw2 = nullptr;  // [count][n] interleaved (w, w') pairs of the above
     double2 *d_twf = nullptr, *d_itwf = nullptr;     // [count][n] (w, w / q) for FP64-pipe limbs (q < 2^42), else 0
     double *d_twd = nullptr, *d_itwd = nullptr;       // [count][n] w as double (FP64-pipe limbs), else 0
-    double *d_twist = nullptr, *d_itwist = nullptr;   // [count][n] pass-2 block twists beta_X^(+-c) (FP64 limbs)
     int32_t *d_sob = nullptr;            // [n] slot-order index of bit-reversed NTT output k
     int32_t *d_bsel = nullptr;           // [n1] pass-2 block of CTA x, position g (ntt_fast.cu)
     int32_t *d_csl = nullptr;            // [n] element index inside its pass-2 block, per slot
@@ -33,9 +32,6 @@ struct Ctx {
     ulonglong2 *d_pmod = nullptr;        // [count] (P mod q_i, Shoup companion)
     int32_t *d_pos = nullptr;            // [n/2] index (5^j mod 2N - 1)/2 : slot j -> odd exponent slot
     int32_t *d_neg = nullptr;            // [n/2] index (2N - 5^j - 1)/2
-    uint16_t *d_hpos = nullptr;          // [n] slot h*n/2 + j -> index inside half h of the bit-reversed NTT output (ntt_fast.cu, k_fwd_half)
-    // per-job-shape limb selections of the forward NTT (FP64 limbs first, then the rest), one period each
-    std::vector<std::pair<uint64_t, int16_t *>> ntt_sel;
     int sp() const { return (int)count - 1; }
 };
 
@@ -57,6 +53,35 @@ extern std::atomic<unsigned long long> g_launch_count;
         ::uh::g_launch_count.fetch_add(1, std::memory_order_relaxed); \
         UH_CHECK(cudaGetLastError());                              \
     } while (0)
+
+// Switch to `device` for a scope and restore the caller's current device afterwards.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int device) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != device) UH_CHECK(cudaSetDevice(device));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard &) = delete;
+    DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
+
+// Opt a kernel in to > 48 KB of dynamic shared memory on the current device.  The
+// attribute is per device, so the "done" record is a per-instance device bitmask
+// (setting it twice is harmless, so concurrent first calls need no lock).
+template <class K>
+void smem_optin(K *kernel, size_t smem) {
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    UH_CHECK(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_relaxed) & bit) return;
+    UH_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done.fetch_or(bit, std::memory_order_relaxed);
+}
 
 // stream-ordered scratch buffer
 struct Scratch {

@@ -690,12 +690,10 @@ void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const 
             // two cp.async stages: D [3][8][L][32] + C [3][8][32] + K [3][2L][32] words each
             const size_t smem = 2 * (size_t)(kTChunk * kTBatch * L * 32 + kTChunk * kTBatch * 32 +
                                              kTChunk * 2 * L * 32) * sizeof(uint64_t);
-            static size_t configured = 0;  // opt in to > 48 KB dynamic shared memory (up to 192 KB at L = 12)
-            if (smem > configured) {
-                UH_CHECK(cudaFuncSetAttribute(k_hoisted_mac_cp<PP, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)smem));
-                configured = smem;
-            }
+            // opt in to > 48 KB dynamic shared memory once per device, at the largest L (12): 192 KB
+            smem_optin(k_hoisted_mac_cp<PP, WW>,
+                       2 * (size_t)(kTChunk * kTBatch * 12 * 32 + kTChunk * kTBatch * 32 + kTChunk * 2 * 12 * 32) *
+                           sizeof(uint64_t));
             k_hoisted_mac_cp<PP, WW><<<grid, WW * 32, smem, s>>>(acc, X, xls, D, masks, keys, key_limbs, shifts, B,
                                                                  I, T, O, diag, L, c.sp(), (int)c.logn, c.d_mods);
         } else {

@@ -410,12 +410,7 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
 template <int L, int NKS, int W>
 void launch_imma_k(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib,
                    const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
-    static bool done = false;  // one opt-in per kernel instance
-    if (!done) {
-        UH_CHECK(cudaFuncSetAttribute(k_hoisted_imma<L, 15, NKS, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)IW<W>::SMEM));
-        done = true;
-    }
+    smem_optin(k_hoisted_imma<L, 15, NKS, W>, IW<W>::SMEM);
     dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / IW<W>::NC), W == 5 ? L - 1 : 2);
     k_hoisted_imma<L, 15, NKS, W><<<grid, 256, IW<W>::SMEM, s>>>(acc, X, D, reinterpret_cast<const uint4 *>(ib), kbank,
                                                                 shifts, B, I, T, O, c.sp(), c.d_mods);

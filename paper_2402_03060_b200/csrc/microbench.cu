@@ -207,6 +207,46 @@ __global__ void k_macn_peak(uint64_t *out, int iters, uint64_t seed) {
     if (s == 0x1234567812345678ull) out[0] = s;
 }
 
+// u8 tensor-core MACs through the legacy warp-level path the engine uses (mma.sync m16n8k32
+// -> IMMA.16832): 8 independent accumulator tiles per warp, 16 * 8 * 32 MACs per instruction
+__global__ void k_imma_peak(uint64_t *out, int iters, uint32_t seed) {
+    uint32_t a[4], b[2];
+#pragma unroll
+    for (int i = 0; i < 4; i++) a[i] = seed * (threadIdx.x + i + 1);
+#pragma unroll
+    for (int i = 0; i < 2; i++) b[i] = seed ^ (threadIdx.x * 7 + i);
+    int d[8][4] = {};
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int t = 0; t < 8; t++)
+            asm volatile(
+                "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                "{%0,%1,%2,%3};"
+                : "+r"(d[t][0]), "+r"(d[t][1]), "+r"(d[t][2]), "+r"(d[t][3])
+                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+    }
+    int s = 0;
+#pragma unroll
+    for (int t = 0; t < 8; t++) s += d[t][0] + d[t][1] + d[t][2] + d[t][3];
+    if (s == 0x12345) out[0] = (uint64_t)s;
+}
+
+// FP64 pipe: dependent-free DFMA streams (8 chains per thread), one FMA per op
+__global__ void k_dfma_peak(double *out, int iters, double seed) {
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = seed + threadIdx.x + i;
+    const double a = 0.999999, b = 1e-7;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) x[i] = fma(x[i], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s += x[i];
+    if (s == 1234.5) out[0] = s;
+}
+
 template <class F> double time_ms(F &&launch) {
     cudaEvent_t a, b;
     UH_CHECK(cudaEventCreate(&a));
@@ -225,7 +265,9 @@ template <class F> double time_ms(F &&launch) {
 
 }  // namespace
 
-// rates[0] = IMAD/s, rates[1] = 128-bit MAC/s, rates[2] = reduced mulmod/s (60-bit prime)
+// rates[0] = IMAD/s, [1] = 128-bit MAC/s, [2] = reduced mulmod/s (60-bit prime), [3] MAC128 plain-C
+// form, [4] lazy Shoup product, [5] exact FP64 modMAC, [6] mixed IMAD+FP64 MAC, [7] split-accumulator
+// MAC, [8] narrow-operand MAC (q < 2^41), [9] u8 IMMA MAC/s (mma.sync), [10] FP64 FMA/s
 void bench_peaks(const Ctx &c, double *rates) {
     int sms = 0;
     UH_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
@@ -254,6 +296,13 @@ void bench_peaks(const Ctx &c, double *rates) {
     rates[7] = lanes * iters * 8 / (ms * 1e-3);
     ms = time_ms([&] { k_macn_peak<<<blocks, threads>>>(out, iters, 7ull); });
     rates[8] = lanes * iters * 8 / (ms * 1e-3);
+    {  // rates[9]: u8 IMMA MACs/s (mma.sync), 8 warps x 4 CTAs per SM
+        const int wb = sms * 4, wt = 256, wi = 1024;
+        ms = time_ms([&] { k_imma_peak<<<wb, wt>>>(out, wi, 3u); });
+        rates[9] = (double)wb * (wt / 32) * wi * 8 * (16.0 * 8 * 32) / (ms * 1e-3);
+    }
+    ms = time_ms([&] { k_dfma_peak<<<blocks, threads>>>((double *)out, iters, 1.0); });
+    rates[10] = lanes * iters * 8 / (ms * 1e-3);  // FP64 FMA/s
     UH_CHECK(cudaGetLastError());
     cudaFree(out);
 }

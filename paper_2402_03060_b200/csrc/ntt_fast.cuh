@@ -34,14 +34,10 @@ struct NttJob {
     const uint64_t *inv = nullptr, *invs = nullptr;
     const uint64_t *inv2 = nullptr, *inv2s = nullptr;  // DIVIDE2: (q_top * P)^-1 mod q_k (Shoup pairs)
     const ulonglong2 *pmod = nullptr;  // DIVIDE2: (P mod q_i, Shoup companion) per modulus
-    // optional limb selection: launch index i -> limb f = (i / sel_cnt) * sel_T + sel[i % sel_cnt]
-    const int16_t *sel = nullptr;
-    int sel_T = 0, sel_cnt = 0;
 };
 
 bool ntt_fast_supported(const Ctx &c);
 void ntt_fast_forward(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s);
 void ntt_fast_inverse(const Ctx &c, const NttJob &J, int limbs, cudaStream_t s);
-bool ntt_fast_modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int L, int in_ps, cudaStream_t s);
 
 }  // namespace uh

@@ -514,15 +514,6 @@ void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, i
 void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level, int in_ps, cudaStream_t s) {
     int L = level + 1;
     size_t N = c.n;
-    if (ntt_fast_modup(c, D, in, n_polys, L, in_ps, s)) {
-        if (N >= 512 && n_polys <= 65535) {
-            k_modup_diag2<<<dim3((unsigned)(N / 512), L, n_polys), 256, 0, s>>>(D, in, L, in_ps, (int)c.logn);
-        } else {
-            k_modup_diag<<<grid_for((size_t)n_polys * L * N), kTB, 0, s>>>(D, in, n_polys, L, in_ps, (int)c.logn);
-        }
-        UH_LAUNCH_CHECK();
-        return;
-    }
     Scratch C((size_t)n_polys * L * N * 8, s);
     if (ntt_fast_supported(c)) {
         NttJob Ji;  // every digit to coefficients (strided in -> compact C)

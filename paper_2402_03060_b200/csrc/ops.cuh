@@ -76,13 +76,9 @@ void decrypt_coeffs(const Ctx &c, double *out, const uint64_t *ct, const uint64_
 void from_signed(const Ctx &c, uint64_t *out, const int64_t *coef, int n_polys, int nq, int special, int out_ps,
                  cudaStream_t s);
 
-// fused.cu -- hoisted layers.  X: [n_in][B][2][xls][N] input ciphertexts; D: [n_in][B][L][L+1][N] ModUp of their
-// c1; keys[t] (device array of device pointers; unused for shift 0); shifts[t] in [0, N/2).
-// conv: acc[O][B][2][L+1][N] (QP basis) = sum_{i,t} masks[o][i][t] * P * rot_t(ct_i)
-void conv_hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D,
-                      const uint64_t *masks, const uint64_t *const *keys, const int32_t *key_limbs, const int32_t *shifts, int B,
-                      int I, int T, int O, int level, cudaStream_t s);
-// hoist.cu -- generic hoisted rotation-MAC: acc[O][B][2][L+1][N] (QP) = sum over terms q of
+// hoist.cu -- generic hoisted rotation-MAC.  X: [n_in][B][2][xls][N] input ciphertexts; D:
+// [n_in][B][L][L+1][N] ModUp of their c1; keys[t] (device array of device pointers; unused for
+// shift 0); shifts[t] in [0, N/2).  acc[O][B][2][L+1][N] (QP) = sum over terms q of
 // masks[o][q] * P * rot_{shifts[t]}(ct_i); terms dense (i, t) or diag (i == t); masks may be null (= 1).
 void hoisted_mac(const Ctx &c, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D, const uint64_t *masks,
                  const uint64_t *const *keys, const int32_t *key_limbs, const int32_t *shifts, int B, int I, int T,
@@ -102,10 +98,6 @@ void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint
                       int level, cudaStream_t s);
 // microbench.cu: rates[0] = IMAD/s, rates[1] = 128-bit MAC/s, rates[2] = reduced mulmod/s
 void bench_peaks(const Ctx &c, double *rates);
-// pool: out[C][B][2][L+1][N] (QP basis) = sum_t P * rot_t(ct_c)
-void rot_sum_hoisted(const Ctx &c, uint64_t *out, const uint64_t *X, int xls, const uint64_t *D,
-                     const uint64_t *const *keys, const int32_t *key_limbs, const int32_t *shifts, int B, int C, int T, int level,
-                     cudaStream_t s);
 // canonical embedding with cuFFT (fp64): slots [n_polys][N/2] -> rounded int64 coefficients.
 void encode_coeffs(const Ctx &c, int64_t *coef, const double *slots, int n_polys, double scale, cudaStream_t s);
 void decode_coeffs(const Ctx &c, double *slots, const double *coef, int n_polys, double scale, cudaStream_t s);

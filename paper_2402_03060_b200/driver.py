@@ -154,21 +154,47 @@ def run_inference(m, samples, params, alignment: int = 1, plan=None, cost_model=
     return outputs, metrics, plan
 
 
-def pack_groups(m, groups, plan) -> np.ndarray:
-    """[B groups of <= capacity samples] -> slot planes [channels, B, num_slots]."""
-    planes = np.zeros((m.channels, len(groups), plan.num_slots))
+def pack_groups(m, groups, plan, out=None) -> np.ndarray:
+    """[B groups of <= capacity samples] -> slot planes [channels, B, num_slots].
+
+    Same layout as ``planner.batch_pack`` (packing.py:94-119: sample i of a group at slot
+    offset ``plan.offsets[i]``, zeros elsewhere), vectorised per group: one scatter of all
+    of a group's samples and channels.  ``out`` (e.g. a numpy view of a pinned host tensor)
+    receives the planes in place."""
+    from .errors import CapacityExceeded, OversizedInput, ShapeMismatch
+
+    C, hw = m.channels, m.height * m.width
+    planes = np.zeros((C, len(groups), plan.num_slots)) if out is None else out
+    if out is not None:
+        planes[...] = 0.0
+    offs = np.asarray(plan.offsets, dtype=np.int64)
+    cols = np.arange(hw, dtype=np.int64)
     for b, group in enumerate(groups):
-        packed = planner.batch_pack([planner.flatten_input(s) for s in group], plan)
-        for ch, pv in enumerate(packed):
-            planes[ch, b] = pv.values
+        k = len(group)
+        if k == 0:
+            continue
+        if k > plan.capacity:
+            raise CapacityExceeded(f"{k} samples exceed the batch capacity {plan.capacity}")
+        arr = np.asarray(group, dtype=np.float64)
+        if arr.ndim != 4 or arr.shape[1] != C:
+            raise ShapeMismatch(f"group {b}: expected samples of shape ({C}, H, W), got {arr.shape[1:]}")
+        if arr.shape[2] * arr.shape[3] > plan.footprint:
+            raise OversizedInput(f"sample vector of length {arr.shape[2] * arr.shape[3]} exceeds the footprint "
+                                 f"{plan.footprint}")
+        flat = arr.reshape(k, C, -1)
+        idx = (offs[:k, None] + cols[None, :flat.shape[2]]).reshape(-1)
+        planes[:, b, idx] = flat.transpose(1, 0, 2).reshape(C, -1)
     return planes
 
 
-def infer_batch(m, planes, params, plan, backend, counts=None, cost_model=None, fused=True):
+def infer_batch(m, planes, params, plan, backend, counts=None, cost_model=None, fused=True, as_tensor=False):
     """Encrypted inference of ``B`` packed ciphertext groups in one pass.
 
     ``planes`` is ``[channels, B, num_slots]`` (host numpy, or a float64
-    tensor).  Returns ``(outputs[B][count_b], metrics)``.
+    tensor).  Returns ``(outputs[B][count_b], metrics)``; with ``as_tensor``
+    the outputs are one float64 tensor ``[B, capacity, out_dim]`` (on the GPU
+    for the GPU backend -- nothing is copied to the host; rows past a group's
+    count hold the junk of empty sample regions).
     """
     report = validate(m, params)
     if not report.ok:
@@ -192,6 +218,8 @@ def infer_batch(m, planes, params, plan, backend, counts=None, cost_model=None, 
                           for ct in state.cts], dim=2)
         if lay.pending_const != 1.0:
             vals = vals * lay.pending_const
+        if as_tensor:
+            return vals, metrics
         host = vals.cpu().numpy()
         outputs = []
         for b in range(host.shape[0]):
@@ -200,6 +228,9 @@ def infer_batch(m, planes, params, plan, backend, counts=None, cost_model=None, 
         return outputs, metrics
     dec = [np.atleast_2d(backend.decrypt(ct)) for ct in state.cts]
     B = dec[0].shape[0]
+    if as_tensor:
+        return torch.from_numpy(np.stack([np.stack(_extract([d[b] for d in dec], state.layout, plan.offsets))
+                                          for b in range(B)])), metrics
     outputs = []
     for b in range(B):
         cnt = plan.capacity if counts is None else counts[b]

@@ -1,17 +1,22 @@
 """Hoisted, fused GPU layer paths (same signatures as :mod:`.schedule`).
 
-``conv``, ``avgpool`` and ``square`` of the reference schedule
-(``pkg/src/slotcnn/layers.py:134-235``) re-expressed as a few large kernels
-over all channels and the whole ciphertext batch:
+``conv``, ``avgpool``, ``square``, ``flatten`` and ``fc`` of the reference
+schedule (``pkg/src/slotcnn/layers.py:134-426``) re-expressed as a few large
+kernels over all channels and the whole ciphertext batch:
 
-* conv    -- one ModUp per input channel, one fused kernel forming every
-  tap's key-switched rotation in the QP basis and multiply-accumulating it
-  with every output channel's weight mask, then one ModDown and one rescale
-  per output channel, then the bias (``uh_conv_hoisted_mac``);
-* avgpool -- one ModUp per channel, one fused rotation-sum kernel, one
-  ModDown per channel (``uh_rot_sum_hoisted``);
+* conv    -- one ModUp per input channel, one fused hoisted rotation-MAC
+  forming every tap's key-switched rotation in the QP basis and
+  multiply-accumulating it with every output channel's weight mask, then one
+  fused ModDown + rescale per output channel, then the bias.  Kernel per
+  shape: ``uh_hoisted_mac_imma`` (dense 5..12-output layers at N = 2^15: mask
+  contraction on the tensor cores), ``uh_hoisted_mac_bank`` (per-layer
+  Galois-key bank, N = 2^15), ``uh_conv_hoisted_mac`` (generic, any N);
+* avgpool -- one ModUp per channel, one unmasked hoisted rotation sum
+  (``uh_hoisted_mac_bank`` / ``uh_rot_sum_hoisted``), one ModDown per channel;
 * square  -- tensor + relinearise + rescale of all channels in one batched
-  launch sequence (``uh_mul_relin_rescale``).
+  launch sequence (``uh_mul_relin_rescale_fused``);
+* flatten / fc -- masked rotation stages as hoisted MACs of the same input
+  with pre-rotated masks (see the section comment below).
 
 Each records exactly the census the op-level schedule records (the same
 rotations, pt_mults, ct_mults and adds at the same levels), so metrics,
@@ -19,8 +24,8 @@ level traces and ``estimate``-style accounting are unchanged.  Decrypted
 results agree with the op-level path to CKKS rounding (one rescale / ModDown
 per output instead of one per product), not bit for bit.
 
-Weight masks are encoded once per (layer, level, layout) into a device
-"mask bank" in the QP basis and reused across batches.
+Weight masks are encoded once per (layer content, level, layout) into a
+device "mask bank" in the QP basis and reused across batches.
 """
 
 from __future__ import annotations
@@ -135,6 +140,27 @@ def key_bank(backend, shifts, level: int) -> torch.Tensor:
     return bank
 
 
+def layer_digest(layer) -> str:
+    """Content key of a layer's plaintext parameters (type, shapes, stride, weight and bias bytes).
+
+    The device banks are cached on the backend under this digest, never under the layer's
+    object id: CPython reuses ids of freed objects, so a long-lived backend evaluating a new
+    model of the same architecture would otherwise hit another model's weights."""
+    import hashlib
+
+    h = hashlib.blake2b(digest_size=16)
+    h.update(type(layer).__name__.encode())
+    for name in ("ch_in", "ch_out", "kernel", "stride", "dat_in", "dat_out"):
+        if hasattr(layer, name):
+            h.update(f"{name}={getattr(layer, name)};".encode())
+    for name in ("weights", "bias"):
+        if hasattr(layer, name):
+            a = np.ascontiguousarray(np.asarray(getattr(layer, name), dtype=np.float64))
+            h.update(f"{name}{a.shape}".encode())
+            h.update(a.tobytes())
+    return h.hexdigest()
+
+
 def _bank(backend, key, build):
     banks = backend.__dict__.setdefault("_mask_banks", {})
     t = banks.get(key)
@@ -173,7 +199,7 @@ def conv_mask_bank(backend, layer, lay, out_lay, w, level):
         O, I, T = w.shape[0], w.shape[1], w.shape[2] * w.shape[3]
         return bank.view(O, I, T, level + 2, backend.n)
 
-    return _bank(backend, ("conv", id(layer), level, lay), build)
+    return _bank(backend, ("conv", layer_digest(layer), level, lay), build)
 
 
 def bias_bank(backend, layer, out_lay, level, scale):
@@ -185,7 +211,30 @@ def bias_bank(backend, layer, out_lay, level, scale):
         bias = torch.from_numpy(np.asarray(layer.bias, dtype=np.float64)).to(backend.device)
         return backend.encode_device(pattern[None, :] * bias[:, None], level, scale)
 
-    return _bank(backend, ("bias", id(layer), level, out_lay, scale), build)
+    return _bank(backend, ("bias", layer_digest(layer), level, out_lay, scale), build)
+
+
+def conv_mac_work(shifts, half, n, B, I, O, level, imma) -> dict:
+    """Algorithmic 64-bit modular multiply-accumulates of one hoisted conv MAC call, split by
+    phase and limb class (the roofline of the call is a mix of pipes):
+
+    * phase A (key switch of every term, per ciphertext, coefficient and QP limb): a non-zero
+      shift costs 2L key MACs (digits x components) plus the P * c0 MAC on the q-limbs; a zero
+      shift costs the two P * c MACs on the q-limbs;
+    * phase B (weight-mask contraction): O x terms x 2 components per QP limb.
+
+    ``a40``/``b40``: the 40-bit limbs q_1..q_level; ``a60``/``b60``: the 60-bit q_0 and P.
+    With the tensor-core kernel (``imma``) b40 runs as 25 u8 byte products per modMAC."""
+    T = len(shifts)
+    nz = sum(1 for s in shifts if s % half)
+    L = level + 1
+    per_a = lambda qlimbs, limbs: nz * (limbs * 2 * L + qlimbs) + (T - nz) * 2 * qlimbs  # noqa: E731
+    a40 = n * B * I * per_a(level, level)
+    a60 = n * B * I * per_a(1, 2)
+    b40 = n * B * O * I * T * 2 * level
+    b60 = n * B * O * I * T * 2 * 2
+    return {"a40": a40, "a60": a60, "b40": b40, "b60": b60, "total": a40 + a60 + b40 + b60, "imma": bool(imma),
+            "B": B, "I": I, "T": T, "O": O, "nz": nz, "level": level}
 
 
 def conv(backend, state: CipherState, layer) -> CipherState:
@@ -222,7 +271,8 @@ def conv(backend, state: CipherState, layer) -> CipherState:
     if timer is not None:
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(torch.cuda.current_stream(backend.device))
-    if _imma_ok(backend, level, O, I * T):
+    imma = _imma_ok(backend, level, O, I * T)
+    if imma:
         kb = key_bank(backend, shifts, level)
         ib = imma_bank(backend, masks, O, I * T, level)
         backend._call("uh_hoisted_mac_imma", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ib), _vp(kb), _vp(sh), B, I,
@@ -237,10 +287,8 @@ def conv(backend, state: CipherState, layer) -> CipherState:
     if timer is not None:
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(torch.cuda.current_stream(backend.device))
-        nz = sum(1 for s in shifts if s % backend.params.num_slots)
-        # algorithmic 64-bit modular multiply-accumulates of the hoisted algorithm
-        work = n * (B * I * (nz * (LP * 2 * L + L) + (T - nz) * 2 * L) + B * O * I * T * LP * 2)
-        timer.append(("conv_hoisted_mac", level, t0, t1, work))
+        timer.append(("conv_hoisted_mac", level, t0, t1, conv_mac_work(shifts, backend.params.num_slots, n, B, I,
+                                                                           O, level, imma)))
     del D
     out = backend._empty(O, B, 2, level, n)  # ModDown + rescale as one centred division by q_level * P
     backend._call("uh_divide_top2", _vp(out), _vp(acc), O * B * 2, level, level, LP, st)
@@ -539,7 +587,7 @@ def fc(backend, state: CipherState, layer) -> CipherState:
     cnt.record("pt_mult", level, 2 * d_out)
     cnt.record("add", level - 1, 2 * (d_out - 1))
     rows = np.stack([f for f, _ in masks] + [w for _, w in masks])  # [2 * d_out, slots]: o=0 front, o=1 wrap
-    bank = _rows_bank(backend, ("fc", id(layer), lay), rows, level, float(backend.modulus(level)))
+    bank = _rows_bank(backend, ("fc", layer_digest(layer), lay), rows, level, float(backend.modulus(level)))
     X = stack_cts(backend, [ct], level)
     acc = _hoist(backend, X, level, list(range(d_out)), bank.view(2, d_out, level + 2, n), 2, False, B)
     fw = _finish(backend, acc, level, rescale=True)  # [2][B][2][level][N]
@@ -560,7 +608,7 @@ def fc(backend, state: CipherState, layer) -> CipherState:
     cnt.record("add", level, 1)
     bias = np.zeros(lay.footprint)
     bias[:d_out] = layer.bias
-    bias_t = _bank(backend, ("fc_bias", id(layer), lay, level, scale), lambda: backend.encode_device(
+    bias_t = _bank(backend, ("fc_bias", layer_digest(layer), lay, level, scale), lambda: backend.encode_device(
         torch.from_numpy(schedule.tile_region(backend.params.num_slots, lay, bias))[None], level, scale))
     Lo = level + 1
     backend._call("uh_elementwise", OP_ADD, _vp(out), _vp(out), _vp(bias_t), B, 1, Lo, Lo, 2 * Lo, 2 * Lo, Lo,

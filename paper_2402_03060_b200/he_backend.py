@@ -98,13 +98,33 @@ class CipherVector:
         return self.backend.decrypt(self)
 
 
-class GpuBackend:
-    """Executes the reference's slot operations as RNS-CKKS on one B200."""
+def _random_u64() -> int:
+    import os
 
-    def __init__(self, params: HEParams = DEFAULT_PARAMS, device: int | None = None):
+    return int.from_bytes(os.urandom(8), "little")
+
+
+class GpuBackend:
+    """Executes the reference's slot operations as RNS-CKKS on one B200.
+
+    Key material: the secret key and the key-switching keys' noise come from
+    the secret seed ``params.seed`` -- a fresh ``os.urandom`` value when it is
+    ``None`` (the default).  Encryption randomness (the uniform ``a`` and the
+    noise ``e`` of every fresh ciphertext) comes from a separate per-backend
+    nonce seed, also drawn from ``os.urandom``, so two backends (ranks,
+    restarts) never reuse an encryption nonce even with the same keys.
+    ``reproducible=True`` (tests, oracle parity) uses ``params.seed`` for the
+    nonce stream as well, so encryptions equal the oracle's bit for bit.
+    """
+
+    def __init__(self, params: HEParams = DEFAULT_PARAMS, device: int | None = None, *, reproducible: bool = False):
         if not torch.cuda.is_available():
             raise _lib.DeviceError("GpuBackend needs a CUDA device (the engine has no CPU fallback)")
         self.params = params
+        self._secret_seed = params.seed if params.seed is not None else _random_u64()
+        if reproducible and params.seed is None:
+            raise ValueError("reproducible=True needs HEParams with an explicit seed")
+        self._enc_seed = params.seed if reproducible else _random_u64()
         self.counter = OpCounter()
         self.chain = rns_chain(params)
         self.n = params.poly_degree
@@ -123,7 +143,7 @@ class GpuBackend:
             _lib.call("uh_ctx_create", ctypes.byref(self._ctx), self.n, ctypes.cast(moduli, ctypes.c_void_p),
                       ctypes.cast(psi, ctypes.c_void_p), self.count, self.device.index)
             self.secret = self._empty(self.count, self.n)
-            _lib.call("uh_secret_gen", self._ctx, _ptr(self.secret), params.seed, self._stream())
+            _lib.call("uh_secret_gen", self._ctx, _ptr(self.secret), self._secret_seed, self._stream())
         self._gk = {}
         self._rk = None
         self._ct_id = 0
@@ -156,14 +176,14 @@ class GpuBackend:
         key = self._gk.get(r)
         if key is None or key.shape[0] < level + 1:
             key = self._empty(level + 1, 2, level + 2, self.n)
-            self._call("uh_galois_keygen", _ptr(key), _ptr(self.secret), self.params.seed, r, level, self._stream())
+            self._call("uh_galois_keygen", _ptr(key), _ptr(self.secret), self._secret_seed, r, level, self._stream())
             self._gk[r] = key
         return key
 
     def relin_key(self, level: int) -> torch.Tensor:
         if self._rk is None or self._rk.shape[0] < level + 1:
             key = self._empty(level + 1, 2, level + 2, self.n)
-            self._call("uh_relin_keygen", _ptr(key), _ptr(self.secret), self.params.seed, level, self._stream())
+            self._call("uh_relin_keygen", _ptr(key), _ptr(self.secret), self._secret_seed, level, self._stream())
             self._rk = key
         return self._rk
 
@@ -173,7 +193,7 @@ class GpuBackend:
 
         torch.cuda.synchronize(self.device)
         u64 = lambda t: t.cpu().numpy().view(np.uint64)  # noqa: E731
-        keys = keyio.EvalKeys(self.n, list(self.chain.moduli), self.params.scale_bits, self.depth, self.params.seed,
+        keys = keyio.EvalKeys(self.n, list(self.chain.moduli), self.params.scale_bits, self.depth,
                               galois={r: u64(k) for r, k in self._gk.items()},
                               relin=None if self._rk is None else u64(self._rk))
         keyio.save_eval_keys(path, keys)
@@ -241,13 +261,25 @@ class GpuBackend:
             p._dev[key] = t
         return t
 
-    def encode_device(self, slots: torch.Tensor, level: int, scale: float) -> torch.Tensor:
-        """slots float64 [R, num_slots] (host or device) -> [R, level+1, N] evaluation form."""
-        vals = slots.to(device=self.device, dtype=torch.float64).contiguous()
-        rows = vals.shape[0]
+    @staticmethod
+    def _check_range(vals: torch.Tensor, scale: float) -> None:
         peak = float(vals.abs().max()) if vals.numel() else 0.0
-        if peak * scale >= 2.0 ** 62:
+        if not peak * scale < 2.0 ** 62:  # also catches NaN
             raise OversizedInput(f"value {peak} at scale 2^{math.log2(scale):.1f} overflows the encoder")
+
+    def encode_device(self, slots: torch.Tensor, level: int, scale: float, checked: bool = False) -> torch.Tensor:
+        """slots float64 [R, num_slots] (host or device) -> [R, level+1, N] evaluation form.
+
+        The encoder's range check (|value| * scale < 2^62) runs on the host for host input;
+        for device input it needs a device->host read, skipped when the caller already
+        checked (``checked=True``: the client path checks its host planes before the copy)."""
+        if not checked and slots.device.type == "cpu":
+            self._check_range(slots, scale)
+            checked = True
+        vals = slots.to(device=self.device, dtype=torch.float64, non_blocking=True).contiguous()
+        rows = vals.shape[0]
+        if not checked:
+            self._check_range(vals, scale)
         coef = torch.empty((rows, self.n), dtype=torch.int64, device=self.device)
         st = self._stream()
         self._call("uh_encode_coeffs", _ptr(coef), _ptr(vals), rows, float(scale), st)
@@ -268,7 +300,7 @@ class GpuBackend:
         B = pt.shape[0]
         out = self._empty(B, 2, lev + 1, self.n)
         self._call("uh_encrypt", _ptr(out), _ptr(pt), _ptr(self.secret), B, lev, lev + 1, lev + 1,
-                   self.params.seed, self._ct_id, self._stream())
+                   self._enc_seed, self._ct_id, self._stream())
         self._ct_id += B
         return CipherVector(out, lev, self.scale0, self)
 
@@ -277,10 +309,13 @@ class GpuBackend:
         (host -- ideally pinned, copied asynchronously -- or device): the batched client path."""
         if slots.dim() != 2 or slots.shape[1] > self.params.num_slots:
             raise OversizedInput(f"encrypt_slots expects [B, <= {self.params.num_slots}], got {tuple(slots.shape)}")
+        checked = slots.device.type == "cpu"
+        if checked:
+            self._check_range(slots, self.scale0)  # host-side: no device sync on the client path
         vals = slots.to(device=self.device, dtype=torch.float64, non_blocking=True)
         if vals.shape[1] < self.params.num_slots:
             vals = torch.nn.functional.pad(vals, (0, self.params.num_slots - vals.shape[1]))
-        return self._encrypt_encoded(self.encode_device(vals, self.depth, self.scale0))
+        return self._encrypt_encoded(self.encode_device(vals, self.depth, self.scale0, checked=checked))
 
     def decrypt_device(self, c: CipherVector) -> torch.Tensor:
         """Slot values [B, num_slots] as a float64 CUDA tensor."""

@@ -17,12 +17,16 @@ Layout (all integers little-endian)::
 
 Header::
 
-    {"format": 1, "poly_degree": N, "moduli": [q_0, .., q_depth, P],
-     "scale_bits": s, "depth": d, "seed": k,
+    {"format": 2, "poly_degree": N, "moduli": [q_0, .., q_depth, P],
+     "scale_bits": s, "depth": d,
      "keys": [{"kind": "galois", "rotation": r, "galois_elt": 5^r mod 2N,
                "level": l, "shape": [l+1, 2, l+2, N], "offset": o,
                "nbytes": b, "crc32": c}, ...,
               {"kind": "relin", "level": l, ...}]}
+
+The container never holds the secret key or anything it can be derived from:
+in particular not the secret seed (``HEParams.seed``; format 1 wrote it, and
+format-1 files are refused).
 
 Every failure to read a file (bad magic, unknown version, truncated data,
 checksum mismatch, parameters that do not match the reader's) raises the
@@ -41,7 +45,7 @@ import numpy as np
 from .errors import ParseError
 
 MAGIC = b"UHEVK\0"
-VERSION = 1
+VERSION = 2
 ALIGN = 64
 
 
@@ -57,7 +61,6 @@ class EvalKeys:
     moduli: list
     scale_bits: int
     depth: int
-    seed: int
     galois: dict = field(default_factory=dict)  # rotation r (mod N/2) -> uint64[l+1][2][l+2][N]
     relin: np.ndarray | None = None            # uint64[l+1][2][l+2][N]
 
@@ -94,7 +97,7 @@ def save_eval_keys(path: str, keys: EvalKeys) -> None:
         entries.append(e)
         blobs.append(raw)
     header = {"format": VERSION, "poly_degree": n, "moduli": [int(q) for q in keys.moduli],
-              "scale_bits": int(keys.scale_bits), "depth": int(keys.depth), "seed": int(keys.seed), "keys": entries}
+              "scale_bits": int(keys.scale_bits), "depth": int(keys.depth), "keys": entries}
     # offsets depend on the header length, which depends on the offsets' digits: iterate to a fixed point
     hlen = 0
     while True:
@@ -132,7 +135,9 @@ def load_eval_keys(path: str, poly_degree: int | None = None, moduli=None) -> Ev
     try:
         header = json.loads(data[16:16 + hlen].decode())
         n, mods = int(header["poly_degree"]), [int(q) for q in header["moduli"]]
-        out = EvalKeys(n, mods, int(header["scale_bits"]), int(header["depth"]), int(header["seed"]))
+        if "seed" in header:
+            raise ParseError("evaluation-key header carries a seed (secret material): refusing it")
+        out = EvalKeys(n, mods, int(header["scale_bits"]), int(header["depth"]))
         entries = list(header["keys"])
     except (ValueError, KeyError, TypeError) as e:
         raise ParseError(f"malformed evaluation-key header: {e}") from e

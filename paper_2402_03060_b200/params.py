@@ -9,8 +9,13 @@ defaults, all ignored by ``from_dict`` when absent):
 * ``first_mod_bits`` -- bit size of the base prime q_0 (60 in every
   BASELINE.json config),
 * ``special_mod_bits`` -- bit size of the key-switching special prime P (60),
-* ``seed`` -- master seed for the secret key, key-switching keys and the
-  encryption randomness (BASELINE.json: "seeded keys and noise").
+* ``seed`` -- the *secret* seed: the secret key and the key-switching keys'
+  noise are derived from it.  ``None`` (the default) draws a fresh 64-bit
+  secret seed from ``os.urandom`` for every backend; an integer is the
+  reproducible opt-in used by the tests, the oracle parity checks and the
+  benchmark (BASELINE.json: "seeded keys and noise").  It is never written to
+  an evaluation-key file (:mod:`.keyio`), and the encryption randomness uses a
+  separate per-backend nonce stream (:class:`.he_backend.GpuBackend`).
 
 The modulus chain is ``q_0`` (``first_mod_bits``), then ``depth`` primes of
 ``scale_bits`` bits (``q_1 .. q_depth``), then ``P``.  A ciphertext at level
@@ -44,7 +49,7 @@ class HEParams:
     log_q: int = 432
     first_mod_bits: int = 60
     special_mod_bits: int = 60
-    seed: int = 0
+    seed: int | None = None
 
     def __post_init__(self) -> None:
         # same rules and messages as he_backend.py:51-59
@@ -58,6 +63,8 @@ class HEParams:
             raise ValueError("log_q must be at least 1")
         if not (2 <= self.first_mod_bits <= 61 and 2 <= self.special_mod_bits <= 61):
             raise ValueError("first_mod_bits and special_mod_bits must lie in [2, 61]")
+        if self.seed is not None and not (0 <= int(self.seed) < 2 ** 64):
+            raise ValueError("seed must be None or an integer in [0, 2^64)")
 
     @property
     def num_slots(self) -> int:

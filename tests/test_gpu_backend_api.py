@@ -133,3 +133,23 @@ def test_eval_key_export_import(tmp_path):
     other = GpuBackend(HEParams(poly_degree=128, depth=3, scale_bits=40, seed=5))
     with pytest.raises(ParseError):
         other.import_keys(path)
+
+
+def test_encryption_nonces_per_backend():
+    """Two backends with the same (seeded) keys never reuse an encryption nonce: their k-th
+    ciphertexts differ in c1 = a, so c0 - c0' does not expose m - m'.  reproducible=True is the
+    explicit opt-in that makes encryption a function of the parameter seed (oracle parity)."""
+    p = HEParams(poly_degree=64, depth=2, scale_bits=40, seed=11)
+    x = np.linspace(-1, 1, p.num_slots)
+    a, b = GpuBackend(p), GpuBackend(p)
+    ca, cb = a.encrypt(a.encode(x)), b.encrypt(b.encode(x))
+    assert torch.equal(a.secret, b.secret)  # same secret seed -> same keys
+    assert not torch.equal(ca.data[:, 1], cb.data[:, 1])  # fresh nonces -> different a
+    assert np.max(np.abs(b.decrypt(ca) - x)) < TOL  # still the same key
+    r1, r2 = GpuBackend(p, reproducible=True), GpuBackend(p, reproducible=True)
+    assert torch.equal(r1.encrypt(r1.encode(x)).data, r2.encrypt(r2.encode(x)).data)
+    u1, u2 = GpuBackend(HEParams(poly_degree=64, depth=2, scale_bits=40)), \
+        GpuBackend(HEParams(poly_degree=64, depth=2, scale_bits=40))
+    assert not torch.equal(u1.secret, u2.secret)  # unseeded: a fresh secret per backend
+    with pytest.raises(ValueError):
+        GpuBackend(HEParams(poly_degree=64, depth=2, scale_bits=40), reproducible=True)

@@ -93,3 +93,19 @@ def test_block_diagonal_hoisted_mac_equals_per_input_sums():
     mods = [be.modulus(k) for k in range(level + 1)] + [be.modulus(be.sp)]
     q = torch.tensor(mods, dtype=torch.int64, device=be.device).view(1, 1, -1, 1)
     assert torch.equal(got, torch.remainder(want, q))
+
+
+def test_backend_reused_across_models():
+    """One long-lived backend evaluates two models of the same architecture with different
+    weights (fused path): the per-layer mask / bias / FC banks are keyed on the layers' content,
+    so the second model never picks up the first model's cached banks."""
+    params = HEParams(poly_degree=1 << 12, depth=7, scale_bits=40)
+    be = GpuBackend(params)
+    rng = np.random.default_rng(30)
+    for seed in (40, 41, 40):
+        m = planner.lenet1(seed=seed)
+        plan = planner.footprint(m, params)
+        samples = list(rng.uniform(0, 1, size=(plan.capacity, 1, 28, 28)))
+        outs, _, _ = driver.run_inference(m, samples, params, plan=plan, backend=be, fused=True)
+        for y, s in zip(outs, samples):
+            assert np.max(np.abs(y - planner.reference_infer(m, s))) < 1e-5

@@ -20,8 +20,8 @@ from paper_2402_03060_b200.params import HEParams
 
 pytestmark = pytest.mark.gpu
 
-C2 = HEParams(poly_degree=1 << 15, depth=9, scale_bits=40)  # BASELINE config 2 / metric
-SMALL = HEParams(poly_degree=1 << 12, depth=4, scale_bits=40)
+C2 = HEParams(poly_degree=1 << 15, depth=9, scale_bits=40, seed=0)  # BASELINE config 2 / metric
+SMALL = HEParams(poly_degree=1 << 12, depth=4, scale_bits=40, seed=0)
 
 _CACHE = {}
 
@@ -41,9 +41,9 @@ def rand_limbs(o, mods, rows=1, seed=0):
     return out
 
 
-@pytest.mark.parametrize("params", [HEParams(poly_degree=16, depth=2, scale_bits=40), SMALL,
-                                    HEParams(poly_degree=1 << 13, depth=3, scale_bits=40), C2,
-                                    HEParams(poly_degree=1 << 16, depth=2, scale_bits=40)],
+@pytest.mark.parametrize("params", [HEParams(poly_degree=16, depth=2, scale_bits=40, seed=0), SMALL,
+                                    HEParams(poly_degree=1 << 13, depth=3, scale_bits=40, seed=0), C2,
+                                    HEParams(poly_degree=1 << 16, depth=2, scale_bits=40, seed=0)],
                          ids=lambda p: f"N{p.poly_degree}")
 def test_ntt_roundtrip_bit_exact(params):
     g, o = pair(params)
@@ -61,7 +61,7 @@ def test_ntt_roundtrip_bit_exact(params):
 
 def test_ntt_more_limbs_than_one_grid():
     """A single call over more than 65535 limbs (the grid.y limit) is split into launches."""
-    params = HEParams(poly_degree=1 << 13, depth=3, scale_bits=40)
+    params = HEParams(poly_degree=1 << 13, depth=3, scale_bits=40, seed=0)
     g, o = pair(params)
     nq = params.depth + 1
     polys = 65535 // (nq + 1) + 7  # > 65535 limbs in the QP basis
@@ -266,20 +266,3 @@ def test_divide_top2_is_centred_division_by_q_level_times_p(params, level):
                 else:  # small-N fallback divides by P then q_level: within one unit
                     diff = (int(gotc[r, k, i]) - want) % qs[k]
                     assert diff in (0, 1, qs[k] - 1)
-
-
-def test_opt_in_pair_ntt_bit_exact():
-    """The opt-in persistent cluster-pair forward NTT (UH_NTT_PAIR=1, ntt_fast.cu k_fwd_pair:
-    TMA-staged halves, DSMEM first stage) gives the same residues as the oracle: NTT, ModUp /
-    key inner product / ModDown, rotation and rescale parity cases re-run in a subprocess
-    (the switch is read once per process)."""
-    import os
-    import subprocess
-    import sys
-
-    env = dict(os.environ, UH_NTT_PAIR="1")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.abspath(__file__),
-                        "-k", "ntt_roundtrip or modup_keyinner or rotate_bit_exact or rescale_and_mul_plain"],
-                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

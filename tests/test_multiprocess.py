@@ -49,7 +49,7 @@ def test_shard_range_partitions():
             assert max(b - a for a, b in parts) - min(b - a for a, b in parts) <= 1
 
 
-@pytest.mark.parametrize("n_samples", [7])
+@pytest.mark.parametrize("n_samples", [7, 1])  # 1: rank 1 owns no group
 def test_two_rank_gloo_equals_single_process(tmp_path, n_samples):
     out = str(tmp_path / "outs.npy")
     mp.spawn(_worker, args=(2, _free_port(), n_samples, out), nprocs=2, join=True)
@@ -68,3 +68,49 @@ def test_two_rank_gloo_equals_single_process(tmp_path, n_samples):
     assert got.shape == (n_samples, 10)
     for a, b in zip(got, want):
         assert np.array_equal(a, b)
+
+
+def _gpu_worker(rank, world, port, n_samples, out_path):
+    """One rank of the GPU sharded path; both ranks share cuda:0 (independent work, no
+    cross-rank waits inside kernels), logits gathered over gloo on host tensors."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2402_03060_b200.he_backend import GpuBackend
+
+    params = HEParams(poly_degree=1 << 12, depth=7, scale_bits=40, seed=21)
+    m = planner.lenet1(4)
+    samples = np.random.default_rng(12).uniform(0, 1, size=(n_samples, 1, 28, 28))
+    be = GpuBackend(params)
+    import torch
+
+    got = run_sharded(m, samples, params, be, fused=True)
+    if rank == 0:
+        np.save(out_path, got)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_gpu_backend_equals_single_process(tmp_path):
+    """world_size 2 on one GPU: GpuBackend per rank (keys from the shared secret seed, own nonce
+    streams), fused layers, logits gathered through the tensor all-gather -- equal to a
+    single-process sharded run and to the plaintext forward pass within CKKS tolerance."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    n_samples = 9  # 5 ciphertext groups of capacity 2: ranks own 3 and 2
+    out = str(tmp_path / "outs.npy")
+    mp.spawn(_gpu_worker, args=(2, _free_port(), n_samples, out), nprocs=2, join=True)
+    got = np.load(out)
+    from paper_2402_03060_b200.he_backend import GpuBackend
+
+    params = HEParams(poly_degree=1 << 12, depth=7, scale_bits=40, seed=21)
+    m = planner.lenet1(4)
+    samples = np.random.default_rng(12).uniform(0, 1, size=(n_samples, 1, 28, 28))
+    single = run_sharded(m, samples, params, GpuBackend(params), fused=True)
+    assert got.shape == single.shape == (n_samples, 10)
+    ref = np.stack([planner.reference_infer(m, s) for s in samples])
+    assert np.max(np.abs(got - single)) < 1e-5
+    assert np.max(np.abs(got - ref)) < 1e-5
+    assert np.array_equal(np.argmax(got, 1), np.argmax(ref, 1))
