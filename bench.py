@@ -207,7 +207,7 @@ def _hbm_peak():
     return 6540.2, "fallback: B200_PROFILING.md measured copy bandwidth"
 
 
-def conv2_roofline(timers, rates, step_ms, traffic_path):
+def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
     """Roofline of the dominant kernel call: the conv2 hoisted MAC (k_hoisted_imma on the 40-bit
     limbs + k_hoisted_bank on q_0 and P), against the pipes it runs on (a mixed bound):
     phase A on the 40-bit limbs at the narrow-operand MAC peak, phase A and phase B of the 60-bit
@@ -247,7 +247,7 @@ def conv2_roofline(timers, rates, step_ms, traffic_path):
             "bound_ms_parts": {k: v * 1e3 for k, v in parts.items()},
             "algorithmic_modmacs": {k: w[k] for k in ("a40", "a60", "b40", "b60", "total")},
             "work_shape": {k: w[k] for k in ("B", "I", "T", "O", "nz", "level")},
-            "share_of_step": tms / step_ms, "conv_mac_share_of_step": total_conv_ms / step_ms,
+            "share_of_step": tms / step_ms, "conv_mac_share_of_step": total_conv_ms / (step_ms * steps),
             "peak_source": "measured in this run (uh_bench_peaks): narrow-operand MAC rates[8], 128-bit MAC "
                            "rates[1], u8 IMMA MAC rates[9]; peak = total modMACs / mixed bound time",
             "frac_vs_all_imad_peak": achieved / r_mac}
@@ -424,7 +424,8 @@ def main():
 
     rates = _peaks(be)
     hbm_gbs, hbm_src = _hbm_peak()
-    roofline = conv2_roofline(timers, rates, step_ms, os.path.join(ROOT, "profiles", "conv2_traffic.json"))
+    roofline = conv2_roofline(timers, rates, step_ms, args.steps,
+                              os.path.join(ROOT, "profiles", "conv2_traffic.json"))
     rooflines = {"ntt": ntt_roofline(be, hbm_gbs, hbm_src), "step": step_roofline(rates, B, step_ms)}
     peaks = {"imad_per_s": rates[0], "mac128_per_s": rates[1], "mulmod_per_s": rates[2], "shoup_per_s": rates[4],
              "fp64_modmac_per_s": rates[5], "narrow_mac_per_s": rates[8], "imma_u8_mac_per_s": rates[9],

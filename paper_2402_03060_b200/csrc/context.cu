@@ -1,5 +1,8 @@
 // Context creation: per-prime constants, twiddle tables and slot-order tables,
 // computed once on the host (exact 128-bit arithmetic) and kept in HBM.
+#include <mutex>
+#include <set>
+
 #include "engine.cuh"
 #include "ops.cuh"
 
@@ -33,6 +36,17 @@ template <class T> T *upload(const std::vector<T> &v) {
     return d;
 }
 }  // namespace
+
+void smem_optin_raw(const void *kernel, size_t smem) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    UH_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({kernel, dev})) return;
+    UH_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done.insert({kernel, dev});
+}
 
 Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_t count, int device) {
     if (n < 4 || (n & (n - 1))) throw std::invalid_argument("n must be a power of two >= 4");
@@ -93,10 +107,11 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
     }
     // slot tables
     uint32_t half = n / 2, two_n = 2 * n;
-    std::vector<int32_t> dlog(two_n, -1), pos(half), neg(half), sob(n);
+    std::vector<int32_t> dlog(two_n, -1), pos(half), neg(half), sob(n), jof(half, -1);
     uint64_t e = 1;
     for (uint32_t j = 0; j < half; j++) {
         dlog[e] = (int32_t)j;
+        jof[(e - 1) / 4] = (int32_t)j;  // e = 1 mod 4 for every power of 5
         dlog[two_n - e] = (int32_t)(half + j);
         pos[j] = (int32_t)((e - 1) / 2);
         neg[j] = (int32_t)((two_n - e - 1) / 2);
@@ -192,6 +207,9 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
     c->d_invs = upload(invs);
     c->d_pos = upload(pos);
     c->d_neg = upload(neg);
+    for (int32_t v : jof)
+        if (v < 0) throw std::logic_error("canonical-embedding slot permutation invariant violated");
+    c->d_jof = upload(jof);
     return c;
 }
 
@@ -200,7 +218,7 @@ void ctx_destroy(Ctx *c) {
     DeviceGuard guard(c->device);
     for (void *p : {(void *)c->d_pmod, (void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_twf, (void *)c->d_itwf, (void *)c->d_twd, (void *)c->d_itwd, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
                     (void *)c->d_ipsi, (void *)c->d_ipsis,
-                    (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_inv2, (void *)c->d_inv2s, (void *)c->d_pos, (void *)c->d_neg})
+                    (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_inv2, (void *)c->d_inv2s, (void *)c->d_pos, (void *)c->d_neg, (void *)c->d_jof})
         if (p) cudaFree(p);
     delete c;
 }

@@ -32,6 +32,7 @@ struct Ctx {
     ulonglong2 *d_pmod = nullptr;        // [count] (P mod q_i, Shoup companion)
     int32_t *d_pos = nullptr;            // [n/2] index (5^j mod 2N - 1)/2 : slot j -> odd exponent slot
     int32_t *d_neg = nullptr;            // [n/2] index (2N - 5^j - 1)/2
+    int32_t *d_jof = nullptr;            // [n/2] slot j of the DFT index l = (5^j mod 2N - 1)/4 (embed.cu)
     int sp() const { return (int)count - 1; }
 };
 
@@ -70,17 +71,11 @@ struct DeviceGuard {
 };
 
 // Opt a kernel in to > 48 KB of dynamic shared memory on the current device.  The
-// attribute is per device, so the "done" record is a per-instance device bitmask
-// (setting it twice is harmless, so concurrent first calls need no lock).
+// attribute is per (kernel, device): the record is a set of both, under a mutex.
+void smem_optin_raw(const void *kernel, size_t smem);
 template <class K>
 void smem_optin(K *kernel, size_t smem) {
-    static std::atomic<uint64_t> done{0};
-    int dev = 0;
-    UH_CHECK(cudaGetDevice(&dev));
-    const uint64_t bit = 1ull << (dev & 63);
-    if (done.load(std::memory_order_relaxed) & bit) return;
-    UH_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    done.fetch_or(bit, std::memory_order_relaxed);
+    smem_optin_raw(reinterpret_cast<const void *>(kernel), smem);
 }
 
 // stream-ordered scratch buffer

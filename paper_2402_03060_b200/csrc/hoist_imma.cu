@@ -26,8 +26,7 @@
 //             pre-split mask bank (16-byte loads, fragment order), B fragments
 //             from shared memory; 4 k-steps x 5 n-tiles of IMMA per unit, then
 //             the byte recombination and the modular reduction per output.
-// The 60-bit limbs (q_0, P) keep the IMAD kernel (hoisted_mac_bank_wide) by default; the same
-// kernel with 8-byte operands (64 byte products, 2 outputs per m-tile) is opt-in.
+// The 60-bit limbs (q_0, P) run on the IMAD key-bank kernel (hoisted_mac_bank_wide, hoist_bank.cu).
 #include <type_traits>
 
 #include "ops.cuh"
@@ -35,29 +34,23 @@
 namespace uh {
 namespace {
 
-#ifndef UH_IMMA_LDSM
-#define UH_IMMA_LDSM 0  // B fragments via ldmatrix (16-byte aligned planes): bit-exact, measured 31.9 vs 31.6 ms (the aligned planes cost phase-A store conflicts)
-#endif
 #ifndef UH_IMMA_MIN_O
 #define UH_IMMA_MIN_O 5  // narrower layers stay on the register-only IMAD kernel
-#endif
-#ifndef UH_IMMA_CT2
-#define UH_IMMA_CT2 1  // phase A of the 40-bit limbs: two ciphertexts per item (shared key loads)
 #endif
 constexpr int kICT = 4;                     // ciphertexts per CTA
 constexpr int kIJ = 2 * kICT;               // columns per value byte (ciphertext x component)
 constexpr int kIRow = 144;                  // bytes per (coefficient, byte, column) row: 128 terms + pad
 constexpr int kIMaxTerms = 128;             // 4 k-steps
-// Byte width W of the residues: 5 for the 40-bit limbs (3 outputs x 5 mask bytes per 16-row
-// m-tile, 4 m-tiles), 8 for the 60-bit limbs q_0 and P (2 outputs x 8 bytes, 6 m-tiles).
+// Byte width W = 5 of the 40-bit residues: 3 outputs x 5 mask bytes per 16-row m-tile, 4 m-tiles.
 template <int W> struct IW {
-    static constexpr int NC = W == 5 ? 8 : 4;           // coefficients per CTA (W = 8: 3 CTAs per SM)
-    static constexpr int OPT = W == 5 ? 3 : 2;          // outputs per m-tile
+    static_assert(W == 5, "40-bit limbs only");
+    static constexpr int NC = 8;                        // coefficients per CTA
+    static constexpr int OPT = 3;                       // outputs per m-tile
     static constexpr int MT = 12 / OPT;                 // m-tiles for 12 outputs
-    static constexpr int COEF = W * kIJ * kIRow + (UH_IMMA_LDSM ? 16 : 4);  // coefficient stride of the B planes
+    static constexpr int COEF = W * kIJ * kIRow + 4;    // coefficient stride of the B planes
     static constexpr int CS = W * 8 + 2;                // C staging row stride (int32)
     static constexpr size_t SMEM = (size_t)NC * COEF + 8 * 16 * CS * 4;
-    static constexpr int MINB = W == 5 ? 3 : 2;         // resident CTAs per SM (W = 8: 128 registers, no spills)
+    static constexpr int MINB = 3;                      // resident CTAs per SM
 };
 
 __device__ __forceinline__ uint32_t rot_index_i(uint32_t n, uint32_t half, uint32_t r) {
@@ -71,13 +64,6 @@ __device__ __forceinline__ uint64_t fold64_i(uint64_t hi, uint64_t lo, const Mod
     const uint64_t v = lo + p;
     return v < p ? v + m.r64 : v;
 }
-// (hi:lo) += t << sh, 0 <= sh < 64
-__device__ __forceinline__ void add_shifted(uint64_t &hi, uint64_t &lo, uint64_t t, int sh) {
-    const uint64_t l = t << sh;
-    const uint64_t h = sh ? t >> (64 - sh) : 0;
-    lo += l;
-    hi += h + (lo < l);
-}
 
 __device__ __forceinline__ void imma(int (&c)[4], const uint4 &a, uint32_t b0, uint32_t b1) {
     asm volatile(
@@ -88,14 +74,13 @@ __device__ __forceinline__ void imma(int (&c)[4], const uint4 &a, uint32_t b0, u
 
 // A-fragment mask bank [limb slot][N][m-tile][k-step][lane][4 words]: per coefficient, the
 // (output x byte) x term matrix.  Row r of m-tile mt is output OPT mt + r / W, byte r % W
-// (rows past OPT W and outputs >= O are zero).  Limb slots: W = 5 -> limbs 1..L-1,
-// W = 8 -> limbs 0 and L (P).
+// (rows past OPT W and outputs >= O are zero).  Limb slots: limbs 1..L-1.
 template <int W>
 __global__ void k_imma_bank(uint32_t *__restrict__ ib, const uint64_t *__restrict__ masks, int O, int Q, int L,
                             int logn, int nks) {
     using C = IW<W>;
     const uint32_t N = 1u << logn;
-    const int nslots = W == 5 ? L - 1 : 2;
+    const int nslots = L - 1;
     const size_t total = (size_t)nslots * N * C::MT * nks * 32;
     const size_t ROW = (size_t)(L + 1) << logn;
     for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
@@ -106,7 +91,7 @@ __global__ void k_imma_bank(uint32_t *__restrict__ ib, const uint64_t *__restric
         const size_t r1 = r0 / C::MT;
         const uint32_t n = (uint32_t)(r1 & (N - 1));
         const int slot = (int)(r1 >> logn);
-        const int k = W == 5 ? slot + 1 : (slot ? L : 0);
+        const int k = slot + 1;
         const int g = lane >> 2, tig = lane & 3;
         uint32_t w[4];
 #pragma unroll
@@ -147,11 +132,11 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
     const int b0 = blockIdx.x * kICT;
     const uint32_t n0 = blockIdx.y * C::NC;
     const int slot = blockIdx.z;
-    const int k = W == 5 ? 1 + slot : (slot ? L : 0);  // limb: q_1..q_{L-1}, or q_0 / P
-    const bool qlimb = W == 5 || k < L;  // the 40-bit slots are all q-limbs
-    const Mod m = mods[qlimb ? k : sp];
+    const int k = 1 + slot;  // limb q_1..q_{L-1}
+    constexpr bool qlimb = true;
+    const Mod m = mods[k];
     const uint64_t P = mods[sp].q;
-    const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
+    const uint64_t Pk = P < m.q ? P : csub(barrett_lite(P, m), m.q);
     const int Q = I * T;
     for (int q = tid; q < Q; q += blockDim.x) {
         const int i = q / T, t = q - i * T;
@@ -165,7 +150,6 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
     // ---- phase A: key-switched P * rot(ct) per (term, ciphertext, coefficient) -> byte planes ----
     // one term per item (Q * 32 items over 256 threads: balanced to within one item per thread);
     // lanes = (ciphertext, coefficient), so the byte stores of a warp hit 32 distinct banks
-#if UH_IMMA_CT2
     {
         // two ciphertexts per item: the Galois-key rows (2L loads) serve both -- a third fewer
         // loads through L1, which is the phase's limit (MIO throttle)
@@ -202,7 +186,7 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
                     db[j] = okb ? __ldg(Db + (uint32_t)j * ROW) : 0;
                 }
                 const uint64_t csa = qlimb ? __ldg(c0a + src) : 0, csb = qlimb && okb ? __ldg(c0b + src) : 0;
-                using A = typename std::conditional<W == 5, AccN, Acc>::type;
+                using A = AccN;
                 A a0, a1, e0, e1;
                 a0.zero();
                 a1.zero();
@@ -220,13 +204,9 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
                     e0.mac(Pk, csb);
                 }
                 auto fin = [&](const A &acc) -> uint64_t {
-                    if constexpr (W == 5) {
-                        uint64_t h, l;
-                        acc.value(h, l);
-                        return csub(barrett_lite(fold64_i(h, l, m), m), m.q);
-                    } else {
-                        return acc.reduce(m);
-                    }
+                    uint64_t h, l;
+                    acc.value(h, l);
+                    return csub(barrett_lite(fold64_i(h, l, m), m), m.q);
                 };
                 v[0][0] = fin(a0);
                 v[0][1] = fin(a1);
@@ -242,74 +222,6 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
                 for (int e = 0; e < 4; e++) pl[bb * kIJ * kIRow + e * kIRow] = (unsigned char)(v[e >> 1][e & 1] >> (8 * bb));
         }
     }
-    if constexpr (!UH_IMMA_CT2) {
-#endif
-    constexpr int LN = kICT * C::NC;  // lanes per term: (ciphertext, coefficient)
-    for (int it = tid; it < Q * LN; it += 256) {
-        const int q = it / LN, ct = (it / C::NC) & 3, cf = it % C::NC;
-        const int b = b0 + ct;
-        const uint32_t n = n0 + cf;
-        uint64_t v0 = 0, v1 = 0;
-        if (b < B) {
-            const uint32_t r = s_r[q];
-            const uint64_t *c0 = X + s_x[q] + (((uint32_t)b * 2 * L + k) << LOGN);
-            if (r == 0) {
-                if (qlimb) {
-                    v0 = mulmod(Pk, __ldg(c0 + n), m);
-                    v1 = mulmod(Pk, __ldg(c0 + ((uint32_t)L << LOGN) + n), m);
-                }
-            } else {
-                const uint32_t src = rot_index_i(n, half, r);
-                const uint64_t *Dj = D + s_d[q] + (((uint32_t)b * L * LP + k) << LOGN) + src;
-                const uint64_t *K = kbank + s_k[q] + ((uint32_t)k * 2 * L << LOGN) + n;
-                uint64_t d[L], x[L], y[L];
-#pragma unroll
-                for (int j = 0; j < L; j++) {
-                    d[j] = __ldg(Dj + (uint32_t)j * ROW);
-                    x[j] = __ldg(K + ((uint32_t)(2 * j) << LOGN));
-                    y[j] = __ldg(K + ((uint32_t)(2 * j + 1) << LOGN));
-                }
-                if constexpr (W == 5) {
-                    const uint64_t cs = __ldg(c0 + src);
-                    AccN a0, a1;
-                    a0.zero();
-                    a1.zero();
-#pragma unroll
-                    for (int j = 0; j < L; j++) {
-                        a0.mac(d[j], x[j]);
-                        a1.mac(d[j], y[j]);
-                    }
-                    a0.mac(Pk, cs);
-                    uint64_t h0, l0, h1, l1;
-                    a0.value(h0, l0);
-                    a1.value(h1, l1);
-                    v0 = csub(barrett_lite(fold64_i(h0, l0, m), m), m.q);
-                    v1 = csub(barrett_lite(fold64_i(h1, l1, m), m), m.q);
-                } else {
-                    Acc a0, a1;
-                    a0.zero();
-                    a1.zero();
-#pragma unroll
-                    for (int j = 0; j < L; j++) {
-                        a0.mac(d[j], x[j]);
-                        a1.mac(d[j], y[j]);
-                    }
-                    if (qlimb) a0.mac(Pk, __ldg(c0 + src));
-                    v0 = a0.reduce(m);
-                    v1 = a1.reduce(m);
-                }
-            }
-        }
-        unsigned char *pl = ism + cf * C::COEF + (2 * ct) * kIRow + q;
-#pragma unroll
-        for (int bb = 0; bb < W; bb++) {
-            pl[bb * kIJ * kIRow] = (unsigned char)(v0 >> (8 * bb));
-            pl[bb * kIJ * kIRow + kIRow] = (unsigned char)(v1 >> (8 * bb));
-        }
-    }
-#if UH_IMMA_CT2
-    }
-#endif
     // terms [Q, 32 NKS) of the B planes are never written: their A bytes are zero (integer
     // products, so whatever the shared memory holds there contributes nothing)
     __syncthreads();
@@ -329,32 +241,6 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
         int Cr[W][4];
 #pragma unroll
         for (int nb = 0; nb < W; nb++) Cr[nb][0] = Cr[nb][1] = Cr[nb][2] = Cr[nb][3] = 0;
-#if UH_IMMA_LDSM
-        // B fragments with ldmatrix: x4 = (k 0-15, k 16-31) of two k-steps, lane l addresses row
-        // l % 8 of matrix l / 8 (16-byte rows: COEF is a multiple of 16)
-        {
-            const uint32_t lb = (uint32_t)__cvta_generic_to_shared(ism + cf * C::COEF + (lane & 7) * kIRow +
-                                                                   ((lane >> 3) & 1) * 16 + (lane >> 4) * 32);
-#pragma unroll
-            for (int nb = 0; nb < W; nb++) {
-#pragma unroll
-                for (int ks = 0; ks < NKS; ks += 2) {
-                    uint32_t r0, r1, r2, r3;
-                    const uint32_t a = lb + nb * kIJ * kIRow + ks * 32;
-                    if (ks + 1 < NKS) {
-                        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                                     : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(a));
-                        imma(Cr[nb], A[ks], r0, r1);
-                        imma(Cr[nb], A[ks + 1], r2, r3);
-                    } else {
-                        asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
-                                     : "=r"(r0), "=r"(r1) : "r"(a));
-                        imma(Cr[nb], A[ks], r0, r1);
-                    }
-                }
-            }
-        }
-#else
         const unsigned char *bp = ism + cf * C::COEF + gid * kIRow + tig * 4;
 #pragma unroll
         for (int ks = 0; ks < NKS; ks++)
@@ -364,7 +250,6 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
                 imma(Cr[nb], A[ks], *reinterpret_cast<const uint32_t *>(p),
                      *reinterpret_cast<const uint32_t *>(p + 16));
             }
-#endif
 #pragma unroll
         for (int nb = 0; nb < W; nb++) {
             const int col = nb * 8 + tig * 2;
@@ -383,23 +268,12 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
                 for (int a = 0; a < W; a++)
 #pragma unroll
                     for (int nb = 0; nb < W; nb++) Ts[a + nb] += (uint32_t)cw[(ol * W + a) * C::CS + nb * 8 + j];
-                uint64_t r;
-                if constexpr (W == 5) {
-                    // value = sum_s Ts[s] 2^(8 s) < 2^89: low part (s <= 4) and high part (s >= 5) * 2^40
-                    const uint64_t lo = Ts[0] + (Ts[1] << 8) + (Ts[2] << 16) + (Ts[3] << 24) + (Ts[4] << 32);
-                    const uint64_t hx = Ts[5] + (Ts[6] << 8) + (Ts[7] << 16) + (Ts[8] << 24);
-                    const uint64_t l2 = lo + (hx << 40);
-                    const uint64_t h2 = (hx >> 24) + (l2 < lo);
-                    r = reduce128(h2, l2, m);
-                } else {
-                    // value = lo128 + hi128 * 2^64 (< 2^138): both halves < 2^83
-                    uint64_t lh = 0, ll = 0, hh = 0, hl = 0;
-#pragma unroll
-                    for (int s2 = 0; s2 < 8; s2++) add_shifted(lh, ll, Ts[s2], 8 * s2);
-#pragma unroll
-                    for (int s2 = 8; s2 < 15; s2++) add_shifted(hh, hl, Ts[s2], 8 * (s2 - 8));
-                    r = addmod(reduce128(lh, ll, m), mulmod(reduce128(hh, hl, m), m.r64, m), m.q);
-                }
+                // value = sum_s Ts[s] 2^(8 s) < 2^89: low part (s <= 4) and high part (s >= 5) * 2^40
+                const uint64_t lo = Ts[0] + (Ts[1] << 8) + (Ts[2] << 16) + (Ts[3] << 24) + (Ts[4] << 32);
+                const uint64_t hx = Ts[5] + (Ts[6] << 8) + (Ts[7] << 16) + (Ts[8] << 24);
+                const uint64_t l2 = lo + (hx << 40);
+                const uint64_t h2 = (hx >> 24) + (l2 < lo);
+                const uint64_t r = reduce128(h2, l2, m);
                 acc_out[((((uint32_t)o * B + b) * 2 + (j & 1)) * LP + k) * N + n] = r;
             }
         }
@@ -411,7 +285,7 @@ template <int L, int NKS, int W>
 void launch_imma_k(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib,
                    const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
     smem_optin(k_hoisted_imma<L, 15, NKS, W>, IW<W>::SMEM);
-    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / IW<W>::NC), W == 5 ? L - 1 : 2);
+    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / IW<W>::NC), L - 1);
     k_hoisted_imma<L, 15, NKS, W><<<grid, 256, IW<W>::SMEM, s>>>(acc, X, D, reinterpret_cast<const uint4 *>(ib), kbank,
                                                                 shifts, B, I, T, O, c.sp(), c.d_mods);
     UH_LAUNCH_CHECK();
@@ -438,19 +312,16 @@ bool hoisted_imma_supported(const Ctx &c, int level, int O, int Q) {
     return (c.h_q[0] >> 40) && (c.h_q[c.count - 1] >> 40);
 }
 
-// words of the 40-bit-limb bank followed by the 60-bit-limb bank (uint32)
+// uint32 words of the 40-bit-limb bank
 size_t imma_bank_words(const Ctx &c, int level, int Q) {
     const int nks = (Q + 31) / 32;
-    return ((size_t)level * IW<5>::MT + 2 * IW<8>::MT) * c.n * nks * 32 * 4;
+    return (size_t)level * IW<5>::MT * c.n * nks * 32 * 4;
 }
 
 void imma_mask_bank(const Ctx &c, uint32_t *ib, const uint64_t *masks, int O, int Q, int level, cudaStream_t s) {
     const int L = level + 1, nks = (Q + 31) / 32;
-    const size_t t5 = (size_t)(L - 1) * c.n * IW<5>::MT * nks * 32, t8 = (size_t)2 * c.n * IW<8>::MT * nks * 32;
+    const size_t t5 = (size_t)(L - 1) * c.n * IW<5>::MT * nks * 32;
     k_imma_bank<5><<<(unsigned)std::min<size_t>((t5 + 255) / 256, 148 * 32), 256, 0, s>>>(ib, masks, O, Q, L,
-                                                                                         (int)c.logn, nks);
-    UH_LAUNCH_CHECK();
-    k_imma_bank<8><<<(unsigned)std::min<size_t>((t8 + 255) / 256, 148 * 32), 256, 0, s>>>(ib + t5 * 4, masks, O, Q, L,
                                                                                          (int)c.logn, nks);
     UH_LAUNCH_CHECK();
 }
@@ -459,16 +330,6 @@ void hoisted_mac_bank_wide(const Ctx &c, uint64_t *acc, const uint64_t *X, const
                            const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, int level,
                            cudaStream_t s);
 
-// Opt-in (UH_IMMA_WIDE=1): the 8-byte IMMA path for q_0 and P as well.  Bit-exact, measured
-// slower than the IMAD kernel on those two limbs (LeNet conv2 at B = 64: 35.2 vs 33.0 ms for
-// the whole call; 64 byte products and 6 m-tiles per coefficient, two 107 KB CTAs per SM).
-static bool imma_wide_on() {
-    static const bool on = [] {
-        const char *e = getenv("UH_IMMA_WIDE");
-        return e && std::string(e) == "1";
-    }();
-    return on;
-}
 
 void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
                       const uint32_t *ib, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O,
@@ -480,14 +341,10 @@ void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint
     if ((double)I * B * 2 * L * c.n > lim || (double)I * B * L * (L + 1) * c.n > lim ||
         (double)O * B * 2 * (L + 1) * c.n > lim)
         throw std::invalid_argument("IMMA hoisted kernel operand exceeds 2^32 elements: split the batch");
-    const int nks = (I * T + 31) / 32;
-    const uint32_t *ib8 = ib + (size_t)(L - 1) * c.n * IW<5>::MT * nks * 32 * 4;
-    const bool wide = imma_wide_on();
-    if (!wide) hoisted_mac_bank_wide(c, acc, X, D, masks, kbank, shifts, B, I, T, O, level, s);
-#define UH_IMMA_CASE(LL)                                                               \
-    case LL:                                                                           \
-        if (wide) launch_imma<LL, 8>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s); \
-        launch_imma<LL, 5>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);            \
+    hoisted_mac_bank_wide(c, acc, X, D, masks, kbank, shifts, B, I, T, O, level, s);  // q_0 and P
+#define UH_IMMA_CASE(LL)                                                    \
+    case LL:                                                                \
+        launch_imma<LL, 5>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); \
         break;
     switch (L) {
         UH_IMMA_CASE(3)

@@ -2,9 +2,6 @@
 // embedding (encode / decode).  Randomness comes from the counter-based RNG
 // in common.cuh, whose definition is shared bit-for-bit with the CPU oracle,
 // so seeded keys, masks and noise are identical on both sides.
-#include <cufft.h>
-#include <map>
-#include <mutex>
 #include "ops.cuh"
 
 namespace uh {
@@ -186,76 +183,6 @@ __global__ void k_from_signed(uint64_t *out, const int64_t *coef, int n_polys, i
     }
 }
 
-// ---- canonical embedding ----
-__global__ void k_embed_scatter(cufftDoubleComplex *V, const double *slots, int n_polys, double scale, int logn,
-                                const int32_t *__restrict__ pos, const int32_t *__restrict__ neg) {
-    size_t half = (size_t)1 << (logn - 1);
-    size_t total = (size_t)n_polys * half;
-    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (size_t)gridDim.x * blockDim.x) {
-        size_t j = idx & (half - 1), p = idx >> (logn - 1);
-        double v = slots[idx] * scale;
-        V[(p << logn) + pos[j]] = make_cuDoubleComplex(v, 0.0);
-        V[(p << logn) + neg[j]] = make_cuDoubleComplex(v, 0.0);
-    }
-}
-
-__global__ void k_embed_round(int64_t *coef, const cufftDoubleComplex *V, size_t total, int logn) {
-    size_t nmask = ((size_t)1 << logn) - 1;
-    double inv_n = 1.0 / (double)(1u << logn);
-    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (size_t)gridDim.x * blockDim.x) {
-        size_t n = idx & nmask;
-        double sn, cn;
-        sincospi((double)n * inv_n, &sn, &cn);
-        cufftDoubleComplex v = V[idx];
-        double re = (v.x * cn + v.y * sn) * inv_n;  // Re(v * zeta^-n) / N
-        coef[idx] = __double2ll_rn(re);
-    }
-}
-
-__global__ void k_twist(cufftDoubleComplex *W, const double *coef, size_t total, int logn) {
-    size_t nmask = ((size_t)1 << logn) - 1;
-    double inv_n = 1.0 / (double)(1u << logn);
-    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (size_t)gridDim.x * blockDim.x) {
-        size_t n = idx & nmask;
-        double sn, cn;
-        sincospi((double)n * inv_n, &sn, &cn);
-        double x = coef[idx];
-        W[idx] = make_cuDoubleComplex(x * cn, x * sn);
-    }
-}
-
-__global__ void k_slots_gather(double *slots, const cufftDoubleComplex *W, int n_polys, double inv_scale, int logn,
-                               const int32_t *__restrict__ pos) {
-    size_t half = (size_t)1 << (logn - 1);
-    size_t total = (size_t)n_polys * half;
-    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (size_t)gridDim.x * blockDim.x) {
-        size_t j = idx & (half - 1), p = idx >> (logn - 1);
-        slots[idx] = W[(p << logn) + pos[j]].x * inv_scale;
-    }
-}
-
-std::mutex g_plan_mu;
-std::map<std::pair<uint32_t, int>, cufftHandle> g_plans;
-
-cufftHandle plan_for(uint32_t n, int batch, cudaStream_t s) {
-    std::lock_guard<std::mutex> lk(g_plan_mu);
-    auto key = std::make_pair(n, batch);
-    auto it = g_plans.find(key);
-    cufftHandle h;
-    if (it == g_plans.end()) {
-        if (cufftPlan1d(&h, (int)n, CUFFT_Z2Z, batch) != CUFFT_SUCCESS) throw CudaError("cufftPlan1d failed");
-        g_plans[key] = h;
-    } else {
-        h = it->second;
-    }
-    if (cufftSetStream(h, s) != CUFFT_SUCCESS) throw CudaError("cufftSetStream failed");
-    return h;
-}
-
 }  // namespace
 
 void secret_gen(const Ctx &c, uint64_t *s_eval, uint64_t seed, cudaStream_t st) {
@@ -335,34 +262,6 @@ void from_signed(const Ctx &c, uint64_t *out, const int64_t *coef, int n_polys, 
                                                                       (int)c.logn, c.d_mods);
     UH_LAUNCH_CHECK();
     ntt_forward(c, out, n_polys, nl, nq, 0, out_ps, s);
-}
-
-void encode_coeffs(const Ctx &c, int64_t *coef, const double *slots, int n_polys, double scale, cudaStream_t s) {
-    size_t N = c.n;
-    Scratch V((size_t)n_polys * N * sizeof(cufftDoubleComplex), s);
-    k_embed_scatter<<<grid_for((size_t)n_polys * N / 2), kTB, 0, s>>>(V.as<cufftDoubleComplex>(), slots, n_polys,
-                                                                      scale, (int)c.logn, c.d_pos, c.d_neg);
-    UH_LAUNCH_CHECK();
-    cufftHandle h = plan_for(c.n, n_polys, s);
-    if (cufftExecZ2Z(h, V.as<cufftDoubleComplex>(), V.as<cufftDoubleComplex>(), CUFFT_FORWARD) != CUFFT_SUCCESS)
-        throw CudaError("cufftExecZ2Z failed");
-    k_embed_round<<<grid_for((size_t)n_polys * N), kTB, 0, s>>>(coef, V.as<cufftDoubleComplex>(), (size_t)n_polys * N,
-                                                                (int)c.logn);
-    UH_LAUNCH_CHECK();
-}
-
-void decode_coeffs(const Ctx &c, double *slots, const double *coef, int n_polys, double scale, cudaStream_t s) {
-    size_t N = c.n;
-    Scratch W((size_t)n_polys * N * sizeof(cufftDoubleComplex), s);
-    k_twist<<<grid_for((size_t)n_polys * N), kTB, 0, s>>>(W.as<cufftDoubleComplex>(), coef, (size_t)n_polys * N,
-                                                          (int)c.logn);
-    UH_LAUNCH_CHECK();
-    cufftHandle h = plan_for(c.n, n_polys, s);
-    if (cufftExecZ2Z(h, W.as<cufftDoubleComplex>(), W.as<cufftDoubleComplex>(), CUFFT_INVERSE) != CUFFT_SUCCESS)
-        throw CudaError("cufftExecZ2Z failed");
-    k_slots_gather<<<grid_for((size_t)n_polys * N / 2), kTB, 0, s>>>(slots, W.as<cufftDoubleComplex>(), n_polys,
-                                                                     1.0 / scale, (int)c.logn, c.d_pos);
-    UH_LAUNCH_CHECK();
 }
 
 }  // namespace uh

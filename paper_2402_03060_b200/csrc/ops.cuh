@@ -98,7 +98,8 @@ void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint
                       int level, cudaStream_t s);
 // microbench.cu: rates[0] = IMAD/s, rates[1] = 128-bit MAC/s, rates[2] = reduced mulmod/s
 void bench_peaks(const Ctx &c, double *rates);
-// canonical embedding with cuFFT (fp64): slots [n_polys][N/2] -> rounded int64 coefficients.
+// embed.cu -- canonical embedding (hand-written FP64 four-step FFT): slots [n_polys][N/2] <-> int64 / double
+// coefficients [n_polys][N] at `scale`.
 void encode_coeffs(const Ctx &c, int64_t *coef, const double *slots, int n_polys, double scale, cudaStream_t s);
 void decode_coeffs(const Ctx &c, double *slots, const double *coef, int n_polys, double scale, cudaStream_t s);
 

@@ -36,7 +36,7 @@ import numpy as np
 import torch
 
 from . import _lib, schedule
-from .planner import AvgPool2d, Conv1d, Conv2d, Square
+from .planner import ApproxReLU, AvgPool2d, Conv1d, Conv2d, Square
 from .schedule import CipherState, conv_geometry, pool_layout, pool_shifts, position_mask, valid_positions
 
 OP_ADD = 0
@@ -107,8 +107,8 @@ def imma_bank(backend, masks: torch.Tensor, O: int, Q: int, level: int, cache: b
     if hit is not None and hit[0] is masks:
         return hit[1]
     nks = (Q + 31) // 32
-    # 40-bit limbs q_1..q_level: 4 m-tiles of 3 outputs x 5 bytes; q_0 and P: 6 m-tiles of 2 x 8 bytes
-    ib = torch.empty(((4 * level + 12) * backend.n * nks * 32 * 4,), dtype=torch.int32, device=backend.device)
+    # 40-bit limbs q_1..q_level: 4 m-tiles of 3 outputs x 5 bytes (q_0 and P stay on the IMAD kernel)
+    ib = torch.empty((4 * level * backend.n * nks * 32 * 4,), dtype=torch.int32, device=backend.device)
     backend._call("uh_imma_mask_bank", _vp(ib), _vp(masks), O, Q, level, backend._stream())
     if cache:
         banks[ck] = (masks, ib)
@@ -364,6 +364,62 @@ def square(backend, state: CipherState) -> CipherState:
     new_scale = scale * scale / float(backend.modulus(level))
     return CipherState([CipherVector(out[c], level - 1, new_scale, backend) for c in range(C)],
                        replace(lay, pending_const=lay.pending_const * lay.pending_const))
+
+
+def approx_relu(backend, state: CipherState, layer) -> CipherState:
+    """a2 x^2 + a1 x + a0 in Horner form over every channel and ciphertext in one batched pass
+    (layers.py:238-260): masked ct x pt (+ rescale), + masked a1, ct x ct (+ relinearise +
+    rescale), + masked a0.  Two levels; the masks scrub the gap slots, the pending constant is
+    folded into the coefficients.  The scale is tracked exactly: s -> s^2 / q_(level-1)."""
+    if not _is_gpu(backend):
+        return schedule.approx_relu(backend, state, layer)
+    from dataclasses import replace
+
+    from .errors import LevelExhausted
+    from .he_backend import CipherVector
+
+    lay = state.layout
+    level = min(c.level for c in state.cts)
+    if level < 2:
+        raise LevelExhausted("ciphertext has no multiplication budget left")
+    C, L, n = len(state.cts), level + 1, backend.n
+    B = state.cts[0].batch
+    scale = state.cts[0].scale
+    for c in state.cts:
+        backend._check_scale(state.cts[0], c)
+    cnt = backend.counter  # census, exactly as schedule.approx_relu records it
+    cnt.record("pt_mult", level, C)
+    cnt.record("add", level - 1, C)
+    cnt.record("ct_mult", level - 1, C)
+    cnt.record("add", level - 2, C)
+    p = lay.pending_const
+    ql, qm = float(backend.modulus(level)), float(backend.modulus(level - 1))
+    out_scale = scale * scale / qm
+    key = ("relu", layer_digest(layer), lay, level, scale)
+
+    def build():
+        ns = backend.params.num_slots
+        pattern = torch.from_numpy(position_mask(ns, lay, valid_positions(lay))).to(backend.device)[None, :]
+        return (backend.encode_device(pattern * (layer.a2 * p * p), level, ql),
+                backend.encode_device(pattern * (layer.a1 * p), level - 1, scale),
+                backend.encode_device(pattern * layer.a0, level - 2, out_scale))
+
+    quad, lin, const = _bank(backend, key, build)
+    X = stack_cts(backend, state.cts, level)  # [C][B][2][L][N]
+    CB = C * B
+    st = backend._stream()
+    t = backend._empty(CB, 2, level, n)  # ct x quad, rescaled: level - 1, scale unchanged
+    backend._call("uh_mul_plain_rescale", _vp(t), _vp(X), _vp(quad), CB, level, level, L, L, 0, st)
+    lm = level  # limbs at level - 1
+    backend._call("uh_elementwise", OP_ADD, _vp(t), _vp(t), _vp(lin), CB, 1, lm, lm, 2 * lm, 2 * lm, lm, st)
+    rk = backend.relin_key(level - 1)
+    out = backend._empty(C, B, 2, level - 1, n)  # (t x ct) relinearised, rescaled: level - 2
+    backend._call("uh_mul_relin_rescale_fused", _vp(out), _vp(t), _vp(X), CB, level - 1, level - 1, lm, L,
+                  _vp(rk), rk.shape[2], st)
+    lo = level - 1
+    backend._call("uh_elementwise", OP_ADD, _vp(out), _vp(out), _vp(const), CB, 1, lo, lo, 2 * lo, 2 * lo, lo, st)
+    return CipherState([CipherVector(out[c], level - 2, out_scale, backend) for c in range(C)],
+                       replace(lay, pending_const=1.0, gaps_zero=True))
 
 
 # -- flatten and FC through the generic hoisted kernel -----------------------------------
@@ -630,4 +686,6 @@ def apply_layer_fused(backend, state: CipherState, layer) -> CipherState:
         return flatten(backend, state)
     if isinstance(layer, FC):
         return fc(backend, state, layer)
+    if isinstance(layer, ApproxReLU):
+        return approx_relu(backend, state, layer)
     return schedule.apply_layer(backend, state, layer)

@@ -214,17 +214,3 @@ def test_imma_kernel_equals_key_bank_kernel(O, level, I, shifts, B, monkeypatch)
     monkeypatch.setenv("UH_IMMA", "0")
     want = fused._hoist(be, X, level, shifts, mdev, O, False, B)
     assert torch.equal(got, want)
-
-
-def test_opt_in_wide_imma_bit_exact():
-    """UH_IMMA_WIDE=1 (8-byte IMMA operands on q_0 and P, read once per process) re-runs the IMMA
-    parity cases in a subprocess."""
-    import os
-    import subprocess
-    import sys
-
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.abspath(__file__),
-                        "-k", "imma_kernel_equals"], cwd=root, env=dict(os.environ, UH_IMMA_WIDE="1"),
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
