@@ -109,3 +109,63 @@ def test_backend_reused_across_models():
         outs, _, _ = driver.run_inference(m, samples, params, plan=plan, backend=be, fused=True)
         for y, s in zip(outs, samples):
             assert np.max(np.abs(y - planner.reference_infer(m, s))) < 1e-5
+
+
+def _census(metrics):
+    return [(r.name, r.rotations, r.pt_mults, r.ct_mults, r.adds, r.level_after) for r in metrics.per_layer]
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["oplevel", "fused"])
+def test_m3_approx_relu_end_to_end(fused):
+    """Builtin M3 (conv -> approx_relu -> pool -> flatten -> fc -> approx_relu -> fc, layers.py:238-260
+    twice, model.py:676-683) at N = 2^14 on the GPU: decrypted logits within 1e-5 of the plaintext
+    forward pass with identical argmax, and the op census / level trace of the reference schedule
+    (the slot simulator's) -- the fused approx_relu is one batched masked ct x pt + plaintext add +
+    ct x ct + add, with the scale tracked through s -> s^2 / q (the ct + ct adds that follow in
+    flatten / fc must not raise ScaleMismatch)."""
+    from oracle.slot_sim import SimBackend
+
+    params = HEParams(poly_degree=1 << 14, depth=9, scale_bits=40)
+    m = planner.builtin("M3", seed=1)
+    plan = planner.footprint(m, params)
+    rng = np.random.default_rng(33)
+    samples = list(rng.uniform(0, 1, size=(plan.capacity, 1, 28, 28)))
+    be = GpuBackend(params)
+    outs, met, _ = driver.run_inference(m, samples, params, plan=plan, backend=be, fused=fused)
+    sim = SimBackend(params)
+    _, sim_met, _ = driver.run_inference(m, samples, params, plan=plan, backend=sim)
+    assert _census(met) == _census(sim_met)
+    assert be.counter.by_level == sim.counter.by_level
+    for y, s in zip(outs, samples):
+        ref = planner.reference_infer(m, s)
+        scale = max(1.0, float(np.max(np.abs(ref))))
+        assert np.max(np.abs(y - ref)) / scale < 1e-5
+        assert int(np.argmax(y)) == int(np.argmax(ref))
+
+
+def test_approx_relu_fused_equals_oplevel():
+    """The fused approx_relu layer equals the op-level schedule on the same input state (3
+    ciphertexts, 6 channels, a pending constant from the conv) to CKKS rounding, with the same
+    census, level and scale."""
+    params = HEParams(poly_degree=1 << 12, depth=9, scale_bits=40)
+    m = planner.builtin("M3", seed=2)
+    plan = planner.footprint(m, params)
+    be = GpuBackend(params)
+    rng = np.random.default_rng(34)
+    groups = [list(rng.uniform(0, 1, size=(plan.capacity, 1, 28, 28))) for _ in range(3)]
+    planes = driver.pack_groups(m, groups, plan)
+    ct = be.encrypt(be.encode_batch(planes[0]))
+    state = schedule.drop_level(be, CipherState([ct], driver._input_layout(m, plan)), 9)
+    state = fused.apply_layer_fused(be, state, m.layers[0])  # conv: 6 channels
+    from paper_2402_03060_b200.counter import diff_snapshots
+
+    c0 = be.counter.snapshot()
+    ref = schedule.apply_layer(be, state, m.layers[1])
+    c1 = be.counter.snapshot()
+    got = fused.apply_layer_fused(be, state, m.layers[1])
+    c2 = be.counter.snapshot()
+    assert diff_snapshots(c0, c1) == diff_snapshots(c1, c2)
+    assert got.layout == ref.layout and got.level == ref.level
+    assert all(abs(a.scale - b.scale) <= 1e-9 * a.scale for a, b in zip(got.cts, ref.cts))
+    a, b = _dec(be, ref), _dec(be, got)
+    assert np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(a)))) < 1e-7

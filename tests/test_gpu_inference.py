@@ -98,3 +98,26 @@ def test_encrypt_slots_rules():
         be.encrypt_slots(torch.zeros((1, params.num_slots + 1), dtype=torch.float64))
     with pytest.raises(OversizedInput):
         be.encrypt_slots(torch.zeros(5, dtype=torch.float64))
+
+
+def test_throughput_config_40960_images():
+    """The realisable throughput configuration (config-2 network, 20 images per
+    ciphertext x 2048 ciphertexts = 40,960 images) in B = 64 chunks through driver.infer_batch:
+    every image's decrypted logits against the plaintext forward pass (engine.py:233-265 style
+    argmax agreement).  Any argmax flip must be an image whose plaintext top-2 gap is below twice
+    the achieved error (a near tie); the committed artifact of the same run is
+    profiles/r02_parity_40960.json."""
+    import importlib.util
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts",
+                        "parity_throughput.py")
+    spec = importlib.util.spec_from_file_location("parity_throughput", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    res = mod.run(n_ct=2048, batch=64)
+    assert res["images"] == 40960
+    assert res["max_abs_err"] < 1e-5  # north star 1e-3; achieved ~1e-6
+    for f in res["argmax_flips"]:
+        assert f["ref_top2_gap"] < 2 * res["max_abs_err"], f
+    assert res["argmax_agreement"] >= 1.0 - len(res["near_ties_below_2x_max_err"]) / 40960
