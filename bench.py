@@ -223,8 +223,11 @@ def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
         d["n"] += 1
     lev, d = max(by_level.items(), key=lambda kv: kv[1]["ms"])
     w, tms = d["w"], d["ms"] / d["n"]
-    r_narrow, r_mac, r_imma = rates[8], rates[1], rates[9]
-    if w["imma"]:
+    r_narrow, r_mac, r_imma, r_tc = rates[8], rates[1], rates[9], rates[11]
+    if w["path"] == "tc":
+        parts = {"phase_a_40bit_narrow_imad": w["a40"] / r_narrow, "phase_a_60bit_imad": w["a60"] / r_mac,
+                 "phase_b_tcgen05_i8": (25 * w["b40"] + 64 * w["b60"]) / r_tc}
+    elif w["path"] == "imma":
         parts = {"phase_a_40bit_narrow_imad": w["a40"] / r_narrow, "q0_P_imad": (w["a60"] + w["b60"]) / r_mac,
                  "phase_b_40bit_imma": 25 * w["b40"] / r_imma}
     else:
@@ -240,8 +243,10 @@ def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
             traffic = t["dram_bytes_per_launch"]
     total_conv_ms = sum(v["ms"] for v in by_level.values())
     return {"bound": "imad+imma (mixed integer pipes)",
-            "kernel": f"LeNet conv2 hoisted MAC call, level {lev}: k_hoisted_imma (40-bit q_1..q_{lev}) + "
-                      f"k_hoisted_bank (60-bit q_0, P)",
+            "kernel": (f"LeNet conv2 hoisted MAC call, level {lev}: k_hoisted_tc (tcgen05 kind::i8, TMEM "
+                       f"accumulators; 40-bit q_1..q_{lev} and 60-bit q_0, P)") if w["path"] == "tc" else
+                      (f"LeNet conv2 hoisted MAC call, level {lev}: k_hoisted_imma (40-bit q_1..q_{lev}) + "
+                       f"k_hoisted_bank (60-bit q_0, P)"),
             "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "T modMAC/s", "frac": achieved / peak,
             "traffic": traffic, "launch_ms": tms, "bound_ms": t_bound * 1e3,
             "bound_ms_parts": {k: v * 1e3 for k, v in parts.items()},
@@ -249,7 +254,8 @@ def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
             "work_shape": {k: w[k] for k in ("B", "I", "T", "O", "nz", "level")},
             "share_of_step": tms / step_ms, "conv_mac_share_of_step": total_conv_ms / (step_ms * steps),
             "peak_source": "measured in this run (uh_bench_peaks): narrow-operand MAC rates[8], 128-bit MAC "
-                           "rates[1], u8 IMMA MAC rates[9]; peak = total modMACs / mixed bound time",
+                           "rates[1], u8 IMMA (mma.sync) MAC rates[9], tcgen05 kind::i8 MAC rates[11]; peak = total "
+                           "modMACs / mixed bound time",
             "frac_vs_all_imad_peak": achieved / r_mac}
 
 
@@ -429,7 +435,8 @@ def main():
     rooflines = {"ntt": ntt_roofline(be, hbm_gbs, hbm_src), "step": step_roofline(rates, B, step_ms)}
     peaks = {"imad_per_s": rates[0], "mac128_per_s": rates[1], "mulmod_per_s": rates[2], "shoup_per_s": rates[4],
              "fp64_modmac_per_s": rates[5], "narrow_mac_per_s": rates[8], "imma_u8_mac_per_s": rates[9],
-             "dfma_per_s": rates[10], "hbm_gbs": hbm_gbs, "hbm_source": hbm_src}
+             "dfma_per_s": rates[10], "tcgen05_i8_mac_per_s": rates[11], "hbm_gbs": hbm_gbs,
+             "hbm_source": hbm_src}
 
     # ---- e2e through the public API from host images ----
     e2e = None

@@ -46,7 +46,8 @@ unsigned long long uh_launch_count(void);
  * IMAD/s, lazy 128-bit multiply-accumulate/s (engine form), reduced 64-bit
  * mulmod/s, 128-bit MAC/s in plain-C form, lazy Shoup products/s, exact FP64
  * modMAC/s, mixed IMAD+FP64 MAC/s, split-accumulator MAC/s, narrow-operand
- * (q < 2^41) MAC/s, u8 IMMA MAC/s (mma.sync m16n8k32), FP64 FMA/s: 11 entries
+ * (q < 2^41) MAC/s, u8 IMMA MAC/s (mma.sync m16n8k32), FP64 FMA/s, tcgen05
+ * kind::i8 MAC/s: 12 entries
  * (the caller's buffer holds at least 16). */
 int uh_bench_peaks(uh_ctx *ctx, double *rates);
 
@@ -190,8 +191,8 @@ int uh_hoisted_mac_bank(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, 
  * outputs and <= 128 terms (LeNet conv2, layers.py:134-197): the weight-mask
  * contraction runs as byte-split u8 IMMA (exact; residues identical to
  * uh_hoisted_mac_bank) on the 40-bit limbs (5-byte operands); q_0 and P run
- * the IMAD kernel (8-byte IMMA operands with UH_IMMA_WIDE=1).  `ib` is the A-fragment mask bank made once per layer by
- * uh_imma_mask_bank from the uint64 mask bank ((4 level + 12) x N x
+ * the IMAD kernel.  `ib` is the A-fragment mask bank made once per layer by
+ * uh_imma_mask_bank from the uint64 mask bank (4 level x N x
  * ceil(Q/32) x 128 uint32 words).  uh_imma_supported: 1 when the shape and the
  * chain (40-bit q_1..q_level, 60-bit q_0 and P) qualify.  `masks` is unused. */
 int uh_imma_supported(uh_ctx *ctx, int level, int O, int Q);
@@ -199,6 +200,19 @@ int uh_imma_mask_bank(uh_ctx *ctx, uint32_t *ib, const uint64_t *masks, int O, i
 int uh_hoisted_mac_imma(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D,
                         const uint64_t *masks, const uint32_t *ib, const uint64_t *kbank, const int32_t *shifts,
                         int B, int I, int T, int O, int level, void *stream);
+/* Same hoisted MAC (layers.conv, layers.py:165-196) with the weight-mask contraction of
+ * every limb on the 5th-generation tensor cores: tcgen05.mma kind::i8 with TMEM
+ * accumulators, byte-split operands (5 bytes on the 40-bit limbs, 8 on q_0 and P; exact,
+ * residues identical to uh_hoisted_mac_bank).  `bank` is the A-operand bank made once
+ * per layer by uh_tc_mask_bank from the uint64 mask bank [O][Q][level+2][N]
+ * (uh_tc_bank_bytes bytes); uh_tc_supported: 1 when N = 2^15, the chain has 40-bit
+ * q_1..q_level and 60-bit q_0, P, 1 <= O <= 12 and Q <= 128. */
+int uh_tc_supported(uh_ctx *ctx, int level, int O, int Q);
+unsigned long long uh_tc_bank_bytes(uh_ctx *ctx, int level, int O, int Q);
+int uh_tc_mask_bank(uh_ctx *ctx, uint8_t *bank, const uint64_t *masks, int O, int Q, int level, void *stream);
+int uh_hoisted_mac_tc(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D,
+                      const uint8_t *bank, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O,
+                      int level, void *stream);
 /* Hoisted rotation sum (layers.avgpool, layers.py:213-218): out[C][B][2][level+2][N]
  * = sum_t P * rot_t(ct_c) in the QP basis; ModDown gives the pooled ciphertexts. */
 int uh_rot_sum_hoisted(uh_ctx *ctx, uint64_t *out, const uint64_t *X, int xls, const uint64_t *D,

@@ -54,13 +54,17 @@ SIGNATURES = {
     "uh_hoisted_mac_bank": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                             _vp],
     "uh_imma_mask_bank": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp],
+    "uh_tc_mask_bank": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp],
+    "uh_hoisted_mac_tc": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_hoisted_mac_imma": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int,
                             _vp],
 }
 EXTRA = {"uh_abi_version": ([], _c_int), "uh_last_error": ([], ctypes.c_char_p),
          "uh_launch_count": ([], ctypes.c_ulonglong), "uh_bench_peaks": ([_vp, _vp], _c_int),
          "uh_hoisted_bank_supported": ([_vp, _c_int, _c_int], _c_int),
-         "uh_imma_supported": ([_vp, _c_int, _c_int, _c_int], _c_int)}
+         "uh_imma_supported": ([_vp, _c_int, _c_int, _c_int], _c_int),
+         "uh_tc_supported": ([_vp, _c_int, _c_int, _c_int], _c_int),
+         "uh_tc_bank_bytes": ([_vp, _c_int, _c_int, _c_int], ctypes.c_ulonglong)}
 
 
 def launch_count() -> int:

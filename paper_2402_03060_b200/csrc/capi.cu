@@ -379,6 +379,37 @@ __attribute__((visibility("default"))) int uh_hoisted_mac_imma(uh_ctx *ctx, uint
     });
 }
 
+__attribute__((visibility("default"))) int uh_tc_supported(uh_ctx *ctx, int level, int O, int Q) {
+    return ctx && uh::hoisted_tc_supported(C(ctx), level, O, Q) ? 1 : 0;
+}
+
+__attribute__((visibility("default"))) unsigned long long uh_tc_bank_bytes(uh_ctx *ctx, int level, int O, int Q) {
+    return ctx && uh::hoisted_tc_supported(C(ctx), level, O, Q) ? uh::tc_bank_bytes(C(ctx), level, O, Q) : 0ull;
+}
+
+__attribute__((visibility("default"))) int uh_tc_mask_bank(uh_ctx *ctx, uint8_t *bank, const uint64_t *masks, int O,
+                                                           int Q, int level, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(uh::hoisted_tc_supported(c, level, O, Q), "tensor-core mask bank: unsupported shape");
+        uh::tc_mask_bank(c, bank, masks, O, Q, level, S(stream));
+    });
+}
+
+__attribute__((visibility("default"))) int uh_hoisted_mac_tc(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls,
+                                                             const uint64_t *D, const uint8_t *bank,
+                                                             const uint64_t *kbank, const int32_t *shifts, int B,
+                                                             int I, int T, int O, int level, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(B > 0 && I > 0 && T > 0 && O > 0 && xls == level + 1, "bad shape (xls must equal level + 1)");
+        need(kbank != nullptr && bank != nullptr, "key bank and tensor-core mask bank are required");
+        uh::hoisted_mac_tc(c, acc, X, D, bank, kbank, shifts, B, I, T, O, level, S(stream));
+    });
+}
+
 __attribute__((visibility("default"))) int uh_decode_coeffs(uh_ctx *ctx, double *slots, const double *coef,
                                                             int n_polys, double scale, void *stream) {
     return guard([&] { uh::decode_coeffs(C(ctx), slots, coef, n_polys, scale, S(stream)); });

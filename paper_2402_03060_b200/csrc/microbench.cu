@@ -247,6 +247,64 @@ __global__ void k_dfma_peak(double *out, int iters, double seed) {
     if (s == 1234.5) out[0] = s;
 }
 
+// tcgen05.mma kind::i8 throughput: one CTA per SM, one thread issuing M = 128, N = 256, K = 32
+// MMAs from shared memory (K-major, no swizzle) into two alternating TMEM accumulators
+__global__ void __launch_bounds__(128, 1) k_tc_peak(uint64_t *out, int iters) {
+    __shared__ __align__(1024) uint8_t tiles[128 * 32 + 256 * 32];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bar;
+    for (int i = threadIdx.x; i < (int)sizeof(tiles); i += blockDim.x) tiles[i] = (uint8_t)(i * 7);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tbase)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (threadIdx.x == 0) {
+        auto desc = [](uint32_t a) {
+            return (uint64_t)((a >> 4) & 0x3FFF) | ((uint64_t)8 << 16) | ((uint64_t)16 << 32) | ((uint64_t)1 << 46);
+        };
+        const uint64_t da = desc((uint32_t)__cvta_generic_to_shared(tiles));
+        const uint64_t db = desc((uint32_t)__cvta_generic_to_shared(tiles + 128 * 32));
+        const uint32_t idesc = (2u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        for (int it = 0; it < iters; it++) {
+            const uint32_t d = tbase + (uint32_t)(256 * (it & 1));
+            const uint32_t acc = it > 1;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar_a));
+    }
+    {
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                : "=r"(ok)
+                : "r"(bar_a), "r"(0)
+                : "memory");
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint32_t v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(tbase + ((32u * (threadIdx.x >> 5)) << 16)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (v == 0x12345u) out[0] = v;
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512));
+}
+
 template <class F> double time_ms(F &&launch) {
     cudaEvent_t a, b;
     UH_CHECK(cudaEventCreate(&a));
@@ -267,7 +325,8 @@ template <class F> double time_ms(F &&launch) {
 
 // rates[0] = IMAD/s, [1] = 128-bit MAC/s, [2] = reduced mulmod/s (60-bit prime), [3] MAC128 plain-C
 // form, [4] lazy Shoup product, [5] exact FP64 modMAC, [6] mixed IMAD+FP64 MAC, [7] split-accumulator
-// MAC, [8] narrow-operand MAC (q < 2^41), [9] u8 IMMA MAC/s (mma.sync), [10] FP64 FMA/s
+// MAC, [8] narrow-operand MAC (q < 2^41), [9] u8 IMMA MAC/s (mma.sync), [10] FP64 FMA/s,
+// [11] tcgen05 kind::i8 MAC/s
 void bench_peaks(const Ctx &c, double *rates) {
     int sms = 0;
     UH_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
@@ -303,6 +362,11 @@ void bench_peaks(const Ctx &c, double *rates) {
     }
     ms = time_ms([&] { k_dfma_peak<<<blocks, threads>>>((double *)out, iters, 1.0); });
     rates[10] = lanes * iters * 8 / (ms * 1e-3);  // FP64 FMA/s
+    {  // rates[11]: tcgen05 kind::i8 MACs/s (M = 128, N = 256, K = 32 per instruction)
+        const int ti = 2048;
+        ms = time_ms([&] { k_tc_peak<<<sms, 128>>>(out, ti); });
+        rates[11] = (double)sms * ti * (128.0 * 256 * 32) / (ms * 1e-3);
+    }
     UH_CHECK(cudaGetLastError());
     cudaFree(out);
 }

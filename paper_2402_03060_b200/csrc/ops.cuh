@@ -96,6 +96,16 @@ void imma_mask_bank(const Ctx &c, uint32_t *ib, const uint64_t *masks, int O, in
 void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
                       const uint32_t *ib, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O,
                       int level, cudaStream_t s);
+// hoist_tc.cu: the weight-mask contraction of dense masked layers (1..12 outputs) on the
+// 5th-generation tensor cores (tcgen05.mma kind::i8, TMEM accumulators), every limb: 5-byte
+// operands on the 40-bit limbs, 8-byte operands on q_0 and P.  `bank` is the per-layer A-operand
+// bank made by tc_mask_bank (tc_bank_bytes bytes).
+bool hoisted_tc_supported(const Ctx &c, int level, int O, int Q);
+size_t tc_bank_bytes(const Ctx &c, int level, int O, int Q);
+void tc_mask_bank(const Ctx &c, uint8_t *bank, const uint64_t *masks, int O, int Q, int level, cudaStream_t s);
+void hoisted_mac_tc(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint8_t *bank,
+                    const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, int level,
+                    cudaStream_t s);
 // microbench.cu: rates[0] = IMAD/s, rates[1] = 128-bit MAC/s, rates[2] = reduced mulmod/s
 void bench_peaks(const Ctx &c, double *rates);
 // embed.cu -- canonical embedding (hand-written FP64 four-step FFT): slots [n_polys][N/2] <-> int64 / double

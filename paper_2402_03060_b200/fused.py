@@ -96,6 +96,29 @@ def _imma_ok(backend, level: int, O: int, Q: int) -> bool:
     return bool(_lib.load().uh_imma_supported(backend._ctx, level, O, Q))
 
 
+def _tc_ok(backend, level: int, O: int, Q: int) -> bool:
+    """Dense masked layers (1..12 outputs, <= 128 terms) at N = 2^15: the mask contraction of every
+    limb on the tcgen05 tensor cores (hoist_tc.cu)."""
+    if os.environ.get("UH_TC", "1") == "0" or not _key_bank_ok(backend, level, O):
+        return False
+    return bool(_lib.load().uh_tc_supported(backend._ctx, level, O, Q))
+
+
+def tc_bank(backend, masks: torch.Tensor, O: int, Q: int, level: int, cache: bool = True) -> torch.Tensor:
+    """The tcgen05 A-operand byte bank of a mask bank (uh_tc_mask_bank), cached like imma_bank."""
+    banks = backend.__dict__.setdefault("_tc_banks", {})
+    ck = (masks.data_ptr(), O, Q, level)
+    hit = banks.get(ck) if cache else None
+    if hit is not None and hit[0] is masks:
+        return hit[1]
+    nbytes = int(_lib.load().uh_tc_bank_bytes(backend._ctx, level, O, Q))
+    tb = torch.empty((nbytes,), dtype=torch.uint8, device=backend.device)
+    backend._call("uh_tc_mask_bank", _vp(tb), _vp(masks), O, Q, level, backend._stream())
+    if cache:
+        banks[ck] = (masks, tb)
+    return tb
+
+
 def imma_bank(backend, masks: torch.Tensor, O: int, Q: int, level: int, cache: bool = True) -> torch.Tensor:
     """The A-fragment byte-plane bank of a mask bank (uh_imma_mask_bank).
 
@@ -214,7 +237,7 @@ def bias_bank(backend, layer, out_lay, level, scale):
     return _bank(backend, ("bias", layer_digest(layer), level, out_lay, scale), build)
 
 
-def conv_mac_work(shifts, half, n, B, I, O, level, imma) -> dict:
+def conv_mac_work(shifts, half, n, B, I, O, level, path) -> dict:
     """Algorithmic 64-bit modular multiply-accumulates of one hoisted conv MAC call, split by
     phase and limb class (the roofline of the call is a mix of pipes):
 
@@ -224,7 +247,8 @@ def conv_mac_work(shifts, half, n, B, I, O, level, imma) -> dict:
     * phase B (weight-mask contraction): O x terms x 2 components per QP limb.
 
     ``a40``/``b40``: the 40-bit limbs q_1..q_level; ``a60``/``b60``: the 60-bit q_0 and P.
-    With the tensor-core kernel (``imma``) b40 runs as 25 u8 byte products per modMAC."""
+    ``path``: "tc" (tcgen05: b40 as 25 and b60 as 64 u8 byte products per modMAC on the tensor
+    cores), "imma" (mma.sync: b40 on the tensor cores, q_0 / P on IMAD) or "imad"."""
     T = len(shifts)
     nz = sum(1 for s in shifts if s % half)
     L = level + 1
@@ -233,7 +257,7 @@ def conv_mac_work(shifts, half, n, B, I, O, level, imma) -> dict:
     a60 = n * B * I * per_a(1, 2)
     b40 = n * B * O * I * T * 2 * level
     b60 = n * B * O * I * T * 2 * 2
-    return {"a40": a40, "a60": a60, "b40": b40, "b60": b60, "total": a40 + a60 + b40 + b60, "imma": bool(imma),
+    return {"a40": a40, "a60": a60, "b40": b40, "b60": b60, "total": a40 + a60 + b40 + b60, "path": path,
             "B": B, "I": I, "T": T, "O": O, "nz": nz, "level": level}
 
 
@@ -271,8 +295,14 @@ def conv(backend, state: CipherState, layer) -> CipherState:
     if timer is not None:
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(torch.cuda.current_stream(backend.device))
-    imma = _imma_ok(backend, level, O, I * T)
-    if imma:
+    tc = _tc_ok(backend, level, O, I * T)
+    imma = not tc and _imma_ok(backend, level, O, I * T)
+    if tc:
+        kb = key_bank(backend, shifts, level)
+        tb = tc_bank(backend, masks, O, I * T, level)
+        backend._call("uh_hoisted_mac_tc", _vp(acc), _vp(X), L, _vp(D), _vp(tb), _vp(kb), _vp(sh), B, I, T, O, level,
+                      st)
+    elif imma:
         kb = key_bank(backend, shifts, level)
         ib = imma_bank(backend, masks, O, I * T, level)
         backend._call("uh_hoisted_mac_imma", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ib), _vp(kb), _vp(sh), B, I,
@@ -288,7 +318,7 @@ def conv(backend, state: CipherState, layer) -> CipherState:
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(torch.cuda.current_stream(backend.device))
         timer.append(("conv_hoisted_mac", level, t0, t1, conv_mac_work(shifts, backend.params.num_slots, n, B, I,
-                                                                           O, level, imma)))
+                                                                           O, level, "tc" if tc else ("imma" if imma else "imad"))))
     del D
     out = backend._empty(O, B, 2, level, n)  # ModDown + rescale as one centred division by q_level * P
     backend._call("uh_divide_top2", _vp(out), _vp(acc), O * B * 2, level, level, LP, st)
@@ -447,6 +477,14 @@ def _hoist(backend, X, level, shifts, masks, O, diag, B, taps=None):
     acc = backend._empty(O, B, 2, LP, n)
     mode = 2 if diag == 2 else (1 if diag else 0)
     T = taps if mode == 2 else len(shifts)
+    if mode == 0 and masks is not None and _tc_ok(backend, level, O, I * T) and os.environ.get("UH_TC_ALL", "1") != "0":
+        kb = key_bank(backend, shifts, level)
+        tb = tc_bank(backend, masks, O, I * T, level, cache=False)
+        sh = torch.tensor([s % backend.params.num_slots for s in shifts], dtype=torch.int32, device=backend.device)
+        backend._call("uh_hoisted_mac_tc", _vp(acc), _vp(X), L, _vp(D), _vp(tb), _vp(kb), _vp(sh), B, I, T, O, level,
+                      st)
+        del D
+        return acc
     if mode == 0 and masks is not None and _imma_ok(backend, level, O, I * T):
         kb = key_bank(backend, shifts, level)
         ib = imma_bank(backend, masks, O, I * T, level, cache=False)

@@ -204,6 +204,7 @@ def test_imma_kernel_equals_key_bank_kernel(O, level, I, shifts, B, monkeypatch)
     kernel on q_0 and P) == the key-bank IMAD kernel (oracle-pinned above), residue for residue, with
     worst-case (uniform up to q - 1) masks."""
     be, o = _c2()
+    monkeypatch.setenv("UH_TC", "0")  # the mma.sync kernel, not the tcgen05 one
     rng = np.random.default_rng(70 + O + level)
     cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, C2.num_slots)))) for _ in range(I)]
     X = fused.stack_cts(be, cts, level)
@@ -214,3 +215,45 @@ def test_imma_kernel_equals_key_bank_kernel(O, level, I, shifts, B, monkeypatch)
     monkeypatch.setenv("UH_IMMA", "0")
     want = fused._hoist(be, X, level, shifts, mdev, O, False, B)
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("O,level,I,shifts,B", [
+    (12, 5, 4, [a + 28 * b for b in range(5) for a in range(5)], 13),  # LeNet conv2 shape, partial ct tiles
+    (4, 7, 1, [a + 28 * b for b in range(5) for a in range(5)], 9),    # LeNet conv1 shape (O <= 8: M = 64 on q_0 / P)
+    (9, 3, 3, [0, 1, 28, -29, 16383, 57, -2, 3, 700], 4),              # Q = 27 (not / 4), 8 < O: M = 128
+    (1, 2, 2, [0, 1, 28, -29, 16383], 3),                              # one output, one K-step
+    (7, 8, 1, [3, 0, -5], 5),                                          # high level, 3 terms
+])
+def test_tcgen05_kernel_equals_key_bank_kernel(O, level, I, shifts, B, monkeypatch):
+    """The tcgen05 kernel (hoist_tc.cu: byte-split u8 tcgen05.mma kind::i8 with TMEM accumulators on
+    every limb -- 5-byte operands on the 40-bit limbs, 8-byte on q_0 and P) == the key-bank IMAD
+    kernel (oracle-pinned above), residue for residue, with worst-case (uniform up to q - 1) masks."""
+    be, o = _c2()
+    rng = np.random.default_rng(90 + O + level)
+    cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, C2.num_slots)))) for _ in range(I)]
+    X = fused.stack_cts(be, cts, level)
+    mdev = torch.from_numpy(_rand_masks(o, rng, O, I * len(shifts), level).view(np.int64)).to(be.device)
+    monkeypatch.setenv("UH_TC", "1")
+    assert fused._tc_ok(be, level, O, I * len(shifts))
+    got = fused._hoist(be, X, level, shifts, mdev, O, False, B)
+    monkeypatch.setenv("UH_TC", "0")
+    monkeypatch.setenv("UH_IMMA", "0")
+    want = fused._hoist(be, X, level, shifts, mdev, O, False, B)
+    assert torch.equal(got, want)
+
+
+def test_tcgen05_kernel_vs_oracle():
+    """The tcgen05 kernel directly against the CPU oracle (no transitive pin): 2 inputs x 5 shifts,
+    12 outputs, level 5 on the BASELINE chain."""
+    be, o = _c2()
+    s = o.secret()
+    B, I, O, level = 2, 2, 12, 5
+    shifts = [0, 1, 28, -29, 16383]
+    rng = np.random.default_rng(99)
+    cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, C2.num_slots)))) for _ in range(I)]
+    X = fused.stack_cts(be, cts, level)
+    masks = _rand_masks(o, rng, O, I * len(shifts), level)
+    assert fused._tc_ok(be, level, O, I * len(shifts))
+    got = fused._hoist(be, X, level, shifts, torch.from_numpy(masks.view(np.int64)).to(be.device), O, False, B)
+    want = _reference(o, s, X.cpu().numpy().view(np.uint64), level, shifts, masks, O, B)
+    assert np.array_equal(got.cpu().numpy().view(np.uint64), want)
