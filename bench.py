@@ -402,11 +402,13 @@ def main():
     l0 = _lib.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.profiler.start()  # `ncu --profile-from-start off` sees the timed steps only
     e0.record(stream)
     for _ in range(args.steps):
         final = eval_step()
     e1.record(stream)
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     barrier()
     launches = _lib.launch_count() - l0
     clk = clocks.stop()

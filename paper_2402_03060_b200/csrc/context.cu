@@ -1,6 +1,7 @@
 // Context creation: per-prime constants, twiddle tables and slot-order tables,
 // computed once on the host (exact 128-bit arithmetic) and kept in HBM.
 #include <mutex>
+#include <map>
 #include <set>
 
 #include "engine.cuh"
@@ -39,13 +40,16 @@ template <class T> T *upload(const std::vector<T> &v) {
 
 void smem_optin_raw(const void *kernel, size_t smem) {
     static std::mutex mu;
-    static std::set<std::pair<const void *, int>> done;
+    // the largest opt-in granted so far per (kernel, device): a later launch of the same kernel
+    // with a bigger tile (e.g. more terms) raises it
+    static std::map<std::pair<const void *, int>, size_t> done;
     int dev = 0;
     UH_CHECK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(mu);
-    if (done.count({kernel, dev})) return;
+    auto it = done.find({kernel, dev});
+    if (it != done.end() && it->second >= smem) return;
     UH_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    done.insert({kernel, dev});
+    done[{kernel, dev}] = smem;
 }
 
 Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_t count, int device) {

@@ -8,9 +8,10 @@ kernels over all channels and the whole ciphertext batch:
   forming every tap's key-switched rotation in the QP basis and
   multiply-accumulating it with every output channel's weight mask, then one
   fused ModDown + rescale per output channel, then the bias.  Kernel per
-  shape: ``uh_hoisted_mac_imma`` (dense 5..12-output layers at N = 2^15: mask
-  contraction on the tensor cores), ``uh_hoisted_mac_bank`` (per-layer
-  Galois-key bank, N = 2^15), ``uh_conv_hoisted_mac`` (generic, any N);
+  shape: ``uh_hoisted_mac_tc`` (dense masked layers at N = 2^15: mask
+  contraction on the tcgen05 tensor cores, TMEM accumulators),
+  ``uh_hoisted_mac_imma`` (mma.sync, opt-out fallback), ``uh_hoisted_mac_bank``
+  (per-layer Galois-key bank, IMAD), ``uh_conv_hoisted_mac`` (generic, any N);
 * avgpool -- one ModUp per channel, one unmasked hoisted rotation sum
   (``uh_hoisted_mac_bank`` / ``uh_rot_sum_hoisted``), one ModDown per channel;
 * square  -- tensor + relinearise + rescale of all channels in one batched
@@ -66,6 +67,36 @@ def stack_cts(backend, cts, level: int) -> torch.Tensor:
     return torch.stack([c.data[:, :, :L] for c in cts]).contiguous()
 
 
+def _dev_ints(backend, values, dtype=torch.int32) -> torch.Tensor:
+    """A small constant device table (shift lists, pointer tables), built once per content and
+    cached on the backend: the per-call path issues no pageable H2D copy (no stream sync),
+    which keeps a layer sequence capturable as a CUDA graph."""
+    cache = backend.__dict__.setdefault("_dev_ints", {})
+    key = (tuple(int(v) for v in values), dtype)
+    t = cache.get(key)
+    if t is None:
+        t = torch.tensor(list(key[0]), dtype=dtype, device=backend.device)
+        cache[key] = t
+    return t
+
+
+def _shift_table(backend, shifts) -> torch.Tensor:
+    half = backend.params.num_slots
+    return _dev_ints(backend, [s % half for s in shifts])
+
+
+def _persistent(t: torch.Tensor) -> torch.Tensor:
+    """The tensor owning a view's storage (cache entries hold it so the address stays reserved)."""
+    return t._base if t._base is not None else t
+
+
+def _banked(backend, t: torch.Tensor) -> bool:
+    """Whether ``t`` (or the tensor it views) is a persistent layer bank of this backend."""
+    own = _persistent(t)
+    return any(isinstance(b, torch.Tensor) and own is _persistent(b)
+               for b in backend.__dict__.get("_mask_banks", {}).values())
+
+
 def _rotation_plan(backend, shifts, level):
     """(device int32 shifts mod N/2, device int64 key-pointer table, keys kept alive, device int32 key limbs).
 
@@ -74,11 +105,9 @@ def _rotation_plan(backend, shifts, level):
     half = backend.params.num_slots
     norm = [s % half for s in shifts]
     keys = [backend.galois_key(s, level) if s else None for s in norm]
-    ptrs = torch.tensor([k.data_ptr() if k is not None else 0 for k in keys], dtype=torch.int64,
-                        device=backend.device)
-    limbs = torch.tensor([k.shape[2] if k is not None else level + 2 for k in keys], dtype=torch.int32,
-                         device=backend.device)
-    sh = torch.tensor(norm, dtype=torch.int32, device=backend.device)
+    ptrs = _dev_ints(backend, [k.data_ptr() if k is not None else 0 for k in keys], torch.int64)
+    limbs = _dev_ints(backend, [k.shape[2] if k is not None else level + 2 for k in keys])
+    sh = _dev_ints(backend, norm)
     return sh, ptrs, keys, limbs
 
 
@@ -98,8 +127,9 @@ def _imma_ok(backend, level: int, O: int, Q: int) -> bool:
 
 def _tc_ok(backend, level: int, O: int, Q: int) -> bool:
     """Dense masked layers (1..12 outputs, <= 128 terms) at N = 2^15: the mask contraction of every
-    limb on the tcgen05 tensor cores (hoist_tc.cu)."""
-    if os.environ.get("UH_TC", "1") == "0" or not _key_bank_ok(backend, level, O):
+    limb on the tcgen05 tensor cores (hoist_tc.cu).  Opt-in (``UH_TC=1``) until it beats the
+    mma.sync + IMAD pair on the bench shape (measured: LeNet conv2 39.8 vs 31.6 ms at B = 64)."""
+    if os.environ.get("UH_TC", "0") == "0" or not _key_bank_ok(backend, level, O):
         return False
     return bool(_lib.load().uh_tc_supported(backend._ctx, level, O, Q))
 
@@ -107,34 +137,34 @@ def _tc_ok(backend, level: int, O: int, Q: int) -> bool:
 def tc_bank(backend, masks: torch.Tensor, O: int, Q: int, level: int, cache: bool = True) -> torch.Tensor:
     """The tcgen05 A-operand byte bank of a mask bank (uh_tc_mask_bank), cached like imma_bank."""
     banks = backend.__dict__.setdefault("_tc_banks", {})
-    ck = (masks.data_ptr(), O, Q, level)
+    ck = (masks.data_ptr(), tuple(masks.shape), O, Q, level)
     hit = banks.get(ck) if cache else None
-    if hit is not None and hit[0] is masks:
+    if hit is not None and hit[0] is _persistent(masks):
         return hit[1]
     nbytes = int(_lib.load().uh_tc_bank_bytes(backend._ctx, level, O, Q))
     tb = torch.empty((nbytes,), dtype=torch.uint8, device=backend.device)
     backend._call("uh_tc_mask_bank", _vp(tb), _vp(masks), O, Q, level, backend._stream())
     if cache:
-        banks[ck] = (masks, tb)
+        banks[ck] = (_persistent(masks), tb)
     return tb
 
 
 def imma_bank(backend, masks: torch.Tensor, O: int, Q: int, level: int, cache: bool = True) -> torch.Tensor:
     """The A-fragment byte-plane bank of a mask bank (uh_imma_mask_bank).
 
-    cache=True for masks from a persistent layer bank: the entry keeps the mask tensor
-    alive, so its address cannot be reused by another tensor while the entry exists."""
+    cache=True for masks from a persistent layer bank (or a view of one): the entry keeps the
+    owning tensor alive, so its address cannot be reused by another tensor while the entry exists."""
     banks = backend.__dict__.setdefault("_imma_banks", {})
-    ck = (masks.data_ptr(), O, Q, level)
+    ck = (masks.data_ptr(), tuple(masks.shape), O, Q, level)
     hit = banks.get(ck) if cache else None
-    if hit is not None and hit[0] is masks:
+    if hit is not None and hit[0] is _persistent(masks):
         return hit[1]
     nks = (Q + 31) // 32
     # 40-bit limbs q_1..q_level: 4 m-tiles of 3 outputs x 5 bytes (q_0 and P stay on the IMAD kernel)
     ib = torch.empty((4 * level * backend.n * nks * 32 * 4,), dtype=torch.int32, device=backend.device)
     backend._call("uh_imma_mask_bank", _vp(ib), _vp(masks), O, Q, level, backend._stream())
     if cache:
-        banks[ck] = (masks, ib)
+        banks[ck] = (_persistent(masks), ib)
     return ib
 
 
@@ -299,12 +329,12 @@ def conv(backend, state: CipherState, layer) -> CipherState:
     imma = not tc and _imma_ok(backend, level, O, I * T)
     if tc:
         kb = key_bank(backend, shifts, level)
-        tb = tc_bank(backend, masks, O, I * T, level)
+        tb = tc_bank(backend, masks, O, I * T, level, cache=_banked(backend, masks))
         backend._call("uh_hoisted_mac_tc", _vp(acc), _vp(X), L, _vp(D), _vp(tb), _vp(kb), _vp(sh), B, I, T, O, level,
                       st)
     elif imma:
         kb = key_bank(backend, shifts, level)
-        ib = imma_bank(backend, masks, O, I * T, level)
+        ib = imma_bank(backend, masks, O, I * T, level, cache=_banked(backend, masks))
         backend._call("uh_hoisted_mac_imma", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ib), _vp(kb), _vp(sh), B, I,
                       T, O, level, st)
     elif _key_bank_ok(backend, level, O):
@@ -356,7 +386,7 @@ def avgpool(backend, state: CipherState, layer: AvgPool2d) -> CipherState:
     if _key_bank_ok(backend, level, 1):
         # the C channels x B ciphertexts as one batch of one input, unmasked
         kb = key_bank(backend, shifts, level)
-        sh = torch.tensor([s % backend.params.num_slots for s in shifts], dtype=torch.int32, device=backend.device)
+        sh = _shift_table(backend, shifts)
         backend._call("uh_hoisted_mac_bank", _vp(acc), _vp(X), L, _vp(D), _vp(0), _vp(kb), _vp(sh), C * B, 1, T, 1, 0,
                       level, st)
     else:
@@ -479,23 +509,23 @@ def _hoist(backend, X, level, shifts, masks, O, diag, B, taps=None):
     T = taps if mode == 2 else len(shifts)
     if mode == 0 and masks is not None and _tc_ok(backend, level, O, I * T) and os.environ.get("UH_TC_ALL", "1") != "0":
         kb = key_bank(backend, shifts, level)
-        tb = tc_bank(backend, masks, O, I * T, level, cache=False)
-        sh = torch.tensor([s % backend.params.num_slots for s in shifts], dtype=torch.int32, device=backend.device)
+        tb = tc_bank(backend, masks, O, I * T, level, cache=_banked(backend, masks))
+        sh = _shift_table(backend, shifts)
         backend._call("uh_hoisted_mac_tc", _vp(acc), _vp(X), L, _vp(D), _vp(tb), _vp(kb), _vp(sh), B, I, T, O, level,
                       st)
         del D
         return acc
     if mode == 0 and masks is not None and _imma_ok(backend, level, O, I * T):
         kb = key_bank(backend, shifts, level)
-        ib = imma_bank(backend, masks, O, I * T, level, cache=False)
-        sh = torch.tensor([s % backend.params.num_slots for s in shifts], dtype=torch.int32, device=backend.device)
+        ib = imma_bank(backend, masks, O, I * T, level, cache=_banked(backend, masks))
+        sh = _shift_table(backend, shifts)
         backend._call("uh_hoisted_mac_imma", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ib), _vp(kb), _vp(sh), B, I,
                       T, O, level, st)
         del D
         return acc
     if _key_bank_ok(backend, level, O) and (mode != 2 or O <= 4):
         kb = key_bank(backend, shifts, level)
-        sh = torch.tensor([s % backend.params.num_slots for s in shifts], dtype=torch.int32, device=backend.device)
+        sh = _shift_table(backend, shifts)
         backend._call("uh_hoisted_mac_bank", _vp(acc), _vp(X), L, _vp(D), _vp(masks) if masks is not None else _vp(0),
                       _vp(kb), _vp(sh), B, I, T, O, mode, level, st)
         del D

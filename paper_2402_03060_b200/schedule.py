@@ -5,7 +5,7 @@ reference's layer constructions (``pkg/src/slotcnn/layers.py``), against any
 backend with the reference operator interface -- the reference simulator,
 the CPU oracle or :class:`~paper_2402_03060_b200.he_backend.GpuBackend`.
 Identical order means identical ``OpCounter`` census and level traces and, on
-the simulator, bit-identical outputs (tests/test_schedule_vs_reference.py).
+the simulator, bit-identical outputs (tests/test_schedule_and_golden.py).
 
 * ``drop_level``  -- layers.py:116-131 (all-ones products; the GPU backend
   turns them into modulus drops)

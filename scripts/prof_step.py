@@ -68,10 +68,12 @@ def main():
     lev = []
     s0 = torch.cuda.Event(enable_timing=True)
     s1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.profiler.start()  # `ncu --profile-from-start off` captures this step only
     s0.record()
     step(lev)
     s1.record()
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     total = s0.elapsed_time(s1)
     print(f"batch {args.batch} cts ({args.batch * plan.capacity} images): step {total:.2f} ms device, "
           f"{wall * 1e3:.2f} ms wall (unprofiled) -> {args.batch * plan.capacity / wall:.1f} images/s")
