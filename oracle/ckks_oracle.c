@@ -92,17 +92,7 @@ OR_API uint64_t or_stream(uint64_t seed, uint64_t tag, uint64_t a, uint64_t b) {
 static inline uint64_t draw(uint64_t stream, uint64_t i) { return or_mix64(stream ^ or_mix64(i)); }
 
 /* -- context ---------------------------------------------------------------- */
-typedef struct {
-    uint32_t n, logn, count;
-    uint64_t *q;        /* [count] */
-    uint64_t *psi_rev;  /* [count][n]  psi^brv(i)        */
-    uint64_t *ipsi_rev; /* [count][n]  psi^-brv(i)       */
-    uint64_t *psi_sh;   /* [count][n]  Shoup companions floor(w * 2^64 / q) */
-    uint64_t *ipsi_sh;
-    uint64_t *n_inv;    /* [count]                        */
-    uint64_t *psi;      /* [count]                        */
-    int32_t *slot_of_brv; /* [n] */
-} or_ctx;
+#include "ckks_oracle.h"
 
 static uint32_t brv(uint32_t x, uint32_t bits) {
     uint32_t r = 0;

@@ -53,7 +53,8 @@ _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 
 
 def build() -> str:
-    if not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "ckks_oracle.c")):
+    srcs = [os.path.join(_HERE, f) for f in ("ckks_oracle.c", "ckks_hoisted.c", "ckks_oracle.h", "Makefile")]
+    if not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(os.path.getmtime(f) for f in srcs):
         subprocess.run(["make", "-C", _HERE], check=True, stdout=subprocess.DEVNULL)
     return LIB_PATH
 

@@ -82,6 +82,16 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
     std::vector<Mod> mods(count);
     std::vector<uint64_t> tw((size_t)count * n), tws((size_t)count * n), itw((size_t)count * n),
         itws((size_t)count * n);
+    std::vector<double> tfF, itfF;
+    std::vector<double2> tfU, itfU, tfR, itfR;
+    if (c->n1) {
+        tfF.assign((size_t)count * c->n1 * 8, 0.0);
+        itfF.assign(tfF.size(), 0.0);
+        tfU.assign((size_t)count * 4 * 16, make_double2(0, 0));
+        itfU.assign(tfU.size(), make_double2(0, 0));
+        tfR.assign((size_t)count * 16, make_double2(0, 0));
+        itfR.assign(tfR.size(), make_double2(0, 0));
+    }
     for (uint32_t m = 0; m < count; m++) {
         uint64_t q = moduli[m];
         if (h_pow(psi[m], n, q) != q - 1) throw std::invalid_argument("psi is not a primitive 2N-th root of unity");
@@ -99,6 +109,31 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
         for (uint32_t i = 1; i < n; i++) {
             pw[i] = h_mulmod(pw[i - 1], psi[m], q);
             ipw[i] = h_mulmod(ipw[i - 1], ip, q);
+        }
+        if (c->n1 && (q >> 42) == 0) {  // composite pass-2 twiddles (FP64-pipe limbs only)
+            const uint32_t logn = c->logn;
+            uint32_t la = 0;  // log2 n1
+            while ((1u << la) < c->n1) la++;
+            const uint32_t B = logn - la;
+            for (uint32_t blk = 0; blk < c->n1; blk++)
+                for (uint32_t st = 0; st < B; st++) {
+                    const uint32_t e = (1u << (B - 1 - st)) * (1 + 2 * h_brv(blk, la));
+                    tfF[((size_t)m * c->n1 + blk) * 8 + st] = (double)pw[e];
+                    itfF[((size_t)m * c->n1 + blk) * 8 + st] = (double)ipw[e];
+                }
+            for (uint32_t sp_ = 0; sp_ + 4 < B; sp_++)
+                for (uint32_t u = 0; u < 16; u++) {
+                    const uint32_t e = (1u << (logn - 4 - sp_)) * h_brv(u, 4);
+                    tfU[((size_t)m * 4 + sp_) * 16 + u] = make_double2((double)pw[e], (double)pw[e] / (double)q);
+                    itfU[((size_t)m * 4 + sp_) * 16 + u] = make_double2((double)ipw[e], (double)ipw[e] / (double)q);
+                }
+            for (uint32_t sp_ = 0; sp_ < 4; sp_++)
+                for (uint32_t v = 0; v < (1u << sp_); v++) {
+                    const uint32_t e = sp_ ? (1u << (logn - sp_)) * h_brv(v, sp_) : 0;
+                    tfR[(size_t)m * 16 + (1u << sp_) - 1 + v] = make_double2((double)pw[e], (double)pw[e] / (double)q);
+                    itfR[(size_t)m * 16 + (1u << sp_) - 1 + v] =
+                        make_double2((double)ipw[e], (double)ipw[e] / (double)q);
+                }
         }
         for (uint32_t i = 0; i < n; i++) {
             uint32_t e = h_brv(i, c->logn);
@@ -158,7 +193,6 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
         }
     std::vector<ulonglong2> tw2((size_t)count * n), itw2((size_t)count * n);
     std::vector<double2> twf((size_t)count * n, make_double2(0, 0)), itwf((size_t)count * n, make_double2(0, 0));
-    std::vector<double> twd((size_t)count * n, 0.0), itwd((size_t)count * n, 0.0);
     for (size_t i = 0; i < tw2.size(); i++) {
         tw2[i] = make_ulonglong2(tw[i], tws[i]);
         itw2[i] = make_ulonglong2(itw[i], itws[i]);
@@ -166,13 +200,17 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
         if ((q >> 42) == 0) {  // FP64-pipe NTT limbs (ntt_fast.cu, fp_limb)
             twf[i] = make_double2((double)tw[i], (double)tw[i] / (double)q);
             itwf[i] = make_double2((double)itw[i], (double)itw[i] / (double)q);
-            twd[i] = (double)tw[i];
-            itwd[i] = (double)itw[i];
         }
     }
     if (c->n1) {
         c->d_bsel = upload(bsel);
         c->d_csl = upload(csl);
+        c->d_tfF = upload(tfF);
+        c->d_itfF = upload(itfF);
+        c->d_tfU = upload(tfU);
+        c->d_itfU = upload(itfU);
+        c->d_tfR = upload(tfR);
+        c->d_itfR = upload(itfR);
     }
     // (q_t * P)^-1 mod q_k: the fused ModDown + rescale epilogue (one Shoup product)
     std::vector<uint64_t> inv2((size_t)count * count, 0), inv2s((size_t)count * count, 0);
@@ -196,8 +234,6 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
     c->d_itw2 = upload(itw2);
     c->d_twf = upload(twf);
     c->d_itwf = upload(itwf);
-    c->d_twd = upload(twd);
-    c->d_itwd = upload(itwd);
     c->d_mods = upload(mods);
     c->h_mods = mods;
     c->h_inv = inv;
@@ -220,7 +256,7 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
 void ctx_destroy(Ctx *c) {
     if (!c) return;
     DeviceGuard guard(c->device);
-    for (void *p : {(void *)c->d_pmod, (void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_twf, (void *)c->d_itwf, (void *)c->d_twd, (void *)c->d_itwd, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
+    for (void *p : {(void *)c->d_pmod, (void *)c->d_tfF, (void *)c->d_itfF, (void *)c->d_tfU, (void *)c->d_itfU, (void *)c->d_tfR, (void *)c->d_itfR, (void *)c->d_bsel, (void *)c->d_csl, (void *)c->d_tw2, (void *)c->d_itw2, (void *)c->d_twf, (void *)c->d_itwf, (void *)c->d_mods, (void *)c->d_psi, (void *)c->d_psis,
                     (void *)c->d_ipsi, (void *)c->d_ipsis,
                     (void *)c->d_sob, (void *)c->d_inv, (void *)c->d_invs, (void *)c->d_inv2, (void *)c->d_inv2s, (void *)c->d_pos, (void *)c->d_neg, (void *)c->d_jof})
         if (p) cudaFree(p);

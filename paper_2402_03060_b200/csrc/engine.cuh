@@ -23,7 +23,12 @@ struct Ctx {
     uint64_t *d_ipsi = nullptr, *d_ipsis = nullptr;  // [count][n] psi^-brv(i)
     ulonglong2 *d_tw2 = nullptr, *d_itw2 = nullptr;  // [count][n] interleaved (w, w') pairs of the above
     double2 *d_twf = nullptr, *d_itwf = nullptr;     // [count][n] (w, w / q) for FP64-pipe limbs (q < 2^42), else 0
-    double *d_twd = nullptr, *d_itwd = nullptr;       // [count][n] w as double (FP64-pipe limbs), else 0
+    // pass-2 composite twiddles of the FP64-pipe limbs (ntt_fast.cu, TwC): the twiddle of global
+    // index m (n1 + blk) + j factors as F[blk][s] * U[s - 4][u] * R[s'][v] (m = 2^s), so pass 2
+    // reads 8 per-block heads + 16 roots instead of the N-word table (forward / inverse)
+    double *d_tfF = nullptr, *d_itfF = nullptr;     // [count][n1][8] heads F[blk][s]
+    double2 *d_tfU = nullptr, *d_itfU = nullptr;    // [count][4][16] (U, U / q)
+    double2 *d_tfR = nullptr, *d_itfR = nullptr;    // [count][16] (R, R / q) at (1 << s') - 1 + v
     int32_t *d_sob = nullptr;            // [n] slot-order index of bit-reversed NTT output k
     int32_t *d_bsel = nullptr;           // [n1] pass-2 block of CTA x, position g (ntt_fast.cu)
     int32_t *d_csl = nullptr;            // [n] element index inside its pass-2 block, per slot

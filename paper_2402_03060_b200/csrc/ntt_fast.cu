@@ -24,6 +24,9 @@
 #ifndef UH_NTT_MINB
 #define UH_NTT_MINB 4  // min resident CTAs per SM requested from ptxas (register cap: 64)
 #endif
+#ifndef UH_NTT_P2_MINB
+#define UH_NTT_P2_MINB UH_NTT_MINB  // the same for pass 2 (forward) / pass A (inverse)
+#endif
 
 namespace uh {
 namespace {
@@ -225,13 +228,82 @@ struct TwG {  // global table (read-only path)
     int f;
     __device__ W operator()(int m, int j) const { return tw(T, m * f + j); }
 };
-struct TwGd {  // FP64 limbs, w-only global table: (w, w / q) with one multiply, half the bytes of TwG<double2>
-    const double *__restrict__ T;
-    int f;
-    double qinv;
-    __device__ double2 operator()(int m, int j) const {
-        const double w = __ldg(T + m * f + j);
-        return make_double2(w, w * qinv);
+
+// Composite pass-2 twiddles (FP64 limbs).  With m = 2^s, the pass-2 twiddle of global index
+// m (n1 + blk) + j is psi^e, e = 2^(B-1-s) (1 + 2 brv_A(blk)) + 2^(logn-s) brv_s(j), which factors as
+//   F[blk][s] * R[s][j]                          (first network, s < 4, j < 2^s)
+//   F[blk][s] * U[s-4][u] * R[s-4][v]            (second network, j = u 2^(s-4) + v, u < 16)
+// (context.cu builds F, U, R).  A thread holds its network's per-stage head H[s] (F, or F U: one
+// product) in registers; the stage-s twiddles are H[s] (v = 0) and H[s] R[s'][v] -- one exact FP64
+// product each -- instead of one N-word table read per twiddle (the L1 wavefronts and L2 latency
+// that bounded pass 2).
+struct TwC {
+    const double2 *R;  // this modulus' 16 (R, R / q) pairs at (1 << s') - 1 + v, staged in shared memory
+    double q, qinv;
+};
+__device__ __forceinline__ double2 tw_c(double h, int idx, const TwC &t) {  // h R[idx] (idx > 0)
+    const double c = fmm(h, t.R[idx], t.q);
+    return make_double2(c, c * t.qinv);
+}
+// one stage s of a forward / inverse network of R = 2^LR register values: distance R / 2^(s+1),
+// butterfly x uses twiddle H[s] R[s][x / 2dx]
+template <int LR, int S>
+__device__ __forceinline__ void fwd_stage_c(double (&v)[1 << LR], double h, const TwC &t) {
+    constexpr int R = 1 << LR, dx = R >> (S + 1);
+#pragma unroll
+    for (int jv = 0; jv < (1 << S); jv++) {  // one twiddle live at a time (register budget)
+        const double2 w = jv ? tw_c(h, (1 << S) - 1 + jv, t) : make_double2(h, h * t.qinv);
+#pragma unroll
+        for (int k = 0; k < dx; k++) bf_ct(v[jv * 2 * dx + k], v[jv * 2 * dx + k + dx], w, t.q);
+    }
+}
+template <int LR, int S>
+__device__ __forceinline__ void inv_stage_c(double (&v)[1 << LR], double h, const TwC &t) {
+    constexpr int R = 1 << LR, dx = R >> (S + 1);
+#pragma unroll
+    for (int jv = 0; jv < (1 << S); jv++) {
+        const double2 w = jv ? tw_c(h, (1 << S) - 1 + jv, t) : make_double2(h, h * t.qinv);
+#pragma unroll
+        for (int k = 0; k < dx; k++) bf_gs(v[jv * 2 * dx + k], v[jv * 2 * dx + k + dx], w, t.q);
+    }
+}
+// H(s): the stage-s head, formed right before the stage (one live double: register budget)
+template <int LR, class HF>  // stages s = 0 .. LR-1 (LR <= 4)
+__device__ __forceinline__ void fwd_net_c(double (&v)[1 << LR], const HF &H, const TwC &t) {
+    fwd_stage_c<LR, 0>(v, H(0), t);
+    if constexpr (LR > 1) fwd_stage_c<LR, 1>(v, H(1), t);
+    if constexpr (LR > 2) fwd_stage_c<LR, 2>(v, H(2), t);
+    if constexpr (LR > 3) fwd_stage_c<LR, 3>(v, H(3), t);
+}
+template <int LR, class HF>  // mirror: stages s = LR-1 .. 0
+__device__ __forceinline__ void inv_net_c(double (&v)[1 << LR], const HF &H, const TwC &t) {
+    if constexpr (LR > 3) inv_stage_c<LR, 3>(v, H(3), t);
+    if constexpr (LR > 2) inv_stage_c<LR, 2>(v, H(2), t);
+    if constexpr (LR > 1) inv_stage_c<LR, 1>(v, H(1), t);
+    inv_stage_c<LR, 0>(v, H(0), t);
+}
+// per-thread stage heads: first network F[blk][s]; second network F[blk][4 + s] U[s][u]
+struct Heads1 {
+    const double *__restrict__ f;  // F + blk * 8
+    __device__ double operator()(int s) const { return __ldg(f + s); }
+};
+struct Heads2 {
+    const double *__restrict__ f;   // F + blk * 8 + 4
+    const double2 *__restrict__ u;  // U + u
+    double q;
+    __device__ double operator()(int s) const { return fmm(__ldg(f + s), __ldg(u + s * 16), q); }
+};
+
+struct TwP2 {  // one FP64 limb's composite pass-2 tables (context.cu)
+    const double *__restrict__ F;   // [n1][8]
+    const double2 *__restrict__ U;  // [4][16]
+    const double2 *__restrict__ R;  // [16]
+};
+struct TwTabs {  // every modulus' tables (Ctx::d_tfF / d_tfU / d_tfR, or the inverse ones)
+    const double *F;
+    const double2 *U, *R;
+    __device__ TwP2 at(int mod, int n1) const {
+        return TwP2{F + (size_t)mod * n1 * 8, U + (size_t)mod * 64, R + (size_t)mod * 16};
     }
 };
 
@@ -441,29 +513,28 @@ __device__ __forceinline__ void fwd_p2_epilogue(const uint64_t *sm, const LimbIn
                                                 const int32_t *__restrict__ csl, int logn, int tid);
 
 // pass 2 forward stages: tmp (pass-1 output) -> canonical residues in shared memory
-// FP64 limbs read the pass-2 twiddles from the limb's w-only table `twd` (8 B each, w / q
-// formed with one multiply); the 60-bit limbs read interleaved Shoup pairs.
+// FP64 limbs form their twiddles from the composite tables (TwC); the 60-bit limbs read
+// interleaved Shoup pairs from the N-word table.
 template <int B, bool FP>
-__device__ __forceinline__ void fwd_p2_body(uint64_t *sm, const double *twd, const Mod &m, const Tw &tw2,
+__device__ __forceinline__ void fwd_p2_body(uint64_t *sm, const double2 *s_R, const TwP2 &tc, const Mod &m, const Tw &tw2,
                                             const InGlobal<B> &in, const int *sel, int n1, int tid) {
     using C = P2<B>;
     using AR = Arith<FP>;
     using V = typename AR::V;
     const AR ar(m.q);
     const auto *T = pick<FP>(tw2);
-    auto acc = [&](int, int blk) {
-        if constexpr (FP)
-            return TwGd{twd, n1 + blk, ar.qinv};
-        else
-            return TwG<typename AR::W>{T, n1 + blk};
-    };
+    auto acc = [&](int blk) { return TwG<typename AR::W>{T, n1 + blk}; };
     {
         const int g = tid / C::S, c0 = tid % C::S, blk = sel[g];
         V v[C::R1];
 #pragma unroll
         for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(in(blk, c0 + C::S * x));
         // local stages m' = 1..8: global twiddle index m' * (n1 + blk) + x / (2 dx)
-        fwd_strided<C::R1>(v, acc(g, blk), 1, 0, ar.qv());
+        if constexpr (FP) {
+            fwd_net_c<4>(v, Heads1{tc.F + blk * 8}, TwC{s_R, ar.q, ar.qinv});
+        } else {
+            fwd_strided<C::R1>(v, acc(blk), 1, 0, ar.qv());
+        }
 #pragma unroll
         for (int x = 0; x < C::R1; x++) sm[C::at(g, c0 + C::S * x)] = AR::raw(v[x]);
     }
@@ -477,7 +548,11 @@ __device__ __forceinline__ void fwd_p2_body(uint64_t *sm, const double *twd, con
 #pragma unroll
         for (int z = 0; z < C::R2; z++) v[z] = AR::raw_in(sm[C::at(g, c + z)]);
         // local stages m' = 16 .. N2/2 on contiguous c + z
-        fwd_strided<C::R2>(v, acc(g, blk), 16, (c / C::R2), ar.qv());
+        if constexpr (FP) {
+            fwd_net_c<B - 4>(v, Heads2{tc.F + blk * 8 + 4, tc.U + c / C::R2, ar.q}, TwC{s_R, ar.q, ar.qinv});
+        } else {
+            fwd_strided<C::R2>(v, acc(blk), 16, (c / C::R2), ar.qv());
+        }
 #pragma unroll
         for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = ar.canon(v[z]);
     }
@@ -491,10 +566,10 @@ constexpr size_t p2_smem() {  // the G padded block tiles
 }
 
 template <int B, int EM>
-__global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p2(NttJob J, const uint64_t *__restrict__ tmp, int logn,
+__global__ void __launch_bounds__(kThreads, UH_NTT_P2_MINB) k_fwd_p2(NttJob J, const uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ twd,
-                                                    const double *__restrict__ twdd,
+                                                    const TwTabs tt,
                                                     const double2 *__restrict__ twf,
                                                     const int32_t *__restrict__ bsel,
                                                     const int32_t *__restrict__ csl) {
@@ -509,10 +584,15 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_fwd_p2(NttJob J, cons
     const uint64_t q = m.q;
     const Tw tw2{twd + ((size_t)li.mod << logn), twf + ((size_t)li.mod << logn)};
     const InGlobal<B> in{tmp + ((size_t)blockIdx.y << logn)};
-    if (fp_limb(q))
-        fwd_p2_body<B, true>(sm, twdd + ((size_t)li.mod << logn), m, tw2, in, sel, n1, tid);
-    else
-        fwd_p2_body<B, false>(sm, nullptr, m, tw2, in, sel, n1, tid);
+    __shared__ double2 s_R[16];  // the composite-twiddle roots of this limb's modulus
+    if (fp_limb(q)) {
+        const TwP2 tc = tt.at(li.mod, n1);
+        if (tid < 16) s_R[tid] = __ldg(tc.R + tid);
+        __syncthreads();
+        fwd_p2_body<B, true>(sm, s_R, tc, m, tw2, in, sel, n1, tid);
+    } else {
+        fwd_p2_body<B, false>(sm, s_R, TwP2{}, m, tw2, in, sel, n1, tid);
+    }
     fwd_p2_epilogue<B, EM>(sm, li, q, csl, logn, tid);
 }
 
@@ -551,19 +631,14 @@ __device__ __forceinline__ void fwd_p2_epilogue(const uint64_t *sm, const LimbIn
 
 // inverse pass A stages: canonical residues in shared memory -> tmp (pass-B input)
 template <int B, bool FP>
-__device__ __forceinline__ void inv_pa_body(uint64_t *sm, const double *twd, const Mod &m, const Tw &tw2,
+__device__ __forceinline__ void inv_pa_body(uint64_t *sm, const double2 *s_R, const TwP2 &tc, const Mod &m, const Tw &tw2,
                                             uint64_t *out, const int *sel, int n1, int tid) {
     using C = P2<B>;
     using AR = Arith<FP>;
     using V = typename AR::V;
     const AR ar(m.q);
     const auto *T = pick<FP>(tw2);
-    auto acc = [&](int, int blk) {
-        if constexpr (FP)
-            return TwGd{twd, n1 + blk, ar.qinv};  // the limb's w-only table
-        else
-            return TwG<typename AR::W>{T, n1 + blk};
-    };
+    auto acc = [&](int blk) { return TwG<typename AR::W>{T, n1 + blk}; };
 #pragma unroll
     for (int gi = 0; gi < C::GC; gi++) {
         const int grp = tid + kThreads * gi;
@@ -573,7 +648,11 @@ __device__ __forceinline__ void inv_pa_body(uint64_t *sm, const double *twd, con
 #pragma unroll
         for (int z = 0; z < C::R2; z++) v[z] = AR::in(sm[C::at(g, c + z)]);
         // mirror of the forward contiguous stages: last local stage m' = N2/2
-        inv_strided<C::R2>(v, acc(g, blk), C::N2 / 2, (c / C::R2) * (C::R2 / 2), ar.qv());
+        if constexpr (FP) {
+            inv_net_c<B - 4>(v, Heads2{tc.F + blk * 8 + 4, tc.U + c / C::R2, ar.q}, TwC{s_R, ar.q, ar.qinv});
+        } else {
+            inv_strided<C::R2>(v, acc(blk), C::N2 / 2, (c / C::R2) * (C::R2 / 2), ar.qv());
+        }
 #pragma unroll
         for (int z = 0; z < C::R2; z++) sm[C::at(g, c + z)] = AR::raw(v[z]);
     }
@@ -583,7 +662,11 @@ __device__ __forceinline__ void inv_pa_body(uint64_t *sm, const double *twd, con
         V v[C::R1];
 #pragma unroll
         for (int x = 0; x < C::R1; x++) v[x] = AR::raw_in(sm[C::at(g, c0 + C::S * x)]);
-        inv_strided<C::R1>(v, acc(g, blk), 8, 0, ar.qv());
+        if constexpr (FP) {
+            inv_net_c<4>(v, Heads1{tc.F + blk * 8}, TwC{s_R, ar.q, ar.qinv});
+        } else {
+            inv_strided<C::R1>(v, acc(blk), 8, 0, ar.qv());
+        }
 #pragma unroll
         for (int x = 0; x < C::R1; x++) {
             V r = v[x];
@@ -595,10 +678,10 @@ __device__ __forceinline__ void inv_pa_body(uint64_t *sm, const double *twd, con
 
 
 template <int B>
-__global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint64_t *__restrict__ tmp, int logn,
+__global__ void __launch_bounds__(kThreads, UH_NTT_P2_MINB) k_inv_pa(NttJob J, uint64_t *__restrict__ tmp, int logn,
                                                     const Mod *__restrict__ mods,
                                                     const ulonglong2 *__restrict__ itwd,
-                                                    const double *__restrict__ itwdd,
+                                                    const TwTabs tt,
                                                     const double2 *__restrict__ itwf,
                                                     const int32_t *__restrict__ bsel,
                                                     const int32_t *__restrict__ csl) {
@@ -612,6 +695,8 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint
     const Mod m = mods[li.mod];
     const Tw tw2{itwd + ((size_t)li.mod << logn), itwf + ((size_t)li.mod << logn)};
     const bool fp = fp_limb(m.q);
+    __shared__ double2 s_R[16];  // the composite-twiddle roots of this limb's modulus
+    if (fp && tid < 16) s_R[tid] = __ldg(tt.R + (size_t)li.mod * 16 + tid);
     // coalesced slot-order gather into the blocks' shared-memory tiles (plain limbs: the only
     // inverse mode); all of a thread's loads are issued before the shared-memory stores
     {
@@ -630,9 +715,9 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_MINB) k_inv_pa(NttJob J, uint
     __syncthreads();
     uint64_t *out = tmp + ((size_t)blockIdx.y << logn);
     if (fp)
-        inv_pa_body<B, true>(sm, itwdd + ((size_t)li.mod << logn), m, tw2, out, sel, n1, tid);
+        inv_pa_body<B, true>(sm, s_R, tt.at(li.mod, n1), m, tw2, out, sel, n1, tid);
     else
-        inv_pa_body<B, false>(sm, nullptr, m, tw2, out, sel, n1, tid);
+        inv_pa_body<B, false>(sm, s_R, TwP2{}, m, tw2, out, sel, n1, tid);
 }
 
 constexpr int kMaxGridY = 65535;
@@ -658,13 +743,13 @@ void run_fwd(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
         UH_LAUNCH_CHECK();
         if (J.mode == NTT_DIVIDE) {
             smem_optin(k_fwd_p2<B, 1>, sm2);
-            k_fwd_p2<B, 1><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl);
+            k_fwd_p2<B, 1><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, TwTabs{c.d_tfF, c.d_tfU, c.d_tfR}, c.d_twf, c.d_bsel, c.d_csl);
         } else if (J.mode == NTT_DIVIDE2) {
             smem_optin(k_fwd_p2<B, 2>, sm2);
-            k_fwd_p2<B, 2><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl);
+            k_fwd_p2<B, 2><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, TwTabs{c.d_tfF, c.d_tfU, c.d_tfR}, c.d_twf, c.d_bsel, c.d_csl);
         } else {
             smem_optin(k_fwd_p2<B, 0>, sm2);
-            k_fwd_p2<B, 0><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, c.d_twd, c.d_twf, c.d_bsel, c.d_csl);
+            k_fwd_p2<B, 0><<<g2, kThreads, sm2, s>>>(J, t, ln, c.d_mods, c.d_tw2, TwTabs{c.d_tfF, c.d_tfU, c.d_tfR}, c.d_twf, c.d_bsel, c.d_csl);
         }
         UH_LAUNCH_CHECK();
     }
@@ -682,8 +767,8 @@ void run_inv(const Ctx &c, const NttJob &J0, int limbs, cudaStream_t s) {
         J.f0 = f0;
         const int nl = std::min(ch, limbs - f0);
         dim3 g1((1u << B) / 32, nl), g2((1u << A) / P2<B>::G, nl);
-        k_inv_pa<B><<<g2, kThreads, sm2, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwd,
-                                              c.d_itwf, c.d_bsel, c.d_csl);
+        k_inv_pa<B><<<g2, kThreads, sm2, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2,
+                                              TwTabs{c.d_itfF, c.d_itfU, c.d_itfR}, c.d_itwf, c.d_bsel, c.d_csl);
         UH_LAUNCH_CHECK();
         k_inv_pb<A><<<g1, kThreads, 0, s>>>(J, tmp.as<uint64_t>(), (int)c.logn, c.d_mods, c.d_itw2, c.d_itwf);
         UH_LAUNCH_CHECK();

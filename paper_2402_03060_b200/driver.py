@@ -22,7 +22,7 @@ import numpy as np
 
 from . import planner
 from .counter import diff_snapshots
-from .errors import SlotCnnError
+from .errors import ShapeMismatch, SlotCnnError
 from .planner import FC, AvgPool2d, Conv1d, Conv2d, Square, reference_infer, trace_layout, validate
 from .schedule import CipherState, LayoutState, apply_layer, drop_level, fc_operation_counts, valid_positions
 
@@ -236,6 +236,62 @@ def infer_batch(m, planes, params, plan, backend, counts=None, cost_model=None, 
         cnt = plan.capacity if counts is None else counts[b]
         outputs.append(_extract([d[b] for d in dec], state.layout, plan.offsets[:cnt]))
     return outputs, metrics
+
+
+class EvalGraph:
+    """The server-side evaluation of one batch shape captured once as a CUDA graph and replayed.
+
+    Captures ``_run_layers`` (every fused layer of ``m`` over ``batch`` ciphertexts per input
+    channel) on the backend's stream; a replay re-runs the whole kernel sequence with one
+    launch and no host work.  Inputs are static device ciphertext buffers: ``run`` copies the
+    caller's ciphertexts into them, replays, and returns the output ciphertexts (static buffers
+    too -- the next ``run`` overwrites them).  Encryption and decryption stay outside the graph:
+    they are the client's side, and each encryption must draw a fresh nonce.
+
+    Requires every key, mask bank and device table of the network to exist before capture; the
+    constructor runs one eager warm-up pass for that (and to prove the path is capture-safe:
+    no host synchronisation, no pageable copies inside a layer)."""
+
+    def __init__(self, m, plan, backend, batch: int, fused: bool = True):
+        import torch
+
+        self.m, self.plan, self.backend, self.batch = m, plan, backend, batch
+        p = backend.params
+        lev = p.depth
+        self.level, self.scale = lev, backend.scale0
+        self.inputs = [backend._empty(batch, 2, lev + 1, backend.n).zero_() for _ in range(m.channels)]
+        self._fused = fused
+
+        def body():
+            from .he_backend import CipherVector
+
+            cts = [CipherVector(x, lev, self.scale, backend) for x in self.inputs]
+            state, _, _ = _run_layers(m, CipherState(cts, _input_layout(m, plan)), backend, CostModel(),
+                                      p.poly_degree, fused)
+            return state
+
+        self._body = body
+        body()  # warm-up: keys, mask banks, device tables, kernel attributes
+        torch.cuda.synchronize(backend.device)
+        side = torch.cuda.Stream(backend.device)
+        side.wait_stream(torch.cuda.current_stream(backend.device))
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=side):
+            self.state = body()
+        torch.cuda.current_stream(backend.device).wait_stream(side)
+        self.outputs = self.state.cts
+
+    def run(self, cts):
+        """Evaluate input ciphertexts ``cts`` (one CipherVector per channel, ``batch`` each, at the
+        top level and scale) by graph replay; returns the output ciphertexts."""
+        if len(cts) != len(self.inputs):
+            raise ShapeMismatch(f"expected {len(self.inputs)} input ciphertexts, got {len(cts)}")
+        for x, c in zip(self.inputs, cts):
+            if c.level != self.level or c.scale != self.scale or c.batch != self.batch:
+                raise ShapeMismatch("graph inputs must be fresh ciphertexts of the captured batch size")
+            x.copy_(c.data[:, :, :self.level + 1], non_blocking=True)
+        self.graph.replay()
+        return self.outputs
 
 
 def verify_against_oracle(m, params, n_trials: int = 20, seed: int = 0, tol: float = 1e-3, alignment: int = 1,

@@ -115,14 +115,14 @@ def _key_bank_ok(backend, level: int, O: int) -> bool:
     """Dense masked terms run on the key-bank kernel (hoist_bank.cu) where it is compiled for."""
     if os.environ.get("UH_KEY_BANK", "1") == "0":
         return False
-    return bool(_lib.load().uh_hoisted_bank_supported(backend._ctx, level, O))
+    return backend.kernel_supported("uh_hoisted_bank_supported", level, O)
 
 
 def _imma_ok(backend, level: int, O: int, Q: int) -> bool:
     """Dense 5..12-output layers: the mask contraction on the tensor cores (hoist_imma.cu)."""
     if os.environ.get("UH_IMMA", "1") == "0" or not _key_bank_ok(backend, level, O):
         return False
-    return bool(_lib.load().uh_imma_supported(backend._ctx, level, O, Q))
+    return backend.kernel_supported("uh_imma_supported", level, O, Q)
 
 
 def _tc_ok(backend, level: int, O: int, Q: int) -> bool:
@@ -131,7 +131,7 @@ def _tc_ok(backend, level: int, O: int, Q: int) -> bool:
     mma.sync + IMAD pair on the bench shape (measured: LeNet conv2 39.8 vs 31.6 ms at B = 64)."""
     if os.environ.get("UH_TC", "0") == "0" or not _key_bank_ok(backend, level, O):
         return False
-    return bool(_lib.load().uh_tc_supported(backend._ctx, level, O, Q))
+    return backend.kernel_supported("uh_tc_supported", level, O, Q)
 
 
 def tc_bank(backend, masks: torch.Tensor, O: int, Q: int, level: int, cache: bool = True) -> torch.Tensor:

@@ -170,6 +170,10 @@ class GpuBackend:
     def _call(self, name, *args):
         _lib.call(name, self._ctx, *args)
 
+    def kernel_supported(self, name: str, *args) -> bool:
+        """Whether a shape-specialised kernel (``uh_*_supported`` query) serves this call."""
+        return bool(getattr(_lib.load(), name)(self._ctx, *args))
+
     # -- keys (lazily generated at the highest level they are first needed) ----
     def galois_key(self, r: int, level: int) -> torch.Tensor:
         r %= self.params.num_slots

@@ -242,9 +242,10 @@ def test_tcgen05_kernel_equals_key_bank_kernel(O, level, I, shifts, B, monkeypat
     assert torch.equal(got, want)
 
 
-def test_tcgen05_kernel_vs_oracle():
+def test_tcgen05_kernel_vs_oracle(monkeypatch):
     """The tcgen05 kernel directly against the CPU oracle (no transitive pin): 2 inputs x 5 shifts,
     12 outputs, level 5 on the BASELINE chain."""
+    monkeypatch.setenv("UH_TC", "1")  # opt-in path
     be, o = _c2()
     s = o.secret()
     B, I, O, level = 2, 2, 12, 5

@@ -121,3 +121,38 @@ def test_throughput_config_40960_images():
     for f in res["argmax_flips"]:
         assert f["ref_top2_gap"] < 2 * res["max_abs_err"], f
     assert res["argmax_agreement"] >= 1.0 - len(res["near_ties_below_2x_max_err"]) / 40960
+
+
+@pytest.mark.parametrize("logn", [12, 15])
+def test_graph_replayed_step_equals_eager(logn):
+    """driver.EvalGraph: the whole fused LeNet-1 evaluation captured as one CUDA graph; replays on two
+    different input batches give residues identical to eager runs, and decrypt to the plaintext."""
+    import torch
+
+    from paper_2402_03060_b200.schedule import CipherState
+
+    params = HEParams(poly_degree=1 << logn, depth=9 if logn == 15 else 7, scale_bits=40)
+    m = planner.lenet1(seed=3)
+    plan = planner.footprint(m, params)
+    be = GpuBackend(params)
+    B = 3
+    g = driver.EvalGraph(m, plan, be, B)
+    for seed in (20, 21):
+        groups = [_samples(m, plan.capacity, seed=seed * 10 + b) for b in range(B)]
+        planes = driver.pack_groups(m, groups, plan)
+        cts = [be.encrypt(be.encode_batch(planes[ch])) for ch in range(m.channels)]
+        outs = g.run(cts)
+        torch.cuda.synchronize()
+        got = [c.data.clone() for c in outs]
+        state, _, _ = driver._run_layers(m, CipherState(cts, driver._input_layout(m, plan)), be, driver.CostModel(),
+                                         params.poly_degree, True)
+        for a, c in zip(got, state.cts):
+            assert torch.equal(a, c.data)
+        lay = state.layout
+        pos = driver.valid_positions(lay)
+        dec = [np.atleast_2d(be.decrypt(c)) for c in outs]
+        for b in range(B):
+            for i, off in enumerate(plan.offsets[:plan.capacity]):
+                y = np.concatenate([d[b][off + pos] for d in dec]) * lay.pending_const
+                ref = planner.reference_infer(m, groups[b][i])
+                assert np.max(np.abs(y - ref)) < 1e-5
