@@ -357,12 +357,25 @@ def ntt_roofline(be, hbm_gbs, hbm_src, polys=64, limbs=8, reps=5):
         gbs = 16 * n / (us_limb * 1e-6) / 1e9
         out[name] = {"us_per_limb": us_limb, "achieved_gbs": gbs}
     f = out["forward"]
+    # the arithmetic bound: FP64 and IMAD share the FMA-heavy pipe on this part (the mixed
+    # IMAD + FP64 microbenchmark rates[6] is no faster than either alone), so the pipe work of a
+    # forward NTT is 8 FP64 ops per butterfly on the 40-bit limbs plus one lazy Shoup product
+    # (rates[0] / rates[4] IMAD slots) per butterfly on the 60-bit limb
+    rates = _peaks(be)
+    bfly = (n // 2) * int(np.log2(n))
+    shoup_slots = rates[0] / rates[4]
+    slots_per_poly = (limbs - 1) * bfly * 8 + bfly * shoup_slots
+    pipe_rate = 0.5 * (rates[0] + rates[10])
+    pipe_us = slots_per_poly / limbs / pipe_rate * 1e6
     return {"bound": "hbm", "kernel": "two-pass NTT k_fwd_p1 + k_fwd_p2 (forward), N = 2^15, "
                                       f"{polys * limbs} limbs (1 x 60-bit + 7 x 40-bit per poly)",
             "achieved": f["achieved_gbs"], "peak": hbm_gbs, "unit": "GB/s", "frac": f["achieved_gbs"] / hbm_gbs,
             "traffic": None, "us_per_limb": f["us_per_limb"], "inverse": out["inverse"],
             "inverse_frac": out["inverse"]["achieved_gbs"] / hbm_gbs,
             "algorithmic_bytes_per_limb": 16 * n, "peak_source": hbm_src,
+            "pipe_bound": {"bound": "fma pipe (FP64 butterflies on 40-bit limbs + IMAD Shoup on the 60-bit limb)",
+                           "bound_us_per_limb": pipe_us, "frac": pipe_us / f["us_per_limb"],
+                           "slots_per_poly": slots_per_poly, "pipe_slots_per_s": pipe_rate},
             "note": "algorithmic bytes = one read + one write of the limb; the two-pass design also "
                     "writes and re-reads an N-word intermediate (L2-resident in part)"}
 
