@@ -15,9 +15,12 @@ switch, masked product, relinearisation and rescale) over B ciphertexts
   image of every ciphertext of the last timed step against the plaintext
   forward pass (max / mean error, argmax flips, near-tie images).
 * ``e2e``: the same through the public API from host images, every step:
-  ``shard.run_sharded`` packs the step's images into pinned host planes ->
-  H2D -> encode + encrypt -> evaluate -> decrypt + decode + gather on the GPU
-  -> logits all-gathered over ranks (NCCL) -> D2H.
+  ``shard.run_sharded_stream`` packs the step's images into pinned host planes
+  -> H2D -> encode + encrypt -> evaluate -> decrypt + decode + gather on the
+  GPU -> logits all-gathered over ranks (NCCL) -> D2H, with the host packing
+  of step i + 1 overlapped with step i.
+* ``graph``: the evaluation captured once as a CUDA graph (driver.EvalGraph)
+  and replayed; ``latency_batch1``: one image in one ciphertext.
 * ``roofline``: the dominant kernel call (hoisted conv2 MAC) in algorithmic
   64-bit modular MACs/s against the mixed bound of the pipes it runs on
   (narrow / 128-bit IMAD MAC and u8 IMMA peaks measured in the same run).
@@ -520,6 +523,53 @@ def main():
              "dfma_per_s": rates[10], "tcgen05_i8_mac_per_s": rates[11], "hbm_gbs": hbm_gbs,
              "hbm_source": hbm_src}
 
+    # ---- the same evaluation captured once as a CUDA graph and replayed (driver.EvalGraph) ----
+    graph = None
+    try:
+        eg = driver.EvalGraph(m, plan, be, B)
+        for _ in range(2):
+            eg.run(ct_in)
+        torch.cuda.synchronize()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            gout = eg.run(ct_in)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = g0.elapsed_time(g1) / args.steps
+        same = all(torch.equal(a.data, b.data) for a, b in zip(gout, final.cts))
+        graph = {"value": world * B * cap / (gms / 1e3), "unit": UNIT, "ms_per_step": gms,
+                 "residues_equal_eager": bool(same), "launches_per_replay": 1}
+        del eg
+    except Exception as exc:  # report, do not fail the bench line
+        graph = {"error": f"{type(exc).__name__}: {exc}"}
+
+    # ---- BASELINE config 2 taken literally: one image in one ciphertext, latency per inference ----
+    lat = None
+    try:
+        one = driver.pack_groups(m, [mine[0][:1]], plan)
+        ct1 = [be.encrypt(be.encode_batch(one[ch])) for ch in range(m.channels)]
+
+        def one_step():
+            driver._run_layers(m, CipherState(ct1, layout), be, driver.CostModel(), params.poly_degree, True)
+
+        for _ in range(3):
+            one_step()
+        torch.cuda.synchronize()
+        l0 = torch.cuda.Event(enable_timing=True)
+        l1 = torch.cuda.Event(enable_timing=True)
+        l0.record(stream)
+        for _ in range(5):
+            one_step()
+        l1.record(stream)
+        torch.cuda.synchronize()
+        lat = {"ms": l0.elapsed_time(l1) / 5, "images": 1, "ciphertexts": 1,
+               "what": "server-side evaluation of one ciphertext holding one 28x28 image (BASELINE config 2 "
+                       "literally), device time"}
+    except Exception as exc:
+        lat = {"error": f"{type(exc).__name__}: {exc}"}
+
     # ---- e2e through the public API from host images ----
     e2e = None
     if not args.no_e2e:
@@ -536,8 +586,11 @@ def main():
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        for _ in range(args.steps):
-            logits = shard.run_sharded(m, flat, params, be, plan=plan)
+        # pipelined over steps: the host packs step i + 1 into pinned planes and enqueues it while
+        # the GPU evaluates step i (every step still does its own pack, H2D, encode + encrypt,
+        # evaluation, decrypt + gather, all-gather and D2H)
+        for logits in shard.run_sharded_stream(m, [flat] * args.steps, params, be, plan=plan):
+            pass
         s1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -549,9 +602,9 @@ def main():
         ec = check_outputs(m, images_all, logits.reshape(world * B, cap, -1)) if rank == 0 else None
         e2e = {"value": world * B * cap * args.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps,
-               "path": "shard.run_sharded -> driver.pack_groups into pinned host planes -> H2D -> GPU "
-                       "encode+encrypt -> fused eval -> GPU decrypt+decode+gather -> logits all-gather over "
-                       "ranks -> D2H",
+               "path": "shard.run_sharded_stream (host packing of step i+1 overlapped with step i) -> "
+                       "driver.pack_groups into pinned host planes -> H2D -> GPU encode+encrypt -> fused eval -> "
+                       "GPU decrypt+decode+gather -> logits all-gather over ranks -> D2H",
                "check": None if ec is None else {k: ec[k] for k in ("images_checked", "max_abs_err_vs_plaintext",
                                                                     "argmax_identical")}}
 
@@ -565,7 +618,8 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues, 64-bit modular)",
                 "data": "synthetic (seeded U[0,1] images, seeded N(0,0.1^2) weights)",
                 "config": _config(B, world), "e2e": e2e, "roofline": roofline, "rooflines": rooflines,
-                "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk, "peaks": peaks, "check": check}
+                "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk, "peaks": peaks, "check": check,
+                "graph": graph, "latency_batch1": lat}
         print(json.dumps(line), flush=True)
         if args.peaks_out:
             with open(args.peaks_out, "w") as f:

@@ -33,6 +33,64 @@ def _out_dim(m) -> int:
     return int(planner.reference_infer(m, np.zeros((m.channels, m.height, m.width))).size)
 
 
+class _Job:
+    """One rank's part of one sharded inference: plan, shard bounds and (packed) host planes."""
+
+    def __init__(self, m, samples, params, backend, group, plan, pinned):
+        import torch
+        import torch.distributed as dist
+
+        dist_on = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if dist_on else 1
+        self.rank = dist.get_rank(group) if dist_on else 0
+        self.plan = plan or planner.footprint(m, params)
+        cap, n = self.plan.capacity, len(samples)
+        self.n, self.cap, self.n_groups = n, cap, math.ceil(n / cap)
+        self.dout = _out_dim(m)
+        self.on_gpu = hasattr(backend, "decrypt_device")
+        self.dev = backend.device if self.on_gpu else torch.device("cpu")
+        lo, hi = shard_range(self.n_groups, self.rank, self.world)
+        mine = [samples[g * cap:min(n, (g + 1) * cap)] for g in range(lo, hi)]
+        self.counts = [len(g) for g in mine]
+        self.planes = None
+        if mine:
+            shape = (m.channels, len(mine), self.plan.num_slots)
+            if self.on_gpu:
+                host = torch.empty(shape, dtype=torch.float64, pin_memory=pinned and torch.cuda.is_available())
+                driver.pack_groups(m, mine, self.plan, out=host.numpy())
+                self.planes = host
+            else:
+                self.planes = driver.pack_groups(m, mine, self.plan)
+
+    def enqueue(self, m, params, backend, group, fused):
+        """Launch encryption, evaluation, decryption and the logits all-gather; no host sync on
+        the GPU path (returns the device tensor of the whole job's logits)."""
+        import torch
+        import torch.distributed as dist
+
+        local = torch.zeros((0, self.dout), dtype=torch.float64, device=self.dev)
+        if self.planes is not None:
+            vals, _ = driver.infer_batch(m, self.planes, params, self.plan, backend, counts=self.counts, fused=fused,
+                                         as_tensor=True)
+            vals = vals.to(self.dev)
+            counts = self.counts
+            keep = torch.cat([vals[b, :c] for b, c in enumerate(counts)]) if len(counts) > 1 else vals[0, :counts[0]]
+            local = keep.reshape(-1, self.dout).contiguous()
+        if self.world > 1:
+            # per-rank sample counts follow from the deterministic sharding: pad to the largest, gather, trim
+            sizes = []
+            for r in range(self.world):
+                a, b = shard_range(self.n_groups, r, self.world)
+                sizes.append(sum(min(self.n, (g + 1) * self.cap) - g * self.cap for g in range(a, b)))
+            width = max(sizes)
+            buf = torch.zeros((width, self.dout), dtype=torch.float64, device=self.dev)
+            buf[:local.shape[0]] = local
+            out = torch.empty((self.world * width, self.dout), dtype=torch.float64, device=self.dev)
+            dist.all_gather_into_tensor(out, buf, group=group)
+            local = torch.cat([out[r * width:r * width + sizes[r]] for r in range(self.world)])
+        return local
+
+
 def run_sharded(m, samples, params, backend, group=None, fused=True, plan=None, pinned=True):
     """Encrypted inference of ``samples`` sharded over the ranks of ``group``.
 
@@ -44,45 +102,25 @@ def run_sharded(m, samples, params, backend, group=None, fused=True, plan=None, 
     packed into pinned host memory (async H2D), its logits stay on the device
     until the NCCL all-gather, and one device-to-host copy ends the call.
     """
-    import torch
-    import torch.distributed as dist
+    job = _Job(m, samples, params, backend, group, plan, pinned)
+    return job.enqueue(m, params, backend, group, fused).cpu().numpy()
 
-    dist_on = dist.is_available() and dist.is_initialized()
-    world = dist.get_world_size(group) if dist_on else 1
-    rank = dist.get_rank(group) if dist_on else 0
-    if plan is None:
-        plan = planner.footprint(m, params)
-    cap, n = plan.capacity, len(samples)
-    n_groups = math.ceil(n / cap)
-    dout = _out_dim(m)
-    on_gpu = hasattr(backend, "decrypt_device")
-    dev = backend.device if on_gpu else torch.device("cpu")
-    lo, hi = shard_range(n_groups, rank, world)
-    mine = [samples[g * cap:min(n, (g + 1) * cap)] for g in range(lo, hi)]
-    counts = [len(g) for g in mine]
-    local = torch.zeros((0, dout), dtype=torch.float64, device=dev)
-    if mine:
-        shape = (m.channels, len(mine), plan.num_slots)
-        if on_gpu:
-            host = torch.empty(shape, dtype=torch.float64, pin_memory=pinned and torch.cuda.is_available())
-            driver.pack_groups(m, mine, plan, out=host.numpy())
-            planes = host
-        else:
-            planes = driver.pack_groups(m, mine, plan)
-        vals, _ = driver.infer_batch(m, planes, params, plan, backend, counts=counts, fused=fused, as_tensor=True)
-        vals = vals.to(dev)
-        keep = torch.cat([vals[b, :c] for b, c in enumerate(counts)]) if len(counts) > 1 else vals[0, :counts[0]]
-        local = keep.reshape(-1, dout).contiguous()
-    if world > 1:
-        # per-rank sample counts follow from the deterministic sharding: pad to the largest, gather, trim
-        sizes = []
-        for r in range(world):
-            a, b = shard_range(n_groups, r, world)
-            sizes.append(sum(min(n, (g + 1) * cap) - g * cap for g in range(a, b)))
-        width = max(sizes)
-        buf = torch.zeros((width, dout), dtype=torch.float64, device=dev)
-        buf[:local.shape[0]] = local
-        out = torch.empty((world * width, dout), dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(out, buf, group=group)
-        local = torch.cat([out[r * width:r * width + sizes[r]] for r in range(world)])
-    return local.cpu().numpy()
+
+def run_sharded_stream(m, batches, params, backend, group=None, fused=True, plan=None, pinned=True):
+    """``run_sharded`` over a sequence of sample batches, pipelined: while the GPU evaluates batch
+    i, the host packs batch i + 1 into pinned planes and enqueues it, and only then waits for
+    batch i's logits -- host packing, H2D and the client-side encode / decrypt overlap the
+    evaluation instead of serialising with it.  Yields one ``[n_i, out_dim]`` array per batch
+    (same values as ``run_sharded`` on each batch)."""
+    it = iter(batches)
+    try:
+        first = next(it)
+    except StopIteration:
+        return
+    pending = _Job(m, first, params, backend, group, plan, pinned).enqueue(m, params, backend, group, fused)
+    for batch in it:
+        nxt = _Job(m, batch, params, backend, group, plan, pinned)  # host packing overlaps the GPU
+        queued = nxt.enqueue(m, params, backend, group, fused)
+        yield pending.cpu().numpy()  # waits for the previous batch only
+        pending = queued
+    yield pending.cpu().numpy()

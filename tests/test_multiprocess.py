@@ -114,3 +114,24 @@ def test_two_rank_gpu_backend_equals_single_process(tmp_path):
     assert np.max(np.abs(got - single)) < 1e-5
     assert np.max(np.abs(got - ref)) < 1e-5
     assert np.array_equal(np.argmax(got, 1), np.argmax(ref, 1))
+
+
+def test_stream_equals_per_batch_runs():
+    """run_sharded_stream (host packing of batch i + 1 overlapped with batch i) returns, batch for
+    batch, what run_sharded returns -- on the hoisted CPU port (the fused path, real CKKS)."""
+    from oracle.cpu_backend import CpuHoistedBackend
+    from paper_2402_03060_b200.shard import run_sharded_stream
+
+    params = HEParams(poly_degree=1 << 12, depth=7, scale_bits=40, seed=9)
+    m = planner.lenet1(5)
+    rng = np.random.default_rng(12)
+    batches = [rng.uniform(0, 1, size=(k, 1, 28, 28)) for k in (3, 1, 2)]
+    be = CpuHoistedBackend(params)
+    streamed = list(run_sharded_stream(m, batches, params, be))
+    assert len(streamed) == len(batches)
+    for b, got in zip(batches, streamed):
+        want = run_sharded(m, b, params, be)
+        assert got.shape == want.shape
+        assert np.allclose(got, want, atol=1e-6)
+        for i in range(len(b)):
+            assert np.max(np.abs(got[i] - planner.reference_infer(m, b[i]))) < 1e-5
