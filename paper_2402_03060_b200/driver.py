@@ -187,6 +187,22 @@ def pack_groups(m, groups, plan, out=None) -> np.ndarray:
     return planes
 
 
+def _gather_index(backend, plan, pos):
+    """Device index of every output slot of every packed sample, built once per (offsets, positions)
+    and cached on the backend: a per-call pageable H2D copy would block the host until the stream
+    drains, serialising the pipelined driver (shard.run_sharded_stream)."""
+    import torch
+
+    key = (tuple(int(o) for o in plan.offsets), tuple(int(p) for p in pos))
+    cache = backend.__dict__.setdefault("_gather_idx", {})
+    idx = cache.get(key)
+    if idx is None:
+        idx = torch.from_numpy((np.asarray(plan.offsets)[:, None] + np.asarray(pos)[None, :]).reshape(-1))
+        idx = idx.to(backend.device)
+        cache[key] = idx
+    return idx
+
+
 def infer_batch(m, planes, params, plan, backend, counts=None, cost_model=None, fused=True, as_tensor=False):
     """Encrypted inference of ``B`` packed ciphertext groups in one pass.
 
@@ -213,7 +229,7 @@ def infer_batch(m, planes, params, plan, backend, counts=None, cost_model=None, 
         # decrypt and gather the output slots on the device; only the logits cross to the host
         lay = state.layout
         pos = valid_positions(lay)
-        idx = torch.from_numpy((np.asarray(plan.offsets)[:, None] + pos[None, :]).reshape(-1)).to(backend.device)
+        idx = _gather_index(backend, plan, pos)
         vals = torch.cat([backend.decrypt_device(ct)[:, idx].view(-1, len(plan.offsets), len(pos))
                           for ct in state.cts], dim=2)
         if lay.pending_const != 1.0:
