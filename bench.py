@@ -225,6 +225,43 @@ class CpuHoistedPort:
                 "max_abs_err_vs_plaintext": self.check()}
 
 
+def _sim_worker(args):
+    """One host process of the slot-simulator baseline: `reps` 20-image ciphertext groups."""
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle.slot_sim import SimBackend
+    from paper_2402_03060_b200 import driver, planner
+
+    seed, reps = args
+    params, m = _params(), _model()
+    plan = planner.footprint(m, params)
+    rng = np.random.default_rng(seed)
+    driver.run_inference(m, list(rng.uniform(0, 1, size=(plan.capacity, 1, 28, 28))), params, plan=plan,
+                         backend=SimBackend(params))  # warm-up (imports, planner caches), untimed
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        samples = list(rng.uniform(0, 1, size=(plan.capacity, 1, 28, 28)))
+        driver.run_inference(m, samples, params, plan=plan, backend=SimBackend(params))
+    return reps * plan.capacity, time.perf_counter() - t0
+
+
+def sim_baseline(reps: int = 40):
+    """the reference's float64 slot simulator (restated, oracle/slot_sim.py) --
+    NO ENCRYPTION -- sharded over all host cores, one process per core."""
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_sim_worker, [(100 + i, reps) for i in range(cores)])
+    wall = time.perf_counter() - t0
+    imgs = sum(r[0] for r in res)
+    per_proc = max(r[1] for r in res)
+    return {"value": imgs / per_proc, "unit": UNIT, "cores": cores, "kind": "slot simulator, no encryption",
+            "sample": f"{cores} processes x {reps} ciphertext groups of 20 images through LeNet-1 on the float64 "
+                      f"slot simulator (N=2^15 slot count), one process per core; slowest process "
+                      f"{per_proc:.1f} s, pool wall {wall:.1f} s (incl. start-up)"}
+
+
 def cpu_baseline():
     """The survey's CPU baseline: the hoisted algorithm on all host cores (kind port-hoisted),
     with the op-level port (the reference's op-by-op schedule) alongside."""
@@ -233,6 +270,13 @@ def cpu_baseline():
     out = hp.describe(min(hp.step() for _ in range(2)))
     op = CpuPort()
     out["oplevel"] = op.describe(op.step())
+    try:
+        out["slot_simulator"] = sim_baseline()
+    except Exception as exc:  # context figure only
+        out["slot_simulator"] = {"error": f"{type(exc).__name__}: {exc}"}
+    out["paper_seal_single_thread_s_per_inference"] = {
+        "value": 30.089, "note": "UniHENN paper, LeNet-1 on SEAL, one CPU thread, other hardware and parameters "
+                                 "(SURVEY.md 8(d)(iii)); historical context only"}
     return out
 
 
