@@ -341,7 +341,9 @@ void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint
     if ((double)I * B * 2 * L * c.n > lim || (double)I * B * L * (L + 1) * c.n > lim ||
         (double)O * B * 2 * (L + 1) * c.n > lim)
         throw std::invalid_argument("IMMA hoisted kernel operand exceeds 2^32 elements: split the batch");
-    hoisted_mac_bank_wide(c, acc, X, D, masks, kbank, shifts, B, I, T, O, level, s);  // q_0 and P
+    // q_0 and P on the IMAD key-bank kernel (the tcgen05 kernel on these limbs alone measured 16.2-16.5 ms
+    // vs 13.6 ms at the LeNet conv2 shape: its 2-4-coefficient tiles cannot coalesce phase A's loads)
+    hoisted_mac_bank_wide(c, acc, X, D, masks, kbank, shifts, B, I, T, O, level, s);
 #define UH_IMMA_CASE(LL)                                                    \
     case LL:                                                                \
         launch_imma<LL, 5>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); \

@@ -35,6 +35,18 @@ namespace {
 
 constexpr int kTcMaxTerms = 128;  // 4 K-steps of 32
 constexpr int kTcThreads = 256;
+#ifndef UH_TC_TQ5
+#define UH_TC_TQ5 4
+#endif
+#ifndef UH_TC_TQ8
+#define UH_TC_TQ8 2
+#endif
+#ifndef UH_TC_NC8
+#define UH_TC_NC8 4  // coefficients per CTA on the 60-bit limbs (TMEM: 64 columns each at M = 128)
+#endif
+#ifndef UH_TC_MINB8
+#define UH_TC_MINB8 2
+#endif
 
 template <int W, int MP_, int NC_, int CT_>
 struct TcCfg {
@@ -130,7 +142,7 @@ __global__ void k_tc_bank(uint8_t *__restrict__ bank, const uint64_t *__restrict
 }
 
 template <int L, int LOGN, int W, class C>
-__global__ void __launch_bounds__(kTcThreads, 2)
+__global__ void __launch_bounds__(kTcThreads, W == 5 ? 2 : UH_TC_MINB8)
     k_hoisted_tc(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, const uint64_t *__restrict__ D,
                  const uint8_t *__restrict__ bank, const uint64_t *__restrict__ kbank,
                  const int32_t *__restrict__ shifts, int B, int I, int T, int O, int sp,
@@ -193,14 +205,18 @@ __global__ void __launch_bounds__(kTcThreads, 2)
     // ---- phase A: items (4 terms, ciphertext pair, coefficient) -> packed B-tile words ----
     {
         constexpr int NPAIR = CT / 2;
-        const int ngrp = (Q + 3) / 4;
+        // terms per item: 4 (one 32-bit B word per (value, byte)) on the 40-bit limbs; 2 (16-bit halves)
+        // on the 60-bit limbs, whose 128-bit MACs make an item twice as long -- twice the items keeps
+        // every thread busy (200 -> 400 items per CTA at the LeNet conv2 shape)
+        constexpr int TQ = W == 5 ? UH_TC_TQ5 : UH_TC_TQ8;
+        const int ngrp = (Q + TQ - 1) / TQ;
         const uint32_t krow = ((uint32_t)(qlimb ? k : L) * 2 * L) << LOGN;
         for (int it = tid; it < ngrp * NPAIR * NC; it += kTcThreads) {
             const int cf = it % NC, cp = (it / NC) % NPAIR, g = it / (NC * NPAIR);
             const int ba = b0 + 2 * cp;
             const bool oka = ba < B, okb = ba + 1 < B;
             const uint32_t n = n0 + cf;
-            // B-tile words: wd[jj][b] = byte b of value jj for terms 4g .. 4g + 3 (term tq -> byte tq);
+            // B-tile words: wd[jj][b] = byte b of value jj for terms TQ g .. TQ g + TQ - 1 (term tq -> byte tq);
             // values jj: (ct a, c0), (ct a, c1), (ct b, c0), (ct b, c1)
             uint32_t wd[4][W];
 #pragma unroll
@@ -208,8 +224,8 @@ __global__ void __launch_bounds__(kTcThreads, 2)
 #pragma unroll
                 for (int b = 0; b < W; b++) wd[jj][b] = 0;
 #pragma unroll
-            for (int tq = 0; tq < 4; tq++) {
-                const int q = 4 * g + tq;
+            for (int tq = 0; tq < TQ; tq++) {
+                const int q = TQ * g + tq;
                 uint64_t v[4] = {0, 0, 0, 0};
                 if (q < Q && oka) {
                 const uint32_t r = s_r[q];
@@ -302,10 +318,15 @@ __global__ void __launch_bounds__(kTcThreads, 2)
                 const int j = 4 * cp + jj;  // (ciphertext 2 cp + jj / 2, component jj % 2)
 #pragma unroll
                 for (int b = 0; b < W; b++)
-                    *reinterpret_cast<uint32_t *>(bt + tc_off(b * 2 * CT + j, 4 * g, kpad)) = wd[jj][b];
+                    if constexpr (TQ == 4)
+                        *reinterpret_cast<uint32_t *>(bt + tc_off(b * 2 * CT + j, 4 * g, kpad)) = wd[jj][b];
+                    else if constexpr (TQ == 2)
+                        *reinterpret_cast<uint16_t *>(bt + tc_off(b * 2 * CT + j, 2 * g, kpad)) = (uint16_t)wd[jj][b];
+                    else
+                        bt[tc_off(b * 2 * CT + j, g, kpad)] = (uint8_t)wd[jj][b];
             }
         }
-        // K columns [4 ngrp, kpad) of the B tiles are never written: their A bytes are zero
+        // K columns [TQ ngrp, kpad) of the B tiles are never written: their A bytes are zero
     }
     // generic-proxy smem writes -> visible to the tensor core (async proxy)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -407,7 +428,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
 template <int L, int W, int MP>
 void launch_tc(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint8_t *bank,
                const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, int kpad, cudaStream_t s) {
-    using C = TcCfg<W, MP, 4, W == 5 ? 8 : 4>;
+    using C = TcCfg<W, MP, W == 5 ? 4 : UH_TC_NC8, W == 5 ? 8 : 4>;
     const size_t smem = (size_t)C::NC * (MP + C::NP) * kpad;
     const size_t tb = (size_t)C::NC * MP * 2 * C::CT * (W == 5 ? 1 : 2) * 8;  // epilogue staging (reuses tiles)
     const size_t need = std::max(smem, tb);
