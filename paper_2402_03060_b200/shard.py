@@ -90,6 +90,21 @@ class _Job:
             local = torch.cat([out[r * width:r * width + sizes[r]] for r in range(self.world)])
         return local
 
+    def enqueue_to_host(self, m, params, backend, group, fused):
+        """``enqueue`` plus an asynchronous device-to-host copy of the logits into pinned memory,
+        queued right behind this job's own work; returns (host tensor, completion event or None).
+        Waiting on the event waits for this job only -- not for jobs enqueued after it."""
+        import torch
+
+        local = self.enqueue(m, params, backend, group, fused)
+        if local.device.type != "cuda":
+            return local, None
+        host = torch.empty(local.shape, dtype=local.dtype, pin_memory=True)
+        host.copy_(local, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(local.device))
+        return host, ev
+
 
 def run_sharded(m, samples, params, backend, group=None, fused=True, plan=None, pinned=True):
     """Encrypted inference of ``samples`` sharded over the ranks of ``group``.
@@ -117,10 +132,16 @@ def run_sharded_stream(m, batches, params, backend, group=None, fused=True, plan
         first = next(it)
     except StopIteration:
         return
-    pending = _Job(m, first, params, backend, group, plan, pinned).enqueue(m, params, backend, group, fused)
+    def done(job):
+        host, ev = job
+        if ev is not None:
+            ev.synchronize()  # this batch's D2H only; later batches keep running
+        return host.numpy()
+
+    pending = _Job(m, first, params, backend, group, plan, pinned).enqueue_to_host(m, params, backend, group, fused)
     for batch in it:
         nxt = _Job(m, batch, params, backend, group, plan, pinned)  # host packing overlaps the GPU
-        queued = nxt.enqueue(m, params, backend, group, fused)
-        yield pending.cpu().numpy()  # waits for the previous batch only
+        queued = nxt.enqueue_to_host(m, params, backend, group, fused)
+        yield done(pending)
         pending = queued
-    yield pending.cpu().numpy()
+    yield done(pending)
