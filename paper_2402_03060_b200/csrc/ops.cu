@@ -232,7 +232,10 @@ __global__ void __launch_bounds__(256) k_key_inner_l(uint64_t *__restrict__ u, c
                                                      const uint64_t *__restrict__ key, int key_limbs, int sp,
                                                      uint32_t r, const Mod *__restrict__ mods,
                                                      const uint64_t *__restrict__ t,
-                                                     const ulonglong2 *__restrict__ pmod) {
+                                                     const ulonglong2 *__restrict__ pmod,
+                                                     const uint64_t *__restrict__ diag) {
+    // diag != nullptr: the ModUp left its diagonal limbs D[p][k][k] unwritten; they are the input
+    // polys' own limbs diag[p][k] (the relinearisation's d2 in evaluation form)
     constexpr int LP = L + 1;
     constexpr uint32_t half = 1u << (LOGN - 1);
     const uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(256) k_key_inner_l(uint64_t *__restrict__ u, c
     uint64_t d[L], x[L], y[L];
 #pragma unroll
     for (int j = 0; j < L; j++) {
-        d[j] = __ldg(Dp + ((size_t)j * LP << LOGN));
+        d[j] = diag && j == k ? __ldg(diag + (((size_t)p * L + k) << LOGN) + src) : __ldg(Dp + ((size_t)j * LP << LOGN));
         x[j] = __ldg(K0 + (2 * j) * kstr);
         y[j] = __ldg(K0 + (2 * j + 1) * kstr);
     }
@@ -511,7 +514,8 @@ void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, i
     ntt_fast_forward(c, Jf, n_polys * level, s);
 }
 
-void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level, int in_ps, cudaStream_t s) {
+void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level, int in_ps, cudaStream_t s,
+           bool diag) {
     int L = level + 1;
     size_t N = c.n;
     Scratch C((size_t)n_polys * L * N * 8, s);
@@ -532,6 +536,7 @@ void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level
         Jf.src = C.as<uint64_t>();
         Jf.dst = D;
         ntt_fast_forward(c, Jf, n_polys * L * L, s);
+        if (!diag) return;  // the consumer reads the diagonal limbs from `in` itself
         if (N >= 512 && n_polys <= 65535) {
             k_modup_diag2<<<dim3((unsigned)(N / 512), L, n_polys), 256, 0, s>>>(D, in, L, in_ps, (int)c.logn);
         } else {
@@ -548,24 +553,28 @@ void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level
     ntt_forward(c, D, n_polys * L, L + 1, L, 0, L + 1, s);
 }
 
-static void key_inner_impl(const Ctx &c, uint64_t *u, const uint64_t *D, const uint64_t *key, int key_limbs,
-                           int n_polys, int level, int64_t r, const uint64_t *t, cudaStream_t s) {
-    int L = level + 1;
-    int64_t half = c.n / 2;
-    uint32_t rr = (uint32_t)(((r % half) + half) % half);
 #ifndef UH_KI_FIXED
 #define UH_KI_FIXED 1
 #endif
-    if (UH_KI_FIXED && c.logn == 15 && L <= 10) {
+static bool key_inner_fixed(const Ctx &c, int L) { return UH_KI_FIXED && c.logn == 15 && L <= 10; }
+// diag: the ModUp input polys when the ModUp skipped its diagonal copy (only with key_inner_fixed(c, L))
+static void key_inner_impl(const Ctx &c, uint64_t *u, const uint64_t *D, const uint64_t *key, int key_limbs,
+                           int n_polys, int level, int64_t r, const uint64_t *t, cudaStream_t s,
+                           const uint64_t *diag = nullptr) {
+    int L = level + 1;
+    int64_t half = c.n / 2;
+    uint32_t rr = (uint32_t)(((r % half) + half) % half);
+    if (key_inner_fixed(c, L)) {
         for (int p0 = 0; p0 < n_polys; p0 += 65535) {
             const int np = std::min(65535, n_polys - p0);
             dim3 g((unsigned)(c.n / 256), L + 1, np);
             uint64_t *up = u + (size_t)p0 * 2 * (L + 1) * c.n;
             const uint64_t *Dp = D + (size_t)p0 * L * (L + 1) * c.n;
+            const uint64_t *dg = diag ? diag + (size_t)p0 * L * c.n : nullptr;
             const uint64_t *tp = t ? t + (size_t)p0 * 2 * L * c.n : nullptr;
 #define UH_KI_CASE(LL)                                                                                          \
     case LL:                                                                                                    \
-        k_key_inner_l<LL, 15><<<g, 256, 0, s>>>(up, Dp, key, key_limbs, c.sp(), rr, c.d_mods, tp, c.d_pmod); \
+        k_key_inner_l<LL, 15><<<g, 256, 0, s>>>(up, Dp, key, key_limbs, c.sp(), rr, c.d_mods, tp, c.d_pmod, dg); \
         break;
             switch (L) {
                 UH_KI_CASE(1) UH_KI_CASE(2) UH_KI_CASE(3) UH_KI_CASE(4) UH_KI_CASE(5)
@@ -576,6 +585,7 @@ static void key_inner_impl(const Ctx &c, uint64_t *u, const uint64_t *D, const u
         }
         return;
     }
+    if (diag) throw std::logic_error("diagonal-free ModUp needs the fixed-L key inner product");
     if (c.n >= 256) {
         for (int p0 = 0; p0 < n_polys; p0 += 65535) {
             const int np = std::min(65535, n_polys - p0);
@@ -665,9 +675,12 @@ void ct_mul_relin_rescale_fused(const Ctx &c, uint64_t *out, const uint64_t *a, 
                                                              b_ls, (int)c.logn, c.d_mods);
     UH_LAUNCH_CHECK();
     Scratch D((size_t)B * L * (L + 1) * N * 8, s), u((size_t)B * 2 * (L + 1) * N * 8, s);
-    modup(c, D.as<uint64_t>(), D2.as<uint64_t>(), B, level, L, s);
-    // u = <D, rk> + P * (d0, d1): the relinearised product times P, in the QP basis
-    key_inner_impl(c, u.as<uint64_t>(), D.as<uint64_t>(), rk, rk_limbs, B, level, 0, T.as<uint64_t>(), s);
+    // u = <D, rk> + P * (d0, d1): the relinearised product times P, in the QP basis (the ModUp's
+    // diagonal limbs are d2's own limbs: read in place instead of copied)
+    const bool skip = ntt_fast_supported(c) && key_inner_fixed(c, L);
+    modup(c, D.as<uint64_t>(), D2.as<uint64_t>(), B, level, L, s, !skip);
+    key_inner_impl(c, u.as<uint64_t>(), D.as<uint64_t>(), rk, rk_limbs, B, level, 0, T.as<uint64_t>(), s,
+                   skip ? D2.as<uint64_t>() : nullptr);
     divide_top2(c, out, u.as<uint64_t>(), 2 * B, level, out_ls, L + 1, s);
 }
 

@@ -36,7 +36,8 @@ void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, i
 
 // ModUp of n_polys polys at level l (L = l + 1 limbs, strided in_ps) into
 // D = [n_polys][L digits][L + 1 limbs (q_0..q_l, P)][N], compact.
-void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level, int in_ps, cudaStream_t s);
+void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level, int in_ps, cudaStream_t s,
+           bool diag = true);  // diag = false: D[p][j][j] left unwritten (it is in[p][j])
 
 // u[p][comp][k] = sum_j rot_r(D[p][j][k]) * key[j][comp][kk],  comp = 0, 1,
 // k over (q_0..q_l, P); key limbs (q_0..q_{key_limbs-2}, P). u compact [n_polys][2][L+1][N].
