@@ -30,8 +30,14 @@
 namespace uh {
 namespace {
 
-constexpr int kChunk = 3;        // terms per shared-memory chunk
-constexpr int kFoldChunks = 18;  // 54 terms between folds of the 128-bit accumulators
+#ifndef UH_BANK_CHUNK
+#define UH_BANK_CHUNK 3
+#endif
+#ifndef UH_BANK_TB
+#define UH_BANK_TB 2
+#endif
+constexpr int kChunk = UH_BANK_CHUNK;        // terms per shared-memory chunk
+constexpr int kFoldChunks = 54 / kChunk;     // 54 terms between folds of the 128-bit accumulators
 constexpr int kBankMaxTerms = 512;
 #ifndef UH_BANK_MINB
 #define UH_BANK_MINB 3  // resident CTAs per SM requested from ptxas (3: 96 registers, no spills; measured 51.9 vs 52.8 ms at 4)
@@ -425,7 +431,10 @@ template <int L>
 void launch_bank(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
                  const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s,
                  int wide_only = 0) {
-    constexpr int W = 6, TB = 2;
+    constexpr int TB = UH_BANK_TB, W = kChunk * TB;  // phase A: one (term, ciphertext) item per warp
+    // phase B: warp w owns outputs 2w, 2w + 1 -- the tile must have a warp for every output pair
+    // (measured: every W >= 6 alternative -- chunk 2 x 3 ciphertexts, chunk 2 x 4 -- was slower)
+    if (O > 2 * W) throw std::invalid_argument("key-bank tiled kernel: more outputs than 2 x warps per CTA");
     dim3 grid((unsigned)((B + TB - 1) / TB), (unsigned)(c.n / 32), wide_only ? 2 : L + 1);
     k_hoisted_bank<L, 15, W, TB, UH_BANK_G><<<grid, W * 32, 0, s>>>(acc, X, D, masks, kbank, shifts, B, I, T, O, c.sp(),
                                                           c.d_mods, wide_only);
