@@ -489,7 +489,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2402_03060_b200 import _lib, driver, planner, shard
-    from paper_2402_03060_b200.he_backend import GpuBackend
+    from paper_2402_03060_b200.he_backend import CipherVector, GpuBackend
     from paper_2402_03060_b200.schedule import CipherState
 
     params, m = _params(), _model()
@@ -614,6 +614,33 @@ def main():
     except Exception as exc:
         lat = {"error": f"{type(exc).__name__}: {exc}"}
 
+    # ---- the drop-in path: the reference's op-by-op layer schedule on GpuBackend (automatic hoisting
+    # of consecutive rotations of one ciphertext), 16 resident ciphertexts ----
+    dropin = None
+    try:
+        bd = min(B, 16)
+        ct_d = [CipherVector(c.data[:bd], c.level, c.scale, be) for c in ct_in]
+
+        def op_step():
+            st, _, _ = driver._run_layers(m, CipherState(ct_d, layout), be, driver.CostModel(), params.poly_degree,
+                                          False)
+            return st
+
+        op_step()
+        torch.cuda.synchronize()
+        d0 = torch.cuda.Event(enable_timing=True)
+        d1 = torch.cuda.Event(enable_timing=True)
+        d0.record(stream)
+        op_step()
+        d1.record(stream)
+        torch.cuda.synchronize()
+        dms = d0.elapsed_time(d1)
+        dropin = {"value": bd * cap / (dms / 1e3), "unit": UNIT, "ms_per_step": dms, "ciphertexts": bd,
+                  "what": "schedule.apply_layer (the reference's op stream, layers.py:116-426) on GpuBackend with "
+                          "automatic rotation hoisting, device time; the fused driver is `value`"}
+    except Exception as exc:
+        dropin = {"error": f"{type(exc).__name__}: {exc}"}
+
     # ---- e2e through the public API from host images ----
     e2e = None
     if not args.no_e2e:
@@ -663,7 +690,7 @@ def main():
                 "data": "synthetic (seeded U[0,1] images, seeded N(0,0.1^2) weights)",
                 "config": _config(B, world), "e2e": e2e, "roofline": roofline, "rooflines": rooflines,
                 "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk, "peaks": peaks, "check": check,
-                "graph": graph, "latency_batch1": lat}
+                "graph": graph, "latency_batch1": lat, "dropin_oplevel": dropin}
         print(json.dumps(line), flush=True)
         if args.peaks_out:
             with open(args.peaks_out, "w") as f:

@@ -104,6 +104,12 @@ int uh_keyswitch(uh_ctx *ctx, uint64_t *out, const uint64_t *d, int n_polys, int
  * (np.roll(v, -r)); r = 0 is a copy. */
 int uh_rotate(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,
               const uint64_t *key, int key_limbs, int64_t r, void *stream);
+/* uh_rotate given the ModUp digits D of in's c1 (uh_modup over the B c1 polys, in_ps = 2 * in_ls):
+ * key product + ModDown + rot(c0) only, bit-identical to uh_rotate.  Backend.rotate
+ * (he_backend.py:249-253) reuses D across consecutive rotations of one ciphertext, so the
+ * reference's per-tap rotate calls (layers.py:165-196) are hoisted automatically. */
+int uh_rotate_hoisted(uh_ctx *ctx, uint64_t *out, const uint64_t *in, const uint64_t *D, int B, int level,
+                      int out_ls, int in_ls, const uint64_t *key, int key_limbs, int64_t r, void *stream);
 
 /* Backend.mul_plain (he_backend.py:226-235): ct x pt then rescale; pt encoded
  * at scale q_level.  pt_batched: one plaintext per ciphertext instead of one shared. */

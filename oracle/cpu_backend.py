@@ -106,6 +106,8 @@ class CpuHoistedBackend(GpuBackend):
             L.hc_hoisted_mac_bank(c, *a[:13])
         elif name == "uh_divide_top":  # out, in, n_polys, nl, top_mod, out_ps, in_ps, st
             L.hc_divide_top(c, *a[:7])
+        elif name == "uh_rescale":  # out, in, B, level, out_ls, in_ls, st (both components)
+            L.hc_divide_top(c, a[0], a[1], 2 * int(a[2]), int(a[3]), int(a[3]), a[4], a[5])
         elif name == "uh_divide_top2":  # out, in, n_polys, level, out_ps, in_ps, st
             L.hc_divide_top2(c, *a[:6])
         elif name == "uh_elementwise":  # op, out, a, b, n_polys, b_polys, nl, nq, out_ps, a_ps, b_ps, st
@@ -150,6 +152,7 @@ class CpuHoistedBackend(GpuBackend):
         return CipherVector(torch.from_numpy(np.stack(cts).view(np.int64)), lev, self.scale0, self)
 
     def decrypt_device(self, c: CipherVector) -> torch.Tensor:
+        c = self._ready(c)
         data = c.data.numpy().view(np.uint64)
         rows = [oc.decode_coeffs(self.o.decrypt_coeffs(data[b], self._s), c.scale, self.n)
                 for b in range(data.shape[0])]

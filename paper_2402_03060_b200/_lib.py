@@ -34,6 +34,7 @@ SIGNATURES = {
     "uh_key_inner": [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_i64, _vp],
     "uh_keyswitch": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
     "uh_rotate": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_i64, _vp],
+    "uh_rotate_hoisted": [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_i64, _vp],
     "uh_mul_plain_rescale": [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_mul_relin_rescale": [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
     "uh_mul_relin_rescale_fused": [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp],

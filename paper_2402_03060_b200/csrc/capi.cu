@@ -178,6 +178,21 @@ __attribute__((visibility("default"))) int uh_keyswitch(uh_ctx *ctx, uint64_t *o
     });
 }
 
+__attribute__((visibility("default"))) int uh_rotate_hoisted(uh_ctx *ctx, uint64_t *out, const uint64_t *in,
+                                                             const uint64_t *D, int B, int level, int out_ls,
+                                                             int in_ls, const uint64_t *key, int key_limbs, int64_t r,
+                                                             void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(out != in, "rotate is out of place");
+        int64_t half = c.n / 2;
+        bool zero = ((r % half) + half) % half == 0;
+        need(zero || key_limbs >= level + 2, "key truncated below the requested level");
+        uh::ct_rotate_hoisted(c, out, in, D, B, level, out_ls, in_ls, key, key_limbs, r, S(stream));
+    });
+}
+
 __attribute__((visibility("default"))) int uh_rotate(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int B, int level,
                                                      int out_ls, int in_ls, const uint64_t *key, int key_limbs,
                                                      int64_t r, void *stream) {

@@ -639,6 +639,29 @@ void ct_rotate(const Ctx &c, uint64_t *out, const uint64_t *in, int B, int level
     UH_LAUNCH_CHECK();
 }
 
+// ct_rotate with the ModUp digits of in's c1 supplied (D [B][L][L+1][N], from uh_modup): the key
+// product with the Galois shift folded, ModDown, and rot(c0) + ks0.  Bit-identical to ct_rotate
+// (the centred digit lift commutes with the automorphism), at the cost of a key product and a
+// ModDown instead of a full key switch -- the op-level backend reuses D across the rotations of
+// one ciphertext (automatic hoisting of the reference's per-tap rotate calls).
+void ct_rotate_hoisted(const Ctx &c, uint64_t *out, const uint64_t *in, const uint64_t *D, int B, int level,
+                       int out_ls, int in_ls, const uint64_t *key, int key_limbs, int64_t r, cudaStream_t s) {
+    int L = level + 1;
+    int64_t half = c.n / 2;
+    uint32_t rr = (uint32_t)(((r % half) + half) % half);
+    if (rr == 0) {
+        elementwise(c, OP_COPY, out, in, nullptr, 2 * B, 1, L, L, out_ls, in_ls, 0, s);
+        return;
+    }
+    size_t N = c.n;
+    Scratch u((size_t)B * 2 * (L + 1) * N * 8, s), ks((size_t)B * 2 * L * N * 8, s);
+    key_inner(c, u.as<uint64_t>(), D, key, key_limbs, B, level, rr, s);
+    divide_top(c, ks.as<uint64_t>(), u.as<uint64_t>(), B * 2, L, c.sp(), L, L + 1, s);
+    k_rot_finish<<<grid_for((size_t)B * 2 * L * N), kTB, 0, s>>>(out, in, ks.as<uint64_t>(), B, L, out_ls, in_ls, rr,
+                                                                 (int)c.logn, c.d_mods);
+    UH_LAUNCH_CHECK();
+}
+
 void ct_rescale(const Ctx &c, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,
                 cudaStream_t s) {
     divide_top(c, out, in, 2 * B, level, level, out_ls, in_ls, s);

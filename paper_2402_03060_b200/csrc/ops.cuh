@@ -51,6 +51,8 @@ void keyswitch(const Ctx &c, uint64_t *out, const uint64_t *d, int n_polys, int 
 // Ciphertext ops on batches (see layout above).
 void ct_rotate(const Ctx &c, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,
                const uint64_t *key, int key_limbs, int64_t r, cudaStream_t s);
+void ct_rotate_hoisted(const Ctx &c, uint64_t *out, const uint64_t *in, const uint64_t *D, int B, int level,
+                       int out_ls, int in_ls, const uint64_t *key, int key_limbs, int64_t r, cudaStream_t s);
 void ct_rescale(const Ctx &c, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,
                 cudaStream_t s);
 void ct_mul_relin_rescale(const Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *b, int B, int level,

@@ -57,6 +57,8 @@ def _is_gpu(backend) -> bool:
 
 def stack_cts(backend, cts, level: int) -> torch.Tensor:
     """[C][B][2][level+1][N] contiguous copy of the live limbs of ``cts``."""
+    if any(getattr(c, "pending", False) for c in cts):
+        cts = [backend._ready(c) for c in cts]  # deferred rescales of an op-level producer
     L = level + 1
     first = cts[0].data
     base = first._base if first._base is not None else None

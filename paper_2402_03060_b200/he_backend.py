@@ -80,6 +80,10 @@ class CipherVector:
     level: int
     scale: float
     backend: object = field(repr=False, default=None)
+    # lazy rescale: a plaintext product whose rescale is deferred -- ``data`` holds limbs
+    # q_0..q_{level+1} at scale ``scale * q_{level+1}``; it is rescaled once, when first used by
+    # anything but an add with another pending product (GpuBackend._ready)
+    pending: bool = False
 
     def __len__(self) -> int:
         return self.data.shape[-1] // 2
@@ -323,6 +327,7 @@ class GpuBackend:
 
     def decrypt_device(self, c: CipherVector) -> torch.Tensor:
         """Slot values [B, num_slots] as a float64 CUDA tensor."""
+        c = self._ready(c)
         B = c.batch
         coef = torch.empty((B, self.n), dtype=torch.float64, device=self.device)
         st = self._stream()
@@ -344,6 +349,19 @@ class GpuBackend:
         """Slot-wise sum; free of level cost."""
         self._check_width(a, b)
         st = self._stream()
+        if (isinstance(b, CipherVector) and a.pending and b.pending and a.level == b.level and a.ls == b.ls
+                and a.batch == b.batch):
+            # two deferred products at the same level: add before the (single, later) rescale
+            self._check_scale(a, b)
+            self.counter.record("add", a.level)
+            L = a.level + 2
+            out = self._empty(a.batch, 2, L, self.n)
+            self._call("uh_elementwise", OP_ADD, _ptr(out), _ptr(a.data), _ptr(b.data), 2 * a.batch, 2 * a.batch,
+                       L, L, L, a.ls, b.ls, st)
+            return CipherVector(out, a.level, a.scale, self, pending=True)
+        a = self._ready(a)
+        if isinstance(b, CipherVector):
+            b = self._ready(b)
         if isinstance(b, PlainVector):
             lev = a.level
             self.counter.record("add", lev)
@@ -368,6 +386,7 @@ class GpuBackend:
         return CipherVector(out, lev, a.scale, self)
 
     def sub(self, a: CipherVector, b: CipherVector) -> CipherVector:
+        a, b = self._ready(a), self._ready(b)
         lev = min(a.level, b.level)
         self._check_scale(a, b)
         self._check_batch(a, b)
@@ -390,6 +409,7 @@ class GpuBackend:
         if cipher.level < 1:
             raise LevelExhausted("ciphertext has no multiplication budget left")
         self._check_width(cipher, plain)
+        cipher = self._ready(cipher)
         lev = cipher.level
         self.counter.record("pt_mult", lev)
         if plain.values.ndim == 1 and np.all(plain.values == 1.0):
@@ -397,6 +417,13 @@ class GpuBackend:
         ql = float(self.modulus(lev))
         pt = self.plain_device(plain, lev, ql)
         B = cipher.batch
+        if self.lazy_rescale:
+            # the product stays at raw level lev; the rescale is deferred (see _ready)
+            L = lev + 1
+            out = self._empty(B, 2, L, self.n)
+            self._call("uh_elementwise", OP_MUL, _ptr(out), _ptr(cipher.data), _ptr(pt), 2 * B,
+                       -B if pt.shape[0] > 1 else 1, L, L, L, cipher.ls, L, self._stream())
+            return CipherVector(out, lev - 1, cipher.scale, self, pending=True)
         out = self._empty(B, 2, lev, self.n)
         self._call("uh_mul_plain_rescale", _ptr(out), _ptr(cipher.data), _ptr(pt), B, lev, lev, cipher.ls,
                    lev + 1, 1 if pt.shape[0] > 1 else 0, self._stream())
@@ -409,6 +436,7 @@ class GpuBackend:
             raise LevelExhausted("ciphertext has no multiplication budget left")
         self._check_width(a, b)
         self._check_batch(a, b)
+        a, b = self._ready(a), self._ready(b)
         self.counter.record("ct_mult", lev)
         rk = self.relin_key(lev)
         out = self._empty(a.batch, 2, lev, self.n)
@@ -420,20 +448,59 @@ class GpuBackend:
         """Cyclic left shift by ``r`` slots (negative ``r`` shifts right)."""
         r = r % self.params.num_slots
         self.counter.record("rotation", cipher.level)
+        cipher = self._ready(cipher)
         if r == 0:
             return CipherVector(cipher.data, cipher.level, cipher.scale, self)
         lev = cipher.level
         key = self.galois_key(r, lev)
         out = self._empty(cipher.batch, 2, lev + 1, self.n)
-        self._call("uh_rotate", _ptr(out), _ptr(cipher.data), cipher.batch, lev, lev + 1, cipher.ls, _ptr(key),
-                   key.shape[2], r, self._stream())
+        D = self._hoisted_digits(cipher) if self.auto_hoist else None
+        if D is None:
+            self._call("uh_rotate", _ptr(out), _ptr(cipher.data), cipher.batch, lev, lev + 1, cipher.ls, _ptr(key),
+                       key.shape[2], r, self._stream())
+        else:
+            self._call("uh_rotate_hoisted", _ptr(out), _ptr(cipher.data), _ptr(D), cipher.batch, lev, lev + 1,
+                       cipher.ls, _ptr(key), key.shape[2], r, self._stream())
         return CipherVector(out, lev, cipher.scale, self)
+
+    # Automatic hoisting for op-by-op callers (the reference's layers.conv / avgpool / flatten issue
+    # one rotate per tap on the same ciphertext, layers.py:165-196): the ModUp digits of the last
+    # rotated ciphertext are kept and reused while the caller keeps rotating it.  Results are
+    # bit-identical to a fresh key switch; the cache holds one entry (keyed on the data tensor, its
+    # in-place version counter and the level) and is dropped when another ciphertext is rotated.
+    auto_hoist = True
+
+    def _hoisted_digits(self, cipher: CipherVector):
+        data = cipher.data
+        key = (id(data), data._version, data.data_ptr(), cipher.level, tuple(data.shape))
+        hit = self.__dict__.get("_hoist_entry")
+        if hit is not None and hit[0] == key and hit[1] is data:
+            return hit[2]
+        self.__dict__["_hoist_entry"] = None  # free the previous digits before allocating new ones
+        lev, L = cipher.level, cipher.level + 1
+        D = self._empty(cipher.batch, L, L + 1, self.n)
+        self._call("uh_modup", _ptr(D), ctypes_vp(data.data_ptr() + cipher.ls * self.n * 8), cipher.batch, lev,
+                   2 * cipher.ls, self._stream())
+        self.__dict__["_hoist_entry"] = (key, data, D)
+        return D
 
     def drop_to(self, cipher: CipherVector, level: int) -> CipherVector:
         """Modulus drop to ``level`` (no census entry; used by level alignment)."""
         if level > cipher.level:
             raise ValueError("cannot raise a ciphertext's level")
+        cipher = self._ready(cipher)
         return CipherVector(cipher.data, level, cipher.scale, self)
+
+    lazy_rescale = True
+
+    def _ready(self, c: CipherVector) -> CipherVector:
+        """The rescaled form of a deferred plaintext product (identity for anything else)."""
+        if not getattr(c, "pending", False):
+            return c
+        raw = c.level + 1
+        out = self._empty(c.batch, 2, raw, self.n)
+        self._call("uh_rescale", _ptr(out), _ptr(c.data), c.batch, raw, raw, c.ls, self._stream())
+        return CipherVector(out, c.level, c.scale, self)
 
 
 # The reference's name for the operator class.

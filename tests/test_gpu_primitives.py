@@ -156,6 +156,30 @@ def test_rotate_bit_exact(params, level, r):
 
 
 @pytest.mark.parametrize("params", [SMALL, C2], ids=lambda p: f"N{p.poly_degree}")
+def test_auto_hoisted_rotations_bit_exact(params):
+    """Backend.rotate with automatic hoisting (ModUp digits reused across the rotations of one
+    ciphertext, uh_rotate_hoisted) equals the oracle's full key switch for every shift, including
+    after a level drop of the same data (the cache is keyed on the level) and across ciphertexts."""
+    from paper_2402_03060_b200.he_backend import CipherVector
+
+    g, o = pair(params)
+    s = o.secret()
+    level = min(5, params.depth)
+    cts = [_oracle_ct(o, level, 20 + i)[0] for i in range(2)]
+    assert g.auto_hoist
+    for ct in cts:
+        cv = CipherVector(dev(ct[None]), level, 2.0 ** 40, g)
+        for r in (1, 28, -29, 16368 % (o.n // 2), 3):
+            got = g.rotate(cv, r)
+            want = o.rotate(ct, o.galois_key(s, r, level), level, r % (o.n // 2))
+            assert np.array_equal(host(got.data)[0], want)
+        low = CipherVector(cv.data, level - 1, cv.scale, g)  # same tensor, one level lower
+        got = g.rotate(low, 5)
+        want = o.rotate(ct[:, :level], o.galois_key(s, 5, level - 1), level - 1, 5)
+        assert np.array_equal(host(got.data)[0][:, :level], want)
+
+
+@pytest.mark.parametrize("params", [SMALL, C2], ids=lambda p: f"N{p.poly_degree}")
 @pytest.mark.parametrize("level", [1, 4])
 def test_rescale_and_mul_plain_bit_exact(params, level):
     g, o = pair(params)
