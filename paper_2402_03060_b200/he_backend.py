@@ -469,15 +469,23 @@ class GpuBackend:
     # bit-identical to a fresh key switch; the cache holds one entry (keyed on the data tensor, its
     # in-place version counter and the level) and is dropped when another ciphertext is rotated.
     auto_hoist = True
+    auto_hoist_max_bytes = 2 << 30  # larger digit sets are recomputed per rotation instead of cached
+
+    def clear_hoist_cache(self) -> None:
+        """Release the cached ModUp digits of the last rotated ciphertext."""
+        self.__dict__["_hoist_entry"] = None
 
     def _hoisted_digits(self, cipher: CipherVector):
+        L = cipher.level + 1
+        if cipher.batch * L * (L + 1) * self.n * 8 > self.auto_hoist_max_bytes:
+            return None
         data = cipher.data
         key = (id(data), data._version, data.data_ptr(), cipher.level, tuple(data.shape))
         hit = self.__dict__.get("_hoist_entry")
         if hit is not None and hit[0] == key and hit[1] is data:
             return hit[2]
         self.__dict__["_hoist_entry"] = None  # free the previous digits before allocating new ones
-        lev, L = cipher.level, cipher.level + 1
+        lev = cipher.level
         D = self._empty(cipher.batch, L, L + 1, self.n)
         self._call("uh_modup", _ptr(D), ctypes_vp(data.data_ptr() + cipher.ls * self.n * 8), cipher.batch, lev,
                    2 * cipher.ls, self._stream())
@@ -494,13 +502,19 @@ class GpuBackend:
     lazy_rescale = True
 
     def _ready(self, c: CipherVector) -> CipherVector:
-        """The rescaled form of a deferred plaintext product (identity for anything else)."""
+        """The rescaled form of a deferred plaintext product (identity for anything else); computed
+        once per pending ciphertext and remembered on it."""
         if not getattr(c, "pending", False):
             return c
+        done = c.__dict__.get("_rescaled")
+        if done is not None:
+            return done
         raw = c.level + 1
         out = self._empty(c.batch, 2, raw, self.n)
         self._call("uh_rescale", _ptr(out), _ptr(c.data), c.batch, raw, raw, c.ls, self._stream())
-        return CipherVector(out, c.level, c.scale, self)
+        done = CipherVector(out, c.level, c.scale, self)
+        c.__dict__["_rescaled"] = done
+        return done
 
 
 # The reference's name for the operator class.
