@@ -30,6 +30,18 @@ typedef unsigned __int128 u128;
 
 #include "ckks_oracle.h"
 
+/* allocation failure aborts: this is test / baseline infrastructure, a partial result would be wrong */
+static void *xmalloc(size_t n) {
+    void *p = malloc(n ? n : 1);
+    if (!p) abort();
+    return p;
+}
+static void *xcalloc(size_t n, size_t sz) {
+    void *p = calloc(n ? n : 1, sz);
+    if (!p) abort();
+    return p;
+}
+
 static inline uint64_t addm(uint64_t a, uint64_t b, uint64_t q) {
     uint64_t s = a + b;
     return s >= q ? s - q : s;
@@ -128,7 +140,7 @@ HC_API void hc_modup(const or_ctx *c, uint64_t *D, const uint64_t *in, int n_pol
         for (int j = 0; j < L; j++) {
             const uint64_t qj = c->q[j];
             const uint64_t *src = in + ((size_t)p * in_ps + j) * N;
-            uint64_t *coef = (uint64_t *)malloc(sizeof(uint64_t) * N);
+            uint64_t *coef = (uint64_t *)xmalloc(sizeof(uint64_t) * N);
             memcpy(coef, src, sizeof(uint64_t) * N);
             or_intt(c, (uint32_t)j, coef);
             for (int k = 0; k < LP; k++) {
@@ -152,7 +164,7 @@ HC_API void hc_divide_top(const or_ctx *c, uint64_t *out, const uint64_t *in, in
                           int out_ps, int in_ps) {
     const size_t N = c->n;
     const uint64_t qt = c->q[top_mod];
-    uint64_t *tops = (uint64_t *)malloc(sizeof(uint64_t) * N * (size_t)(n_polys > 0 ? n_polys : 1));
+    uint64_t *tops = (uint64_t *)xmalloc(sizeof(uint64_t) * N * (size_t)(n_polys > 0 ? n_polys : 1));
 #pragma omp parallel for schedule(dynamic)
     for (int p = 0; p < n_polys; p++) {
         memcpy(tops + (size_t)p * N, in + ((size_t)p * in_ps + nl) * N, sizeof(uint64_t) * N);
@@ -163,7 +175,7 @@ HC_API void hc_divide_top(const or_ctx *c, uint64_t *out, const uint64_t *in, in
         for (int k = 0; k < nl; k++) {
             const uint64_t q = c->q[k], inv = invm(qt % q, q);
             const uint64_t *top = tops + (size_t)p * N;
-            uint64_t *t = (uint64_t *)malloc(sizeof(uint64_t) * N);
+            uint64_t *t = (uint64_t *)xmalloc(sizeof(uint64_t) * N);
             for (size_t i = 0; i < N; i++) t[i] = centred(top[i], qt, q);
             or_ntt(c, (uint32_t)k, t);
             const uint64_t *x = in + ((size_t)p * in_ps + k) * N;
@@ -184,9 +196,9 @@ HC_API void hc_divide_top2(const or_ctx *c, uint64_t *out, const uint64_t *in, i
     const uint64_t pinv = invm(P % qt, qt);
     const u128 M = (u128)qt * P, half = (M - 1) / 2;
     /* per coefficient: y = ((x_t - x_P) P^-1 mod q_t), x = x_P + P y; neg when x > (M - 1) / 2 */
-    uint64_t *Y = (uint64_t *)malloc(sizeof(uint64_t) * N * (size_t)(n_polys > 0 ? n_polys : 1));
-    uint64_t *XP = (uint64_t *)malloc(sizeof(uint64_t) * N * (size_t)(n_polys > 0 ? n_polys : 1));
-    uint8_t *NEG = (uint8_t *)malloc(N * (size_t)(n_polys > 0 ? n_polys : 1));
+    uint64_t *Y = (uint64_t *)xmalloc(sizeof(uint64_t) * N * (size_t)(n_polys > 0 ? n_polys : 1));
+    uint64_t *XP = (uint64_t *)xmalloc(sizeof(uint64_t) * N * (size_t)(n_polys > 0 ? n_polys : 1));
+    uint8_t *NEG = (uint8_t *)xmalloc(N * (size_t)(n_polys > 0 ? n_polys : 1));
 #pragma omp parallel for schedule(dynamic)
     for (int p = 0; p < n_polys; p++) {
         uint64_t *yt = Y + (size_t)p * N, *xp = XP + (size_t)p * N;
@@ -207,7 +219,7 @@ HC_API void hc_divide_top2(const or_ctx *c, uint64_t *out, const uint64_t *in, i
             const uint64_t q = c->q[k];
             const uint64_t inv = invm(mulm(qt % q, P % q, q), q);
             const uint64_t Mq = (uint64_t)(M % q), Pq = P % q;
-            uint64_t *t = (uint64_t *)malloc(sizeof(uint64_t) * N);
+            uint64_t *t = (uint64_t *)xmalloc(sizeof(uint64_t) * N);
             for (size_t i = 0; i < N; i++) {
                 /* (x_P + P y) mod q, minus M when the centred value is negative */
                 uint64_t v = addm(XP[(size_t)p * N + i] % q, mulm(Pq, Y[(size_t)p * N + i] % q, q), q);
@@ -257,8 +269,8 @@ HC_API void hc_mul_relin_rescale_fused(const or_ctx *c, uint64_t *out, const uin
                                        int level, int out_ls, int a_ls, int b_ls, const uint64_t *rk, int rk_limbs) {
     const size_t N = c->n;
     const int L = level + 1, LP = level + 2;
-    uint64_t *T = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)B * 2 * L * N);
-    uint64_t *D2 = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)B * L * N);
+    uint64_t *T = (uint64_t *)xmalloc(sizeof(uint64_t) * (size_t)B * 2 * L * N);
+    uint64_t *D2 = (uint64_t *)xmalloc(sizeof(uint64_t) * (size_t)B * L * N);
 #pragma omp parallel for collapse(2) schedule(static)
     for (int bb = 0; bb < B; bb++)
         for (int k = 0; k < L; k++) {
@@ -273,8 +285,8 @@ HC_API void hc_mul_relin_rescale_fused(const or_ctx *c, uint64_t *out, const uin
                 d2[i] = mulm(a1[i], b1[i], q);
             }
         }
-    uint64_t *D = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)B * L * LP * N);
-    uint64_t *u = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)B * 2 * LP * N);
+    uint64_t *D = (uint64_t *)xmalloc(sizeof(uint64_t) * (size_t)B * L * LP * N);
+    uint64_t *u = (uint64_t *)xmalloc(sizeof(uint64_t) * (size_t)B * 2 * LP * N);
     hc_modup(c, D, D2, B, level, L);
     key_inner_add(c, u, D, rk, rk_limbs, B, level, T);
     hc_divide_top2(c, out, u, 2 * B, level, out_ls, LP);
@@ -308,7 +320,7 @@ HC_API void hc_hoisted_mac_bank(const or_ctx *c, uint64_t *acc, const uint64_t *
                 const int qlimb = k < L;
                 const uint64_t q = c->q[qlimb ? k : sp], Pk = qlimb ? P % q : 0;
                 const size_t n0 = (size_t)blk * HC_NB, nn = N - n0 < HC_NB ? N - n0 : HC_NB;
-                u128 *s = (u128 *)calloc((size_t)OM * 2 * HC_NB, sizeof(u128));
+                u128 *s = (u128 *)xcalloc((size_t)OM * 2 * HC_NB, sizeof(u128));
                 uint64_t v0[HC_NB], v1[HC_NB];
                 int pending = 0;
                 for (int qq = 0; qq < Q; qq++) {

@@ -16,7 +16,6 @@ the GPU fused path.  Never imported by the product package.
 from __future__ import annotations
 
 import ctypes
-import os
 
 import numpy as np
 import torch
@@ -62,11 +61,9 @@ def _view(p, dtype, count: int) -> np.ndarray:
 class CpuHoistedBackend(GpuBackend):
     """GpuBackend's interface on CPU tensors, every engine call served by ckks_hoisted.c."""
 
-    def __init__(self, params: HEParams, threads: int | None = None):  # noqa: D107 (no CUDA init)
+    def __init__(self, params: HEParams):  # noqa: D107 (no CUDA init); threads: OMP_NUM_THREADS at process start
         if params.seed is None:
             raise ValueError("the CPU port derives its keys from the oracle: give HEParams an explicit seed")
-        if threads:
-            os.environ["OMP_NUM_THREADS"] = str(threads)
         self.params = params
         self._secret_seed = self._enc_seed = params.seed
         self.counter = OpCounter()
