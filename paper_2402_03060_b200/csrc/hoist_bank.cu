@@ -46,7 +46,7 @@ constexpr int kBankMaxTerms = 512;
 #define UH_BANK_DIRECT_MINB 4  // narrow layers (<= 2 outputs): 64 registers, no spills (flatten 22.2 vs 22.7 ms, pools -0.2 ms at B = 64)
 #endif
 #ifndef UH_BANK_DIRECT_G
-#define UH_BANK_DIRECT_G 2
+#define UH_BANK_DIRECT_G 4  // digits per load group (measured G = 4 at 62 registers: narrow MAC calls 27.6 vs 28.0 ms)
 #endif
 #ifndef UH_BANK_G
 #define UH_BANK_G 6  // phase-A load group (digits): all of a term's loads in flight for L <= 6
