@@ -34,6 +34,12 @@
 namespace uh {
 namespace {
 
+#ifndef UH_IMMA_NC
+#define UH_IMMA_NC 8
+#endif
+#ifndef UH_IMMA_MINB
+#define UH_IMMA_MINB 3
+#endif
 #ifndef UH_IMMA_MIN_O
 #define UH_IMMA_MIN_O 5  // narrower layers stay on the register-only IMAD kernel
 #endif
@@ -44,13 +50,13 @@ constexpr int kIMaxTerms = 128;             // 4 k-steps
 // Byte width W = 5 of the 40-bit residues: 3 outputs x 5 mask bytes per 16-row m-tile, 4 m-tiles.
 template <int W> struct IW {
     static_assert(W == 5, "40-bit limbs only");
-    static constexpr int NC = 8;                        // coefficients per CTA
+    static constexpr int NC = UH_IMMA_NC;               // coefficients per CTA
     static constexpr int OPT = 3;                       // outputs per m-tile
     static constexpr int MT = 12 / OPT;                 // m-tiles for 12 outputs
     static constexpr int COEF = W * kIJ * kIRow + 4;    // coefficient stride of the B planes
     static constexpr int CS = W * 8 + 2;                // C staging row stride (int32)
     static constexpr size_t SMEM = (size_t)NC * COEF + 8 * 16 * CS * 4;
-    static constexpr int MINB = 3;                      // resident CTAs per SM
+    static constexpr int MINB = UH_IMMA_MINB;           // resident CTAs per SM
 };
 
 __device__ __forceinline__ uint32_t rot_index_i(uint32_t n, uint32_t half, uint32_t r) {
