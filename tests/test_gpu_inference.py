@@ -156,3 +156,38 @@ def test_graph_replayed_step_equals_eager(logn):
                 y = np.concatenate([d[b][off + pos] for d in dec]) * lay.pending_const
                 ref = planner.reference_infer(m, groups[b][i])
                 assert np.max(np.abs(y - ref)) < 1e-5
+
+
+def test_stream_on_gpu_equals_per_batch_runs():
+    """shard.run_sharded_stream on GpuBackend (pinned planes, async D2H per batch) returns what
+    run_sharded returns for each batch, within CKKS noise (fresh encryption nonces per call)."""
+    from paper_2402_03060_b200.shard import run_sharded, run_sharded_stream
+
+    params = HEParams(poly_degree=1 << 12, depth=7, scale_bits=40)
+    m = planner.lenet1(seed=6)
+    be = GpuBackend(params)
+    rng = np.random.default_rng(31)
+    batches = [rng.uniform(0, 1, size=(k, 1, 28, 28)) for k in (5, 2, 3)]
+    streamed = list(run_sharded_stream(m, batches, params, be))
+    for b, got in zip(batches, streamed):
+        want = run_sharded(m, b, params, be)
+        assert got.shape == want.shape == (len(b), 10)
+        assert np.max(np.abs(got - want)) < 1e-5
+        for i in range(len(b)):
+            assert np.max(np.abs(got[i] - planner.reference_infer(m, b[i]))) < 1e-5
+
+
+def test_eval_graph_rejects_other_shapes():
+    from paper_2402_03060_b200.errors import ShapeMismatch
+
+    params = HEParams(poly_degree=1 << 12, depth=7, scale_bits=40)
+    m = planner.lenet1(seed=3)
+    plan = planner.footprint(m, params)
+    be = GpuBackend(params)
+    g = driver.EvalGraph(m, plan, be, 2)
+    planes = driver.pack_groups(m, [_samples(m, plan.capacity, seed=1)] * 3, plan)
+    cts = [be.encrypt(be.encode_batch(planes[ch])) for ch in range(m.channels)]  # 3 ciphertexts, not 2
+    with pytest.raises(ShapeMismatch):
+        g.run(cts)
+    with pytest.raises(ShapeMismatch):
+        g.run([])

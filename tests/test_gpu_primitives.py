@@ -290,3 +290,22 @@ def test_divide_top2_is_centred_division_by_q_level_times_p(params, level):
                 else:  # small-N fallback divides by P then q_level: within one unit
                     diff = (int(gotc[r, k, i]) - want) % qs[k]
                     assert diff in (0, 1, qs[k] - 1)
+
+
+def test_auto_hoist_cache_follows_in_place_updates():
+    """The hoisting cache is keyed on the tensor's in-place version: rotating, modifying the same
+    tensor in place, and rotating again must use fresh ModUp digits (result == a fresh key switch)."""
+    from paper_2402_03060_b200.he_backend import CipherVector
+
+    g, o = pair(SMALL)
+    s = o.secret()
+    level = 3
+    ct0 = _oracle_ct(o, level, 40)[0]
+    ct1 = _oracle_ct(o, level, 41)[0]
+    data = dev(ct0[None])
+    cv = CipherVector(data, level, 2.0 ** 40, g)
+    g.rotate(cv, 1)
+    data.copy_(dev(ct1[None]))  # same tensor object, new contents
+    got = g.rotate(cv, 1)
+    want = o.rotate(ct1, o.galois_key(s, 1, level), level, 1)
+    assert np.array_equal(host(got.data)[0], want)
