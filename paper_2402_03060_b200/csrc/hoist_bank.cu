@@ -48,6 +48,12 @@ constexpr int kBankMaxTerms = 512;
 #ifndef UH_BANK_DIRECT_G
 #define UH_BANK_DIRECT_G 4  // digits per load group (measured G = 4 at 62 registers: narrow MAC calls 27.6 vs 28.0 ms)
 #endif
+#ifndef UH_BANK_DIRECT4_G
+#define UH_BANK_DIRECT4_G 8  // 3-4-output layers (LeNet conv1): every digit's loads in flight
+#endif
+#ifndef UH_BANK_DIRECT4_MINB
+#define UH_BANK_DIRECT4_MINB 2
+#endif
 #ifndef UH_BANK_G
 #define UH_BANK_G 6  // phase-A load group (digits): all of a term's loads in flight for L <= 6
 #endif
@@ -403,8 +409,8 @@ void launch_direct_bank(const Ctx &c, uint64_t *acc, const uint64_t *X, const ui
     // 4-output layers (LeNet conv1): all of a term's digit / key loads in flight at 2 CTAs per SM
     // (measured 13.5 vs 15.5 ms for conv1 at B = 64 with 3 CTAs and groups of 2); narrower
     // layers are unchanged by either knob
-    constexpr int G = OM >= 4 ? 8 : UH_BANK_DIRECT_G;
-    constexpr int MINB = OM >= 4 ? 2 : UH_BANK_DIRECT_MINB;
+    constexpr int G = OM >= 4 ? UH_BANK_DIRECT4_G : UH_BANK_DIRECT_G;
+    constexpr int MINB = OM >= 4 ? UH_BANK_DIRECT4_MINB : UH_BANK_DIRECT_MINB;
     k_direct_bank<L, 15, OM, MASKS, G, MINB><<<grid, 256, 0, s>>>(acc, X, D, masks, kbank, shifts, B, I, T, O, diag,
                                                                   c.sp(), c.d_mods);
     UH_LAUNCH_CHECK();

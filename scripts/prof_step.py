@@ -8,8 +8,11 @@ and around every layer, after warm-up; prints a table sorted by device time.
 
 import argparse
 import os
+import signal
 import sys
 import time
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)  # quiet when piped into head
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
