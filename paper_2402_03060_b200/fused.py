@@ -327,25 +327,36 @@ def conv(backend, state: CipherState, layer) -> CipherState:
     if timer is not None:
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(torch.cuda.current_stream(backend.device))
-    tc = _tc_ok(backend, level, O, I * T)
-    imma = not tc and _imma_ok(backend, level, O, I * T)
-    if tc:
-        kb = key_bank(backend, shifts, level)
-        tb = tc_bank(backend, masks, O, I * T, level, cache=_banked(backend, masks))
-        backend._call("uh_hoisted_mac_tc", _vp(acc), _vp(X), L, _vp(D), _vp(tb), _vp(kb), _vp(sh), B, I, T, O, level,
-                      st)
-    elif imma:
-        kb = key_bank(backend, shifts, level)
-        ib = imma_bank(backend, masks, O, I * T, level, cache=_banked(backend, masks))
-        backend._call("uh_hoisted_mac_imma", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ib), _vp(kb), _vp(sh), B, I,
-                      T, O, level, st)
-    elif _key_bank_ok(backend, level, O):
-        kb = key_bank(backend, shifts, level)
-        backend._call("uh_hoisted_mac_bank", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(kb), _vp(sh), B, I, T, O,
-                      0, level, st)
-    else:
-        backend._call("uh_conv_hoisted_mac", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ptrs), _vp(key_limbs),
-                      _vp(sh), B, I, T, O, level, st)
+    # wide layers (more outputs than the specialised kernels hold, e.g. the CIFAR-shape 16 / 32-output
+    # convs) run as output groups of <= 12 sharing the same ModUp digits: each group re-does the
+    # key switching (phase A) but gets the tiled / tensor-core weight contraction
+    groups = [(0, O)]
+    if O > 12 and _key_bank_ok(backend, level, 12):
+        groups = [(o0, min(O, o0 + 12)) for o0 in range(0, O, 12)]
+    tc = imma = False
+    for o0, o1 in groups:
+        Og = o1 - o0
+        mg = masks[o0:o1]
+        accg = acc[o0:o1]
+        tc = _tc_ok(backend, level, Og, I * T)
+        imma = not tc and _imma_ok(backend, level, Og, I * T)
+        if tc:
+            kb = key_bank(backend, shifts, level)
+            tb = tc_bank(backend, mg, Og, I * T, level, cache=_banked(backend, mg))
+            backend._call("uh_hoisted_mac_tc", _vp(accg), _vp(X), L, _vp(D), _vp(tb), _vp(kb), _vp(sh), B, I, T, Og,
+                          level, st)
+        elif imma:
+            kb = key_bank(backend, shifts, level)
+            ib = imma_bank(backend, mg, Og, I * T, level, cache=_banked(backend, mg))
+            backend._call("uh_hoisted_mac_imma", _vp(accg), _vp(X), L, _vp(D), _vp(mg), _vp(ib), _vp(kb), _vp(sh), B,
+                          I, T, Og, level, st)
+        elif _key_bank_ok(backend, level, Og) and I * T <= 512:
+            kb = key_bank(backend, shifts, level)
+            backend._call("uh_hoisted_mac_bank", _vp(accg), _vp(X), L, _vp(D), _vp(mg), _vp(kb), _vp(sh), B, I, T,
+                          Og, 0, level, st)
+        else:
+            backend._call("uh_conv_hoisted_mac", _vp(accg), _vp(X), L, _vp(D), _vp(mg), _vp(ptrs), _vp(key_limbs),
+                          _vp(sh), B, I, T, Og, level, st)
     if timer is not None:
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(torch.cuda.current_stream(backend.device))

@@ -32,22 +32,25 @@ def main():
     ap.add_argument("--oplevel", action="store_true")
     ap.add_argument("--logn", type=int, default=15)
     ap.add_argument("--trace", action="store_true", help="print every engine call in order, per layer")
+    ap.add_argument("--model", default="lenet1", help="planner builder: lenet1, cifar_net, config1_net, lr_model, svm_model")
+    ap.add_argument("--depth", type=int, default=9)
     args = ap.parse_args()
-    params = HEParams(poly_degree=1 << args.logn, depth=9, scale_bits=40, seed=2)
-    m = planner.lenet1(0)
+    params = HEParams(poly_degree=1 << args.logn, depth=args.depth, scale_bits=40, seed=2)
+    m = getattr(planner, args.model)(0)
     plan = planner.footprint(m, params)
     be = GpuBackend(params)
     rng = np.random.default_rng(0)
-    groups = [list(rng.uniform(0, 1, size=(plan.capacity, 1, 28, 28))) for _ in range(args.batch)]
+    groups = [list(rng.uniform(0, 1, size=(plan.capacity, m.channels, m.height, m.width))) for _ in range(args.batch)]
     planes = driver.pack_groups(m, groups, plan)
-    ct = be.encrypt(be.encode_batch(planes[0]))
+    cts = [be.encrypt(be.encode_batch(planes[ch])) for ch in range(m.channels)]
     apply = schedule.apply_layer if args.oplevel else fused.apply_layer_fused
+    need = sum(r.mults for r in planner.trace_layout(m))
 
     marks = []
 
     def step(layer_events=None):
-        st = CipherState([ct], driver._input_layout(m, plan))
-        st = schedule.drop_level(be, st, 7)
+        st = CipherState(cts, driver._input_layout(m, plan))
+        st = schedule.drop_level(be, st, need)
         for layer in m.layers:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
