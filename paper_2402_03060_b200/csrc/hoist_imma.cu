@@ -10,7 +10,7 @@
 // are residues below q_k < 2^40 (the 40-bit limbs of the chain), so they split
 // exactly into 5 bytes each, and
 //   acc = sum_{a,b < 5} 2^(8(a+b)) * sum_q M_a[o][q] V_b[q][j]
-// where each inner sum is a u8 x u8 dot product of length <= 128 (< 2^23 in
+// where each inner sum is a u8 x u8 dot product of length <= 256 (< 2^24 in
 // s32: exact).  Rows of the MMA are (output, mask byte a), columns (value byte
 // b, ciphertext, component); one m16n8k32 covers 3 outputs x 5 mask bytes by
 // 8 columns by 32 terms.  The epilogue recombines the 25 byte products of each
@@ -24,7 +24,7 @@
 //             the B-fragment layout ([coefficient][byte][column][term]);
 //   phase B : warp w takes (coefficient, m-tile) units; A fragments come from a
 //             pre-split mask bank (16-byte loads, fragment order), B fragments
-//             from shared memory; 4 k-steps x 5 n-tiles of IMMA per unit, then
+//             from shared memory; ceil(Q / 32) k-steps x 5 n-tiles of IMMA per unit, then
 //             the byte recombination and the modular reduction per output.
 // The 60-bit limbs (q_0, P) run on the IMAD key-bank kernel (hoisted_mac_bank_wide, hoist_bank.cu).
 #include <type_traits>
@@ -45,19 +45,27 @@ namespace {
 #endif
 constexpr int kICT = 4;                     // ciphertexts per CTA
 constexpr int kIJ = 2 * kICT;               // columns per value byte (ciphertext x component)
-constexpr int kIRow = 144;                  // bytes per (coefficient, byte, column) row: 128 terms + pad
-constexpr int kIMaxTerms = 128;             // 4 k-steps
+#ifndef UH_IMMA_NC_WIDE
+#define UH_IMMA_NC_WIDE 4  // coefficients per CTA past 4 k-steps (keeps 3 CTAs / SM)
+#endif
+constexpr int kIMaxTerms = 256;             // 8 k-steps
 // Byte width W = 5 of the 40-bit residues: 3 outputs x 5 mask bytes per 16-row m-tile, 4 m-tiles.
-template <int W> struct IW {
+// NKS k-steps of 32 terms.  A B-plane row (coefficient, byte, column) holds 32 NKS terms + 16 bytes
+// of pad: its word stride is 4 mod 8, so the 8 gid rows x 4 tig words of a fragment load hit 32
+// distinct banks.
+template <int W, int NKS> struct IW {
     static_assert(W == 5, "40-bit limbs only");
-    static constexpr int NC = UH_IMMA_NC;               // coefficients per CTA
-    static constexpr int OPT = 3;                       // outputs per m-tile
-    static constexpr int MT = 12 / OPT;                 // m-tiles for 12 outputs
-    static constexpr int COEF = W * kIJ * kIRow + 4;    // coefficient stride of the B planes
+    static constexpr int NC = NKS > 4 ? UH_IMMA_NC_WIDE : UH_IMMA_NC;  // coefficients per CTA
+    static constexpr int OPT = 3;                       // outputs per m-tile (m-tiles: ceil(O / 3))
+    static constexpr int ROWB = NKS > 4 ? 32 * NKS + 16 : 144;  // bytes per B-plane row
+    static constexpr int COEF = W * kIJ * ROWB + 4;     // coefficient stride of the B planes
     static constexpr int CS = W * 8 + 2;                // C staging row stride (int32)
     static constexpr size_t SMEM = (size_t)NC * COEF + 8 * 16 * CS * 4;
     static constexpr int MINB = UH_IMMA_MINB;           // resident CTAs per SM
 };
+constexpr int kIOPT = 3;
+constexpr int kIMaxO = 48;                  // 16 m-tiles
+__host__ __device__ constexpr int imma_mtiles(int O) { return (O + kIOPT - 1) / kIOPT; }
 
 __device__ __forceinline__ uint32_t rot_index_i(uint32_t n, uint32_t half, uint32_t r) {
     uint32_t h = n >= half ? half : 0;
@@ -78,23 +86,24 @@ __device__ __forceinline__ void imma(int (&c)[4], const uint4 &a, uint32_t b0, u
         : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
 
-// A-fragment mask bank [limb slot][N][m-tile][k-step][lane][4 words]: per coefficient, the
-// (output x byte) x term matrix.  Row r of m-tile mt is output OPT mt + r / W, byte r % W
-// (rows past OPT W and outputs >= O are zero).  Limb slots: limbs 1..L-1.
+// A-fragment mask bank [limb slot][N][m-tile][k-step][lane][4 words], ceil(O / 3) m-tiles: per
+// coefficient, the (output x byte) x term matrix.  Row r of m-tile mt is output OPT mt + r / W,
+// byte r % W (rows past OPT W and outputs >= O are zero).  Limb slots: limbs 1..L-1.
 template <int W>
 __global__ void k_imma_bank(uint32_t *__restrict__ ib, const uint64_t *__restrict__ masks, int O, int Q, int L,
                             int logn, int nks) {
-    using C = IW<W>;
+    using C = IW<W, 1>;
     const uint32_t N = 1u << logn;
     const int nslots = L - 1;
-    const size_t total = (size_t)nslots * N * C::MT * nks * 32;
+    const int MT = imma_mtiles(O);
+    const size_t total = (size_t)nslots * N * MT * nks * 32;
     const size_t ROW = (size_t)(L + 1) << logn;
     for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
         const int lane = (int)(idx & 31);
         const int ks = (int)((idx >> 5) % nks);
         const size_t r0 = (idx >> 5) / nks;
-        const int mt = (int)(r0 % C::MT);
-        const size_t r1 = r0 / C::MT;
+        const int mt = (int)(r0 % MT);
+        const size_t r1 = r0 / MT;
         const uint32_t n = (uint32_t)(r1 & (N - 1));
         const int slot = (int)(r1 >> logn);
         const int k = slot + 1;
@@ -118,22 +127,23 @@ __global__ void k_imma_bank(uint32_t *__restrict__ ib, const uint64_t *__restric
             }
             w[reg] = v;
         }
-        reinterpret_cast<uint4 *>(ib)[(((r1 * C::MT + mt) * nks + ks) << 5) + lane] = make_uint4(w[0], w[1], w[2], w[3]);
+        reinterpret_cast<uint4 *>(ib)[(((r1 * MT + mt) * nks + ks) << 5) + lane] = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
 template <int L, int LOGN, int NKS, int W>
-__global__ void __launch_bounds__(256, IW<W>::MINB)
+__global__ void __launch_bounds__(256, IW<W, NKS>::MINB)
     k_hoisted_imma(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, const uint64_t *__restrict__ D,
                    const uint4 *__restrict__ ib, const uint64_t *__restrict__ kbank, const int32_t *__restrict__ shifts,
                    int B, int I, int T, int O, int sp, const Mod *__restrict__ mods) {
-    using C = IW<W>;
+    using C = IW<W, NKS>;
+    constexpr int kIRow = C::ROWB;
     constexpr int LP = L + 1;
     constexpr uint32_t N = 1u << LOGN, half = N >> 1;
     constexpr uint32_t ROW = (uint32_t)LP << LOGN;
     extern __shared__ __align__(16) unsigned char ism[];
     int *cst = reinterpret_cast<int *>(ism + (size_t)C::NC * C::COEF);
-    __shared__ uint32_t s_x[kIMaxTerms], s_d[kIMaxTerms], s_k[kIMaxTerms], s_r[kIMaxTerms];
+    __shared__ uint32_t s_x[32 * NKS], s_d[32 * NKS], s_k[32 * NKS], s_r[32 * NKS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int b0 = blockIdx.x * kICT;
     const uint32_t n0 = blockIdx.y * C::NC;
@@ -235,12 +245,11 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
     // ---- phase B: IMMA per (coefficient, m-tile), byte recombination, reduction ----
     const int gid = lane >> 2, tig = lane & 3;
     int *cw = cst + warp * 16 * C::CS;
-    const int nmt = (O + C::OPT - 1) / C::OPT;
-    for (int u = warp; u < C::NC * C::MT; u += 8) {
-        const int cf = u / C::MT, mt = u % C::MT;
-        if (mt >= nmt) continue;
+    const int nmt = imma_mtiles(O);
+    for (int u = warp; u < C::NC * nmt; u += 8) {
+        const int cf = u / nmt, mt = u - cf * nmt;
         const uint32_t n = n0 + cf;
-        const uint4 *af = ib + ((((size_t)slot * N + n) * C::MT + mt) * NKS << 5) + lane;
+        const uint4 *af = ib + ((((size_t)slot * N + n) * nmt + mt) * NKS << 5) + lane;
         uint4 A[NKS];
 #pragma unroll
         for (int ks = 0; ks < NKS; ks++) A[ks] = __ldg(af + (ks << 5));
@@ -290,9 +299,10 @@ __global__ void __launch_bounds__(256, IW<W>::MINB)
 template <int L, int NKS, int W>
 void launch_imma_k(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib,
                    const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
-    smem_optin(k_hoisted_imma<L, 15, NKS, W>, IW<W>::SMEM);
-    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / IW<W>::NC), L - 1);
-    k_hoisted_imma<L, 15, NKS, W><<<grid, 256, IW<W>::SMEM, s>>>(acc, X, D, reinterpret_cast<const uint4 *>(ib), kbank,
+    using C = IW<W, NKS>;
+    smem_optin(k_hoisted_imma<L, 15, NKS, W>, C::SMEM);
+    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / C::NC), L - 1);
+    k_hoisted_imma<L, 15, NKS, W><<<grid, 256, C::SMEM, s>>>(acc, X, D, reinterpret_cast<const uint4 *>(ib), kbank,
                                                                 shifts, B, I, T, O, c.sp(), c.d_mods);
     UH_LAUNCH_CHECK();
 }
@@ -304,29 +314,34 @@ void launch_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t 
     if (nks <= 1) launch_imma_k<L, 1, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
     else if (nks == 2) launch_imma_k<L, 2, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
     else if (nks == 3) launch_imma_k<L, 3, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
-    else launch_imma_k<L, 4, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    else if (nks == 4) launch_imma_k<L, 4, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    else if (nks == 5) launch_imma_k<L, 5, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    else if (nks == 6) launch_imma_k<L, 6, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    else if (nks == 7) launch_imma_k<L, 7, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
+    else launch_imma_k<L, 8, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
 }
 
 }  // namespace
 
 // Applicable when N = 2^15, the level has 40-bit limbs q_1..q_{L-1} (< 2^40) and 60-bit
-// q_0 and P, 5..12 dense masked outputs and at most 128 terms.
+// q_0 and P, 5..48 dense masked outputs and at most 256 terms.
 bool hoisted_imma_supported(const Ctx &c, int level, int O, int Q) {
-    if (c.logn != 15 || level < 2 || level + 1 > 10 || O < UH_IMMA_MIN_O || O > 12 || Q < 1 || Q > kIMaxTerms) return false;
+    if (c.logn != 15 || level < 2 || level + 1 > 10 || O < UH_IMMA_MIN_O || O > kIMaxO || Q < 1 || Q > kIMaxTerms)
+        return false;
     for (int k = 1; k <= level; k++)
         if (c.h_q[k] >> 40) return false;
     return (c.h_q[0] >> 40) && (c.h_q[c.count - 1] >> 40);
 }
 
 // uint32 words of the 40-bit-limb bank
-size_t imma_bank_words(const Ctx &c, int level, int Q) {
+size_t imma_bank_words(const Ctx &c, int level, int O, int Q) {
     const int nks = (Q + 31) / 32;
-    return (size_t)level * IW<5>::MT * c.n * nks * 32 * 4;
+    return (size_t)level * imma_mtiles(O) * c.n * nks * 32 * 4;
 }
 
 void imma_mask_bank(const Ctx &c, uint32_t *ib, const uint64_t *masks, int O, int Q, int level, cudaStream_t s) {
     const int L = level + 1, nks = (Q + 31) / 32;
-    const size_t t5 = (size_t)(L - 1) * c.n * IW<5>::MT * nks * 32;
+    const size_t t5 = (size_t)(L - 1) * c.n * imma_mtiles(O) * nks * 32;
     k_imma_bank<5><<<(unsigned)std::min<size_t>((t5 + 255) / 256, 148 * 32), 256, 0, s>>>(ib, masks, O, Q, L,
                                                                                          (int)c.logn, nks);
     UH_LAUNCH_CHECK();
@@ -341,15 +356,20 @@ void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint
                       const uint32_t *ib, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O,
                       int level, cudaStream_t s) {
     if (!hoisted_imma_supported(c, level, O, I * T))
-        throw std::invalid_argument("IMMA hoisted kernel: needs N = 2^15, 40-bit q_1..q_level, 5 <= O <= 12, <= 128 terms");
+        throw std::invalid_argument("IMMA hoisted kernel: needs N = 2^15, 40-bit q_1..q_level, 5 <= O <= 48, <= 256 terms");
     const double lim = 4294967295.0;
     const int L = level + 1;
     if ((double)I * B * 2 * L * c.n > lim || (double)I * B * L * (L + 1) * c.n > lim ||
         (double)O * B * 2 * (L + 1) * c.n > lim)
         throw std::invalid_argument("IMMA hoisted kernel operand exceeds 2^32 elements: split the batch");
     // q_0 and P on the IMAD key-bank kernel (the tcgen05 kernel on these limbs alone measured 16.2-16.5 ms
-    // vs 13.6 ms at the LeNet conv2 shape: its 2-4-coefficient tiles cannot coalesce phase A's loads)
-    hoisted_mac_bank_wide(c, acc, X, D, masks, kbank, shifts, B, I, T, O, level, s);
+    // vs 13.6 ms at the LeNet conv2 shape: its 2-4-coefficient tiles cannot coalesce phase A's loads),
+    // in groups of <= 12 outputs (its register tile); the 40-bit limbs take every output in one pass,
+    // so their key switching (phase A) is done once for all of them
+    const size_t LPN = (size_t)(L + 1) * c.n;
+    for (int o0 = 0; o0 < O; o0 += 12)
+        hoisted_mac_bank_wide(c, acc + (size_t)o0 * B * 2 * LPN, X, D, masks + (size_t)o0 * I * T * LPN, kbank, shifts,
+                              B, I, T, std::min(12, O - o0), level, s);
 #define UH_IMMA_CASE(LL)                                                    \
     case LL:                                                                \
         launch_imma<LL, 5>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); \

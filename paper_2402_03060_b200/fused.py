@@ -121,8 +121,9 @@ def _key_bank_ok(backend, level: int, O: int) -> bool:
 
 
 def _imma_ok(backend, level: int, O: int, Q: int) -> bool:
-    """Dense 5..12-output layers: the mask contraction on the tensor cores (hoist_imma.cu)."""
-    if os.environ.get("UH_IMMA", "1") == "0" or not _key_bank_ok(backend, level, O):
+    """Dense 5..48-output layers, <= 256 terms: the 40-bit limbs' mask contraction on the tensor cores
+    (hoist_imma.cu); q_0 and P on the key-bank kernel in groups of <= 12 outputs."""
+    if os.environ.get("UH_IMMA", "1") == "0" or not _key_bank_ok(backend, level, min(O, 12)):
         return False
     return backend.kernel_supported("uh_imma_supported", level, O, Q)
 
@@ -162,8 +163,8 @@ def imma_bank(backend, masks: torch.Tensor, O: int, Q: int, level: int, cache: b
     if hit is not None and hit[0] is _persistent(masks):
         return hit[1]
     nks = (Q + 31) // 32
-    # 40-bit limbs q_1..q_level: 4 m-tiles of 3 outputs x 5 bytes (q_0 and P stay on the IMAD kernel)
-    ib = torch.empty((4 * level * backend.n * nks * 32 * 4,), dtype=torch.int32, device=backend.device)
+    # 40-bit limbs q_1..q_level: ceil(O / 3) m-tiles of 3 outputs x 5 bytes (q_0 and P stay on the IMAD kernel)
+    ib = torch.empty(((O + 2) // 3 * level * backend.n * nks * 32 * 4,), dtype=torch.int32, device=backend.device)
     backend._call("uh_imma_mask_bank", _vp(ib), _vp(masks), O, Q, level, backend._stream())
     if cache:
         banks[ck] = (_persistent(masks), ib)
@@ -327,11 +328,11 @@ def conv(backend, state: CipherState, layer) -> CipherState:
     if timer is not None:
         t0 = torch.cuda.Event(enable_timing=True)
         t0.record(torch.cuda.current_stream(backend.device))
-    # wide layers (more outputs than the specialised kernels hold, e.g. the CIFAR-shape 16 / 32-output
-    # convs) run as output groups of <= 12 sharing the same ModUp digits: each group re-does the
-    # key switching (phase A) but gets the tiled / tensor-core weight contraction
+    # wide layers (more outputs than a kernel holds, e.g. the CIFAR-shape 16 / 32-output convs): the
+    # IMMA kernel takes up to 48 outputs in one pass on the 40-bit limbs (one key switch per term);
+    # otherwise output groups of <= 12 share the ModUp digits, each re-doing the key switching
     groups = [(0, O)]
-    if O > 12 and _key_bank_ok(backend, level, 12):
+    if O > 12 and not _imma_ok(backend, level, O, I * T) and _key_bank_ok(backend, level, 12):
         groups = [(o0, min(O, o0 + 12)) for o0 in range(0, O, 12)]
     tc = imma = False
     for o0, o1 in groups:

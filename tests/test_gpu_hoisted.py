@@ -198,6 +198,11 @@ def test_key_bank_kernels_equal_generic_every_mode(O, with_masks, diag, monkeypa
     (7, 3, 3, [0, 1, 28, -29, 16383, 57, -2, 3, 700], 4),              # partial m-tile, Q = 27 (not / 4)
     (5, 2, 2, [0, 1, 28, -29, 16383], 3),                              # one k-step, 2 m-tiles
     (9, 8, 1, [3, 0, -5], 9),                                          # high level, 3 terms, 3 ct tiles
+    (6, 2, 16, [a + 32 * b for b in range(4) for a in range(4)], 5),   # CIFAR conv2 terms: Q = 256, 8 k-steps
+    (5, 3, 5, [a + 28 * b for b in range(5) for a in range(5)], 4),    # Q = 125: 4 k-steps, one short
+    (7, 2, 6, [a + 28 * b for b in range(5) for a in range(5)], 6),    # Q = 150: 5 k-steps (wide tile)
+    (32, 2, 4, [a + 32 * b for b in range(4) for a in range(4)], 5),   # CIFAR conv2 outputs: 11 m-tiles, 3 q_0/P groups
+    (16, 3, 3, [0, 1, 2, 32, 33, 34, 64, 65, 66], 4),                  # CIFAR conv1 shape: 6 m-tiles, 12 + 4 on q_0/P
 ])
 def test_imma_kernel_equals_key_bank_kernel(O, level, I, shifts, B, monkeypatch):
     """Tensor-core mask contraction (hoist_imma.cu: byte-split u8 IMMA on the 40-bit limbs, the IMAD
