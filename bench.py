@@ -25,13 +25,19 @@ switch, masked product, relinearisation and rescale) over B ciphertexts
   64-bit modular MACs/s against the mixed bound of the pipes it runs on
   (narrow / 128-bit IMAD MAC and u8 IMMA peaks measured in the same run).
   ``rooflines.ntt``: the two-pass NTT (16 algorithmic bytes per coefficient)
-  against HBM; ``rooflines.step``: the whole step against SURVEY.md 8(d)'s
-  W_hoist at the IMAD modmul peak.
+  against HBM, against the FMA pipe it runs on, and against north_star's own
+  bound (the slower of HBM and int32-IMAD modmul); ``rooflines.step``: the whole
+  step against SURVEY.md 8(d)'s W_hoist at the IMAD modmul peak.
 * ``cpu_baseline``: the same hoisted algorithm on the host (kind
   ``port-hoisted``: the unchanged fused layer code over the OpenMP C port
   oracle/ckks_hoisted.c, all host cores, 4 resident ciphertexts = 80 images per
   step), with the op-level oracle port (the reference's op-by-op schedule, one
   ciphertext) alongside under ``oplevel``; rank 0 at N=1.
+
+Multi-GPU: one rank per GPU under torchrun over NCCL (timings max over ranks).
+``UH_BENCH_DIST_BACKEND=gloo`` runs every rank on cuda:0 with host-side
+collectives -- a functional smoke of that path on one GPU
+(tests/test_bench_contract.py), not a scaling number.
 
 ``--impl reference`` runs the op-level CPU oracle port (the reference's own
 op-by-op schedule; the reference package has no RNS-CKKS implementation and
@@ -506,9 +512,24 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
+    # UH_BENCH_DIST_BACKEND=gloo: a functional smoke of the multi-rank path on ONE GPU (every rank on
+    # cuda:0, host-side collectives; independent ranks, so no kernel waits on another rank's) -- the
+    # numbers of such a run are not a scaling measurement.  The default is one rank per GPU over NCCL.
+    dist_backend = os.environ.get("UH_BENCH_DIST_BACKEND", "nccl")
+    dev_index = local if dist_backend == "nccl" else local % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(dist_backend)
+
+    def allreduce_max(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev if dist_backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     from paper_2402_03060_b200 import _lib, driver, planner, shard
     from paper_2402_03060_b200.he_backend import CipherVector, GpuBackend
     from paper_2402_03060_b200.schedule import CipherState
@@ -560,11 +581,7 @@ def main():
     barrier()
     launches = _lib.launch_count() - l0
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = allreduce_max(e0.elapsed_time(e1))
     value = world * B * cap * args.steps / (ms / 1e3)
     timers = be.kernel_timer
     be.kernel_timer = None
@@ -697,11 +714,7 @@ def main():
         s1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        ems = s0.elapsed_time(s1)
-        te = torch.tensor([ems], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        ems = float(te.item())
+        ems = allreduce_max(s0.elapsed_time(s1))
         ec = check_outputs(m, images_all, logits.reshape(world * B, cap, -1)) if rank == 0 else None
         e2e = {"value": world * B * cap * args.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps,
