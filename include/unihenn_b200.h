@@ -197,12 +197,13 @@ int uh_hoisted_mac_bank(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, 
  * outputs and <= 256 terms (LeNet conv2, the CIFAR-shape convs; layers.py:134-197):
  * the weight-mask contraction runs as byte-split u8 IMMA (exact; residues identical
  * to uh_hoisted_mac_bank) on the 40-bit limbs (5-byte operands), every output in
- * one pass; q_0 and P run the IMAD kernel from `masks`, <= 12 outputs per launch.
- * `ib` is the A-fragment mask bank made once per layer by uh_imma_mask_bank from
- * the uint64 mask bank (ceil(O/3) x level x N x ceil(Q/32) x 128 uint32 words).
- * uh_imma_supported: 1 when the shape and the chain (40-bit q_1..q_level, 60-bit
- * q_0 and P) qualify. */
+ * one pass; q_0 and P (below 2^60) run 8-byte IMMA for <= 128 terms, else the IMAD
+ * kernel from `masks` (<= 12 outputs per launch).  `ib` is the A-fragment mask bank
+ * made once per layer by uh_imma_mask_bank from the uint64 mask bank
+ * (uh_imma_bank_words uint32 words).  uh_imma_supported: 1 when the shape and the
+ * chain (40-bit q_1..q_level, 60-bit q_0 and P) qualify. */
 int uh_imma_supported(uh_ctx *ctx, int level, int O, int Q);
+unsigned long long uh_imma_bank_words(uh_ctx *ctx, int level, int O, int Q);
 int uh_imma_mask_bank(uh_ctx *ctx, uint32_t *ib, const uint64_t *masks, int O, int Q, int level, void *stream);
 int uh_hoisted_mac_imma(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D,
                         const uint64_t *masks, const uint32_t *ib, const uint64_t *kbank, const int32_t *shifts,

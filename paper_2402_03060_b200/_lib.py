@@ -64,6 +64,7 @@ EXTRA = {"uh_abi_version": ([], _c_int), "uh_last_error": ([], ctypes.c_char_p),
          "uh_launch_count": ([], ctypes.c_ulonglong), "uh_bench_peaks": ([_vp, _vp], _c_int),
          "uh_hoisted_bank_supported": ([_vp, _c_int, _c_int], _c_int),
          "uh_imma_supported": ([_vp, _c_int, _c_int, _c_int], _c_int),
+         "uh_imma_bank_words": ([_vp, _c_int, _c_int, _c_int], ctypes.c_ulonglong),
          "uh_tc_supported": ([_vp, _c_int, _c_int, _c_int], _c_int),
          "uh_tc_bank_bytes": ([_vp, _c_int, _c_int, _c_int], ctypes.c_ulonglong)}
 

@@ -370,6 +370,10 @@ __attribute__((visibility("default"))) int uh_imma_supported(uh_ctx *ctx, int le
     return ctx && uh::hoisted_imma_supported(C(ctx), level, O, Q) ? 1 : 0;
 }
 
+__attribute__((visibility("default"))) unsigned long long uh_imma_bank_words(uh_ctx *ctx, int level, int O, int Q) {
+    return ctx && uh::hoisted_imma_supported(C(ctx), level, O, Q) ? uh::imma_bank_words(C(ctx), level, O, Q) : 0ull;
+}
+
 __attribute__((visibility("default"))) int uh_imma_mask_bank(uh_ctx *ctx, uint32_t *ib, const uint64_t *masks, int O,
                                                              int Q, int level, void *stream) {
     return guard([&] {

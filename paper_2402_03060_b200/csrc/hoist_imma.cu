@@ -27,6 +27,7 @@
 //             from shared memory; ceil(Q / 32) k-steps x 5 n-tiles of IMMA per unit, then
 //             the byte recombination and the modular reduction per output.
 // The 60-bit limbs (q_0, P) run on the IMAD key-bank kernel (hoisted_mac_bank_wide, hoist_bank.cu).
+#include <cstdlib>
 #include <type_traits>
 
 #include "ops.cuh"
@@ -59,7 +60,9 @@ template <int W, int NKS> struct IW {
     static constexpr int OPT = 3;                       // outputs per m-tile (m-tiles: ceil(O / 3))
     static constexpr int ROWB = NKS > 4 ? 32 * NKS + 16 : 144;  // bytes per B-plane row
     static constexpr int COEF = W * kIJ * ROWB + 4;     // coefficient stride of the B planes
-    static constexpr int CS = W * 8 + 2;                // C staging row stride (int32)
+    // C staging row stride (int32): 40 = 8 mod 32 puts both the fragment stores (4 rows per
+    // half-warp) and the epilogue reads (rows o W + a of 3 outputs) on 32 distinct banks
+    static constexpr int CS = W * 8;
     static constexpr size_t SMEM = (size_t)NC * COEF + 8 * 16 * CS * 4;
     static constexpr int MINB = UH_IMMA_MINB;           // resident CTAs per SM
 };
@@ -321,6 +324,268 @@ void launch_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t 
     else launch_imma_k<L, 8, W>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s);
 }
 
+// ---------------------------------------------------------------------------
+// The 60-bit limbs q_0 and P: the same contraction with 8-byte operands.  Canonical residues
+// below 2^60 and <= 128 terms keep sum_q M V < 2^127, so the 64 byte products of each
+// (output, column) recombine exactly in 128 bits.  An m-tile is 2 outputs x 8 mask bytes; n-tiles
+// are the 8 value bytes.  Phase A is hoist_bank.cu's 60-bit key switch (128-bit accumulators);
+// the epilogue stages each warp's C fragments in shared memory and recombines every (output,
+// column) on two lanes (4 mask bytes each), summed with one 128-bit shuffle.
+#ifndef UH_IMMA8_NC
+#define UH_IMMA8_NC 4  // coefficients per CTA (3 CTAs / SM: 70.7 KB of shared memory each)
+#endif
+#ifndef UH_IMMA8_MINB
+#define UH_IMMA8_MINB 3
+#endif
+constexpr int kI8MaxTerms = 128;
+constexpr int kI8OPT = 2;
+__host__ __device__ constexpr int imma8_mtiles(int O) { return (O + kI8OPT - 1) / kI8OPT; }
+struct IW8 {
+    static constexpr int W = 8;
+    static constexpr int NC = UH_IMMA8_NC;
+    static constexpr int ROWB = 144;                     // 128 terms + pad (word stride 4 mod 8)
+    static constexpr int COEF = W * kIJ * ROWB + 4;
+    // C staging: 16 rows x 64 columns per warp, the 8-column groups of row r rotated by 8 g(r),
+    // g(4 q + i) = (i + q) mod 4 -- a Latin square, so both the fragment stores (4 consecutive rows
+    // per half-warp) and the epilogue reads (rows i, i + 4, i + 8, i + 12) hit 32 distinct banks
+    static constexpr int CS = 64;
+    static constexpr size_t SMEM = (size_t)NC * COEF + 8 * 16 * CS * 4;
+};
+__device__ __forceinline__ int stage8_col(int row, int col) {
+    const int g = ((row & 3) + (row >> 2)) & 3;
+    return (col + 8 * g) & 63;
+}
+
+// A-fragment bank of the 60-bit limbs [slot 0: q_0, 1: P][N][m-tile][k-step][lane][4 words]:
+// row r of m-tile mt is output 2 mt + r / 8, mask byte r % 8
+__global__ void k_imma_bank8(uint32_t *__restrict__ ib, const uint64_t *__restrict__ masks, int O, int Q, int L,
+                             int logn, int nks) {
+    const uint32_t N = 1u << logn;
+    const int MT = imma8_mtiles(O);
+    const size_t total = (size_t)2 * N * MT * nks * 32;
+    const size_t ROW = (size_t)(L + 1) << logn;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const int lane = (int)(idx & 31);
+        const int ks = (int)((idx >> 5) % nks);
+        const size_t r0 = (idx >> 5) / nks;
+        const int mt = (int)(r0 % MT);
+        const size_t r1 = r0 / MT;
+        const uint32_t n = (uint32_t)(r1 & (N - 1));
+        const int slot = (int)(r1 >> logn);
+        const int k = slot ? L : 0;
+        const int g = lane >> 2, tig = lane & 3;
+        uint32_t w[4];
+#pragma unroll
+        for (int reg = 0; reg < 4; reg++) {
+            const int row = g + (reg & 1) * 8;
+            const int kb = ks * 32 + tig * 4 + (reg >> 1) * 16;
+            const int o = mt * kI8OPT + (row >> 3), a = row & 7;
+            uint32_t v = 0;
+            if (o < O) {
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    const int q = kb + t;
+                    if (q < Q) {
+                        const uint64_t mv = masks[((size_t)o * Q + q) * ROW + ((size_t)k << logn) + n];
+                        v |= (uint32_t)((mv >> (8 * a)) & 0xFF) << (8 * t);
+                    }
+                }
+            }
+            w[reg] = v;
+        }
+        reinterpret_cast<uint4 *>(ib)[(((r1 * MT + mt) * nks + ks) << 5) + lane] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+template <int L, int LOGN, int NKS>
+__global__ void __launch_bounds__(256, UH_IMMA8_MINB)
+    k_hoisted_imma8(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, const uint64_t *__restrict__ D,
+                    const uint4 *__restrict__ ib, const uint64_t *__restrict__ kbank, const int32_t *__restrict__ shifts,
+                    int B, int I, int T, int O, int sp, const Mod *__restrict__ mods) {
+    using C = IW8;
+    constexpr int W = C::W;
+    constexpr int kIRow = C::ROWB;
+    constexpr int LP = L + 1;
+    constexpr uint32_t N = 1u << LOGN, half = N >> 1;
+    constexpr uint32_t ROW = (uint32_t)LP << LOGN;
+    extern __shared__ __align__(16) unsigned char ism[];
+    int *cst = reinterpret_cast<int *>(ism + (size_t)C::NC * C::COEF);
+    __shared__ uint32_t s_x[32 * NKS], s_d[32 * NKS], s_k[32 * NKS], s_r[32 * NKS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b0 = blockIdx.x * kICT;
+    const uint32_t n0 = blockIdx.y * C::NC;
+    const int slot = blockIdx.z;  // 0: q_0, 1: P
+    const int k = slot ? L : 0;   // QP-basis limb
+    const bool qlimb = slot == 0;
+    const Mod m = mods[qlimb ? 0 : sp];
+    const uint64_t P = mods[sp].q;
+    const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
+    const int Q = I * T;
+    for (int q = tid; q < Q; q += blockDim.x) {
+        const int i = q / T, t = q - i * T;
+        s_x[q] = (uint32_t)i * (uint32_t)B * (2u * L << LOGN);
+        s_d[q] = (uint32_t)i * (uint32_t)B * ((uint32_t)L * LP << LOGN);
+        s_k[q] = (uint32_t)t * ((uint32_t)LP * 2 * L << LOGN);
+        s_r[q] = (uint32_t)shifts[t];
+    }
+    __syncthreads();
+
+    // ---- phase A: canonical P * rot(ct) per (term, ciphertext pair, coefficient) -> 8 byte planes ----
+    {
+        constexpr int LH = 2 * C::NC;
+        for (int it = tid; it < Q * LH; it += 256) {
+            const int q = it / LH, cp = (it / C::NC) & 1, cf = it % C::NC;
+            const int ba = b0 + 2 * cp;
+            const bool oka = ba < B, okb = ba + 1 < B;
+            const uint32_t n = n0 + cf;
+            uint64_t v[2][2] = {{0, 0}, {0, 0}};
+            const uint32_t r = s_r[q];
+            const uint64_t *c0a = X + s_x[q] + (((uint32_t)ba * 2 * L + k) << LOGN);
+            const uint64_t *c0b = c0a + ((uint32_t)(2 * L) << LOGN);
+            if (r == 0) {
+                if (oka && qlimb) {
+                    v[0][0] = mulmod(Pk, __ldg(c0a + n), m);
+                    v[0][1] = mulmod(Pk, __ldg(c0a + ((uint32_t)L << LOGN) + n), m);
+                }
+                if (okb && qlimb) {
+                    v[1][0] = mulmod(Pk, __ldg(c0b + n), m);
+                    v[1][1] = mulmod(Pk, __ldg(c0b + ((uint32_t)L << LOGN) + n), m);
+                }
+            } else if (oka) {
+                const uint32_t src = rot_index_i(n, half, r);
+                const uint64_t *Da = D + s_d[q] + (((uint32_t)ba * L * LP + k) << LOGN) + src;
+                const uint64_t *Db = Da + ((uint32_t)(L * LP) << LOGN);
+                const uint64_t *K = kbank + s_k[q] + ((uint32_t)k * 2 * L << LOGN) + n;
+                uint64_t da[L], db[L], x[L], y[L];
+#pragma unroll
+                for (int j = 0; j < L; j++) {
+                    x[j] = __ldg(K + ((uint32_t)(2 * j) << LOGN));
+                    y[j] = __ldg(K + ((uint32_t)(2 * j + 1) << LOGN));
+                    da[j] = __ldg(Da + (uint32_t)j * ROW);
+                    db[j] = okb ? __ldg(Db + (uint32_t)j * ROW) : 0;
+                }
+                Acc a0, a1, e0, e1;
+                a0.zero();
+                a1.zero();
+                e0.zero();
+                e1.zero();
+#pragma unroll
+                for (int j = 0; j < L; j++) {
+                    a0.mac(da[j], x[j]);
+                    a1.mac(da[j], y[j]);
+                    e0.mac(db[j], x[j]);
+                    e1.mac(db[j], y[j]);
+                }
+                if (qlimb) {
+                    a0.mac(Pk, __ldg(c0a + src));
+                    if (okb) e0.mac(Pk, __ldg(c0b + src));
+                }
+                v[0][0] = a0.reduce(m);
+                v[0][1] = a1.reduce(m);
+                if (okb) {
+                    v[1][0] = e0.reduce(m);
+                    v[1][1] = e1.reduce(m);
+                }
+            }
+            unsigned char *pl = ism + cf * C::COEF + (4 * cp) * kIRow + q;
+#pragma unroll
+            for (int bb = 0; bb < W; bb++)
+#pragma unroll
+                for (int e = 0; e < 4; e++) pl[bb * kIJ * kIRow + e * kIRow] = (unsigned char)(v[e >> 1][e & 1] >> (8 * bb));
+        }
+    }
+    __syncthreads();
+
+    // ---- phase B: IMMA per (coefficient, m-tile), staged recombination, reduction ----
+    const int gid = lane >> 2, tig = lane & 3;
+    int *cw = cst + warp * 16 * C::CS;
+    const int nmt = imma8_mtiles(O);
+    for (int u = warp; u < C::NC * nmt; u += 8) {
+        const int cf = u / nmt, mt = u - cf * nmt;
+        const uint32_t n = n0 + cf;
+        const uint4 *af = ib + ((((size_t)slot * N + n) * nmt + mt) * NKS << 5) + lane;
+        uint4 A[NKS];
+#pragma unroll
+        for (int ks = 0; ks < NKS; ks++) A[ks] = __ldg(af + (ks << 5));
+        int Cr[W][4];
+#pragma unroll
+        for (int nb = 0; nb < W; nb++) Cr[nb][0] = Cr[nb][1] = Cr[nb][2] = Cr[nb][3] = 0;
+        const unsigned char *bp = ism + cf * C::COEF + gid * kIRow + tig * 4;
+#pragma unroll
+        for (int ks = 0; ks < NKS; ks++)
+#pragma unroll
+            for (int nb = 0; nb < W; nb++) {
+                const unsigned char *p = bp + nb * kIJ * kIRow + ks * 32;
+                imma(Cr[nb], A[ks], *reinterpret_cast<const uint32_t *>(p),
+                     *reinterpret_cast<const uint32_t *>(p + 16));
+            }
+#pragma unroll
+        for (int nb = 0; nb < W; nb++) {
+            const int col = nb * 8 + tig * 2;
+            *reinterpret_cast<int2 *>(cw + gid * C::CS + stage8_col(gid, col)) = make_int2(Cr[nb][0], Cr[nb][1]);
+            *reinterpret_cast<int2 *>(cw + (gid + 8) * C::CS + stage8_col(gid + 8, col)) =
+                make_int2(Cr[nb][2], Cr[nb][3]);
+        }
+        __syncwarp();
+        {
+            // lane pair (2 pr, 2 pr + 1): output 2 mt + ol, column j; half h sums mask bytes 4h..4h+3
+            const int pr = lane >> 1, h = lane & 1;
+            const int ol = pr >> 3, j = pr & 7;
+            uint32_t Ts[11];
+#pragma unroll
+            for (int s2 = 0; s2 < 11; s2++) Ts[s2] = 0;
+#pragma unroll
+            for (int a4 = 0; a4 < 4; a4++)
+#pragma unroll
+                for (int nb = 0; nb < W; nb++) {
+                    const int row = ol * 8 + 4 * h + a4;
+                    Ts[a4 + nb] += (uint32_t)cw[row * C::CS + stage8_col(row, nb * 8 + j)];
+                }
+            // value of this half = 2^(32 h) sum_s Ts[s] 2^(8 s)  (Ts < 2^25: the half sum < 2^106)
+            u128 v = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < 11; s2++) v += (u128)Ts[s2] << (8 * s2);
+            v <<= 32 * h;
+            uint64_t lo = (uint64_t)v, hi = (uint64_t)(v >> 64);
+            const uint64_t lo2 = __shfl_xor_sync(0xffffffffu, lo, 1), hi2 = __shfl_xor_sync(0xffffffffu, hi, 1);
+            lo += lo2;
+            hi += hi2 + (lo < lo2);
+            const int o = mt * kI8OPT + ol, b = b0 + (j >> 1);
+            if (h == 0 && o < O && b < B)
+                acc_out[((((uint32_t)o * B + b) * 2 + (j & 1)) * LP + k) * N + n] = reduce128(hi, lo, m);
+        }
+        __syncwarp();
+    }
+}
+
+template <int L, int NKS>
+void launch_imma8_k(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib8,
+                    const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
+    smem_optin(k_hoisted_imma8<L, 15, NKS>, IW8::SMEM);
+    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / IW8::NC), 2);
+    k_hoisted_imma8<L, 15, NKS><<<grid, 256, IW8::SMEM, s>>>(acc, X, D, reinterpret_cast<const uint4 *>(ib8), kbank,
+                                                             shifts, B, I, T, O, c.sp(), c.d_mods);
+    UH_LAUNCH_CHECK();
+}
+
+template <int L>
+void launch_imma8(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib8,
+                  const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
+    const int nks = (I * T + 31) / 32;
+    if (nks <= 1) launch_imma8_k<L, 1>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
+    else if (nks == 2) launch_imma8_k<L, 2>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
+    else if (nks == 3) launch_imma8_k<L, 3>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
+    else launch_imma8_k<L, 4>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
+}
+
+// the 60-bit limbs on the 8-byte IMMA kernel: every term count up to 128, q_0 and P below 2^60
+bool imma8_ok(const Ctx &c, int Q) {
+    if (Q > kI8MaxTerms) return false;
+    const char *e = getenv("UH_IMMA8");
+    if (e && e[0] == '0') return false;
+    return !(c.h_q[0] >> 60) && !(c.h_q[c.count - 1] >> 60);
+}
+
 }  // namespace
 
 // Applicable when N = 2^15, the level has 40-bit limbs q_1..q_{L-1} (< 2^40) and 60-bit
@@ -334,9 +599,14 @@ bool hoisted_imma_supported(const Ctx &c, int level, int O, int Q) {
 }
 
 // uint32 words of the 40-bit-limb bank
-size_t imma_bank_words(const Ctx &c, int level, int O, int Q) {
+static size_t imma_bank5_words(const Ctx &c, int level, int O, int Q) {
     const int nks = (Q + 31) / 32;
     return (size_t)level * imma_mtiles(O) * c.n * nks * 32 * 4;
+}
+// the whole bank: the 40-bit limbs' part, then (when the 60-bit limbs run the 8-byte kernel) q_0 / P's
+size_t imma_bank_words(const Ctx &c, int level, int O, int Q) {
+    const int nks = (Q + 31) / 32;
+    return imma_bank5_words(c, level, O, Q) + (imma8_ok(c, Q) ? (size_t)2 * imma8_mtiles(O) * c.n * nks * 32 * 4 : 0);
 }
 
 void imma_mask_bank(const Ctx &c, uint32_t *ib, const uint64_t *masks, int O, int Q, int level, cudaStream_t s) {
@@ -345,6 +615,12 @@ void imma_mask_bank(const Ctx &c, uint32_t *ib, const uint64_t *masks, int O, in
     k_imma_bank<5><<<(unsigned)std::min<size_t>((t5 + 255) / 256, 148 * 32), 256, 0, s>>>(ib, masks, O, Q, L,
                                                                                          (int)c.logn, nks);
     UH_LAUNCH_CHECK();
+    if (imma8_ok(c, Q)) {
+        const size_t t8 = (size_t)2 * c.n * imma8_mtiles(O) * nks * 32;
+        k_imma_bank8<<<(unsigned)std::min<size_t>((t8 + 255) / 256, 148 * 32), 256, 0, s>>>(
+            ib + imma_bank5_words(c, level, O, Q), masks, O, Q, L, (int)c.logn, nks);
+        UH_LAUNCH_CHECK();
+    }
 }
 
 void hoisted_mac_bank_wide(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
@@ -366,10 +642,31 @@ void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint
     // vs 13.6 ms at the LeNet conv2 shape: its 2-4-coefficient tiles cannot coalesce phase A's loads),
     // in groups of <= 12 outputs (its register tile); the 40-bit limbs take every output in one pass,
     // so their key switching (phase A) is done once for all of them
-    const size_t LPN = (size_t)(L + 1) * c.n;
-    for (int o0 = 0; o0 < O; o0 += 12)
-        hoisted_mac_bank_wide(c, acc + (size_t)o0 * B * 2 * LPN, X, D, masks + (size_t)o0 * I * T * LPN, kbank, shifts,
-                              B, I, T, std::min(12, O - o0), level, s);
+    // -- or, for <= 128 terms, on the 8-byte IMMA kernel (every output in one pass)
+    if (imma8_ok(c, I * T)) {
+        const uint32_t *ib8 = ib + imma_bank5_words(c, level, O, I * T);
+#define UH_IMMA8_CASE(LL)                                                    \
+    case LL:                                                                 \
+        launch_imma8<LL>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);   \
+        break;
+        switch (L) {
+            UH_IMMA8_CASE(3)
+            UH_IMMA8_CASE(4)
+            UH_IMMA8_CASE(5)
+            UH_IMMA8_CASE(6)
+            UH_IMMA8_CASE(7)
+            UH_IMMA8_CASE(8)
+            UH_IMMA8_CASE(9)
+            UH_IMMA8_CASE(10)
+            default: throw std::invalid_argument("IMMA hoisted kernel: 3 <= level + 1 <= 10");
+        }
+#undef UH_IMMA8_CASE
+    } else {
+        const size_t LPN = (size_t)(L + 1) * c.n;
+        for (int o0 = 0; o0 < O; o0 += 12)
+            hoisted_mac_bank_wide(c, acc + (size_t)o0 * B * 2 * LPN, X, D, masks + (size_t)o0 * I * T * LPN, kbank,
+                                  shifts, B, I, T, std::min(12, O - o0), level, s);
+    }
 #define UH_IMMA_CASE(LL)                                                    \
     case LL:                                                                \
         launch_imma<LL, 5>(c, acc, X, D, ib, kbank, shifts, B, I, T, O, s); \

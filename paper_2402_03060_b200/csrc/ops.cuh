@@ -95,6 +95,7 @@ void hoisted_mac_bank(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint
 // hoist_imma.cu: the weight-mask contraction of the dense 5..12-output layers on the tensor
 // cores (u8 byte-split IMMA) for the 40-bit limbs; the 60-bit limbs stay on the IMAD kernel
 bool hoisted_imma_supported(const Ctx &c, int level, int O, int Q);
+size_t imma_bank_words(const Ctx &c, int level, int O, int Q);
 void imma_mask_bank(const Ctx &c, uint32_t *ib, const uint64_t *masks, int O, int Q, int level, cudaStream_t s);
 void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
                       const uint32_t *ib, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O,

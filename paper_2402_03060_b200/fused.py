@@ -162,9 +162,10 @@ def imma_bank(backend, masks: torch.Tensor, O: int, Q: int, level: int, cache: b
     hit = banks.get(ck) if cache else None
     if hit is not None and hit[0] is _persistent(masks):
         return hit[1]
-    nks = (Q + 31) // 32
-    # 40-bit limbs q_1..q_level: ceil(O / 3) m-tiles of 3 outputs x 5 bytes (q_0 and P stay on the IMAD kernel)
-    ib = torch.empty(((O + 2) // 3 * level * backend.n * nks * 32 * 4,), dtype=torch.int32, device=backend.device)
+    # 40-bit limbs q_1..q_level: ceil(O / 3) m-tiles of 3 outputs x 5 bytes; then q_0 / P: ceil(O / 2)
+    # m-tiles of 2 outputs x 8 bytes (when they run the 8-byte kernel)
+    words = int(_lib.load().uh_imma_bank_words(backend._ctx, level, O, Q))
+    ib = torch.empty((words,), dtype=torch.int32, device=backend.device)
     backend._call("uh_imma_mask_bank", _vp(ib), _vp(masks), O, Q, level, backend._stream())
     if cache:
         banks[ck] = (_persistent(masks), ib)
