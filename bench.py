@@ -338,10 +338,10 @@ def _hbm_peak():
 
 def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
     """Roofline of the dominant kernel call: the conv2 hoisted MAC (k_hoisted_imma on the 40-bit
-    limbs + k_hoisted_bank on q_0 and P), against the pipes it runs on (a mixed bound):
-    phase A on the 40-bit limbs at the narrow-operand MAC peak, phase A and phase B of the 60-bit
-    limbs at the 128-bit MAC peak, phase B of the 40-bit limbs as 25 u8 byte products per modMAC
-    at the measured IMMA (mma.sync) MAC peak."""
+    limbs + k_hoisted_imma8 on q_0 and P), against the pipes it runs on (a mixed bound): phase A
+    on the 40-bit limbs at the narrow-operand MAC peak, phase A of the 60-bit limbs at the 128-bit
+    MAC peak, phase B as 25 (40-bit) / 64 (60-bit) u8 byte products per modMAC at the measured
+    IMMA (mma.sync) MAC peak."""
     calls = [t for t in timers if t[0] == "conv_hoisted_mac"]
     if not calls:
         return None
@@ -356,6 +356,9 @@ def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
     if w["path"] == "tc":
         parts = {"phase_a_40bit_narrow_imad": w["a40"] / r_narrow, "phase_a_60bit_imad": w["a60"] / r_mac,
                  "phase_b_tcgen05_i8": (25 * w["b40"] + 64 * w["b60"]) / r_tc}
+    elif w["path"] == "imma8":
+        parts = {"phase_a_40bit_narrow_imad": w["a40"] / r_narrow, "phase_a_60bit_imad": w["a60"] / r_mac,
+                 "phase_b_imma": (25 * w["b40"] + 64 * w["b60"]) / r_imma}
     elif w["path"] == "imma":
         parts = {"phase_a_40bit_narrow_imad": w["a40"] / r_narrow, "q0_P_imad": (w["a60"] + w["b60"]) / r_mac,
                  "phase_b_40bit_imma": 25 * w["b40"] / r_imma}
@@ -375,7 +378,8 @@ def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
             "kernel": (f"LeNet conv2 hoisted MAC call, level {lev}: k_hoisted_tc (tcgen05 kind::i8, TMEM "
                        f"accumulators; 40-bit q_1..q_{lev} and 60-bit q_0, P)") if w["path"] == "tc" else
                       (f"LeNet conv2 hoisted MAC call, level {lev}: k_hoisted_imma (40-bit q_1..q_{lev}) + "
-                       f"k_hoisted_bank (60-bit q_0, P)"),
+                       + ("k_hoisted_imma8 (60-bit q_0, P; 8-byte IMMA)" if w["path"] == "imma8"
+                          else "k_hoisted_bank (60-bit q_0, P)")),
             "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "T modMAC/s", "frac": achieved / peak,
             "traffic": traffic, "launch_ms": tms, "bound_ms": t_bound * 1e3,
             "bound_ms_parts": {k: v * 1e3 for k, v in parts.items()},

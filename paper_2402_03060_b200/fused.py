@@ -282,7 +282,8 @@ def conv_mac_work(shifts, half, n, B, I, O, level, path) -> dict:
 
     ``a40``/``b40``: the 40-bit limbs q_1..q_level; ``a60``/``b60``: the 60-bit q_0 and P.
     ``path``: "tc" (tcgen05: b40 as 25 and b60 as 64 u8 byte products per modMAC on the tensor
-    cores), "imma" (mma.sync: b40 on the tensor cores, q_0 / P on IMAD) or "imad"."""
+    cores), "imma8" (mma.sync: b40 and b60 on the tensor cores, both phase A on IMAD), "imma"
+    (mma.sync: b40 on the tensor cores, q_0 / P on IMAD) or "imad"."""
     T = len(shifts)
     nz = sum(1 for s in shifts if s % half)
     L = level + 1
@@ -362,8 +363,11 @@ def conv(backend, state: CipherState, layer) -> CipherState:
     if timer is not None:
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(torch.cuda.current_stream(backend.device))
-        timer.append(("conv_hoisted_mac", level, t0, t1, conv_mac_work(shifts, backend.params.num_slots, n, B, I,
-                                                                           O, level, "tc" if tc else ("imma" if imma else "imad"))))
+        # imma8: q_0 / P contracted on the 8-byte IMMA kernel too (hoist_imma.cu imma8_ok: <= 128 terms)
+        path = "tc" if tc else (("imma8" if I * T <= 128 and os.environ.get("UH_IMMA8", "1") != "0" else "imma")
+                                if imma else "imad")
+        timer.append(("conv_hoisted_mac", level, t0, t1,
+                      conv_mac_work(shifts, backend.params.num_slots, n, B, I, O, level, path)))
     del D
     out = backend._empty(O, B, 2, level, n)  # ModDown + rescale as one centred division by q_level * P
     backend._call("uh_divide_top2", _vp(out), _vp(acc), O * B * 2, level, level, LP, st)
