@@ -197,7 +197,7 @@ int uh_hoisted_mac_bank(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, 
  * outputs and <= 256 terms (LeNet conv2, the CIFAR-shape convs; layers.py:134-197):
  * the weight-mask contraction runs as byte-split u8 IMMA (exact; residues identical
  * to uh_hoisted_mac_bank) on the 40-bit limbs (5-byte operands), every output in
- * one pass; q_0 and P (below 2^60) run 8-byte IMMA for <= 128 terms, else the IMAD
+ * one pass; q_0 and P run 8-byte IMMA when both are below 2^60, else the IMAD
  * kernel from `masks` (<= 12 outputs per launch).  `ib` is the A-fragment mask bank
  * made once per layer by uh_imma_mask_bank from the uint64 mask bank
  * (uh_imma_bank_words uint32 words).  uh_imma_supported: 1 when the shape and the

@@ -326,7 +326,7 @@ void launch_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t 
 
 // ---------------------------------------------------------------------------
 // The 60-bit limbs q_0 and P: the same contraction with 8-byte operands.  Canonical residues
-// below 2^60 and <= 128 terms keep sum_q M V < 2^127, so the 64 byte products of each
+// below 2^60 and <= 256 terms keep sum_q M V <= 256 (q - 1)^2 < 2^128, so the 64 byte products of each
 // (output, column) recombine exactly in 128 bits.  An m-tile is 2 outputs x 8 mask bytes; n-tiles
 // are the 8 value bytes.  Phase A is hoist_bank.cu's 60-bit key switch (128-bit accumulators);
 // the epilogue stages each warp's C fragments in shared memory and recombines every (output,
@@ -337,13 +337,16 @@ void launch_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t 
 #ifndef UH_IMMA8_MINB
 #define UH_IMMA8_MINB 3
 #endif
-constexpr int kI8MaxTerms = 128;
+#ifndef UH_IMMA8_NC_WIDE
+#define UH_IMMA8_NC_WIDE 2  // past 4 k-steps (3 CTAs / SM)
+#endif
+constexpr int kI8MaxTerms = 256;  // (q - 1)^2 * 256 < 2^128 for q < 2^60
 constexpr int kI8OPT = 2;
 __host__ __device__ constexpr int imma8_mtiles(int O) { return (O + kI8OPT - 1) / kI8OPT; }
-struct IW8 {
+template <int NKS> struct IW8 {
     static constexpr int W = 8;
-    static constexpr int NC = UH_IMMA8_NC;
-    static constexpr int ROWB = 144;                     // 128 terms + pad (word stride 4 mod 8)
+    static constexpr int NC = NKS > 4 ? UH_IMMA8_NC_WIDE : UH_IMMA8_NC;
+    static constexpr int ROWB = NKS > 4 ? 32 * NKS + 16 : 144;  // terms + pad (word stride 4 mod 8)
     static constexpr int COEF = W * kIJ * ROWB + 4;
     // C staging: 16 rows x 64 columns per warp, the 8-column groups of row r rotated by 8 g(r),
     // g(4 q + i) = (i + q) mod 4 -- a Latin square, so both the fragment stores (4 consecutive rows
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(256, UH_IMMA8_MINB)
     k_hoisted_imma8(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, const uint64_t *__restrict__ D,
                     const uint4 *__restrict__ ib, const uint64_t *__restrict__ kbank, const int32_t *__restrict__ shifts,
                     int B, int I, int T, int O, int sp, const Mod *__restrict__ mods) {
-    using C = IW8;
+    using C = IW8<NKS>;
     constexpr int W = C::W;
     constexpr int kIRow = C::ROWB;
     constexpr int LP = L + 1;
@@ -561,9 +564,10 @@ __global__ void __launch_bounds__(256, UH_IMMA8_MINB)
 template <int L, int NKS>
 void launch_imma8_k(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib8,
                     const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
-    smem_optin(k_hoisted_imma8<L, 15, NKS>, IW8::SMEM);
-    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / IW8::NC), 2);
-    k_hoisted_imma8<L, 15, NKS><<<grid, 256, IW8::SMEM, s>>>(acc, X, D, reinterpret_cast<const uint4 *>(ib8), kbank,
+    using C = IW8<NKS>;
+    smem_optin(k_hoisted_imma8<L, 15, NKS>, C::SMEM);
+    dim3 grid((unsigned)((B + kICT - 1) / kICT), (unsigned)(c.n / C::NC), 2);
+    k_hoisted_imma8<L, 15, NKS><<<grid, 256, C::SMEM, s>>>(acc, X, D, reinterpret_cast<const uint4 *>(ib8), kbank,
                                                              shifts, B, I, T, O, c.sp(), c.d_mods);
     UH_LAUNCH_CHECK();
 }
@@ -575,7 +579,11 @@ void launch_imma8(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t
     if (nks <= 1) launch_imma8_k<L, 1>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
     else if (nks == 2) launch_imma8_k<L, 2>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
     else if (nks == 3) launch_imma8_k<L, 3>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
-    else launch_imma8_k<L, 4>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
+    else if (nks == 4) launch_imma8_k<L, 4>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
+    else if (nks == 5) launch_imma8_k<L, 5>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
+    else if (nks == 6) launch_imma8_k<L, 6>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
+    else if (nks == 7) launch_imma8_k<L, 7>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
+    else launch_imma8_k<L, 8>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);
 }
 
 // the 60-bit limbs on the 8-byte IMMA kernel: every term count up to 128, q_0 and P below 2^60
@@ -642,7 +650,7 @@ void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint
     // vs 13.6 ms at the LeNet conv2 shape: its 2-4-coefficient tiles cannot coalesce phase A's loads),
     // in groups of <= 12 outputs (its register tile); the 40-bit limbs take every output in one pass,
     // so their key switching (phase A) is done once for all of them
-    // -- or, for <= 128 terms, on the 8-byte IMMA kernel (every output in one pass)
+    // -- or on the 8-byte IMMA kernel (every output in one pass)
     if (imma8_ok(c, I * T)) {
         const uint32_t *ib8 = ib + imma_bank5_words(c, level, O, I * T);
 #define UH_IMMA8_CASE(LL)                                                    \

@@ -363,9 +363,8 @@ def conv(backend, state: CipherState, layer) -> CipherState:
     if timer is not None:
         t1 = torch.cuda.Event(enable_timing=True)
         t1.record(torch.cuda.current_stream(backend.device))
-        # imma8: q_0 / P contracted on the 8-byte IMMA kernel too (hoist_imma.cu imma8_ok: <= 128 terms)
-        path = "tc" if tc else (("imma8" if I * T <= 128 and os.environ.get("UH_IMMA8", "1") != "0" else "imma")
-                                if imma else "imad")
+        # imma8: q_0 / P contracted on the 8-byte IMMA kernel too (hoist_imma.cu imma8_ok)
+        path = "tc" if tc else (("imma8" if os.environ.get("UH_IMMA8", "1") != "0" else "imma") if imma else "imad")
         timer.append(("conv_hoisted_mac", level, t0, t1,
                       conv_mac_work(shifts, backend.params.num_slots, n, B, I, O, level, path)))
     del D
