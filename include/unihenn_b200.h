@@ -193,6 +193,19 @@ int uh_hoisted_mac_bank(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, 
                         const uint64_t *masks, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T,
                         int O, int diag, int level, void *stream);
 
+/* One masked output (the flatten stages, layers.py:281-339) with the masks folded into the
+ * key bank: uh_km_bank makes km[Q][level+2][2*(level+1)+1][N] from the mask bank
+ * [Q][level+2][N] and the key bank (rows 2j + c of entry q = masks[q] (.) key row of the term's
+ * shift, t = q mod T for dense terms and q otherwise; row 2*(level+1) = masks[q] * P on the
+ * q-limbs), once per layer.  uh_hoisted_mac_km then needs 2*(level+1) + 1 multiply-accumulates
+ * per term and no per-term reduction; acc[1][B][2][level+2][N] is residue-identical to
+ * uh_hoisted_mac_bank with O = 1.  Supported when uh_hoisted_bank_supported(ctx, level, 1). */
+int uh_km_supported(uh_ctx *ctx, int level);
+int uh_km_bank(uh_ctx *ctx, uint64_t *km, const uint64_t *masks, const uint64_t *kbank, const int32_t *shifts, int Q,
+               int T, int diag, int level, void *stream);
+int uh_hoisted_mac_km(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D, const uint64_t *km,
+                      const int32_t *shifts, int B, int I, int T, int diag, int level, void *stream);
+
 /* Tensor-core variant of uh_hoisted_mac_bank for dense masked layers with 5..48
  * outputs and <= 256 terms (LeNet conv2, the CIFAR-shape convs; layers.py:134-197):
  * the weight-mask contraction runs as byte-split u8 IMMA (exact; residues identical

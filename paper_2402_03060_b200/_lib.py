@@ -54,6 +54,8 @@ SIGNATURES = {
                        _vp],
     "uh_hoisted_mac_bank": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int,
                             _vp],
+    "uh_km_bank": [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp],
+    "uh_hoisted_mac_km": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_imma_mask_bank": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp],
     "uh_tc_mask_bank": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp],
     "uh_hoisted_mac_tc": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
@@ -63,6 +65,7 @@ SIGNATURES = {
 EXTRA = {"uh_abi_version": ([], _c_int), "uh_last_error": ([], ctypes.c_char_p),
          "uh_launch_count": ([], ctypes.c_ulonglong), "uh_bench_peaks": ([_vp, _vp], _c_int),
          "uh_hoisted_bank_supported": ([_vp, _c_int, _c_int], _c_int),
+         "uh_km_supported": ([_vp, _c_int], _c_int),
          "uh_imma_supported": ([_vp, _c_int, _c_int, _c_int], _c_int),
          "uh_imma_bank_words": ([_vp, _c_int, _c_int, _c_int], ctypes.c_ulonglong),
          "uh_tc_supported": ([_vp, _c_int, _c_int, _c_int], _c_int),

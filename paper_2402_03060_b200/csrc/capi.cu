@@ -366,6 +366,36 @@ __attribute__((visibility("default"))) int uh_hoisted_mac_bank(uh_ctx *ctx, uint
     });
 }
 
+__attribute__((visibility("default"))) int uh_km_supported(uh_ctx *ctx, int level) {
+    return ctx && uh::hoisted_bank_supported(C(ctx), level, 1) ? 1 : 0;
+}
+
+__attribute__((visibility("default"))) int uh_km_bank(uh_ctx *ctx, uint64_t *km, const uint64_t *masks,
+                                                      const uint64_t *kbank, const int32_t *shifts, int Q, int T,
+                                                      int diag, int level, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(Q > 0 && T > 0 && diag >= 0 && diag <= 2, "bad shape");
+        need(km && masks && kbank && shifts, "null operand");
+        uh::km_bank(c, km, masks, kbank, shifts, Q, T, diag, level, S(stream));
+    });
+}
+
+__attribute__((visibility("default"))) int uh_hoisted_mac_km(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls,
+                                                             const uint64_t *D, const uint64_t *km,
+                                                             const int32_t *shifts, int B, int I, int T, int diag,
+                                                             int level, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(B > 0 && I > 0 && T > 0 && xls == level + 1, "bad shape (xls must equal level + 1)");
+        need(diag >= 0 && diag <= 2, "term mode must be 0 (dense), 1 (diagonal) or 2 (block-diagonal)");
+        need(km != nullptr, "key-mask bank is required");
+        uh::hoisted_mac_km(c, acc, X, D, km, shifts, B, I, T, diag, level, S(stream));
+    });
+}
+
 __attribute__((visibility("default"))) int uh_imma_supported(uh_ctx *ctx, int level, int O, int Q) {
     return ctx && uh::hoisted_imma_supported(C(ctx), level, O, Q) ? 1 : 0;
 }

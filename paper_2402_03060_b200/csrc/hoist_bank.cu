@@ -258,13 +258,21 @@ __global__ void __launch_bounds__(W * 32, UH_BANK_MINB)
 // once into the per-term offset tables.  Warp w of the CTA serves ciphertext
 // 8 * blockIdx.x + w (ciphertext groups fastest in the grid: CTAs sharing the
 // same key and mask rows run together).
-template <int L, int LOGN, int OM, bool MASKS, int G, int MINB>
+//
+// PRE (one masked output): the bank is a key-mask bank km[Q][L+1][2L+1][N] (k_km_bank) whose entry
+// q holds the key rows of term q already multiplied by the term's mask, plus the row M_q * P, so
+//   acc = sum_q sum_j rot(D_j) (M_q K_{q,j}) + (M_q P) rot(c0)
+// needs no per-term reduction and no mask multiply: 2L + 1 MACs per term instead of 2L + 3 and two
+// reductions.  Same canonical residues as the masked form (the sums agree mod q_k).
+template <int L, int LOGN, int OM, bool MASKS, int G, int MINB, bool PRE = false>
 __global__ void __launch_bounds__(256, MINB)
     k_direct_bank(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, const uint64_t *__restrict__ D,
                   const uint64_t *__restrict__ masks, const uint64_t *__restrict__ kbank,
                   const int32_t *__restrict__ shifts, int B, int I, int T, int O, int diag, int sp,
                   const Mod *__restrict__ mods) {
+    static_assert(!PRE || (!MASKS && OM == 1), "key-mask bank: one output, masks folded into the bank");
     constexpr int LP = L + 1;
+    constexpr int KR = PRE ? 2 * L + 1 : 2 * L;  // rows per (entry, limb) of the bank
     constexpr uint32_t N = 1u << LOGN, half = N >> 1;
     constexpr uint32_t ROW = (uint32_t)LP << LOGN;
     __shared__ uint32_t s_x[kBankMaxTerms], s_d[kBankMaxTerms], s_k[kBankMaxTerms], s_r[kBankMaxTerms];
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__(256, MINB)
         }
         s_x[q] = (uint32_t)i * (uint32_t)B * (2u * L << LOGN);
         s_d[q] = (uint32_t)i * (uint32_t)B * ((uint32_t)L * LP << LOGN);
-        s_k[q] = (uint32_t)t * ((uint32_t)LP * 2 * L << LOGN);
+        s_k[q] = (uint32_t)(PRE ? q : t) * ((uint32_t)LP * KR << LOGN);
         s_r[q] = (uint32_t)shifts[t];
     }
     __syncthreads();
@@ -295,7 +303,7 @@ __global__ void __launch_bounds__(256, MINB)
     const uint64_t Pk = qlimb ? (P < m.q ? P : csub(barrett_lite(P, m), m.q)) : 0;
     const uint32_t xrow = ((uint32_t)b * 2 * L + k) << LOGN;
     const uint32_t drow = ((uint32_t)b * L * LP + k) << LOGN;
-    const uint32_t krow = (((uint32_t)(qlimb ? k : L)) * 2 * L << LOGN) + n;
+    const uint32_t krow = (((uint32_t)(qlimb ? k : L)) * KR << LOGN) + n;
     const uint64_t *mrow = masks + ((uint32_t)k << LOGN) + n;
 
     auto body = [&](auto acc_tag) {
@@ -308,7 +316,63 @@ __global__ void __launch_bounds__(256, MINB)
             acc[o][1].zero();
         }
         int since = 0;
-        for (int q = 0; q < Q; q++) {
+        if constexpr (!MASKS) {
+            // mask-free sums (and the key-mask bank): every term's MACs go straight into the running
+            // sums; these fold back below 2^64 before the accumulator can overflow (narrow: the
+            // x1 y1 word holds 2^14 products; wide: 256 products below 2^120)
+            constexpr int kBudget = NARROW ? 8192 : 240;
+            A &a0 = acc[0][0], &a1 = acc[0][1];
+            for (int q = 0; q < Q; q++) {
+                const uint32_t r = s_r[q];
+                const uint64_t *c0 = X + s_x[q] + xrow;
+                const uint64_t *K = kbank + s_k[q] + krow;
+                if (since + 2 * L + 1 > kBudget) {
+                    since = 0;
+                    uint64_t h, l;
+                    a0.value(h, l);
+                    a0.set(smallq ? fold64_b(h, l, m) : reduce128_lazy_b(h, l, m), 0);
+                    a1.value(h, l);
+                    a1.set(smallq ? fold64_b(h, l, m) : reduce128_lazy_b(h, l, m), 0);
+                }
+                since += 2 * L + 1;
+                if (r == 0) {
+                    if (qlimb) {
+                        const uint64_t pm = PRE ? __ldg(K + ((uint32_t)(2 * L) << LOGN)) : Pk;
+                        a0.mac(pm, __ldg(c0 + n));
+                        a1.mac(pm, __ldg(c0 + ((uint32_t)L << LOGN) + n));
+                    }
+                    continue;
+                }
+                const uint32_t src = rot_index_b(n, half, r);
+                const uint64_t *Dj = D + s_d[q] + drow + src;
+                uint64_t pm = Pk, cs = 0;
+                if (qlimb) {
+                    if (PRE) pm = __ldg(K + ((uint32_t)(2 * L) << LOGN));
+                    cs = __ldg(c0 + src);
+                }
+#pragma unroll
+                for (int j0 = 0; j0 < L; j0 += G) {
+                    uint64_t d[G], x[G], y[G];
+#pragma unroll
+                    for (int g = 0; g < G; g++) {
+                        if (j0 + g < L) {
+                            d[g] = __ldg(Dj + (uint32_t)(j0 + g) * ROW);
+                            x[g] = __ldg(K + ((uint32_t)(2 * (j0 + g)) << LOGN));
+                            y[g] = __ldg(K + ((uint32_t)(2 * (j0 + g) + 1) << LOGN));
+                        }
+                    }
+#pragma unroll
+                    for (int g = 0; g < G; g++) {
+                        if (j0 + g < L) {
+                            a0.mac(d[g], x[g]);
+                            a1.mac(d[g], y[g]);
+                        }
+                    }
+                }
+                if (qlimb) a0.mac(pm, cs);
+            }
+        }
+        for (int q = 0; MASKS && q < Q; q++) {
             uint64_t mk[OM];
             if (MASKS) {
 #pragma unroll
@@ -380,10 +444,6 @@ __global__ void __launch_bounds__(256, MINB)
                             acc[o][c].set(reduce128_lazy_b(h, l, m), 0);
                         }
                 }
-            } else {
-                // the term's 128-bit sums fold into the running 128-bit sum (up to 2^60 terms)
-                acc[0][0].add(smallq ? fold64_b(h0, l0, m) : reduce128_lazy_b(h0, l0, m));
-                acc[0][1].add(smallq ? fold64_b(h1, l1, m) : reduce128_lazy_b(h1, l1, m));
             }
         }
 #pragma unroll
@@ -433,6 +493,44 @@ void direct_bank_L(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_
     }
 }
 
+// Key-mask bank km[Q][L+1][2L+1][N] of a one-output masked layer: rows 2j + c of entry q are
+// M_q (.) K_{t(q)}[j][c] (zero for a zero shift), row 2L is M_q * P on the q-limbs (zero on P).
+// t(q) = q mod T for dense terms, q otherwise (diagonal / block-diagonal: one key entry per term).
+__global__ void k_km_bank(uint64_t *__restrict__ km, const uint64_t *__restrict__ masks,
+                          const uint64_t *__restrict__ kbank, const int32_t *__restrict__ shifts, int Q, int T,
+                          int diag, int L, int logn, int sp, const Mod *__restrict__ mods) {
+    const int LP = L + 1, KR = 2 * L + 1;
+    const size_t N = (size_t)1 << logn;
+    const size_t total = (size_t)Q * LP * KR * N;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t n = idx & (N - 1);
+        size_t r = idx >> logn;
+        const int row = (int)(r % KR);
+        r /= KR;
+        const int k = (int)(r % LP), q = (int)(r / LP);
+        const int t = diag == 0 ? q % T : q;
+        const Mod m = mods[k < L ? k : sp];
+        const uint64_t mk = masks[((size_t)q * LP + k) * N + n];
+        uint64_t v = 0;
+        if (row < 2 * L) {
+            if (shifts[t] != 0) v = mulmod(mk, kbank[(((size_t)t * LP + k) * 2 * L + row) * N + n], m);
+        } else if (k < L) {
+            const uint64_t P = mods[sp].q;
+            v = mulmod(mk, P < m.q ? P : csub(barrett_lite(P, m), m.q), m);
+        }
+        km[idx] = v;
+    }
+}
+
+template <int L>
+void launch_km(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *km,
+               const int32_t *shifts, int B, int I, int T, int diag, cudaStream_t s) {
+    dim3 grid((unsigned)((B + 7) / 8), (unsigned)(c.n / 32), L + 1);
+    k_direct_bank<L, 15, 1, false, UH_BANK_DIRECT_G, UH_BANK_DIRECT_MINB, true><<<grid, 256, 0, s>>>(
+        acc, X, D, nullptr, km, shifts, B, I, T, 1, diag, c.sp(), c.d_mods);
+    UH_LAUNCH_CHECK();
+}
+
 template <int L>
 void launch_bank(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
                  const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s,
@@ -465,6 +563,46 @@ void hoisted_mac_bank_wide(const Ctx &c, uint64_t *acc, const uint64_t *X, const
         case 10: launch_bank<10>(c, acc, X, D, masks, kbank, shifts, B, I, T, O, s, 1); break;
         default: throw std::invalid_argument("wide-limb hoisted kernel: 2 <= level + 1 <= 10");
     }
+}
+
+void km_bank(const Ctx &c, uint64_t *km, const uint64_t *masks, const uint64_t *kbank, const int32_t *shifts, int Q,
+             int T, int diag, int level, cudaStream_t s) {
+    const int L = level + 1;
+    const size_t total = (size_t)Q * (L + 1) * (2 * L + 1) * c.n;
+    const unsigned blocks = (unsigned)std::min<size_t>((total + 255) / 256, 148 * 32);
+    k_km_bank<<<blocks, 256, 0, s>>>(km, masks, kbank, shifts, Q, T, diag, L, (int)c.logn, c.sp(), c.d_mods);
+    UH_LAUNCH_CHECK();
+}
+
+// one masked output over a key-mask bank (every term mode): the register-only kernel, 2L + 1 MACs per term
+void hoisted_mac_km(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *km,
+                    const int32_t *shifts, int B, int I, int T, int diag, int level, cudaStream_t s) {
+    if (!hoisted_bank_supported(c, level, 1))
+        throw std::invalid_argument("key-mask bank kernel: needs N = 2^15, level + 1 <= 10");
+    const int Q = diag == 1 ? I : I * T;
+    if (Q > kBankMaxTerms) throw std::invalid_argument("key-mask bank kernel supports up to 512 terms");
+    if (diag == 1 && I != T) throw std::invalid_argument("diagonal terms need I == T");
+    const int L = level + 1;
+    const double lim = 4294967295.0;  // 32-bit element offsets inside the kernel
+    if ((double)I * B * 2 * L * c.n > lim || (double)I * B * L * (L + 1) * c.n > lim ||
+        (double)B * 2 * (L + 1) * c.n > lim || (double)Q * (L + 1) * (2 * L + 1) * c.n > lim)
+        throw std::invalid_argument("key-mask bank kernel operand exceeds 2^32 elements: split the batch");
+#define UH_KM_CASE(LL) \
+    case LL: launch_km<LL>(c, acc, X, D, km, shifts, B, I, T, diag, s); break;
+    switch (L) {
+        UH_KM_CASE(1)
+        UH_KM_CASE(2)
+        UH_KM_CASE(3)
+        UH_KM_CASE(4)
+        UH_KM_CASE(5)
+        UH_KM_CASE(6)
+        UH_KM_CASE(7)
+        UH_KM_CASE(8)
+        UH_KM_CASE(9)
+        UH_KM_CASE(10)
+        default: throw std::invalid_argument("key-mask bank kernel: level + 1 <= 10");
+    }
+#undef UH_KM_CASE
 }
 
 bool hoisted_bank_supported(const Ctx &c, int level, int O) {

@@ -21,6 +21,9 @@
 //                  mod q_k and the epilogue writes (in[p][k] - y) * q_top^-1.
 #include "ntt_fast.cuh"
 
+#ifndef UH_NTT_KP
+#define UH_NTT_KP 0
+#endif
 #ifndef UH_NTT_MINB
 #define UH_NTT_MINB 4  // min resident CTAs per SM requested from ptxas (register cap: 64)
 #endif
@@ -162,7 +165,13 @@ constexpr double kTwo52 = 4503599627370496.0;
 __device__ __forceinline__ double fmm(double y, double2 w, double q) {
     const double p = y * w.x;
     const double e = fma(y, w.x, -p);
+#if UH_NTT_KP == 1   // quotient from the rounded product: no w / q operand (experiment)
+    const double k = fma(p, 1.0 / q, kMagic) - kMagic;
+#elif UH_NTT_KP == 2  // rint instruction instead of the magic-number pair
+    const double k = rint(y * w.y);
+#else
     const double k = fma(y, w.y, kMagic) - kMagic;
+#endif
     return fma(-k, q, p) + e;
 }
 __device__ __forceinline__ void bf_ct(double &x, double &y, double2 w, double q) {

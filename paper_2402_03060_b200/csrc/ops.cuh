@@ -92,6 +92,13 @@ bool hoisted_bank_supported(const Ctx &c, int level, int O);
 void hoisted_mac_bank(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
                       const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O, int diag, int level,
                       cudaStream_t s);
+// one masked output with the masks folded into the key bank: km[Q][L+1][2L+1][N] (km_bank: rows
+// M_q K_{t(q)} and M_q P), 2L + 1 MACs per term and no per-term reduction; same residues as
+// hoisted_mac_bank with O = 1
+void km_bank(const Ctx &c, uint64_t *km, const uint64_t *masks, const uint64_t *kbank, const int32_t *shifts, int Q,
+             int T, int diag, int level, cudaStream_t s);
+void hoisted_mac_km(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *km,
+                    const int32_t *shifts, int B, int I, int T, int diag, int level, cudaStream_t s);
 // hoist_imma.cu: the weight-mask contraction of the dense 5..12-output layers on the tensor
 // cores (u8 byte-split IMMA) for the 40-bit limbs; the 60-bit limbs stay on the IMAD kernel
 bool hoisted_imma_supported(const Ctx &c, int level, int O, int Q);

@@ -172,6 +172,33 @@ def imma_bank(backend, masks: torch.Tensor, O: int, Q: int, level: int, cache: b
     return ib
 
 
+def _km_ok(backend, level: int) -> bool:
+    """One-output masked stages fold their masks into the key bank (hoist_bank.cu k_km_bank)."""
+    if os.environ.get("UH_KM_BANK", "1") == "0" or not _key_bank_ok(backend, level, 1):
+        return False
+    return backend.kernel_supported("uh_km_supported", level)
+
+
+def km_bank(backend, masks: torch.Tensor, kb: torch.Tensor, sh: torch.Tensor, Q: int, T: int, mode: int,
+            level: int, cache: bool = True) -> torch.Tensor:
+    """The key-mask bank [Q][level+2][2(level+1)+1][N] of a one-output mask bank [Q][level+2][N]
+    (uh_km_bank): every key row pre-multiplied by its term's mask, plus the row mask * P.
+
+    Cached like imma_bank: the entry keeps the mask bank's and the key bank's owning tensors alive,
+    so neither address can be reused while the entry exists."""
+    banks = backend.__dict__.setdefault("_km_banks", {})
+    ck = (masks.data_ptr(), tuple(masks.shape), kb.data_ptr(), sh.data_ptr(), Q, T, mode, level)
+    hit = banks.get(ck) if cache else None
+    if hit is not None and hit[0] is _persistent(masks) and hit[1] is kb:
+        return hit[2]
+    L = level + 1
+    km = backend._empty(Q, L + 1, 2 * L + 1, backend.n)
+    backend._call("uh_km_bank", _vp(km), _vp(masks), _vp(kb), _vp(sh), Q, T, mode, level, backend._stream())
+    if cache:
+        banks[ck] = (_persistent(masks), kb, km)
+    return km
+
+
 def key_bank(backend, shifts, level: int) -> torch.Tensor:
     """Galois keys of ``shifts`` re-laid for the key-bank kernel: [T][level+2][2(level+1)][N].
 
@@ -539,6 +566,14 @@ def _hoist(backend, X, level, shifts, masks, O, diag, B, taps=None):
         sh = _shift_table(backend, shifts)
         backend._call("uh_hoisted_mac_imma", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ib), _vp(kb), _vp(sh), B, I,
                       T, O, level, st)
+        del D
+        return acc
+    if masks is not None and O == 1 and _km_ok(backend, level):
+        kb = key_bank(backend, shifts, level)
+        sh = _shift_table(backend, shifts)
+        Q = I if mode == 1 else I * T
+        km = km_bank(backend, masks, kb, sh, Q, T, mode, level, cache=_banked(backend, masks))
+        backend._call("uh_hoisted_mac_km", _vp(acc), _vp(X), L, _vp(D), _vp(km), _vp(sh), B, I, T, mode, level, st)
         del D
         return acc
     if _key_bank_ok(backend, level, O) and (mode != 2 or O <= 4):

@@ -193,6 +193,55 @@ def test_key_bank_kernels_equal_generic_every_mode(O, with_masks, diag, monkeypa
     assert torch.equal(got, want)
 
 
+@pytest.mark.parametrize("diag,I,T", [(0, 2, 35), (2, 3, 12), (1, 3, 3), (0, 1, 4)])
+def test_key_mask_bank_kernel_equals_masked_kernel(diag, I, T, monkeypatch):
+    """One masked output over the key-mask bank (masks folded into the key rows, hoist_bank.cu
+    k_km_bank / k_direct_bank<PRE>) == the masked register-only kernel (oracle-pinned above), bit
+    for bit, in every term mode; enough terms that the running sums fold (wide limbs: 240 MACs)."""
+    be, o = _c2()
+    level, B = 3, 9
+    rng = np.random.default_rng(70 + diag + T)
+    if diag == 1:
+        shifts, taps, Q = [0, 5, -11], None, 3
+    elif diag == 2:
+        shifts = [int(x) for x in rng.choice(np.arange(1, 400), size=I * T, replace=False)]
+        shifts[5] = 0
+        taps, Q = T, I * T
+    else:
+        shifts = [0] + [int(x) for x in rng.choice(np.arange(1, 400), size=T - 1, replace=False)]
+        taps, Q = None, I * T
+    cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, C2.num_slots)))) for _ in range(I)]
+    X = fused.stack_cts(be, cts, level)
+    mdev = torch.from_numpy(_rand_masks(o, rng, 1, Q, level).view(np.int64)).to(be.device)
+    mode = 2 if diag == 2 else bool(diag)
+    monkeypatch.setenv("UH_KM_BANK", "1")
+    assert fused._km_ok(be, level)
+    from paper_2402_03060_b200 import _lib
+
+    launches = _lib.launch_count()
+    got = fused._hoist(be, X, level, shifts, mdev, 1, mode, B, taps=taps)
+    monkeypatch.setenv("UH_KM_BANK", "0")
+    want = fused._hoist(be, X, level, shifts, mdev, 1, mode, B, taps=taps)
+    assert torch.equal(got, want)
+    assert _lib.launch_count() > launches
+
+
+def test_long_unmasked_rotation_sum_folds(monkeypatch):
+    """An unmasked rotation sum long enough that the register-only kernel folds its running sums
+    (60 terms x 9 MACs > the 240-MAC budget of the 60-bit limbs) == the generic kernel."""
+    be, o = _c2()
+    level, B, I = 3, 3, 1
+    rng = np.random.default_rng(81)
+    shifts = [0] + [int(x) for x in rng.choice(np.arange(1, 300), size=59, replace=False)]
+    cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, C2.num_slots)))) for _ in range(I)]
+    X = fused.stack_cts(be, cts, level)
+    monkeypatch.setenv("UH_KEY_BANK", "1")
+    got = fused._hoist(be, X, level, shifts, None, 1, False, B)
+    monkeypatch.setenv("UH_KEY_BANK", "0")
+    want = fused._hoist(be, X, level, shifts, None, 1, False, B)
+    assert torch.equal(got, want)
+
+
 @pytest.mark.parametrize("O,level,I,shifts,B", [
     (12, 5, 4, [a + 28 * b for b in range(5) for a in range(5)], 5),   # LeNet conv2 shape, partial ct tile
     (7, 3, 3, [0, 1, 28, -29, 16383, 57, -2, 3, 700], 4),              # partial m-tile, Q = 27 (not / 4)
