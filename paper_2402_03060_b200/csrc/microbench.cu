@@ -207,6 +207,50 @@ __global__ void k_macn_peak(uint64_t *out, int iters, uint64_t seed) {
     if (s == 0x1234567812345678ull) out[0] = s;
 }
 
+// split-FP64 MAC for operands below 2^40: x = xh 2^20 + xl, w = wh 2^20 + wl (20-bit halves held
+// exactly in doubles); x w accumulates exactly in three FP64 sums (hh, mid, ll: 40-bit products,
+// 2^12 of them fit 53 bits) with 4 DFMA and no carries.  SPLIT: x arrives as a 64-bit integer and
+// is split per MAC (2 ALU + 2 DADD), w is pre-split (a bank operand); otherwise both are doubles.
+template <bool SPLIT>
+__global__ void k_fpsplit_peak(uint64_t *out, int iters, uint64_t seed) {
+    double hh[8], mm[8], ll[8];
+    uint64_t x[8];
+    constexpr uint64_t M40 = (1ull << 40) - 1;
+    const uint64_t w = (0x0FEDCBA987654321ull + blockIdx.x) & M40;
+    const double wh = (double)(w >> 20), wl = (double)(w & 0xFFFFF);
+    const double two52 = 4503599627370496.0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        hh[i] = mm[i] = ll[i] = 0.0;
+        x[i] = (seed + threadIdx.x * 8 + i) & M40;
+    }
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            double xh, xl;
+            if (SPLIT) {
+                xl = __longlong_as_double((long long)((x[i] & 0xFFFFF) | 0x4330000000000000ull)) - two52;
+                xh = __longlong_as_double((long long)((x[i] >> 20) | 0x4330000000000000ull)) - two52;
+            } else {
+                xl = __longlong_as_double((long long)x[i]);
+                xh = xl;
+            }
+            hh[i] = fma(xh, wh, hh[i]);
+            mm[i] = fma(xh, wl, mm[i]);
+            mm[i] = fma(xl, wh, mm[i]);
+            ll[i] = fma(xl, wl, ll[i]);
+            if (SPLIT)
+                x[i] ^= (uint64_t)__double_as_longlong(ll[i]) & M40;
+            else
+                x[i] ^= (uint64_t)__double_as_longlong(ll[i]) & 0x000FFFFF00000000ull;
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s += hh[i] + mm[i] + ll[i];
+    if (s == 0.123) out[0] = 1;
+}
+
 // u8 tensor-core MACs through the legacy warp-level path the engine uses (mma.sync m16n8k32
 // -> IMMA.16832): 8 independent accumulator tiles per warp, 16 * 8 * 32 MACs per instruction
 __global__ void k_imma_peak(uint64_t *out, int iters, uint32_t seed) {
@@ -326,7 +370,8 @@ template <class F> double time_ms(F &&launch) {
 // rates[0] = IMAD/s, [1] = 128-bit MAC/s, [2] = reduced mulmod/s (60-bit prime), [3] MAC128 plain-C
 // form, [4] lazy Shoup product, [5] exact FP64 modMAC, [6] mixed IMAD+FP64 MAC, [7] split-accumulator
 // MAC, [8] narrow-operand MAC (q < 2^41), [9] u8 IMMA MAC/s (mma.sync), [10] FP64 FMA/s,
-// [11] tcgen05 kind::i8 MAC/s
+// [11] tcgen05 kind::i8 MAC/s, [12] split-FP64 MAC (one operand split per MAC), [13] split-FP64 MAC
+// (both operands pre-split: 4 DFMA)
 void bench_peaks(const Ctx &c, double *rates) {
     int sms = 0;
     UH_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
@@ -367,6 +412,11 @@ void bench_peaks(const Ctx &c, double *rates) {
         ms = time_ms([&] { k_tc_peak<<<sms, 128>>>(out, ti); });
         rates[11] = (double)sms * ti * (128.0 * 256 * 32) / (ms * 1e-3);
     }
+    // rates[12]: split-FP64 MAC, one operand split per MAC; rates[13]: both operands pre-split
+    ms = time_ms([&] { k_fpsplit_peak<true><<<blocks, threads>>>(out, iters, 7ull); });
+    rates[12] = lanes * iters * 8 / (ms * 1e-3);
+    ms = time_ms([&] { k_fpsplit_peak<false><<<blocks, threads>>>(out, iters, 7ull); });
+    rates[13] = lanes * iters * 8 / (ms * 1e-3);
     UH_CHECK(cudaGetLastError());
     cudaFree(out);
 }
