@@ -221,6 +221,21 @@ int uh_imma_mask_bank(uh_ctx *ctx, uint32_t *ib, const uint64_t *masks, int O, i
 int uh_hoisted_mac_imma(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D,
                         const uint64_t *masks, const uint32_t *ib, const uint64_t *kbank, const int32_t *shifts,
                         int B, int I, int T, int O, int level, void *stream);
+/* uh_hoisted_mac_imma with the key switch of every term (phase A) on the tensor cores as well
+ * (40-bit limbs; layers.conv's rotate + key switch, layers.py:165-196 via he_backend.rotate,
+ * he_backend.py:249-253): the ModUp digits split into bytes, the byte weight 2^(8a) folded into
+ * the Galois key (again 5 bytes), so one u8 m16n8k32 per (term, coefficient, component) forms the
+ * key inner product of 16 ciphertexts; exact, residues identical to uh_hoisted_mac_imma.
+ * `kt` is the per-layer key bank in fragment order made once by uh_imma_ta_bank from the key
+ * bank (uh_imma_ta_bank_bytes bytes).  uh_imma_ta_supported: the uh_imma_supported shapes with
+ * 5 * (level + 1) <= 32 and Q <= 128 (LeNet conv2). */
+int uh_imma_ta_supported(uh_ctx *ctx, int level, int O, int Q);
+unsigned long long uh_imma_ta_bank_bytes(uh_ctx *ctx, int level, int T);
+int uh_imma_ta_bank(uh_ctx *ctx, uint8_t *kt, const uint64_t *kbank, const int32_t *shifts, int T, int level,
+                    void *stream);
+int uh_hoisted_mac_imma_ta(uh_ctx *ctx, uint64_t *acc, const uint64_t *X, int xls, const uint64_t *D,
+                           const uint32_t *ib, const uint8_t *kt, const uint64_t *kbank, const int32_t *shifts,
+                           int B, int I, int T, int O, int level, void *stream);
 /* Same hoisted MAC (layers.conv, layers.py:165-196) with the weight-mask contraction of
  * every limb on the 5th-generation tensor cores: tcgen05.mma kind::i8 with TMEM
  * accumulators, byte-split operands (5 bytes on the 40-bit limbs, 8 on q_0 and P; exact,

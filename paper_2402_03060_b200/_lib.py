@@ -56,6 +56,9 @@ SIGNATURES = {
                             _vp],
     "uh_km_bank": [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_hoisted_mac_km": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
+    "uh_imma_ta_bank": [_vp, _vp, _vp, _vp, _c_int, _c_int, _vp],
+    "uh_hoisted_mac_imma_ta": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int,
+                               _vp],
     "uh_imma_mask_bank": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp],
     "uh_tc_mask_bank": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp],
     "uh_hoisted_mac_tc": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
@@ -67,6 +70,8 @@ EXTRA = {"uh_abi_version": ([], _c_int), "uh_last_error": ([], ctypes.c_char_p),
          "uh_hoisted_bank_supported": ([_vp, _c_int, _c_int], _c_int),
          "uh_km_supported": ([_vp, _c_int], _c_int),
          "uh_imma_supported": ([_vp, _c_int, _c_int, _c_int], _c_int),
+         "uh_imma_ta_supported": ([_vp, _c_int, _c_int, _c_int], _c_int),
+         "uh_imma_ta_bank_bytes": ([_vp, _c_int, _c_int], ctypes.c_ulonglong),
          "uh_imma_bank_words": ([_vp, _c_int, _c_int, _c_int], ctypes.c_ulonglong),
          "uh_tc_supported": ([_vp, _c_int, _c_int, _c_int], _c_int),
          "uh_tc_bank_bytes": ([_vp, _c_int, _c_int, _c_int], ctypes.c_ulonglong)}

@@ -428,6 +428,39 @@ __attribute__((visibility("default"))) int uh_hoisted_mac_imma(uh_ctx *ctx, uint
     });
 }
 
+__attribute__((visibility("default"))) int uh_imma_ta_supported(uh_ctx *ctx, int level, int O, int Q) {
+    return ctx && uh::hoisted_imma_ta_supported(C(ctx), level, O, Q) ? 1 : 0;
+}
+
+__attribute__((visibility("default"))) unsigned long long uh_imma_ta_bank_bytes(uh_ctx *ctx, int level, int T) {
+    return ctx && level >= 1 && T >= 1 ? uh::imma_ta_bank_bytes(C(ctx), level, T) : 0ull;
+}
+
+__attribute__((visibility("default"))) int uh_imma_ta_bank(uh_ctx *ctx, uint8_t *kt, const uint64_t *kbank,
+                                                           const int32_t *shifts, int T, int level, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(kt && kbank && shifts && T > 0, "null operand");
+        need(5 * (level + 1) <= 32, "tensor-core phase A needs level + 1 <= 6");
+        uh::imma_ta_bank(c, kt, kbank, shifts, T, level, S(stream));
+    });
+}
+
+__attribute__((visibility("default"))) int uh_hoisted_mac_imma_ta(uh_ctx *ctx, uint64_t *acc, const uint64_t *X,
+                                                                  int xls, const uint64_t *D, const uint32_t *ib,
+                                                                  const uint8_t *kt, const uint64_t *kbank,
+                                                                  const int32_t *shifts, int B, int I, int T, int O,
+                                                                  int level, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(B > 0 && I > 0 && T > 0 && O > 0 && xls == level + 1, "bad shape (xls must equal level + 1)");
+        need(kbank != nullptr && ib != nullptr && kt != nullptr, "key bank, IMMA mask bank and tensor key bank are required");
+        uh::hoisted_mac_imma_ta(c, acc, X, D, ib, kt, kbank, shifts, B, I, T, O, level, S(stream));
+    });
+}
+
 __attribute__((visibility("default"))) int uh_tc_supported(uh_ctx *ctx, int level, int O, int Q) {
     return ctx && uh::hoisted_tc_supported(C(ctx), level, O, Q) ? 1 : 0;
 }

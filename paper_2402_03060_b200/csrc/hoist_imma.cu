@@ -594,6 +594,304 @@ bool imma8_ok(const Ctx &c, int Q) {
     return !(c.h_q[0] >> 60) && !(c.h_q[c.count - 1] >> 60);
 }
 
+
+// ---------------------------------------------------------------------------
+// Phase A on the tensor cores too (40-bit limbs, 5 (level + 1) <= 32).  The key switch of a term,
+//   V[b][c] = sum_j D_j[b][n + s] K_{t,j,c}[n]  (mod q),
+// splits D_j into bytes d_{j,a} and folds the byte weight into the key,
+//   V = sum_{(j,a)} d_{j,a}[b] * K'_{(j,a),c},   K' = 2^(8a) K_{t,j,c} mod q  (again 5 bytes e),
+// so for one (term, coefficient) the sums S_e[b][c] = sum_{(j,a)} d_{j,a}[b] byte_e(K'_{(j,a),c}) are ONE
+// m16n8k32 per component: rows = 16 ciphertexts, K = the 5 L <= 32 digit bytes, columns = the 5 key
+// bytes (+3 zero).  V = sum_e 2^(8e) S_e < 2^54 is recombined on the quad that holds a row
+// (three 32-bit shuffles), P * c0 (pre-multiplied once per call) is added, one Barrett reduction
+// gives the canonical residue -- the same value the IMAD phase A produces -- and its bytes go to
+// the phase-B planes.  Operands: dp = the ModUp digits re-laid as bytes [slot][N][I * B][32]
+// (k_ta_digits), kt = the key bank in B-fragment order [slot][N][T][lane][4 words] (k_ta_bank,
+// once per layer), pc = P * (c0, c1) [I * B][2][slot][N].
+// CTA tile: 16 ciphertexts x NC coefficients x one 40-bit limb; phase B as k_hoisted_imma over the
+// tile's 32 columns (four n-tile groups per A-fragment load).
+#ifndef UH_IMMA_TA_NC
+#define UH_IMMA_TA_NC 2
+#endif
+#ifndef UH_IMMA_TA_MINB
+#define UH_IMMA_TA_MINB 3
+#endif
+constexpr int kTCT = 16;
+template <int NKS> struct IWT {
+    static constexpr int W = 5, NC = UH_IMMA_TA_NC, OPT = 3;
+    static constexpr int ROWB = NKS > 4 ? 32 * NKS + 16 : 144;  // bytes per B-plane row (terms + pad)
+    static constexpr int GRP = 8 * ROWB + 4;   // one n-tile (8 columns) + a word: the 4 groups sit on distinct banks
+    static constexpr int PLANE = 4 * GRP;      // 32 columns (ciphertext, component) of one byte
+    static constexpr int COEF = W * PLANE;
+    static constexpr int CS = W * 8;
+    static constexpr size_t SMEM = (size_t)NC * COEF + 8 * 16 * CS * 4;
+};
+
+// digit bytes: dp[slot][n][r][32], r = i * B + b; byte 5 j + a = byte a of D[i][b][j][1 + slot][n]
+__global__ void k_ta_digits(unsigned char *__restrict__ dp, const uint64_t *__restrict__ D, int R, int L, int logn) {
+    const size_t N = (size_t)1 << logn;
+    const int NS = L - 1, LP = L + 1;
+    const size_t total = (size_t)NS * R * N;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t n = idx & (N - 1);
+        const size_t r1 = idx >> logn;
+        const int r = (int)(r1 % R), slot = (int)(r1 / R);
+        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int j = 0; j < L; j++) {
+            const uint64_t d = D[(((size_t)r * L + j) * LP + 1 + slot) * N + n];
+#pragma unroll
+            for (int a = 0; a < 5; a++) {
+                const int pos = 5 * j + a;
+                w[pos >> 2] |= (uint32_t)((d >> (8 * a)) & 0xFF) << (8 * (pos & 3));
+            }
+        }
+        uint4 *dst = reinterpret_cast<uint4 *>(dp + (((size_t)slot * N + n) * R + r) * 32);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+}
+
+// pc[r][slot][n] = P * c0 = P * X[r][0][1 + slot][n] mod q_{1+slot}
+__global__ void k_ta_pc(uint64_t *__restrict__ pc, const uint64_t *__restrict__ X, int R, int L, int logn, int sp,
+                        const Mod *__restrict__ mods) {
+    const size_t N = (size_t)1 << logn;
+    const int NS = L - 1;
+    const size_t total = (size_t)R * NS * N;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const size_t n = idx & (N - 1);
+        const size_t r1 = idx >> logn;
+        const int slot = (int)(r1 % NS);
+        const size_t r = r1 / NS;
+        const Mod m = mods[1 + slot];
+        const uint64_t P = mods[sp].q;
+        const uint64_t Pk = P < m.q ? P : csub(barrett_lite(P, m), m.q);
+        pc[idx] = mulmod(Pk, X[(r * 2 * L + 1 + slot) * N + n], m);
+    }
+}
+
+// x mod q in [0, 2q) for x < 2^56 and 2^39 < q < 2^40 (bar = floor(2^64 / q) < 2^25): the high word of
+// x * bar from two 32 x 32 products
+__device__ __forceinline__ uint64_t barrett_small(uint64_t x, uint32_t bar, uint64_t q) {
+    const uint32_t x0 = (uint32_t)x, x1 = (uint32_t)(x >> 32);
+    const uint64_t t = (uint64_t)x0 * bar;
+    const uint64_t u = (uint64_t)x1 * bar + (t >> 32);
+    const uint32_t qh = (uint32_t)(u >> 32);
+    return x - (uint64_t)qh * q;
+}
+
+// key bank in B-fragment order: kt[slot][n][t][lane] = (comp 0: b0, b1; comp 1: b0, b1).  Lane (g, tig)
+// holds column e = g (key byte) and the digit-byte positions 8 tig + x (b0) and 8 tig + 4 + x (b1), x < 4
+// -- the bytes of a dp row a lane loads as its A fragment (one 8-byte load per row).
+__global__ void k_ta_bank(uint4 *__restrict__ kt, const uint64_t *__restrict__ kbank, const int32_t *__restrict__ shifts,
+                          int T, int L, int logn, const Mod *__restrict__ mods) {
+    const size_t N = (size_t)1 << logn;
+    const int NS = L - 1, LP = L + 1;
+    const size_t total = (size_t)NS * N * T * 32;
+    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const int lane = (int)(idx & 31);
+        const size_t r0 = idx >> 5;
+        const int t = (int)(r0 % T);
+        const size_t r1 = r0 / T;
+        const size_t n = r1 & (N - 1);
+        const int slot = (int)(r1 >> logn), k = 1 + slot;
+        const int g = lane >> 2, tig = lane & 3;
+        const Mod m = mods[k];
+        uint32_t w[4] = {0, 0, 0, 0};
+        if (g < 5 && shifts[t] != 0) {
+#pragma unroll
+            for (int reg = 0; reg < 2; reg++)
+#pragma unroll
+                for (int x = 0; x < 4; x++) {
+                    const int pos = 8 * tig + 4 * reg + x;
+                    const int j = pos / 5, a = pos - 5 * j;
+                    if (j < L) {
+#pragma unroll
+                        for (int c = 0; c < 2; c++) {
+                            const uint64_t kv = kbank[(((size_t)t * LP + k) * 2 * L + 2 * j + c) * N + n];
+                            const uint64_t kw = mulmod(kv, (uint64_t)1 << (8 * a), m);  // 2^(8a) < q
+                            w[2 * c + reg] |= (uint32_t)((kw >> (8 * g)) & 0xFF) << (8 * x);
+                        }
+                    }
+                }
+        }
+        kt[idx] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+template <int L, int LOGN, int NKS>
+__global__ void __launch_bounds__(256, UH_IMMA_TA_MINB)
+    k_hoisted_imma_ta(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X,
+                      const unsigned char *__restrict__ dp, const uint64_t *__restrict__ pc,
+                      const uint4 *__restrict__ ib, const uint4 *__restrict__ kt, const int32_t *__restrict__ shifts,
+                      int B, int I, int T, int O, int sp, const Mod *__restrict__ mods) {
+    using C = IWT<NKS>;
+    constexpr int W = C::W;
+    constexpr int LP = L + 1, NS = L - 1;
+    constexpr uint32_t N = 1u << LOGN, half = N >> 1;
+    static_assert(5 * L <= 32, "one k-step holds the digit bytes");
+    extern __shared__ __align__(16) unsigned char ism[];
+    int *cst = reinterpret_cast<int *>(ism + (size_t)C::NC * C::COEF);
+    __shared__ uint32_t s_ib[32 * NKS], s_t[32 * NKS], s_r[32 * NKS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int b0 = blockIdx.x * kTCT;
+    const uint32_t n0 = blockIdx.y * C::NC;
+    const int slot = blockIdx.z;
+    const int k = 1 + slot;
+    const Mod m = mods[k];
+    const int Q = I * T;
+    const uint32_t R = (uint32_t)I * B;
+    for (int q = tid; q < Q; q += blockDim.x) {
+        const int i = q / T, t = q - i * T;
+        s_ib[q] = (uint32_t)i * B;
+        s_t[q] = t;
+        s_r[q] = (uint32_t)shifts[t];
+    }
+    __syncthreads();
+
+    // ---- phase A: one (term, coefficient) unit per warp iteration ----
+    {
+        // after the quad exchange lane (gid, tig) owns ciphertext gid + 8 (tig >> 1), component tig & 1
+        const int ctl = gid + 8 * (tig >> 1), comp = tig & 1;
+        const int b = b0 + ctl;
+        const int col = 2 * ctl + comp;
+        const bool rowa = b0 + gid < B, rowb = b0 + gid + 8 < B, pc_on = comp == 0 && b < B;
+        unsigned char *plane = ism + (col >> 3) * C::GRP + (col & 7) * C::ROWB;
+        // per-lane bases; the per-unit offsets fit 32 bits (checked on the host)
+        const unsigned char *dbase = dp + ((size_t)slot * N * R + b0 + gid) * 32 + tig * 8;
+        const uint4 *kbase = kt + (((size_t)slot * N + n0) * T << 5) + lane;
+        const uint64_t *pbase = pc + ((size_t)b * NS + slot) * N;
+        const uint32_t bar = (uint32_t)m.bar;
+        const uint32_t sh_own = 16 * tig;
+        for (int u = warp; u < Q * C::NC; u += 8) {
+            const int q = u / C::NC, cf = u - q * C::NC;
+            const uint32_t n = n0 + cf;
+            const uint32_t r = s_r[q];
+            const uint32_t ib0 = s_ib[q];
+            uint64_t v = 0;
+            if (r == 0) {
+                if (b < B) {
+                    const uint64_t P = mods[sp].q;
+                    const uint64_t Pk = P < m.q ? P : csub(barrett_lite(P, m), m.q);
+                    v = mulmod(Pk, __ldg(X + (((size_t)(ib0 + b) * 2 + comp) * L + k) * N + n), m);
+                }
+            } else {
+                const uint32_t src = rot_index_i(n, half, r);
+                const unsigned char *drow = dbase + (size_t)((src * R + ib0) << 5);
+                uint2 ra = make_uint2(0, 0), rb = make_uint2(0, 0);
+                if (rowa) ra = __ldg(reinterpret_cast<const uint2 *>(drow));
+                if (rowb) rb = __ldg(reinterpret_cast<const uint2 *>(drow + 8 * 32));
+                const uint4 kb = __ldg(kbase + ((cf * (uint32_t)T + s_t[q]) << 5));
+                uint64_t pcv = 0;
+                if (pc_on) pcv = __ldg(pbase + (size_t)(ib0 * (uint32_t)(NS * N) + src));
+                const uint4 af = make_uint4(ra.x, rb.x, ra.y, rb.y);
+                int c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+                imma(c0, af, kb.x, kb.y);
+                imma(c1, af, kb.z, kb.w);
+                // this lane's share (key bytes 2 tig, 2 tig + 1) of the four (row, component) values
+                uint32_t p[4];
+                p[0] = (uint32_t)c0[0] + ((uint32_t)c0[1] << 8);  // row gid,     component 0
+                p[1] = (uint32_t)c1[0] + ((uint32_t)c1[1] << 8);  // row gid,     component 1
+                p[2] = (uint32_t)c0[2] + ((uint32_t)c0[3] << 8);  // row gid + 8, component 0
+                p[3] = (uint32_t)c1[2] + ((uint32_t)c1[3] << 8);  // row gid + 8, component 1
+                // quad exchange: lane tig collects value tig's shares from lanes tig' = tig + d (weight 2^(16 tig'))
+                auto sel4 = [&](int x) { return x & 2 ? (x & 1 ? p[3] : p[2]) : (x & 1 ? p[1] : p[0]); };
+                v = (uint64_t)sel4(tig) << sh_own;
+#pragma unroll
+                for (int d = 1; d < 4; d++) {
+                    const uint32_t snd = sel4((tig - d) & 3);
+                    const int from = (tig + d) & 3;
+                    const uint32_t got = __shfl_sync(0xffffffffu, snd, (lane & ~3) | from);
+                    v += (uint64_t)got << (16 * from);
+                }
+                v += pcv;
+                v = csub(barrett_small(v, bar, m.q), m.q);
+            }
+            unsigned char *pl = plane + cf * C::COEF + q;
+#pragma unroll
+            for (int bb = 0; bb < W; bb++) pl[bb * C::PLANE] = (unsigned char)(v >> (8 * bb));
+        }
+    }
+    __syncthreads();
+
+    // ---- phase B: IMMA per (coefficient, m-tile, column group), byte recombination, reduction ----
+    int *cw = cst + warp * 16 * C::CS;
+    const int nmt = imma_mtiles(O);
+    for (int u = warp; u < C::NC * nmt; u += 8) {
+        const int cf = u / nmt, mt = u - cf * nmt;
+        const uint32_t n = n0 + cf;
+        const uint4 *af = ib + ((((size_t)slot * N + n) * nmt + mt) * NKS << 5) + lane;
+        uint4 A[NKS];
+#pragma unroll
+        for (int ks = 0; ks < NKS; ks++) A[ks] = __ldg(af + (ks << 5));
+#pragma unroll 1
+        for (int cg = 0; cg < 4; cg++) {
+            if (b0 + 4 * cg >= B) break;
+            int Cr[W][4];
+#pragma unroll
+            for (int nb = 0; nb < W; nb++) Cr[nb][0] = Cr[nb][1] = Cr[nb][2] = Cr[nb][3] = 0;
+            const unsigned char *bp = ism + cf * C::COEF + cg * C::GRP + gid * C::ROWB + tig * 4;
+#pragma unroll
+            for (int ks = 0; ks < NKS; ks++)
+#pragma unroll
+                for (int nb = 0; nb < W; nb++) {
+                    const unsigned char *p = bp + nb * C::PLANE + ks * 32;
+                    imma(Cr[nb], A[ks], *reinterpret_cast<const uint32_t *>(p),
+                         *reinterpret_cast<const uint32_t *>(p + 16));
+                }
+#pragma unroll
+            for (int nb = 0; nb < W; nb++) {
+                const int cc = nb * 8 + tig * 2;
+                *reinterpret_cast<int2 *>(cw + gid * C::CS + cc) = make_int2(Cr[nb][0], Cr[nb][1]);
+                *reinterpret_cast<int2 *>(cw + (gid + 8) * C::CS + cc) = make_int2(Cr[nb][2], Cr[nb][3]);
+            }
+            __syncwarp();
+            if (lane < C::OPT * 8) {
+                const int ol = lane >> 3, j = lane & 7;
+                const int o = mt * C::OPT + ol, b = b0 + 4 * cg + (j >> 1);
+                if (o < O && b < B) {
+                    uint64_t Ts[2 * W - 1];
+#pragma unroll
+                    for (int s2 = 0; s2 < 2 * W - 1; s2++) Ts[s2] = 0;
+#pragma unroll
+                    for (int a = 0; a < W; a++)
+#pragma unroll
+                        for (int nb = 0; nb < W; nb++) Ts[a + nb] += (uint32_t)cw[(ol * W + a) * C::CS + nb * 8 + j];
+                    const uint64_t lo = Ts[0] + (Ts[1] << 8) + (Ts[2] << 16) + (Ts[3] << 24) + (Ts[4] << 32);
+                    const uint64_t hx = Ts[5] + (Ts[6] << 8) + (Ts[7] << 16) + (Ts[8] << 24);
+                    const uint64_t l2 = lo + (hx << 40);
+                    const uint64_t h2 = (hx >> 24) + (l2 < lo);
+                    acc_out[((((uint32_t)o * B + b) * 2 + (j & 1)) * LP + k) * N + n] = reduce128(h2, l2, m);
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+template <int L, int NKS>
+void launch_imma_ta_k(const Ctx &c, uint64_t *acc, const uint64_t *X, const unsigned char *dp, const uint64_t *pc,
+                      const uint32_t *ib,
+                      const uint4 *kt, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
+    using C = IWT<NKS>;
+    smem_optin(k_hoisted_imma_ta<L, 15, NKS>, C::SMEM);
+    dim3 grid((unsigned)((B + kTCT - 1) / kTCT), (unsigned)(c.n / C::NC), L - 1);
+    k_hoisted_imma_ta<L, 15, NKS><<<grid, 256, C::SMEM, s>>>(acc, X, dp, pc, reinterpret_cast<const uint4 *>(ib), kt,
+                                                               shifts, B, I, T, O, c.sp(), c.d_mods);
+    UH_LAUNCH_CHECK();
+}
+
+template <int L>
+void launch_imma_ta(const Ctx &c, uint64_t *acc, const uint64_t *X, const unsigned char *dp, const uint64_t *pc,
+                    const uint32_t *ib,
+                    const uint4 *kt, const int32_t *shifts, int B, int I, int T, int O, cudaStream_t s) {
+    const int nks = (I * T + 31) / 32;
+    if (nks <= 1) launch_imma_ta_k<L, 1>(c, acc, X, dp, pc, ib, kt, shifts, B, I, T, O, s);
+    else if (nks == 2) launch_imma_ta_k<L, 2>(c, acc, X, dp, pc, ib, kt, shifts, B, I, T, O, s);
+    else if (nks == 3) launch_imma_ta_k<L, 3>(c, acc, X, dp, pc, ib, kt, shifts, B, I, T, O, s);
+    else launch_imma_ta_k<L, 4>(c, acc, X, dp, pc, ib, kt, shifts, B, I, T, O, s);
+}
+
 }  // namespace
 
 // Applicable when N = 2^15, the level has 40-bit limbs q_1..q_{L-1} (< 2^40) and 60-bit
@@ -691,6 +989,64 @@ void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint
         default: throw std::invalid_argument("IMMA hoisted kernel: 3 <= level + 1 <= 10");
     }
 #undef UH_IMMA_CASE
+}
+
+
+// Tensor-core phase A (k_hoisted_imma_ta): the IMMA shapes with 5 (level + 1) <= 32 digit bytes and
+// at most 128 terms (the phase-B planes of 32 columns at 3 CTAs / SM).
+bool hoisted_imma_ta_supported(const Ctx &c, int level, int O, int Q) {
+    return hoisted_imma_supported(c, level, O, Q) && 5 * (level + 1) <= 32 && Q <= 128 && imma8_ok(c, Q);
+}
+size_t imma_ta_bank_bytes(const Ctx &c, int level, int T) { return (size_t)level * c.n * T * 32 * 16; }
+void imma_ta_bank(const Ctx &c, uint8_t *kt, const uint64_t *kbank, const int32_t *shifts, int T, int level,
+                  cudaStream_t s) {
+    const size_t total = (size_t)level * c.n * T * 32;
+    k_ta_bank<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 32), 256, 0, s>>>(
+        reinterpret_cast<uint4 *>(kt), kbank, shifts, T, level + 1, (int)c.logn, c.d_mods);
+    UH_LAUNCH_CHECK();
+}
+
+void hoisted_mac_imma_ta(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib,
+                         const uint8_t *kt, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O,
+                         int level, cudaStream_t s) {
+    if (!hoisted_imma_ta_supported(c, level, O, I * T))
+        throw std::invalid_argument("tensor-core phase A: needs the IMMA shape with level + 1 <= 6 and <= 128 terms");
+    const int L = level + 1, R = I * B;
+    const double lim = 4294967295.0;
+    if ((double)I * B * 2 * L * c.n > lim || (double)I * B * L * (L + 1) * c.n > lim ||
+        (double)O * B * 2 * (L + 1) * c.n > lim)
+        throw std::invalid_argument("IMMA hoisted kernel operand exceeds 2^32 elements: split the batch");
+    // q_0 and P: the 8-byte IMMA kernel (IMAD phase A on the 60-bit limbs)
+    const uint32_t *ib8 = ib + imma_bank5_words(c, level, O, I * T);
+    // 32-bit per-unit offsets inside the kernel: digit bytes of one limb, the key fragments of one
+    // limb's coefficient tile, the P c0 rows
+    if ((double)c.n * R * 32 > lim || (double)c.n * T * 32 > lim || (double)R * level * c.n > lim)
+        throw std::invalid_argument("tensor-core phase A operand exceeds 2^32 elements: split the batch");
+    Scratch dp((size_t)level * c.n * R * 32, s), pc((size_t)R * level * c.n * 8, s);
+    {
+        const size_t t1 = (size_t)level * R * c.n;
+        k_ta_digits<<<(unsigned)std::min<size_t>((t1 + 255) / 256, 148 * 64), 256, 0, s>>>(dp.as<unsigned char>(), D, R, L,
+                                                                                         (int)c.logn);
+        UH_LAUNCH_CHECK();
+        const size_t t2 = (size_t)R * level * c.n;
+        k_ta_pc<<<(unsigned)std::min<size_t>((t2 + 255) / 256, 148 * 64), 256, 0, s>>>(pc.as<uint64_t>(), X, R, L,
+                                                                                     (int)c.logn, c.sp(), c.d_mods);
+        UH_LAUNCH_CHECK();
+    }
+#define UH_TA_CASE(LL)                                                                                      \
+    case LL:                                                                                                \
+        launch_imma8<LL>(c, acc, X, D, ib8, kbank, shifts, B, I, T, O, s);                                  \
+        launch_imma_ta<LL>(c, acc, X, dp.as<unsigned char>(), pc.as<uint64_t>(), ib,                        \
+                           reinterpret_cast<const uint4 *>(kt), shifts, B, I, T, O, s);                     \
+        break;
+    switch (L) {
+        UH_TA_CASE(3)
+        UH_TA_CASE(4)
+        UH_TA_CASE(5)
+        UH_TA_CASE(6)
+        default: throw std::invalid_argument("tensor-core phase A: 3 <= level + 1 <= 6");
+    }
+#undef UH_TA_CASE
 }
 
 }  // namespace uh

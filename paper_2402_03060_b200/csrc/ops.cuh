@@ -107,6 +107,17 @@ void imma_mask_bank(const Ctx &c, uint32_t *ib, const uint64_t *masks, int O, in
 void hoisted_mac_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint64_t *masks,
                       const uint32_t *ib, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O,
                       int level, cudaStream_t s);
+// the same with phase A (the key switch of every term) on the tensor cores as well: digit bytes x
+// byte-weighted key bytes, one m16n8k32 per (term, coefficient, component) for 16 ciphertexts
+// (level + 1 <= 6, <= 128 terms).  `kt` is the per-layer key bank in B-fragment order (imma_ta_bank,
+// imma_ta_bank_bytes bytes); residues identical to hoisted_mac_imma.
+bool hoisted_imma_ta_supported(const Ctx &c, int level, int O, int Q);
+size_t imma_ta_bank_bytes(const Ctx &c, int level, int T);
+void imma_ta_bank(const Ctx &c, uint8_t *kt, const uint64_t *kbank, const int32_t *shifts, int T, int level,
+                  cudaStream_t s);
+void hoisted_mac_imma_ta(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t *D, const uint32_t *ib,
+                         const uint8_t *kt, const uint64_t *kbank, const int32_t *shifts, int B, int I, int T, int O,
+                         int level, cudaStream_t s);
 // hoist_tc.cu: the weight-mask contraction of dense masked layers (1..12 outputs) on the
 // 5th-generation tensor cores (tcgen05.mma kind::i8, TMEM accumulators), every limb: 5-byte
 // operands on the 40-bit limbs, 8-byte operands on q_0 and P.  `bank` is the per-layer A-operand

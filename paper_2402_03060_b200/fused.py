@@ -128,6 +128,46 @@ def _imma_ok(backend, level: int, O: int, Q: int) -> bool:
     return backend.kernel_supported("uh_imma_supported", level, O, Q)
 
 
+def _imma_ta_ok(backend, level: int, O: int, Q: int) -> bool:
+    """IMMA layers whose key switch (phase A) also runs on the tensor cores (hoist_imma.cu
+    k_hoisted_imma_ta: level + 1 <= 6 digits, <= 128 terms -- LeNet conv2).  Opt-in (``UH_IMMA_TA=1``):
+    bit-exact, but measured 33.4 ms + 3.2 ms of operand re-layout vs 34.7 ms for the IMAD phase A at
+    B = 128 -- both kernels sit on the L1 data pipe (LSU wavefronts ~70-75%), which the tensor-core
+    phase A does not relieve (same bytes per value through L1 and shared memory)."""
+    if os.environ.get("UH_IMMA_TA", "0") == "0":
+        return False
+    return backend.kernel_supported("uh_imma_ta_supported", level, O, Q)
+
+
+def imma_ta_bank(backend, kb: torch.Tensor, sh: torch.Tensor, T: int, level: int) -> torch.Tensor:
+    """The key bank in tensor-core fragment order with the byte weights folded in (uh_imma_ta_bank),
+    cached per key bank (the entry keeps the key bank alive)."""
+    banks = backend.__dict__.setdefault("_imma_ta_banks", {})
+    ck = (kb.data_ptr(), sh.data_ptr(), T, level)
+    hit = banks.get(ck)
+    if hit is not None and hit[0] is kb:
+        return hit[1]
+    nbytes = int(_lib.load().uh_imma_ta_bank_bytes(backend._ctx, level, T))
+    kt = torch.empty((nbytes,), dtype=torch.uint8, device=backend.device)
+    backend._call("uh_imma_ta_bank", _vp(kt), _vp(kb), _vp(sh), T, level, backend._stream())
+    banks[ck] = (kb, kt)
+    return kt
+
+
+def _imma_mac(backend, acc, X, L, D, masks, shifts, sh, B, I, T, O, level, st):
+    """The dense 5..48-output hoisted MAC on the tensor-core kernels: mask contraction on IMMA, and the
+    key switch too where the shape allows (uh_hoisted_mac_imma_ta), else on IMAD (uh_hoisted_mac_imma)."""
+    kb = key_bank(backend, shifts, level)
+    ib = imma_bank(backend, masks, O, I * T, level, cache=_banked(backend, masks))
+    if _imma_ta_ok(backend, level, O, I * T):
+        kt = imma_ta_bank(backend, kb, sh, T, level)
+        backend._call("uh_hoisted_mac_imma_ta", _vp(acc), _vp(X), L, _vp(D), _vp(ib), _vp(kt), _vp(kb), _vp(sh), B, I,
+                      T, O, level, st)
+    else:
+        backend._call("uh_hoisted_mac_imma", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ib), _vp(kb), _vp(sh), B, I,
+                      T, O, level, st)
+
+
 def _tc_ok(backend, level: int, O: int, Q: int) -> bool:
     """Dense masked layers (1..12 outputs, <= 128 terms) at N = 2^15: the mask contraction of every
     limb on the tcgen05 tensor cores (hoist_tc.cu).  Opt-in (``UH_TC=1``) until it beats the
@@ -376,10 +416,7 @@ def conv(backend, state: CipherState, layer) -> CipherState:
             backend._call("uh_hoisted_mac_tc", _vp(accg), _vp(X), L, _vp(D), _vp(tb), _vp(kb), _vp(sh), B, I, T, Og,
                           level, st)
         elif imma:
-            kb = key_bank(backend, shifts, level)
-            ib = imma_bank(backend, mg, Og, I * T, level, cache=_banked(backend, mg))
-            backend._call("uh_hoisted_mac_imma", _vp(accg), _vp(X), L, _vp(D), _vp(mg), _vp(ib), _vp(kb), _vp(sh), B,
-                          I, T, Og, level, st)
+            _imma_mac(backend, accg, X, L, D, mg, shifts, sh, B, I, T, Og, level, st)
         elif _key_bank_ok(backend, level, Og) and I * T <= 512:
             kb = key_bank(backend, shifts, level)
             backend._call("uh_hoisted_mac_bank", _vp(accg), _vp(X), L, _vp(D), _vp(mg), _vp(kb), _vp(sh), B, I, T,
@@ -561,11 +598,7 @@ def _hoist(backend, X, level, shifts, masks, O, diag, B, taps=None):
         del D
         return acc
     if mode == 0 and masks is not None and _imma_ok(backend, level, O, I * T):
-        kb = key_bank(backend, shifts, level)
-        ib = imma_bank(backend, masks, O, I * T, level, cache=_banked(backend, masks))
-        sh = _shift_table(backend, shifts)
-        backend._call("uh_hoisted_mac_imma", _vp(acc), _vp(X), L, _vp(D), _vp(masks), _vp(ib), _vp(kb), _vp(sh), B, I,
-                      T, O, level, st)
+        _imma_mac(backend, acc, X, L, D, masks, shifts, _shift_table(backend, shifts), B, I, T, O, level, st)
         del D
         return acc
     if masks is not None and O == 1 and _km_ok(backend, level):

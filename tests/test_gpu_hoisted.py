@@ -259,12 +259,40 @@ def test_imma_kernel_equals_key_bank_kernel(O, level, I, shifts, B, monkeypatch)
     worst-case (uniform up to q - 1) masks."""
     be, o = _c2()
     monkeypatch.setenv("UH_TC", "0")  # the mma.sync kernel, not the tcgen05 one
+    monkeypatch.setenv("UH_IMMA_TA", "0")  # IMAD phase A (the tensor-core phase A has its own test below)
     rng = np.random.default_rng(70 + O + level)
     cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, C2.num_slots)))) for _ in range(I)]
     X = fused.stack_cts(be, cts, level)
     mdev = torch.from_numpy(_rand_masks(o, rng, O, I * len(shifts), level).view(np.int64)).to(be.device)
     monkeypatch.setenv("UH_IMMA", "1")
     assert fused._imma_ok(be, level, O, I * len(shifts))
+    got = fused._hoist(be, X, level, shifts, mdev, O, False, B)
+    monkeypatch.setenv("UH_IMMA", "0")
+    want = fused._hoist(be, X, level, shifts, mdev, O, False, B)
+    assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("O,level,I,shifts,B", [
+    (12, 5, 4, [a + 28 * b for b in range(5) for a in range(5)], 21),  # LeNet conv2 shape, 16 + 5 ciphertexts
+    (12, 5, 4, [a + 28 * b for b in range(5) for a in range(5)], 16),  # one full 16-ciphertext tile
+    (7, 3, 3, [0, 1, 28, -29, 16383, 57, -2, 3, 700], 4),              # partial m-tile, Q = 27, zero shift
+    (5, 2, 2, [0, 1, 28, -29, 16383], 3),                              # one k-step, 15 digit bytes
+    (5, 3, 5, [a + 28 * b for b in range(5) for a in range(5)], 9),    # Q = 125: 4 k-steps, one short; rows 8.. empty but one
+    (48, 4, 2, [0, 5, -7, 64], 33),                                    # 16 m-tiles, three ciphertext tiles
+])
+def test_imma_tensor_phase_a_equals_key_bank_kernel(O, level, I, shifts, B, monkeypatch):
+    """Key switch on the tensor cores (hoist_imma.cu k_hoisted_imma_ta: digit bytes x byte-weighted key
+    bytes, quad recombination, P c0 pre-multiplied) + IMMA mask contraction == the key-bank IMAD kernel
+    (oracle-pinned above), residue for residue, with worst-case masks."""
+    be, o = _c2()
+    monkeypatch.setenv("UH_TC", "0")
+    monkeypatch.setenv("UH_IMMA_TA", "1")
+    rng = np.random.default_rng(170 + O + level)
+    cts = [be.encrypt(be.encode_batch(rng.uniform(-1, 1, size=(B, C2.num_slots)))) for _ in range(I)]
+    X = fused.stack_cts(be, cts, level)
+    mdev = torch.from_numpy(_rand_masks(o, rng, O, I * len(shifts), level).view(np.int64)).to(be.device)
+    monkeypatch.setenv("UH_IMMA", "1")
+    assert fused._imma_ok(be, level, O, I * len(shifts)) and fused._imma_ta_ok(be, level, O, I * len(shifts))
     got = fused._hoist(be, X, level, shifts, mdev, O, False, B)
     monkeypatch.setenv("UH_IMMA", "0")
     want = fused._hoist(be, X, level, shifts, mdev, O, False, B)
