@@ -50,6 +50,14 @@ constexpr int kIJ = 2 * kICT;               // columns per value byte (ciphertex
 #define UH_IMMA_NC_WIDE 4  // coefficients per CTA past 4 k-steps (keeps 3 CTAs / SM)
 #endif
 constexpr int kIMaxTerms = 256;             // 8 k-steps
+// D = A x B (zero accumulator: the A fragment stays live for a second product)
+__device__ __forceinline__ void imma0(int (&d)[4], const uint4 &a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%10,%10,%10};"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1), "r"(0));
+}
+
 // Byte width W = 5 of the 40-bit residues: 3 outputs x 5 mask bytes per 16-row m-tile, 4 m-tiles.
 // NKS k-steps of 32 terms.  A B-plane row (coefficient, byte, column) holds 32 NKS terms + 16 bytes
 // of pad: its word stride is 4 mod 8, so the 8 gid rows x 4 tig words of a fragment load hit 32
@@ -627,45 +635,70 @@ template <int NKS> struct IWT {
     static constexpr size_t SMEM = (size_t)NC * COEF + 8 * 16 * CS * 4;
 };
 
-// digit bytes: dp[slot][n][r][32], r = i * B + b; byte 5 j + a = byte a of D[i][b][j][1 + slot][n]
-__global__ void k_ta_digits(unsigned char *__restrict__ dp, const uint64_t *__restrict__ D, int R, int L, int logn) {
+// Operand re-layout for the tensor-core phase A, one pass over the ModUp digits and c0:
+//   dp[slot][n][r][32]: digit bytes, r = i * B + b; byte 5 j + a = byte a of D[i][b][j][1 + slot][n]
+//   pc[slot][n][r]    : P * c0 = P * X[r][0][1 + slot][n] mod q_{1+slot}
+// (ciphertext innermost: the 16 ciphertexts of a phase-A unit read whole lines).  A CTA transposes a
+// 32-coefficient x 32-ciphertext tile through shared memory: coalesced limb reads (lanes = n), coalesced
+// row writes (lanes = consecutive words of one coefficient's 32 rows); the tile's row strides (257 / 65
+// words) keep both sides bank-conflict-free.
+template <int L>
+__global__ void __launch_bounds__(256)
+    k_ta_pack(unsigned char *__restrict__ dp, uint64_t *__restrict__ pc, const uint64_t *__restrict__ D,
+              const uint64_t *__restrict__ X, int R, int logn, int sp, const Mod *__restrict__ mods) {
+    __shared__ uint32_t tw[32 * 257];
+    __shared__ uint32_t tp[32 * 65];
     const size_t N = (size_t)1 << logn;
-    const int NS = L - 1, LP = L + 1;
-    const size_t total = (size_t)NS * R * N;
-    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-        const size_t n = idx & (N - 1);
-        const size_t r1 = idx >> logn;
-        const int r = (int)(r1 % R), slot = (int)(r1 / R);
-        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int j = 0; j < L; j++) {
-            const uint64_t d = D[(((size_t)r * L + j) * LP + 1 + slot) * N + n];
+    const int LP = L + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t n0 = (size_t)blockIdx.x * 32;
+    const int r0 = blockIdx.y * 32, slot = blockIdx.z, k = 1 + slot;
+    const Mod m = mods[k];
+    const uint64_t P = mods[sp].q;
+    const uint64_t Pk = P < m.q ? P : csub(barrett_lite(P, m), m.q);
 #pragma unroll
-            for (int a = 0; a < 5; a++) {
-                const int pos = 5 * j + a;
-                w[pos >> 2] |= (uint32_t)((d >> (8 * a)) & 0xFF) << (8 * (pos & 3));
+    for (int rr = 0; rr < 4; rr++) {
+        const int rl = warp + 8 * rr, r = r0 + rl;
+        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint64_t pv = 0;
+        if (r < R) {
+            uint64_t d[L];
+#pragma unroll
+            for (int j = 0; j < L; j++) d[j] = D[(((size_t)r * L + j) * LP + k) * N + n0 + lane];
+            const uint64_t x0 = X[((size_t)r * 2 * L + k) * N + n0 + lane];
+            // the 40-bit digits concatenated little-endian: digit j occupies bits [40 j, 40 j + 40)
+#pragma unroll
+            for (int j = 0; j < L; j++) {
+                const int bit = 40 * j, wi = bit >> 5, sh = bit & 31;  // compile-time
+                const uint64_t lo = d[j] << sh;                         // bits of words wi, wi + 1
+                w[wi] |= (uint32_t)lo;
+                w[wi + 1] |= (uint32_t)(lo >> 32);
+                if (sh > 24) w[wi + 2] |= (uint32_t)(d[j] >> (64 - sh));  // spill past two words
             }
+            pv = mulmod(Pk, x0, m);
         }
-        uint4 *dst = reinterpret_cast<uint4 *>(dp + (((size_t)slot * N + n) * R + r) * 32);
-        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+        for (int i = 0; i < 8; i++) tw[lane * 257 + rl * 8 + i] = w[i];
+        tp[lane * 65 + rl * 2] = (uint32_t)pv;
+        tp[lane * 65 + rl * 2 + 1] = (uint32_t)(pv >> 32);
     }
-}
-
-// pc[r][slot][n] = P * c0 = P * X[r][0][1 + slot][n] mod q_{1+slot}
-__global__ void k_ta_pc(uint64_t *__restrict__ pc, const uint64_t *__restrict__ X, int R, int L, int logn, int sp,
-                        const Mod *__restrict__ mods) {
-    const size_t N = (size_t)1 << logn;
-    const int NS = L - 1;
-    const size_t total = (size_t)R * NS * N;
-    for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-        const size_t n = idx & (N - 1);
-        const size_t r1 = idx >> logn;
-        const int slot = (int)(r1 % NS);
-        const size_t r = r1 / NS;
-        const Mod m = mods[1 + slot];
-        const uint64_t P = mods[sp].q;
-        const uint64_t Pk = P < m.q ? P : csub(barrett_lite(P, m), m.q);
-        pc[idx] = mulmod(Pk, X[(r * 2 * L + 1 + slot) * N + n], m);
+    __syncthreads();
+    uint32_t *dpw = reinterpret_cast<uint32_t *>(dp);
+    uint32_t *pcw = reinterpret_cast<uint32_t *>(pc);
+#pragma unroll
+    for (int nn = 0; nn < 4; nn++) {
+        const int nl = warp + 8 * nn;
+        const size_t row = ((size_t)slot * N + n0 + nl) * R + r0;  // first row of this coefficient's tile
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int idx = lane + 32 * i;  // word of the 32 rows x 8 words
+            if (r0 + (idx >> 3) < R) dpw[row * 8 + idx] = tw[nl * 257 + idx];
+        }
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+            const int idx = lane + 32 * i;
+            if (r0 + (idx >> 1) < R) pcw[row * 2 + idx] = tp[nl * 65 + idx];
+        }
     }
 }
 
@@ -726,7 +759,7 @@ __global__ void __launch_bounds__(256, UH_IMMA_TA_MINB)
                       int B, int I, int T, int O, int sp, const Mod *__restrict__ mods) {
     using C = IWT<NKS>;
     constexpr int W = C::W;
-    constexpr int LP = L + 1, NS = L - 1;
+    constexpr int LP = L + 1;
     constexpr uint32_t N = 1u << LOGN, half = N >> 1;
     static_assert(5 * L <= 32, "one k-step holds the digit bytes");
     extern __shared__ __align__(16) unsigned char ism[];
@@ -760,56 +793,68 @@ __global__ void __launch_bounds__(256, UH_IMMA_TA_MINB)
         // per-lane bases; the per-unit offsets fit 32 bits (checked on the host)
         const unsigned char *dbase = dp + ((size_t)slot * N * R + b0 + gid) * 32 + tig * 8;
         const uint4 *kbase = kt + (((size_t)slot * N + n0) * T << 5) + lane;
-        const uint64_t *pbase = pc + ((size_t)b * NS + slot) * N;
+        const uint64_t *pbase = pc + (size_t)slot * N * R + b;
         const uint32_t bar = (uint32_t)m.bar;
-        const uint32_t sh_own = 16 * tig;
-        for (int u = warp; u < Q * C::NC; u += 8) {
-            const int q = u / C::NC, cf = u - q * C::NC;
+        const bool t1 = tig & 1, t2 = tig & 2;
+        const uint64_t P = mods[sp].q;
+        const uint64_t Pk = P < m.q ? P : csub(barrett_lite(P, m), m.q);
+        // the canonical key-switched value of (term q, coefficient n0 + cf) for this lane's (ciphertext, component)
+        auto unit = [&](int q, int cf) -> uint64_t {
             const uint32_t n = n0 + cf;
             const uint32_t r = s_r[q];
             const uint32_t ib0 = s_ib[q];
-            uint64_t v = 0;
             if (r == 0) {
-                if (b < B) {
-                    const uint64_t P = mods[sp].q;
-                    const uint64_t Pk = P < m.q ? P : csub(barrett_lite(P, m), m.q);
-                    v = mulmod(Pk, __ldg(X + (((size_t)(ib0 + b) * 2 + comp) * L + k) * N + n), m);
-                }
-            } else {
-                const uint32_t src = rot_index_i(n, half, r);
-                const unsigned char *drow = dbase + (size_t)((src * R + ib0) << 5);
-                uint2 ra = make_uint2(0, 0), rb = make_uint2(0, 0);
-                if (rowa) ra = __ldg(reinterpret_cast<const uint2 *>(drow));
-                if (rowb) rb = __ldg(reinterpret_cast<const uint2 *>(drow + 8 * 32));
-                const uint4 kb = __ldg(kbase + ((cf * (uint32_t)T + s_t[q]) << 5));
-                uint64_t pcv = 0;
-                if (pc_on) pcv = __ldg(pbase + (size_t)(ib0 * (uint32_t)(NS * N) + src));
-                const uint4 af = make_uint4(ra.x, rb.x, ra.y, rb.y);
-                int c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
-                imma(c0, af, kb.x, kb.y);
-                imma(c1, af, kb.z, kb.w);
-                // this lane's share (key bytes 2 tig, 2 tig + 1) of the four (row, component) values
-                uint32_t p[4];
-                p[0] = (uint32_t)c0[0] + ((uint32_t)c0[1] << 8);  // row gid,     component 0
-                p[1] = (uint32_t)c1[0] + ((uint32_t)c1[1] << 8);  // row gid,     component 1
-                p[2] = (uint32_t)c0[2] + ((uint32_t)c0[3] << 8);  // row gid + 8, component 0
-                p[3] = (uint32_t)c1[2] + ((uint32_t)c1[3] << 8);  // row gid + 8, component 1
-                // quad exchange: lane tig collects value tig's shares from lanes tig' = tig + d (weight 2^(16 tig'))
-                auto sel4 = [&](int x) { return x & 2 ? (x & 1 ? p[3] : p[2]) : (x & 1 ? p[1] : p[0]); };
-                v = (uint64_t)sel4(tig) << sh_own;
-#pragma unroll
-                for (int d = 1; d < 4; d++) {
-                    const uint32_t snd = sel4((tig - d) & 3);
-                    const int from = (tig + d) & 3;
-                    const uint32_t got = __shfl_sync(0xffffffffu, snd, (lane & ~3) | from);
-                    v += (uint64_t)got << (16 * from);
-                }
-                v += pcv;
-                v = csub(barrett_small(v, bar, m.q), m.q);
+                if (b >= B) return 0;
+                return mulmod(Pk, __ldg(X + (((size_t)(ib0 + b) * 2 + comp) * L + k) * N + n), m);
             }
+            const uint32_t src = rot_index_i(n, half, r);
+            const unsigned char *drow = dbase + (size_t)((src * R + ib0) << 5);
+            uint2 ra = make_uint2(0, 0), rb = make_uint2(0, 0);
+            if (rowa) ra = __ldg(reinterpret_cast<const uint2 *>(drow));
+            if (rowb) rb = __ldg(reinterpret_cast<const uint2 *>(drow + 8 * 32));
+            uint4 kb = make_uint4(0, 0, 0, 0);  // key-byte columns 5..7 are zero padding: not loaded
+            if (gid < 5) kb = __ldg(kbase + ((cf * (uint32_t)T + s_t[q]) << 5));
+            uint64_t pcv = 0;
+            if (pc_on) pcv = __ldg(pbase + (size_t)(src * R + ib0));
+            const uint4 af = make_uint4(ra.x, rb.x, ra.y, rb.y);
+            int c0[4], c1[4];
+            imma0(c0, af, kb.x, kb.y);
+            imma0(c1, af, kb.z, kb.w);
+            // this lane's share (key bytes 2 tig, 2 tig + 1) of the four (row, component) values
+            const uint32_t p0 = (uint32_t)c0[0] + ((uint32_t)c0[1] << 8);  // row gid,     component 0
+            const uint32_t p1 = (uint32_t)c1[0] + ((uint32_t)c1[1] << 8);  // row gid,     component 1
+            const uint32_t p2 = (uint32_t)c0[2] + ((uint32_t)c0[3] << 8);  // row gid + 8, component 0
+            const uint32_t p3 = (uint32_t)c1[2] + ((uint32_t)c1[3] << 8);  // row gid + 8, component 1
+            // quad exchange: lane tig owns value tig.  Round d sends e_d = p[(tig - d) & 3] (a barrel
+            // rotation of the four shares by tig) to lane tig - d and receives lane tig + d's share
+            // with b = (p0, p3, p2, p1), e_d = b[(d - tig) & 3]: rotate b by tig & 1, then by tig & 2
+            const uint32_t a0 = t1 ? p1 : p0, a1 = t1 ? p0 : p3, a2 = t1 ? p3 : p2, a3 = t1 ? p2 : p1;
+            const uint32_t e0 = t2 ? a2 : a0, e1 = t2 ? a3 : a1, e2 = t2 ? a0 : a2, e3 = t2 ? a1 : a3;
+            const uint32_t g1 = __shfl_sync(0xffffffffu, e1, (lane & ~3) | ((tig + 1) & 3));
+            const uint32_t g2 = __shfl_sync(0xffffffffu, e2, (lane & ~3) | ((tig + 2) & 3));
+            const uint32_t g3 = __shfl_sync(0xffffffffu, e3, (lane & ~3) | ((tig + 3) & 3));
+            // shares by source lane s = (tig + d) & 3 (the inverse rotation); lane 3's share is zero
+            // (key-byte columns 6, 7), so only sources 0, 1, 2 are placed
+            // S[s] = g[(s - tig) & 3] (g_0 = e0): the same rotation applied to the received shares
+            const uint32_t h0 = t1 ? g3 : e0, h1 = t1 ? e0 : g1, h2 = t1 ? g1 : g2, h3 = t1 ? g2 : g3;
+            const uint32_t s0 = t2 ? h2 : h0, s1 = t2 ? h3 : h1, s2 = t2 ? h0 : h2;
+            uint64_t v = (uint64_t)s0 + ((uint64_t)s1 << 16) + ((uint64_t)s2 << 32) + pcv;
+            return csub(barrett_small(v, bar, m.q), m.q);
+        };
+        const int QP = (Q + 1) >> 1;
+        for (int u = warp; u < QP * C::NC; u += 8) {
+            const int qp = u / C::NC, cf = u - qp * C::NC;
+            const int q = 2 * qp;
+            const uint64_t va = unit(q, cf);
+            const uint64_t vb = q + 1 < Q ? unit(q + 1, cf) : 0;  // warp-uniform
             unsigned char *pl = plane + cf * C::COEF + q;
-#pragma unroll
-            for (int bb = 0; bb < W; bb++) pl[bb * C::PLANE] = (unsigned char)(v >> (8 * bb));
+            const uint32_t al = (uint32_t)va, bl = (uint32_t)vb;
+            *reinterpret_cast<unsigned short *>(pl) = (unsigned short)__byte_perm(al, bl, 0x0040);
+            *reinterpret_cast<unsigned short *>(pl + C::PLANE) = (unsigned short)__byte_perm(al, bl, 0x0051);
+            *reinterpret_cast<unsigned short *>(pl + 2 * C::PLANE) = (unsigned short)__byte_perm(al, bl, 0x0062);
+            *reinterpret_cast<unsigned short *>(pl + 3 * C::PLANE) = (unsigned short)__byte_perm(al, bl, 0x0073);
+            *reinterpret_cast<unsigned short *>(pl + 4 * C::PLANE) =
+                (unsigned short)(((uint32_t)(va >> 32) & 0xFF) | (((uint32_t)(vb >> 32) & 0xFF) << 8));
         }
     }
     __syncthreads();
@@ -1024,13 +1069,20 @@ void hoisted_mac_imma_ta(const Ctx &c, uint64_t *acc, const uint64_t *X, const u
         throw std::invalid_argument("tensor-core phase A operand exceeds 2^32 elements: split the batch");
     Scratch dp((size_t)level * c.n * R * 32, s), pc((size_t)R * level * c.n * 8, s);
     {
-        const size_t t1 = (size_t)level * R * c.n;
-        k_ta_digits<<<(unsigned)std::min<size_t>((t1 + 255) / 256, 148 * 64), 256, 0, s>>>(dp.as<unsigned char>(), D, R, L,
-                                                                                         (int)c.logn);
-        UH_LAUNCH_CHECK();
-        const size_t t2 = (size_t)R * level * c.n;
-        k_ta_pc<<<(unsigned)std::min<size_t>((t2 + 255) / 256, 148 * 64), 256, 0, s>>>(pc.as<uint64_t>(), X, R, L,
-                                                                                     (int)c.logn, c.sp(), c.d_mods);
+        dim3 grid((unsigned)(c.n / 32), (unsigned)((R + 31) / 32), (unsigned)level);
+#define UH_TA_PACK(LL)                                                                                         \
+    case LL:                                                                                                   \
+        k_ta_pack<LL><<<grid, 256, 0, s>>>(dp.as<unsigned char>(), pc.as<uint64_t>(), D, X, R, (int)c.logn,    \
+                                           c.sp(), c.d_mods);                                                  \
+        break;
+        switch (L) {
+            UH_TA_PACK(3)
+            UH_TA_PACK(4)
+            UH_TA_PACK(5)
+            UH_TA_PACK(6)
+            default: throw std::invalid_argument("tensor-core phase A: 3 <= level + 1 <= 6");
+        }
+#undef UH_TA_PACK
         UH_LAUNCH_CHECK();
     }
 #define UH_TA_CASE(LL)                                                                                      \

@@ -130,11 +130,10 @@ def _imma_ok(backend, level: int, O: int, Q: int) -> bool:
 
 def _imma_ta_ok(backend, level: int, O: int, Q: int) -> bool:
     """IMMA layers whose key switch (phase A) also runs on the tensor cores (hoist_imma.cu
-    k_hoisted_imma_ta: level + 1 <= 6 digits, <= 128 terms -- LeNet conv2).  Opt-in (``UH_IMMA_TA=1``):
-    bit-exact, but measured 33.4 ms + 3.2 ms of operand re-layout vs 34.7 ms for the IMAD phase A at
-    B = 128 -- both kernels sit on the L1 data pipe (LSU wavefronts ~70-75%), which the tensor-core
-    phase A does not relieve (same bytes per value through L1 and shared memory)."""
-    if os.environ.get("UH_IMMA_TA", "0") == "0":
+    k_hoisted_imma_ta: level + 1 <= 6 digits, <= 128 terms -- LeNet conv2).  Bit-exact; measured
+    54.2 vs 56.9 ms for the LeNet conv2 call at B = 128 (30.4 ms kernel + 1.5 ms operand re-layout vs
+    34.7 ms for the IMAD phase A).  ``UH_IMMA_TA=0`` keeps phase A on IMAD."""
+    if os.environ.get("UH_IMMA_TA", "1") == "0":
         return False
     return backend.kernel_supported("uh_imma_ta_supported", level, O, Q)
 
