@@ -337,11 +337,15 @@ def _hbm_peak():
 
 
 def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
-    """Roofline of the dominant kernel call: the conv2 hoisted MAC (k_hoisted_imma on the 40-bit
-    limbs + k_hoisted_imma8 on q_0 and P), against the pipes it runs on (a mixed bound): phase A
-    on the 40-bit limbs at the narrow-operand MAC peak, phase A of the 60-bit limbs at the 128-bit
-    MAC peak, phase B as 25 (40-bit) / 64 (60-bit) u8 byte products per modMAC at the measured
-    IMMA (mma.sync) MAC peak."""
+    """Roofline of the dominant kernel call: the conv2 hoisted MAC (k_hoisted_imma_ta or k_hoisted_imma
+    on the 40-bit limbs + k_hoisted_imma8 on q_0 and P), against the pipes it runs on (a mixed bound):
+    phase A on the 40-bit limbs as 25 u8 byte products per modMAC at the IMMA peak (path "ta": the
+    default for the LeNet shape) or at the narrow-operand IMAD MAC peak (path "imma8"), phase A of
+    the 60-bit limbs at the 128-bit MAC peak, phase B as 25 (40-bit) / 64 (60-bit) u8 byte products
+    per modMAC at the measured IMMA (mma.sync) MAC peak.  ``frac_vs_imad_phase_a_bound`` keeps the
+    previous kernel pair's bound next to it (the tensor-core phase A lowers the bound by more than it
+    lowers the call time: what is left is byte re-layout, recombination and shared-memory traffic,
+    which a MAC count does not see)."""
     calls = [t for t in timers if t[0] == "conv_hoisted_mac"]
     if not calls:
         return None
@@ -356,6 +360,9 @@ def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
     if w["path"] == "tc":
         parts = {"phase_a_40bit_narrow_imad": w["a40"] / r_narrow, "phase_a_60bit_imad": w["a60"] / r_mac,
                  "phase_b_tcgen05_i8": (25 * w["b40"] + 64 * w["b60"]) / r_tc}
+    elif w["path"] == "ta":
+        parts = {"phase_a_40bit_imma": 25 * w["a40"] / r_imma, "phase_a_60bit_imad": w["a60"] / r_mac,
+                 "phase_b_imma": (25 * w["b40"] + 64 * w["b60"]) / r_imma}
     elif w["path"] == "imma8":
         parts = {"phase_a_40bit_narrow_imad": w["a40"] / r_narrow, "phase_a_60bit_imad": w["a60"] / r_mac,
                  "phase_b_imma": (25 * w["b40"] + 64 * w["b60"]) / r_imma}
@@ -368,6 +375,9 @@ def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
     t_bound = sum(parts.values())
     achieved = w["total"] / (tms / 1e3)
     peak = w["total"] / t_bound
+    # the bound of the same call with the 40-bit key switch on IMAD (the kernel pair it replaced):
+    # moving work onto the tensor cores lowers the bound faster than the call time, so both are shown
+    t_imad_a = w["a40"] / r_narrow + w["a60"] / r_mac + (25 * w["b40"] + 64 * w["b60"]) / r_imma
     traffic = None
     if os.path.exists(traffic_path):
         t = json.load(open(traffic_path)).get("by_batch", {}).get(str(w["B"]))
@@ -377,8 +387,11 @@ def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
     return {"bound": "imad+imma (mixed integer pipes)",
             "kernel": (f"LeNet conv2 hoisted MAC call, level {lev}: k_hoisted_tc (tcgen05 kind::i8, TMEM "
                        f"accumulators; 40-bit q_1..q_{lev} and 60-bit q_0, P)") if w["path"] == "tc" else
-                      (f"LeNet conv2 hoisted MAC call, level {lev}: k_hoisted_imma (40-bit q_1..q_{lev}) + "
-                       + ("k_hoisted_imma8 (60-bit q_0, P; 8-byte IMMA)" if w["path"] == "imma8"
+                      (f"LeNet conv2 hoisted MAC call, level {lev}: "
+                       + ("k_ta_pack + k_hoisted_imma_ta (key switch and mask contraction on mma.sync u8; " if
+                          w["path"] == "ta" else "k_hoisted_imma (")
+                       + f"40-bit q_1..q_{lev}) + "
+                       + ("k_hoisted_imma8 (60-bit q_0, P; 8-byte IMMA)" if w["path"] in ("imma8", "ta")
                           else "k_hoisted_bank (60-bit q_0, P)")),
             "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "T modMAC/s", "frac": achieved / peak,
             "traffic": traffic, "launch_ms": tms, "bound_ms": t_bound * 1e3,
@@ -389,7 +402,8 @@ def conv2_roofline(timers, rates, step_ms, steps, traffic_path):
             "peak_source": "measured in this run (uh_bench_peaks): narrow-operand MAC rates[8], 128-bit MAC "
                            "rates[1], u8 IMMA (mma.sync) MAC rates[9], tcgen05 kind::i8 MAC rates[11]; peak = total "
                            "modMACs / mixed bound time",
-            "frac_vs_all_imad_peak": achieved / r_mac}
+            "frac_vs_all_imad_peak": achieved / r_mac,
+            "frac_vs_imad_phase_a_bound": t_imad_a * 1e3 / tms, "imad_phase_a_bound_ms": t_imad_a * 1e3}
 
 
 def ntt_roofline(be, hbm_gbs, hbm_src, polys=64, limbs=8, reps=5):

@@ -26,7 +26,9 @@
 //             pre-split mask bank (16-byte loads, fragment order), B fragments
 //             from shared memory; ceil(Q / 32) k-steps x 5 n-tiles of IMMA per unit, then
 //             the byte recombination and the modular reduction per output.
-// The 60-bit limbs (q_0, P) run on the IMAD key-bank kernel (hoisted_mac_bank_wide, hoist_bank.cu).
+// The 60-bit limbs (q_0, P) run k_hoisted_imma8 below (8-byte operands), or the IMAD key-bank kernel
+// (hoisted_mac_bank_wide, hoist_bank.cu).  k_hoisted_imma_ta (further below) is this kernel with phase A
+// on the tensor cores as well, the default where the level's digit bytes fit one k-step.
 #include <cstdlib>
 #include <type_traits>
 
@@ -798,55 +800,72 @@ __global__ void __launch_bounds__(256, UH_IMMA_TA_MINB)
         const bool t1 = tig & 1, t2 = tig & 2;
         const uint64_t P = mods[sp].q;
         const uint64_t Pk = P < m.q ? P : csub(barrett_lite(P, m), m.q);
-        // the canonical key-switched value of (term q, coefficient n0 + cf) for this lane's (ciphertext, component)
-        auto unit = [&](int q, int cf) -> uint64_t {
+        // operands of one (term q, coefficient n0 + cf) unit, loaded ahead of the arithmetic so the two
+        // units of an iteration have their loads in flight together
+        struct Unit {
+            uint2 ra, rb;
+            uint4 kb;
+            uint64_t pcv;  // P c0 at the rotated slot (component-0 lanes); for a zero shift: the c value itself
+            bool zero;
+        };
+        auto load = [&](int q, int cf) -> Unit {
+            Unit w;
             const uint32_t n = n0 + cf;
             const uint32_t r = s_r[q];
             const uint32_t ib0 = s_ib[q];
-            if (r == 0) {
-                if (b >= B) return 0;
-                return mulmod(Pk, __ldg(X + (((size_t)(ib0 + b) * 2 + comp) * L + k) * N + n), m);
+            w.zero = r == 0;
+            w.ra = w.rb = make_uint2(0, 0);
+            w.kb = make_uint4(0, 0, 0, 0);
+            w.pcv = 0;
+            if (w.zero) {
+                if (b < B) w.pcv = __ldg(X + (((size_t)(ib0 + b) * 2 + comp) * L + k) * N + n);
+                return w;
             }
             const uint32_t src = rot_index_i(n, half, r);
             const unsigned char *drow = dbase + (size_t)((src * R + ib0) << 5);
-            uint2 ra = make_uint2(0, 0), rb = make_uint2(0, 0);
-            if (rowa) ra = __ldg(reinterpret_cast<const uint2 *>(drow));
-            if (rowb) rb = __ldg(reinterpret_cast<const uint2 *>(drow + 8 * 32));
-            uint4 kb = make_uint4(0, 0, 0, 0);  // key-byte columns 5..7 are zero padding: not loaded
-            if (gid < 5) kb = __ldg(kbase + ((cf * (uint32_t)T + s_t[q]) << 5));
-            uint64_t pcv = 0;
-            if (pc_on) pcv = __ldg(pbase + (size_t)(src * R + ib0));
-            const uint4 af = make_uint4(ra.x, rb.x, ra.y, rb.y);
+            if (rowa) w.ra = __ldg(reinterpret_cast<const uint2 *>(drow));
+            if (rowb) w.rb = __ldg(reinterpret_cast<const uint2 *>(drow + 8 * 32));
+            if (gid < 5) w.kb = __ldg(kbase + ((cf * (uint32_t)T + s_t[q]) << 5));  // columns 5..7: zero padding
+            if (pc_on) w.pcv = __ldg(pbase + (size_t)(src * R + ib0));
+            return w;
+        };
+        // the canonical key-switched value of the unit for this lane's (ciphertext, component)
+        auto compute = [&](const Unit &w) -> uint64_t {
+            if (w.zero) return b < B ? mulmod(Pk, w.pcv, m) : 0;  // warp-uniform branch
+            const uint4 af = make_uint4(w.ra.x, w.rb.x, w.ra.y, w.rb.y);
             int c0[4], c1[4];
-            imma0(c0, af, kb.x, kb.y);
-            imma0(c1, af, kb.z, kb.w);
+            imma0(c0, af, w.kb.x, w.kb.y);
+            imma0(c1, af, w.kb.z, w.kb.w);
             // this lane's share (key bytes 2 tig, 2 tig + 1) of the four (row, component) values
             const uint32_t p0 = (uint32_t)c0[0] + ((uint32_t)c0[1] << 8);  // row gid,     component 0
             const uint32_t p1 = (uint32_t)c1[0] + ((uint32_t)c1[1] << 8);  // row gid,     component 1
             const uint32_t p2 = (uint32_t)c0[2] + ((uint32_t)c0[3] << 8);  // row gid + 8, component 0
             const uint32_t p3 = (uint32_t)c1[2] + ((uint32_t)c1[3] << 8);  // row gid + 8, component 1
-            // quad exchange: lane tig owns value tig.  Round d sends e_d = p[(tig - d) & 3] (a barrel
-            // rotation of the four shares by tig) to lane tig - d and receives lane tig + d's share
-            // with b = (p0, p3, p2, p1), e_d = b[(d - tig) & 3]: rotate b by tig & 1, then by tig & 2
+            // quad exchange: lane tig owns value tig.  Round d sends e_d = p[(tig - d) & 3] to lane tig - d
+            // and receives lane tig + d's share.  With b = (p0, p3, p2, p1), e_d = b[(d - tig) & 3]: a
+            // barrel rotation of b by tig & 1, then by tig & 2
             const uint32_t a0 = t1 ? p1 : p0, a1 = t1 ? p0 : p3, a2 = t1 ? p3 : p2, a3 = t1 ? p2 : p1;
             const uint32_t e0 = t2 ? a2 : a0, e1 = t2 ? a3 : a1, e2 = t2 ? a0 : a2, e3 = t2 ? a1 : a3;
             const uint32_t g1 = __shfl_sync(0xffffffffu, e1, (lane & ~3) | ((tig + 1) & 3));
             const uint32_t g2 = __shfl_sync(0xffffffffu, e2, (lane & ~3) | ((tig + 2) & 3));
             const uint32_t g3 = __shfl_sync(0xffffffffu, e3, (lane & ~3) | ((tig + 3) & 3));
-            // shares by source lane s = (tig + d) & 3 (the inverse rotation); lane 3's share is zero
-            // (key-byte columns 6, 7), so only sources 0, 1, 2 are placed
-            // S[s] = g[(s - tig) & 3] (g_0 = e0): the same rotation applied to the received shares
+            // shares by source lane, S[s] = g[(s - tig) & 3] (g_0 = e0): the same rotation applied to the
+            // received shares; lane 3's share is zero (key-byte columns 6, 7), so sources 0, 1, 2 are placed
             const uint32_t h0 = t1 ? g3 : e0, h1 = t1 ? e0 : g1, h2 = t1 ? g1 : g2, h3 = t1 ? g2 : g3;
             const uint32_t s0 = t2 ? h2 : h0, s1 = t2 ? h3 : h1, s2 = t2 ? h0 : h2;
-            uint64_t v = (uint64_t)s0 + ((uint64_t)s1 << 16) + ((uint64_t)s2 << 32) + pcv;
+            const uint64_t v = (uint64_t)s0 + ((uint64_t)s1 << 16) + ((uint64_t)s2 << 32) + w.pcv;
             return csub(barrett_small(v, bar, m.q), m.q);
         };
         const int QP = (Q + 1) >> 1;
         for (int u = warp; u < QP * C::NC; u += 8) {
             const int qp = u / C::NC, cf = u - qp * C::NC;
             const int q = 2 * qp;
-            const uint64_t va = unit(q, cf);
-            const uint64_t vb = q + 1 < Q ? unit(q + 1, cf) : 0;  // warp-uniform
+            const bool two = q + 1 < Q;  // warp-uniform
+            const Unit wa = load(q, cf);
+            Unit wb;
+            if (two) wb = load(q + 1, cf);
+            const uint64_t va = compute(wa);
+            const uint64_t vb = two ? compute(wb) : 0;
             unsigned char *pl = plane + cf * C::COEF + q;
             const uint32_t al = (uint32_t)va, bl = (uint32_t)vb;
             *reinterpret_cast<unsigned short *>(pl) = (unsigned short)__byte_perm(al, bl, 0x0040);

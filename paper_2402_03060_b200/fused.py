@@ -131,7 +131,7 @@ def _imma_ok(backend, level: int, O: int, Q: int) -> bool:
 def _imma_ta_ok(backend, level: int, O: int, Q: int) -> bool:
     """IMMA layers whose key switch (phase A) also runs on the tensor cores (hoist_imma.cu
     k_hoisted_imma_ta: level + 1 <= 6 digits, <= 128 terms -- LeNet conv2).  Bit-exact; measured
-    54.2 vs 56.9 ms for the LeNet conv2 call at B = 128 (30.4 ms kernel + 1.5 ms operand re-layout vs
+    53.3 vs 56.9 ms for the LeNet conv2 call at B = 128 (29.4 ms kernel + 1.5 ms operand re-layout vs
     34.7 ms for the IMAD phase A).  ``UH_IMMA_TA=0`` keeps phase A on IMAD."""
     if os.environ.get("UH_IMMA_TA", "1") == "0":
         return False
@@ -348,7 +348,8 @@ def conv_mac_work(shifts, half, n, B, I, O, level, path) -> dict:
 
     ``a40``/``b40``: the 40-bit limbs q_1..q_level; ``a60``/``b60``: the 60-bit q_0 and P.
     ``path``: "tc" (tcgen05: b40 as 25 and b60 as 64 u8 byte products per modMAC on the tensor
-    cores), "imma8" (mma.sync: b40 and b60 on the tensor cores, both phase A on IMAD), "imma"
+    cores), "ta" (as "imma8" with a40 -- the key switch of the 40-bit limbs -- on the tensor cores as
+    well, 25 u8 products per modMAC), "imma8" (mma.sync: b40 and b60 on the tensor cores, both phase A on IMAD), "imma"
     (mma.sync: b40 on the tensor cores, q_0 / P on IMAD) or "imad"."""
     T = len(shifts)
     nz = sum(1 for s in shifts if s % half)
@@ -428,6 +429,8 @@ def conv(backend, state: CipherState, layer) -> CipherState:
         t1.record(torch.cuda.current_stream(backend.device))
         # imma8: q_0 / P contracted on the 8-byte IMMA kernel too (hoist_imma.cu imma8_ok)
         path = "tc" if tc else (("imma8" if os.environ.get("UH_IMMA8", "1") != "0" else "imma") if imma else "imad")
+        if path == "imma8" and _imma_ta_ok(backend, level, O, I * T):
+            path = "ta"  # phase A of the 40-bit limbs on the tensor cores too (k_hoisted_imma_ta)
         timer.append(("conv_hoisted_mac", level, t0, t1,
                       conv_mac_work(shifts, backend.params.num_slots, n, B, I, O, level, path)))
     del D
