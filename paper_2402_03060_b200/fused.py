@@ -128,12 +128,16 @@ def _imma_ok(backend, level: int, O: int, Q: int) -> bool:
     return backend.kernel_supported("uh_imma_supported", level, O, Q)
 
 
-def _imma_ta_ok(backend, level: int, O: int, Q: int) -> bool:
+def _imma_ta_ok(backend, level: int, O: int, Q: int, B: int) -> bool:
     """IMMA layers whose key switch (phase A) also runs on the tensor cores (hoist_imma.cu
     k_hoisted_imma_ta: level + 1 <= 6 digits, <= 128 terms -- LeNet conv2).  Bit-exact; measured
     53.3 vs 56.9 ms for the LeNet conv2 call at B = 128 (29.4 ms kernel + 1.5 ms operand re-layout vs
     34.7 ms for the IMAD phase A).  ``UH_IMMA_TA=0`` keeps phase A on IMAD."""
     if os.environ.get("UH_IMMA_TA", "1") == "0":
+        return False
+    # its tile is 16 ciphertexts (one m16 MMA), the IMAD kernel's 4: a batch that leaves the last tile
+    # mostly empty (a single ciphertext: 6.2 vs 4.2 ms per evaluation) stays on the IMAD phase A
+    if os.environ.get("UH_IMMA_TA") != "1" and 0.87 * 16 * -(-B // 16) > 4 * -(-B // 4):
         return False
     return backend.kernel_supported("uh_imma_ta_supported", level, O, Q)
 
@@ -158,7 +162,7 @@ def _imma_mac(backend, acc, X, L, D, masks, shifts, sh, B, I, T, O, level, st):
     key switch too where the shape allows (uh_hoisted_mac_imma_ta), else on IMAD (uh_hoisted_mac_imma)."""
     kb = key_bank(backend, shifts, level)
     ib = imma_bank(backend, masks, O, I * T, level, cache=_banked(backend, masks))
-    if _imma_ta_ok(backend, level, O, I * T):
+    if _imma_ta_ok(backend, level, O, I * T, B):
         kt = imma_ta_bank(backend, kb, sh, T, level)
         backend._call("uh_hoisted_mac_imma_ta", _vp(acc), _vp(X), L, _vp(D), _vp(ib), _vp(kt), _vp(kb), _vp(sh), B, I,
                       T, O, level, st)
@@ -429,7 +433,7 @@ def conv(backend, state: CipherState, layer) -> CipherState:
         t1.record(torch.cuda.current_stream(backend.device))
         # imma8: q_0 / P contracted on the 8-byte IMMA kernel too (hoist_imma.cu imma8_ok)
         path = "tc" if tc else (("imma8" if os.environ.get("UH_IMMA8", "1") != "0" else "imma") if imma else "imad")
-        if path == "imma8" and _imma_ta_ok(backend, level, O, I * T):
+        if path == "imma8" and _imma_ta_ok(backend, level, O, I * T, B):
             path = "ta"  # phase A of the 40-bit limbs on the tensor cores too (k_hoisted_imma_ta)
         timer.append(("conv_hoisted_mac", level, t0, t1,
                       conv_mac_work(shifts, backend.params.num_slots, n, B, I, O, level, path)))

@@ -292,7 +292,7 @@ def test_imma_tensor_phase_a_equals_key_bank_kernel(O, level, I, shifts, B, monk
     X = fused.stack_cts(be, cts, level)
     mdev = torch.from_numpy(_rand_masks(o, rng, O, I * len(shifts), level).view(np.int64)).to(be.device)
     monkeypatch.setenv("UH_IMMA", "1")
-    assert fused._imma_ok(be, level, O, I * len(shifts)) and fused._imma_ta_ok(be, level, O, I * len(shifts))
+    assert fused._imma_ok(be, level, O, I * len(shifts)) and fused._imma_ta_ok(be, level, O, I * len(shifts), B)
     got = fused._hoist(be, X, level, shifts, mdev, O, False, B)
     monkeypatch.setenv("UH_IMMA", "0")
     want = fused._hoist(be, X, level, shifts, mdev, O, False, B)
