@@ -342,10 +342,10 @@ void launch_imma(const Ctx &c, uint64_t *acc, const uint64_t *X, const uint64_t 
 // the epilogue stages each warp's C fragments in shared memory and recombines every (output,
 // column) on two lanes (4 mask bytes each), summed with one 128-bit shuffle.
 #ifndef UH_IMMA8_NC
-#define UH_IMMA8_NC 4  // coefficients per CTA (3 CTAs / SM: 70.7 KB of shared memory each)
-#endif
+#define UH_IMMA8_NC 8  // coefficients per CTA up to 4 k-steps: 64-byte runs at 2 CTAs / SM (106 KB each) measured
+#endif                 // 52.35 vs 53.3 ms for the LeNet conv2 call at B = 128 against 4 coefficients at 3 CTAs / SM
 #ifndef UH_IMMA8_MINB
-#define UH_IMMA8_MINB 3
+#define UH_IMMA8_MINB 2
 #endif
 #ifndef UH_IMMA8_NC_WIDE
 #define UH_IMMA8_NC_WIDE 2  // past 4 k-steps (3 CTAs / SM)
@@ -363,6 +363,7 @@ template <int NKS> struct IW8 {
     // per half-warp) and the epilogue reads (rows i, i + 4, i + 8, i + 12) hit 32 distinct banks
     static constexpr int CS = 64;
     static constexpr size_t SMEM = (size_t)NC * COEF + 8 * 16 * CS * 4;
+    static constexpr int MINB = NKS > 4 ? 3 : UH_IMMA8_MINB;  // the wide tiles keep 3 CTAs / SM
 };
 __device__ __forceinline__ int stage8_col(int row, int col) {
     const int g = ((row & 3) + (row >> 2)) & 3;
@@ -411,7 +412,7 @@ __global__ void k_imma_bank8(uint32_t *__restrict__ ib, const uint64_t *__restri
 }
 
 template <int L, int LOGN, int NKS>
-__global__ void __launch_bounds__(256, UH_IMMA8_MINB)
+__global__ void __launch_bounds__(256, IW8<NKS>::MINB)
     k_hoisted_imma8(uint64_t *__restrict__ acc_out, const uint64_t *__restrict__ X, const uint64_t *__restrict__ D,
                     const uint4 *__restrict__ ib, const uint64_t *__restrict__ kbank, const int32_t *__restrict__ shifts,
                     int B, int I, int T, int O, int sp, const Mod *__restrict__ mods) {
