@@ -52,8 +52,12 @@ class _Job:
         lo, hi = shard_range(self.n_groups, self.rank, self.world)
         mine = [samples[g * cap:min(n, (g + 1) * cap)] for g in range(lo, hi)]
         self.counts = [len(g) for g in mine]
+        if (isinstance(samples, np.ndarray) and samples.ndim == 4 and samples.dtype == np.float64 and mine
+                and min(self.counts) == cap):
+            # full groups of one contiguous array: hand pack_groups the [B, capacity, C, H, W] view
+            mine = samples[lo * cap:hi * cap].reshape((hi - lo, cap) + samples.shape[1:])
         self.planes = None
-        if mine:
+        if len(mine):
             shape = (m.channels, len(mine), self.plan.num_slots)
             if self.on_gpu:
                 host = torch.empty(shape, dtype=torch.float64, pin_memory=pinned and torch.cuda.is_available())

@@ -128,3 +128,24 @@ def test_batched_sim_equals_solo():
         solo, _, _ = driver.run_inference(m, g, params, plan=plan, backend=SimBackend(params))
         for x, y in zip(outs[b], solo):
             assert np.array_equal(x, y)
+
+
+def test_pack_groups_fast_path_equals_reference_packing():
+    """driver.pack_groups' block-copy path (full groups given as one [B, capacity, C, H, W] array,
+    regular offsets) writes exactly planner.batch_pack's layout (packing.py:94-119), into a dirty
+    ``out`` buffer too; ragged groups keep the general path."""
+    params = HEParams(poly_degree=1 << 13, depth=9, scale_bits=40)
+    m = planner.lenet1(0)
+    plan = planner.footprint(m, params)
+    rng = np.random.default_rng(3)
+    B, cap = 3, plan.capacity
+    imgs = rng.uniform(0, 1, size=(B * cap, m.channels, m.height, m.width))
+    want = np.stack([[pv.values for pv in planner.batch_pack([planner.flatten_input(s) for s in imgs[b * cap:(b + 1) * cap]],
+                                                            plan)] for b in range(B)], axis=1)
+    out = np.full((m.channels, B, plan.num_slots), 7.0)
+    got = driver.pack_groups(m, imgs.reshape(B, cap, m.channels, m.height, m.width), plan, out=out)
+    assert got is out and np.array_equal(got, want)
+    slow = driver.pack_groups(m, [list(imgs[b * cap:(b + 1) * cap]) for b in range(B)], plan)
+    assert np.array_equal(slow, want)
+    ragged = driver.pack_groups(m, [imgs[:cap], imgs[cap:cap + 2]], plan)
+    assert np.array_equal(ragged[:, 0], want[:, 0]) and not ragged[:, 1, plan.offsets[2]:].any()
