@@ -299,6 +299,19 @@ def test_imma_tensor_phase_a_equals_key_bank_kernel(O, level, I, shifts, B, monk
     assert torch.equal(got, want)
 
 
+def test_tensor_phase_a_selection(monkeypatch):
+    """The tensor-core phase A serves the shapes it is compiled for (level + 1 <= 6, <= 128 terms) and
+    only batches that fill its 16-ciphertext tiles; everything else keeps the IMAD phase A."""
+    be, _ = _c2()
+    monkeypatch.delenv("UH_IMMA_TA", raising=False)
+    assert fused._imma_ta_ok(be, 5, 12, 100, 128) and fused._imma_ta_ok(be, 5, 12, 100, 13)
+    assert not fused._imma_ta_ok(be, 5, 12, 100, 1) and not fused._imma_ta_ok(be, 5, 12, 100, 17)
+    assert not fused._imma_ta_ok(be, 6, 12, 100, 128)   # 7 digits: 35 bytes > one k-step
+    assert not fused._imma_ta_ok(be, 5, 12, 150, 128)   # > 128 terms
+    monkeypatch.setenv("UH_IMMA_TA", "0")
+    assert not fused._imma_ta_ok(be, 5, 12, 100, 128)
+
+
 @pytest.mark.parametrize("O,level,I,shifts,B", [
     (12, 5, 4, [a + 28 * b for b in range(5) for a in range(5)], 13),  # LeNet conv2 shape, partial ct tiles
     (4, 7, 1, [a + 28 * b for b in range(5) for a in range(5)], 9),    # LeNet conv1 shape (O <= 8: M = 64 on q_0 / P)
