@@ -159,14 +159,15 @@ Ctx *ctx_create(uint32_t n, const uint64_t *moduli, const uint64_t *psi, uint32_
     for (uint32_t k = 0; k < n; k++) sob[k] = dlog[2 * h_brv(k, c->logn) + 1];
     // pass-2 block selection and per-slot element index for the coalesced
     // slot-order I/O of the fast NTT (see ntt_fast.cu, cta_slot)
-    std::vector<int32_t> bsel, csl;
+    std::vector<int32_t> bsel;
+    std::vector<uint8_t> csl;
     if (c->n1) {
         const uint32_t n1 = c->n1, n2 = c->n2, G = 4096 / n2, per_half = (n1 / 2) / G;
         bsel.assign(n1, -1);
         csl.assign(n, 0);
         std::vector<int32_t> k_of(n);
         for (uint32_t k = 0; k < n; k++) {
-            csl[sob[k]] = (int32_t)(k % n2);
+            csl[sob[k]] = (uint8_t)(k % n2);  // n2 <= 256
             k_of[sob[k]] = (int32_t)k;
         }
         for (uint32_t blk = 0; blk < n1; blk++) {

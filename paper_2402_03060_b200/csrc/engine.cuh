@@ -31,7 +31,7 @@ struct Ctx {
     double2 *d_tfR = nullptr, *d_itfR = nullptr;    // [count][16] (R, R / q) at (1 << s') - 1 + v
     int32_t *d_sob = nullptr;            // [n] slot-order index of bit-reversed NTT output k
     int32_t *d_bsel = nullptr;           // [n1] pass-2 block of CTA x, position g (ntt_fast.cu)
-    int32_t *d_csl = nullptr;            // [n] element index inside its pass-2 block, per slot
+    uint8_t *d_csl = nullptr;            // [n] element index (< 256) inside its pass-2 block, per slot: 32 KB, L1-resident
     uint64_t *d_inv = nullptr, *d_invs = nullptr;  // [count][count]: q_j^-1 mod q_i at [i*count+j]
     uint64_t *d_inv2 = nullptr, *d_inv2s = nullptr;  // [count][count]: (q_j * P)^-1 mod q_i at [i*count+j]
     ulonglong2 *d_pmod = nullptr;        // [count] (P mod q_i, Shoup companion)

@@ -522,7 +522,7 @@ struct InGlobal {
 };
 template <int B, int EM>
 __device__ __forceinline__ void fwd_p2_epilogue(const uint64_t *sm, const LimbInfo &li, uint64_t q,
-                                                const int32_t *__restrict__ csl, int logn, int tid);
+                                                const uint8_t *__restrict__ csl, int logn, int tid);
 
 // pass 2 forward stages: tmp (pass-1 output) -> canonical residues in shared memory
 // FP64 limbs form their twiddles from the composite tables (TwC); the 60-bit limbs read
@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_P2_MINB) k_fwd_p2(NttJob J, c
                                                     const TwTabs tt,
                                                     const double2 *__restrict__ twf,
                                                     const int32_t *__restrict__ bsel,
-                                                    const int32_t *__restrict__ csl) {
+                                                    const uint8_t *__restrict__ csl) {
     using C = P2<B>;
     extern __shared__ uint64_t dsm[];
     uint64_t *sm = dsm;
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_P2_MINB) k_fwd_p2(NttJob J, c
 // issued together, then the shared-memory gathers and the stores
 template <int B, int EM>
 __device__ __forceinline__ void fwd_p2_epilogue(const uint64_t *sm, const LimbInfo &li, uint64_t q,
-                                                const int32_t *__restrict__ csl, int logn, int tid) {
+                                                const uint8_t *__restrict__ csl, int logn, int tid) {
     using C = P2<B>;
     constexpr int E = EM ? 8 : 16;  // loads in flight per round (register budget)
 #pragma unroll
@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_P2_MINB) k_inv_pa(NttJob J, u
                                                     const TwTabs tt,
                                                     const double2 *__restrict__ itwf,
                                                     const int32_t *__restrict__ bsel,
-                                                    const int32_t *__restrict__ csl) {
+                                                    const uint8_t *__restrict__ csl) {
     using C = P2<B>;
     extern __shared__ uint64_t dsm[];
     uint64_t *sm = dsm;
