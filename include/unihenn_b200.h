@@ -86,6 +86,14 @@ int uh_divide_top(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int n_polys, i
  * from ModDown-then-rescale by < 1 unit). */
 int uh_divide_top2(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int n_polys, int level, int out_ps, int in_ps,
                    void *stream);
+/* uh_divide_top2 with the conv bias (layers.conv, layers.py:193-195) added in the same pass:
+ * bias[n_polys / bias_group][level][N] (evaluation form at the output level), row set p / bias_group
+ * added to the even polynomials (the c0 of each (c0, c1) pair); residues identical to
+ * uh_divide_top2 followed by uh_elementwise_grouped.  Supported with the fast NTT
+ * (uh_divide_top2_bias_supported: 2^13 <= N <= 2^15). */
+int uh_divide_top2_bias_supported(uh_ctx *ctx);
+int uh_divide_top2_bias(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int n_polys, int level, int out_ps,
+                        int in_ps, const uint64_t *bias, int bias_group, void *stream);
 
 /* Rescale of a ciphertext batch at `level` (the level-1 of he_backend.py:226-247). */
 int uh_rescale(uh_ctx *ctx, uint64_t *out, const uint64_t *in, int B, int level, int out_ls, int in_ls,

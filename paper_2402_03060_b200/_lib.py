@@ -30,6 +30,7 @@ SIGNATURES = {
     "uh_divide_top": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_rescale": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp],
     "uh_divide_top2": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp],
+    "uh_divide_top2_bias": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
     "uh_modup": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp],
     "uh_key_inner": [_vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_i64, _vp],
     "uh_keyswitch": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
@@ -69,6 +70,7 @@ EXTRA = {"uh_abi_version": ([], _c_int), "uh_last_error": ([], ctypes.c_char_p),
          "uh_launch_count": ([], ctypes.c_ulonglong), "uh_bench_peaks": ([_vp, _vp], _c_int),
          "uh_hoisted_bank_supported": ([_vp, _c_int, _c_int], _c_int),
          "uh_km_supported": ([_vp, _c_int], _c_int),
+         "uh_divide_top2_bias_supported": ([_vp], _c_int),
          "uh_imma_supported": ([_vp, _c_int, _c_int, _c_int], _c_int),
          "uh_imma_ta_supported": ([_vp, _c_int, _c_int, _c_int], _c_int),
          "uh_imma_ta_bank_bytes": ([_vp, _c_int, _c_int], ctypes.c_ulonglong),

@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <string>
 #include "../../include/unihenn_b200.h"
+#include "ntt_fast.cuh"
 #include "ops.cuh"
 
 struct uh_ctx {
@@ -134,6 +135,24 @@ __attribute__((visibility("default"))) int uh_divide_top2(uh_ctx *ctx, uint64_t 
         need(level >= 1, "fused ModDown + rescale needs level >= 1");
         need(out != in, "out of place");
         uh::divide_top2(c, out, in, n_polys, level, out_ps, in_ps, S(stream));
+    });
+}
+
+__attribute__((visibility("default"))) int uh_divide_top2_bias_supported(uh_ctx *ctx) {
+    return ctx && uh::ntt_fast_supported(C(ctx)) ? 1 : 0;
+}
+
+__attribute__((visibility("default"))) int uh_divide_top2_bias(uh_ctx *ctx, uint64_t *out, const uint64_t *in,
+                                                               int n_polys, int level, int out_ps, int in_ps,
+                                                               const uint64_t *bias, int bias_group, void *stream) {
+    return guard([&] {
+        const uh::Ctx &c = C(ctx);
+        check_level(c, level);
+        need(level >= 1, "fused ModDown + rescale needs level >= 1");
+        need(out != in, "out of place");
+        need(bias != nullptr && bias_group >= 2 && bias_group % 2 == 0 && n_polys % bias_group == 0,
+             "bias rows cover whole (c0, c1) pairs: even bias_group dividing n_polys");
+        uh::divide_top2(c, out, in, n_polys, level, out_ps, in_ps, S(stream), bias, bias_group);
     });
 }
 

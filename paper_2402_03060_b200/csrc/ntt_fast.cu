@@ -54,6 +54,7 @@ struct LimbInfo {
     ulonglong2 pinv;      // P^-1 mod q_top (Shoup pair)
     ulonglong2 pk;        // P mod q_k (Shoup pair)
     Mod mt;               // the top modulus
+    const uint64_t *bias; // DIVIDE2: row added to the result (c0 polynomials), or null
 };
 
 __device__ __forceinline__ int job_limb(const NttJob &J, int i) { return i; }
@@ -63,6 +64,7 @@ __device__ __forceinline__ LimbInfo limb_info(const NttJob &J, int f, int logn, 
     li.mode = J.mode;
     li.qsrc = 0;
     li.in = nullptr;
+    li.bias = nullptr;
     li.w = li.ws = 0;
     if (J.mode == NTT_DIVIDE2) {
         const int p = f / J.nl, k = f - p * J.nl;
@@ -74,6 +76,7 @@ __device__ __forceinline__ LimbInfo limb_info(const NttJob &J, int f, int logn, 
         li.qsrc = 1;
         li.dst = J.dst + (((size_t)p * J.dst_ps + k) << logn);
         li.in = J.in + (((size_t)p * J.in_ps + k) << logn);
+        li.bias = J.bias && !(p & 1) ? J.bias + (((size_t)(p / J.bias_group) * J.nl + k) << logn) : nullptr;
         li.w = J.inv2[(size_t)k * cnt + t];  // (q_t P)^-1 mod q_k
         li.ws = J.inv2s[(size_t)k * cnt + t];
         li.mt = mods[t];
@@ -637,8 +640,11 @@ __device__ __forceinline__ void fwd_p2_epilogue(const uint64_t *sm, const LimbIn
             const uint64_t y = sm[C::at(i % C::G, cs[e])];
             if (EM == 1)
                 li.dst[s] = csub(shoup_lazy(submod(a[e], y, q), li.w, li.ws, q), q);
-            else if (EM == 2)
-                li.dst[s] = shoup(submod(a[e], y, q), li.w, li.ws, q);
+            else if (EM == 2) {
+                uint64_t r = shoup(submod(a[e], y, q), li.w, li.ws, q);
+                if (li.bias) r = addmod(r, __ldg(li.bias + s), q);  // CTA-uniform
+                li.dst[s] = r;
+            }
             else
                 li.dst[s] = y;
         }

@@ -34,6 +34,10 @@ struct NttJob {
     const uint64_t *inv = nullptr, *invs = nullptr;
     const uint64_t *inv2 = nullptr, *inv2s = nullptr;  // DIVIDE2: (q_top * P)^-1 mod q_k (Shoup pairs)
     const ulonglong2 *pmod = nullptr;  // DIVIDE2: (P mod q_i, Shoup companion) per modulus
+    // DIVIDE2: optional plaintext rows added to the even polynomials (c0) in the epilogue -- the conv
+    // bias: bias[p / bias_group][nl][N], one row set per bias_group polynomials
+    const uint64_t *bias = nullptr;
+    int bias_group = 1;
 };
 
 bool ntt_fast_supported(const Ctx &c);

@@ -465,9 +465,11 @@ __global__ void k_crt2_pre(uint64_t *top, int n_polys, int logn, Mod mt, uint64_
 }  // namespace
 
 void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, int level, int out_ps, int in_ps,
-                 cudaStream_t s) {
+                 cudaStream_t s, const uint64_t *bias, int bias_group) {
     if (!n_polys) return;
     const size_t N = c.n;
+    if (bias && (!ntt_fast_supported(c) || level == 0 || bias_group < 1))
+        throw std::invalid_argument("fused bias needs the fast NTT (2^13 <= N <= 2^15) and level >= 1");
     if (!ntt_fast_supported(c)) {  // small N: the two divisions in sequence
         Scratch t((size_t)n_polys * (level + 1) * N * 8, s);
         divide_top(c, t.as<uint64_t>(), in, n_polys, level + 1, c.sp(), level + 1, in_ps, s);
@@ -510,6 +512,8 @@ void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, i
     Jf.invs = c.d_invs;
     Jf.inv2 = c.d_inv2;
     Jf.inv2s = c.d_inv2s;
+    Jf.bias = bias;
+    Jf.bias_group = bias ? bias_group : 1;
     Jf.pmod = c.d_pmod;
     ntt_fast_forward(c, Jf, n_polys * level, s);
 }

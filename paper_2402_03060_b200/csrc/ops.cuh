@@ -31,8 +31,10 @@ void divide_top(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, in
 
 // Fused ModDown + rescale: in n_polys x (level + 2) limbs (q_0..q_level, P) -> out n_polys x level limbs,
 // the centred division by q_level * P (one inverse NTT pair, one forward NTT per output limb).
+// bias (optional): plaintext rows bias[p / bias_group][level][N] added to the even polynomials (c0) in the
+// forward NTT's epilogue -- the conv bias, without a pass of its own.
 void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, int level, int out_ps, int in_ps,
-                 cudaStream_t s);
+                 cudaStream_t s, const uint64_t *bias = nullptr, int bias_group = 1);
 
 // ModUp of n_polys polys at level l (L = l + 1 limbs, strided in_ps) into
 // D = [n_polys][L digits][L + 1 limbs (q_0..q_l, P)][N], compact.

@@ -439,13 +439,18 @@ def conv(backend, state: CipherState, layer) -> CipherState:
                       conv_mac_work(shifts, backend.params.num_slots, n, B, I, O, level, path)))
     del D
     out = backend._empty(O, B, 2, level, n)  # ModDown + rescale as one centred division by q_level * P
-    backend._call("uh_divide_top2", _vp(out), _vp(acc), O * B * 2, level, level, LP, st)
-    del acc
     bias = bias_bank(backend, layer, out_lay, level - 1, scale)
-    Lo = level
-    # bias of output channel o onto c0 of its B ciphertexts, all channels in one launch
-    backend._call("uh_elementwise_grouped", OP_ADD, _vp(out), _vp(out), _vp(bias), O * B, O, B, Lo, Lo, 2 * Lo,
-                  2 * Lo, Lo, st)
+    if os.environ.get("UH_FUSED_BIAS", "1") != "0" and backend.kernel_supported("uh_divide_top2_bias_supported"):
+        # ... with the bias of output channel o added to c0 of its B ciphertexts in the same epilogue
+        backend._call("uh_divide_top2_bias", _vp(out), _vp(acc), O * B * 2, level, level, LP, _vp(bias), 2 * B, st)
+        del acc
+    else:
+        backend._call("uh_divide_top2", _vp(out), _vp(acc), O * B * 2, level, level, LP, st)
+        del acc
+        Lo = level
+        # bias of output channel o onto c0 of its B ciphertexts, all channels in one launch
+        backend._call("uh_elementwise_grouped", OP_ADD, _vp(out), _vp(out), _vp(bias), O * B, O, B, Lo, Lo, 2 * Lo,
+                      2 * Lo, Lo, st)
     del keys
     return CipherState([CipherVector(out[o], level - 1, scale, backend) for o in range(O)], out_lay)
 
