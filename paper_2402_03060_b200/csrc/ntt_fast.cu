@@ -730,10 +730,17 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_P2_MINB) k_inv_pa(NttJob J, u
         int cs[E];
         uint64_t a[E];
 #pragma unroll
+        uint64_t *dg = nullptr;  // ModUp diagonal D[p][k][k] (CTA-uniform)
+        if (J.diag) {
+            const int p = f / J.nl, k = f - p * J.nl;
+            dg = J.diag + (((size_t)(p * J.nl + k) * (J.nl + 1) + k) << logn);
+        }
+#pragma unroll
         for (int e = 0; e < E; e++) {
             const size_t s = cta_slot<B>(tid + kThreads * e, logn);
             cs[e] = __ldg(csl + s);
             a[e] = li.src[s];
+            if (dg) dg[s] = a[e];
         }
 #pragma unroll
         for (int e = 0; e < E; e++) sm[C::at((tid + kThreads * e) % C::G, cs[e])] = a[e];

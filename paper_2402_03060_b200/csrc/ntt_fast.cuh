@@ -38,6 +38,9 @@ struct NttJob {
     // bias: bias[p / bias_group][nl][N], one row set per bias_group polynomials
     const uint64_t *bias = nullptr;
     int bias_group = 1;
+    // inverse, PLAIN: optional copy of every input limb (p, k) to diag[((p * nl + k) * (nl + 1) + k)][N] --
+    // the diagonal of a ModUp output, written while the limb streams through the first pass
+    uint64_t *diag = nullptr;
 };
 
 bool ntt_fast_supported(const Ctx &c);

@@ -518,6 +518,9 @@ void divide_top2(const Ctx &c, uint64_t *out, const uint64_t *in, int n_polys, i
     ntt_fast_forward(c, Jf, n_polys * level, s);
 }
 
+#ifndef UH_MODUP_DIAG_IN_NTT
+#define UH_MODUP_DIAG_IN_NTT 1
+#endif
 void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level, int in_ps, cudaStream_t s,
            bool diag) {
     int L = level + 1;
@@ -532,7 +535,10 @@ void modup(const Ctx &c, uint64_t *D, const uint64_t *in, int n_polys, int level
         Ji.src_ps = in_ps;
         Ji.dst = C.as<uint64_t>();
         Ji.dst_ps = L;
+        const bool diag_in_ntt = diag && UH_MODUP_DIAG_IN_NTT;
+        if (diag_in_ntt) Ji.diag = D;  // D[p][j][j] = in[p][j], written by the inverse NTT's first pass
         ntt_fast_inverse(c, Ji, n_polys * L, s);
+        if (diag_in_ntt) diag = false;
         NttJob Jf;  // centred lift of digit j into every QP limb, fused into the forward NTT's loads
         Jf.mode = NTT_MODUP;
         Jf.L = L;
