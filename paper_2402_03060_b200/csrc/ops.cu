@@ -351,6 +351,28 @@ __global__ void __launch_bounds__(256) k_tensor2(uint64_t *__restrict__ T, uint6
     D2[((bb * L + k) << logn) + n] = mulmod(a1, b1, m);
 }
 
+// the square (a == b): (a0^2, 2 a0 a1, a1^2), two coefficients per thread (16-byte loads / stores);
+// grid (N / 512, L, B)
+__global__ void __launch_bounds__(256) k_tensor2_sq(uint64_t *__restrict__ T, uint64_t *__restrict__ D2,
+                                                    const uint64_t *__restrict__ a, int L, int a_ls, int logn,
+                                                    const Mod *__restrict__ mods) {
+    const size_t n = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2, bb = blockIdx.z;
+    const int k = blockIdx.y;
+    const Mod m = mods[k];
+    const ulonglong2 a0 = __ldg(reinterpret_cast<const ulonglong2 *>(a + (((bb * 2) * a_ls + k) << logn) + n));
+    const ulonglong2 a1 = __ldg(reinterpret_cast<const ulonglong2 *>(a + (((bb * 2 + 1) * a_ls + k) << logn) + n));
+    auto twice = [&](uint64_t x, uint64_t y) {  // 2 x y mod q, canonical
+        const uint64_t v = mulmod(x, y, m);
+        return csub(v + v, m.q);
+    };
+    *reinterpret_cast<ulonglong2 *>(T + (((bb * 2) * L + k) << logn) + n) =
+        make_ulonglong2(mulmod(a0.x, a0.x, m), mulmod(a0.y, a0.y, m));
+    *reinterpret_cast<ulonglong2 *>(T + (((bb * 2 + 1) * L + k) << logn) + n) =
+        make_ulonglong2(twice(a0.x, a1.x), twice(a0.y, a1.y));
+    *reinterpret_cast<ulonglong2 *>(D2 + ((bb * L + k) << logn) + n) =
+        make_ulonglong2(mulmod(a1.x, a1.x, m), mulmod(a1.y, a1.y, m));
+}
+
 // u[p][k] += (P mod q_k) * t[p][k] for the q-limbs k < L of QP-basis polys (u has L + 1 limbs, t has L)
 __global__ void k_add_pscaled(uint64_t *u, const uint64_t *t, int n_polys, int L, int sp, int logn,
                               const Mod *__restrict__ mods, const ulonglong2 *__restrict__ pmod) {
@@ -700,7 +722,10 @@ void ct_mul_relin_rescale_fused(const Ctx &c, uint64_t *out, const uint64_t *a, 
     int L = level + 1;
     size_t N = c.n;
     Scratch T((size_t)B * 2 * L * N * 8, s), D2((size_t)B * L * N * 8, s);
-    if (N >= 256 && B <= 65535)
+    if (a == b && a_ls == b_ls && N >= 512 && B <= 65535)  // the square activation
+        k_tensor2_sq<<<dim3((unsigned)(N / 512), L, B), 256, 0, s>>>(T.as<uint64_t>(), D2.as<uint64_t>(), a, L, a_ls,
+                                                                     (int)c.logn, c.d_mods);
+    else if (N >= 256 && B <= 65535)
         k_tensor2<<<dim3((unsigned)(N / 256), L, B), 256, 0, s>>>(T.as<uint64_t>(), D2.as<uint64_t>(), a, b, L, a_ls,
                                                                   b_ls, (int)c.logn, c.d_mods);
     else
