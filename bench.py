@@ -582,24 +582,36 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region: value ----
-    be.kernel_timer = []
-    clocks = Clocks(local)
-    barrier()
-    torch.cuda.synchronize()
-    l0 = _lib.launch_count()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    torch.cuda.profiler.start()  # `ncu --profile-from-start off` sees the timed steps only
-    e0.record(stream)
-    for _ in range(args.steps):
-        final = eval_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    torch.cuda.profiler.stop()
-    barrier()
-    launches = _lib.launch_count() - l0
-    clk = clocks.stop()
-    ms = allreduce_max(e0.elapsed_time(e1))
+    # EXACTLY args.steps steps between one event pair (barrier + synchronize on both sides, max over
+    # ranks).  Every step also gets its own event, only to detect a one-off stall from outside the
+    # engine (an NVML query or an allocator growth holding kernel submission: one run in ~8 on the
+    # pool's boxes showed a single ~230 ms gap, the CUDA-graph replay of the same steps none): if one
+    # step takes more than 1.15x the median step the region is measured once more, like the contract's
+    # re-measurement of a throttled run, and the first attempt is reported next to it.
+    first_attempt = None
+    for attempt in range(2):
+        be.kernel_timer = []
+        clocks = Clocks(local)
+        barrier()
+        torch.cuda.synchronize()
+        l0 = _lib.launch_count()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        torch.cuda.profiler.start()  # `ncu --profile-from-start off` sees the timed steps only
+        ev[0].record(stream)
+        for i in range(args.steps):
+            final = eval_step()
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        barrier()
+        launches = _lib.launch_count() - l0
+        clk = clocks.stop()
+        ms = allreduce_max(ev[0].elapsed_time(ev[-1]))
+        each = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+        stalled = allreduce_max(max(each) / float(np.median(each))) > 1.15 if args.steps >= 3 else False
+        if not stalled or attempt == 1:
+            break
+        first_attempt = {"ms_per_step": ms / args.steps, "step_ms_each": each}
     value = world * B * cap * args.steps / (ms / 1e3)
     timers = be.kernel_timer
     be.kernel_timer = None
@@ -753,7 +765,8 @@ def main():
                 "data": "synthetic (seeded U[0,1] images, seeded N(0,0.1^2) weights)",
                 "config": _config(B, world), "e2e": e2e, "roofline": roofline, "rooflines": rooflines,
                 "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk, "peaks": peaks, "check": check,
-                "graph": graph, "latency_batch1": lat, "dropin_oplevel": dropin}
+                "graph": graph, "latency_batch1": lat, "dropin_oplevel": dropin,
+                "step_ms_each": each, "remeasured_after_stall": first_attempt}
         print(json.dumps(line), flush=True)
         if args.peaks_out:
             with open(args.peaks_out, "w") as f:
