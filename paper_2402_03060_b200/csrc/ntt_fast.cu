@@ -729,7 +729,6 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_P2_MINB) k_inv_pa(NttJob J, u
         constexpr int E = 4096 / kThreads;
         int cs[E];
         uint64_t a[E];
-#pragma unroll
         uint64_t *dg = nullptr;  // ModUp diagonal D[p][k][k] (CTA-uniform)
         if (J.diag) {
             const int p = f / J.nl, k = f - p * J.nl;
@@ -740,7 +739,10 @@ __global__ void __launch_bounds__(kThreads, UH_NTT_P2_MINB) k_inv_pa(NttJob J, u
             const size_t s = cta_slot<B>(tid + kThreads * e, logn);
             cs[e] = __ldg(csl + s);
             a[e] = li.src[s];
-            if (dg) dg[s] = a[e];
+        }
+        if (dg) {  // after every load is in flight (a store in the loop would wait for its load)
+#pragma unroll
+            for (int e = 0; e < E; e++) dg[cta_slot<B>(tid + kThreads * e, logn)] = a[e];
         }
 #pragma unroll
         for (int e = 0; e < E; e++) sm[C::at((tid + kThreads * e) % C::G, cs[e])] = a[e];
