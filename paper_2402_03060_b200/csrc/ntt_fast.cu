@@ -21,6 +21,9 @@
 //                  mod q_k and the epilogue writes (in[p][k] - y) * q_top^-1.
 #include "ntt_fast.cuh"
 
+#ifndef UH_NTT_P1_LOADS_FIRST
+#define UH_NTT_P1_LOADS_FIRST 1
+#endif
 #ifndef UH_NTT_P2_WARPSYNC
 #define UH_NTT_P2_WARPSYNC 1  // N2 = 256: the pass-2 exchange is warp-local (0.306 vs 0.310 us/limb forward)
 #endif
@@ -131,6 +134,18 @@ template <int LM>
 __device__ __forceinline__ uint64_t load_t(const LimbInfo &li, size_t idx, const Mod &m, bool red) {
     if (LM == 2) return crt2_to(li.src[idx], li.src2[idx], li, m);
     const uint64_t x = li.src[idx];
+    if (LM == 0) return x;
+    const uint64_t p = li.qsrc;
+    const bool neg = x > ((p - 1) >> 1);
+    uint64_t v = neg ? p - x : x;
+    if (red) v = csub(barrett_lite(v, m), m.q);
+    const uint64_t nv = v ? m.q - v : 0;
+    return neg ? nv : v;
+}
+
+// the transform of load_t on an already loaded word (LM 0 / 1)
+template <int LM>
+__device__ __forceinline__ uint64_t lift_t(uint64_t x, const LimbInfo &li, const Mod &m, bool red) {
     if (LM == 0) return x;
     const uint64_t p = li.qsrc;
     const bool neg = x > ((p - 1) >> 1);
@@ -383,9 +398,23 @@ __device__ __forceinline__ void fwd_p1_body(uint64_t *sm, const LimbInfo &li, co
     for (int g = 0; g < C::GS; g++) {
         const int r0 = wq + 8 * g;  // < S1
         V v[C::R1];
+#if UH_NTT_P1_LOADS_FIRST
+        if constexpr (LM != 2) {
+            // every row of the column is requested before the first lift / butterfly (left to itself the
+            // compiler sinks the later loads between the butterflies, where each waits out its own latency)
+            uint64_t raw[C::R1];
 #pragma unroll
-        for (int x = 0; x < C::R1; x++)
-            v[x] = AR::in(load_t<LM>(li, (size_t)(r0 + C::S1 * x) * n2 + col, m, red));
+            for (int x = 0; x < C::R1; x++) raw[x] = li.src[(size_t)(r0 + C::S1 * x) * n2 + col];
+            asm volatile("" ::: "memory");
+#pragma unroll
+            for (int x = 0; x < C::R1; x++) v[x] = AR::in(lift_t<LM>(raw[x], li, m, red));
+        } else
+#endif
+        {
+#pragma unroll
+            for (int x = 0; x < C::R1; x++)
+                v[x] = AR::in(load_t<LM>(li, (size_t)(r0 + C::S1 * x) * n2 + col, m, red));
+        }
         fwd_strided<C::R1>(v, TwG<typename AR::W>{T, 1}, 1, 0, ar.qv());
 #pragma unroll
         for (int x = 0; x < C::R1; x++) sm[(r0 + C::S1 * x) * 32 + lane] = AR::raw(v[x]);
