@@ -478,6 +478,8 @@ __global__ void __launch_bounds__(256, IW8<NKS>::MINB)
                     da[j] = __ldg(Da + (uint32_t)j * ROW);
                     db[j] = okb ? __ldg(Db + (uint32_t)j * ROW) : 0;
                 }
+                // requested with the rest (left after the MAC loop, the compiler issues one of them there)
+                const uint64_t csa = qlimb ? __ldg(c0a + src) : 0, csb = qlimb && okb ? __ldg(c0b + src) : 0;
                 Acc a0, a1, e0, e1;
                 a0.zero();
                 a1.zero();
@@ -491,8 +493,8 @@ __global__ void __launch_bounds__(256, IW8<NKS>::MINB)
                     e1.mac(db[j], y[j]);
                 }
                 if (qlimb) {
-                    a0.mac(Pk, __ldg(c0a + src));
-                    if (okb) e0.mac(Pk, __ldg(c0b + src));
+                    a0.mac(Pk, csa);
+                    if (okb) e0.mac(Pk, csb);
                 }
                 v[0][0] = a0.reduce(m);
                 v[0][1] = a1.reduce(m);
